@@ -1,0 +1,178 @@
+/*
+ * gsr.h -- C-ABI of libgsr.so: B200-native (sm_100a) differentiable scale-aware 2D Gaussian
+ * rasterization of GSASR (arXiv 2501.06838).
+ *
+ * Operation (PAPER.md line numbers):
+ *   Eq. 1  G_i(x,y) = alpha_i c_i f_i(x,y)
+ *   Eq. 2  f_i(x,y) = (2 pi sx sy sqrt(1-rho^2))^-1 exp[-Q/2],
+ *          Q = (dx^2/sx^2 - 2 rho dx dy/(sx sy) + dy^2/sy^2)/(1-rho^2)
+ *   Eq. 4  I_SR(x,y;s) = sum_i G_i(x/s, y/s),  x in [0,sW-1], y in [0,sH-1]
+ *   Alg. 1 only pairs inside the window ("rasterization ratio" r, default 0.1)
+ * with the readings recorded in DESIGN.md ("Readings"):
+ *   - output size  Hs = floor(s*H), Ws = floor(s*W)  (fp64)                          [R4]
+ *   - sample point (x/s, y/s), no half-pixel offset                                  [R3]
+ *   - window: x paired with W, y with H; pixel x is inside iff x0 <= x <= x1 with
+ *       x0 = floor(s*(mu_x - r*W)) + 1,  x1 = ceil(s*(mu_x + r*W)) - 1
+ *     (IEEE fp64, this operation order, no FMA; bounds clamped to +-2^30), y likewise
+ *     with H; clipped to the image                                                    [R1,R2]
+ *   - no clamping of parameters or output                                            [R8]
+ *   - a Gaussian with a non-finite field, sigma_x <= 0, sigma_y <= 0 or |rho| >= 1 is
+ *     invalid: it contributes 0 and receives 0 gradient                               [R20]
+ *   - backward: gradient of the fixed pair set (window edges do not move)            [R11]
+ *
+ * Conventions shared by every entry point:
+ *   - Parameters are float32 SoA device arrays (struct-of-arrays, C order):
+ *       alpha[n]            opacity alpha
+ *       mu[n][2]            centre (mu_x, mu_y) in LR pixels, mu = p + o
+ *       sigma[n][2]         (sigma_x, sigma_y) in LR pixels
+ *       rho[n]              correlation coefficient
+ *       color[n][3]         (c_r, c_g, c_b)
+ *   - Images are HWC float32: out[y][x][k], k = r,g,b (Alg. 1 l.1 "(sH, sW, 3)").
+ *   - ratio r is passed as double (0.1 is not an fp32-exact value); 0 < r <= 1.
+ *   - Ownership: the caller allocates every buffer (inputs, outputs, workspace). The library
+ *     allocates nothing, keeps no state between calls and never synchronises the stream.
+ *   - Asynchrony: every compute entry point enqueues its kernels on `stream` (a cudaStream_t
+ *     passed as void*; NULL = legacy default stream) and returns immediately.
+ *   - Errors: GSR_EINVAL for host-checkable argument errors (nothing is launched);
+ *     GSR_EWORKSPACE if workspace_bytes is smaller than the matching *_workspace_bytes();
+ *     GSR_ECUDA if a launch failed (cudaGetLastError after the launches). Parameter-domain
+ *     violations inside the arrays are NOT errors: such Gaussians are invalid (R20).
+ *   - Limits: Hs, Ws <= 65535; n < 2^31 per call; up to GSR_MAX_IMAGES images per batched call.
+ *   - Thread safety: concurrent calls are safe when they use different workspaces/outputs.
+ */
+#ifndef GSR_H
+#define GSR_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    GSR_OK = 0,
+    GSR_EINVAL = 1,
+    GSR_EWORKSPACE = 2,
+    GSR_ECUDA = 3
+} gsr_status;
+
+#define GSR_MAX_IMAGES 64
+
+/* One image of a (ragged) batch. All images of a call share the parameter arrays: image k owns
+ * Gaussians [g_off, g_off + g_cnt). Its output block starts at float offset out_off of `out`
+ * (and of grad_out for the backward) and holds rows [row_begin, row_end) of the HR image:
+ * (row_end - row_begin) * Ws * 3 floats, row-major HWC. row_begin = 0, row_end = -1 means the
+ * whole image (Hs rows). Row bands are how the multi-GPU path shards an image. */
+typedef struct gsr_image {
+    int32_t lr_h;      /* H >= 1 */
+    int32_t lr_w;      /* W >= 1 */
+    double scale;      /* s >= 1, finite */
+    int64_t g_off;     /* first Gaussian of this image */
+    int64_t g_cnt;     /* number of Gaussians of this image (may be 0) */
+    int64_t out_off;   /* float offset of this image's output block */
+    int32_t row_begin; /* first HR row of the band, 0 <= row_begin */
+    int32_t row_end;   /* one past the last HR row (-1 = Hs); row_begin <= row_end <= Hs */
+} gsr_image;
+
+/* Library version string (static storage). */
+const char* gsr_version(void);
+
+/* Hs = floor(s*H), Ws = floor(s*W) in fp64 (reading R4). GSR_EINVAL on bad arguments. */
+gsr_status gsr_out_dims(int32_t lr_h, int32_t lr_w, double scale, int32_t* out_h, int32_t* out_w);
+
+/* Device workspace needed by the forward or backward of one batched call (bytes, 256-aligned
+ * internally). Returns 0 if the arguments are invalid. The same size serves both passes. */
+size_t gsr_workspace_bytes_batched(const gsr_image* imgs, int32_t n_imgs, int64_t n_total,
+                                   double ratio);
+/* Single-image convenience: n Gaussians, whole image. */
+size_t gsr_workspace_bytes(int64_t n, int32_t lr_h, int32_t lr_w, double scale, double ratio);
+
+/* Forward render (Alg. 1 / Eq. 4) of one image: out[Hs][Ws][3] is overwritten with
+ * I_SR(x,y;s) = sum over valid Gaussians i whose window contains pixel (x,y) of
+ * alpha_i c_i f_i(x/s, y/s). n = 0 gives an all-zero image. */
+gsr_status gsr_render_fwd(const float* alpha, const float* mu, const float* sigma,
+                          const float* rho, const float* color, int64_t n, int32_t lr_h,
+                          int32_t lr_w, double scale, double ratio, float* out, void* workspace,
+                          size_t workspace_bytes, void* stream);
+
+/* Backward of the forward above for L with dL/dI_SR = grad_out[Hs][Ws][3]: writes
+ * (overwrites) d_alpha[n], d_mu[n][2], d_sigma[n][2], d_rho[n], d_color[n][3] (float32,
+ * same layouts as the inputs; d_mu is also dL/d(offset o) since mu = p + o). */
+gsr_status gsr_render_bwd(const float* alpha, const float* mu, const float* sigma,
+                          const float* rho, const float* color, int64_t n, int32_t lr_h,
+                          int32_t lr_w, double scale, double ratio, const float* grad_out,
+                          float* d_alpha, float* d_mu, float* d_sigma, float* d_rho,
+                          float* d_color, void* workspace, size_t workspace_bytes, void* stream);
+
+/* Batched/ragged forward: every image of imgs[0..n_imgs) (host array, read during the call
+ * only) is rendered into its block of `out`. Blocks must not overlap. */
+gsr_status gsr_render_fwd_batched(const float* alpha, const float* mu, const float* sigma,
+                                  const float* rho, const float* color, int64_t n_total,
+                                  const gsr_image* imgs, int32_t n_imgs, double ratio, float* out,
+                                  void* workspace, size_t workspace_bytes, void* stream);
+
+/* Batched backward: grads for all n_total Gaussians (Gaussians not owned by any image get 0). */
+gsr_status gsr_render_bwd_batched(const float* alpha, const float* mu, const float* sigma,
+                                  const float* rho, const float* color, int64_t n_total,
+                                  const gsr_image* imgs, int32_t n_imgs, double ratio,
+                                  const float* grad_out, float* d_alpha, float* d_mu,
+                                  float* d_sigma, float* d_rho, float* d_color, void* workspace,
+                                  size_t workspace_bytes, void* stream);
+
+/* Backward split in two for row-band sharding:
+ * gsr_render_bwd_moments_batched ACCUMULATES (+=) into moments[n_total][8] (float64, caller
+ * zeroes it first) the per-Gaussian pair sums over the pixels of each image's row band, with
+ * e = exp(-Q/2), g = dL/dI at the pixel, c' = alpha c K, K = (2 pi sx sy sqrt(1-rho^2))^-1,
+ * w = e (g . c'), (dx, dy) = (x/s - mu_x, y/s - mu_y):
+ *   m[0..2] = sum e g_k,  m[3] = sum w dx,  m[4] = sum w dy,
+ *   m[5] = sum w dx^2,    m[6] = sum w dx dy,  m[7] = sum w dy^2.
+ * Sums of moments over bands (e.g. an all-reduce across ranks) are moments of the union.
+ * gsr_finalize_grads turns moments into the gradients (closed forms in DESIGN.md). */
+gsr_status gsr_render_bwd_moments_batched(const float* alpha, const float* mu, const float* sigma,
+                                          const float* rho, const float* color, int64_t n_total,
+                                          const gsr_image* imgs, int32_t n_imgs, double ratio,
+                                          const float* grad_out, double* moments, void* workspace,
+                                          size_t workspace_bytes, void* stream);
+gsr_status gsr_finalize_grads(const float* alpha, const float* mu, const float* sigma,
+                              const float* rho, const float* color, int64_t n_total,
+                              const double* moments, float* d_alpha, float* d_mu, float* d_sigma,
+                              float* d_rho, float* d_color, void* stream);
+
+/* Number of (Gaussian, pixel) pairs inside the windows, P = sum_i |rect_i| restricted to each
+ * image's row band (the work unit of the roofline). Writes one int64 to *d_pairs
+ * (device pointer). Uses the workspace. */
+gsr_status gsr_pair_count_batched(const float* alpha, const float* mu, const float* sigma,
+                                  const float* rho, const float* color, int64_t n_total,
+                                  const gsr_image* imgs, int32_t n_imgs, double ratio,
+                                  int64_t* d_pairs, void* workspace, size_t workspace_bytes,
+                                  void* stream);
+
+/* ---- introspection for the parity tests (same kernels as the render path) ---------------- */
+
+/* Per-Gaussian integer window rect as computed on the GPU (reading R2), clipped to the image:
+ * rects[i] = {x0, x1, y0, y1}; an empty/invalid rect is {1, 0, 1, 0}. Single image. */
+gsr_status gsr_debug_rects(const float* alpha, const float* mu, const float* sigma,
+                           const float* rho, const float* color, int64_t n, int32_t lr_h,
+                           int32_t lr_w, double scale, double ratio, int32_t* rects, void* stream);
+
+/* Tile binning, materialised: for every render tile of the single image (tiles of
+ * tile_w x tile_h HR px in row-major tile order, as reported by gsr_tile_shape), the exact list of
+ * Gaussians whose rect intersects the tile, in the order the render kernels visit them (cell
+ * order, ascending index within a cell). Two calls: first with ids == NULL to fill
+ * counts[ntiles] (device int32); then with ids (device int32, sum(counts) entries, CSR by tile)
+ * and cells (device int32, same length, the sort key = cell of each entry). */
+gsr_status gsr_debug_tile_lists(const float* alpha, const float* mu, const float* sigma,
+                                const float* rho, const float* color, int64_t n, int32_t lr_h,
+                                int32_t lr_w, double scale, double ratio, int32_t* counts,
+                                int32_t* ids, int32_t* cells, void* workspace,
+                                size_t workspace_bytes, void* stream);
+
+/* Render-tile and cell geometry used by the kernels (compile-time constants). */
+void gsr_tile_shape(int32_t* tile_w, int32_t* tile_h, int32_t* cell_w, int32_t* cell_h);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* GSR_H */

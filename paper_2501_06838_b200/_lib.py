@@ -1,0 +1,109 @@
+"""ctypes loader for libgsr.so (the C-ABI of include/gsr.h). Argument marshalling only.
+
+There is no fallback: if the library is missing or cannot be loaded the import of the ops fails
+loudly (RuntimeError) -- the product path never routes through the oracle or a CPU renderer.
+"""
+from __future__ import annotations
+
+import ctypes
+from pathlib import Path
+
+_PKG = Path(__file__).resolve().parent
+LIB_PATH = _PKG / "libgsr.so"
+
+GSR_OK, GSR_EINVAL, GSR_EWORKSPACE, GSR_ECUDA = 0, 1, 2, 3
+_ERR = {GSR_EINVAL: "GSR_EINVAL (invalid argument)", GSR_EWORKSPACE: "GSR_EWORKSPACE",
+        GSR_ECUDA: "GSR_ECUDA (kernel launch failed)"}
+MAX_IMAGES = 64
+
+# Every symbol include/gsr.h declares (checked by tests/test_abi.py).
+EXPORTS = ["gsr_version", "gsr_out_dims", "gsr_workspace_bytes_batched", "gsr_workspace_bytes",
+           "gsr_render_fwd", "gsr_render_bwd", "gsr_render_fwd_batched", "gsr_render_bwd_batched",
+           "gsr_render_bwd_moments_batched", "gsr_finalize_grads", "gsr_pair_count_batched",
+           "gsr_debug_rects", "gsr_debug_tile_lists", "gsr_tile_shape"]
+
+
+class GsrImage(ctypes.Structure):
+    _fields_ = [("lr_h", ctypes.c_int32), ("lr_w", ctypes.c_int32), ("scale", ctypes.c_double),
+                ("g_off", ctypes.c_int64), ("g_cnt", ctypes.c_int64), ("out_off", ctypes.c_int64),
+                ("row_begin", ctypes.c_int32), ("row_end", ctypes.c_int32)]
+
+
+class GsrError(RuntimeError):
+    pass
+
+
+_P = ctypes.c_void_p
+_I64 = ctypes.c_int64
+_I32 = ctypes.c_int32
+_D = ctypes.c_double
+_SZ = ctypes.c_size_t
+_IMGP = ctypes.POINTER(GsrImage)
+_lib = None
+
+
+def load(path: Path | str | None = None):
+    """Load libgsr.so once and declare every signature."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    p = Path(path) if path else LIB_PATH
+    if not p.exists():
+        raise RuntimeError(f"libgsr.so not built ({p}); run __graft_entry__.build() or "
+                           f"python -m paper_2501_06838_b200.build")
+    lib = ctypes.CDLL(str(p))
+    par = [_P, _P, _P, _P, _P]
+    lib.gsr_version.restype = ctypes.c_char_p
+    lib.gsr_version.argtypes = []
+    lib.gsr_out_dims.argtypes = [_I32, _I32, _D, ctypes.POINTER(_I32), ctypes.POINTER(_I32)]
+    lib.gsr_workspace_bytes_batched.argtypes = [_IMGP, _I32, _I64, _D]
+    lib.gsr_workspace_bytes_batched.restype = _SZ
+    lib.gsr_workspace_bytes.argtypes = [_I64, _I32, _I32, _D, _D]
+    lib.gsr_workspace_bytes.restype = _SZ
+    lib.gsr_render_fwd.argtypes = par + [_I64, _I32, _I32, _D, _D, _P, _P, _SZ, _P]
+    lib.gsr_render_bwd.argtypes = par + [_I64, _I32, _I32, _D, _D, _P, _P, _P, _P, _P, _P, _P,
+                                         _SZ, _P]
+    lib.gsr_render_fwd_batched.argtypes = par + [_I64, _IMGP, _I32, _D, _P, _P, _SZ, _P]
+    lib.gsr_render_bwd_batched.argtypes = par + [_I64, _IMGP, _I32, _D, _P, _P, _P, _P, _P, _P,
+                                                 _P, _SZ, _P]
+    lib.gsr_render_bwd_moments_batched.argtypes = par + [_I64, _IMGP, _I32, _D, _P, _P, _P, _SZ,
+                                                         _P]
+    lib.gsr_finalize_grads.argtypes = par + [_I64, _P, _P, _P, _P, _P, _P, _P]
+    lib.gsr_pair_count_batched.argtypes = par + [_I64, _IMGP, _I32, _D, _P, _P, _SZ, _P]
+    lib.gsr_debug_rects.argtypes = par + [_I64, _I32, _I32, _D, _D, _P, _P]
+    lib.gsr_debug_tile_lists.argtypes = par + [_I64, _I32, _I32, _D, _D, _P, _P, _P, _P, _SZ, _P]
+    lib.gsr_tile_shape.argtypes = [ctypes.POINTER(_I32)] * 4
+    lib.gsr_tile_shape.restype = None
+    _lib = lib
+    return lib
+
+
+def check(status: int, what: str) -> None:
+    if status != GSR_OK:
+        raise GsrError(f"{what} failed: {_ERR.get(status, status)}")
+
+
+def images_array(imgs):
+    """[(H, W, s, g_off, g_cnt, out_off, row_begin, row_end), ...] -> ctypes array."""
+    arr = (GsrImage * len(imgs))()
+    for k, t in enumerate(imgs):
+        H, W, s, go, gc, oo, rb, re = t
+        arr[k] = GsrImage(int(H), int(W), float(s), int(go), int(gc), int(oo), int(rb), int(re))
+    return arr
+
+
+def out_dims(H: int, W: int, s: float):
+    h, w = _I32(), _I32()
+    check(load().gsr_out_dims(int(H), int(W), float(s), ctypes.byref(h), ctypes.byref(w)),
+          "gsr_out_dims")
+    return h.value, w.value
+
+
+def tile_shape():
+    v = [_I32() for _ in range(4)]
+    load().gsr_tile_shape(*[ctypes.byref(x) for x in v])
+    return tuple(x.value for x in v)
+
+
+def version() -> str:
+    return load().gsr_version().decode()

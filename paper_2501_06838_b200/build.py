@@ -1,0 +1,56 @@
+"""Build libgsr.so (sm_100a) in-tree with nvcc. Called by __graft_entry__.build()."""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+CSRC = PKG / "csrc"
+LIB = PKG / "libgsr.so"
+ROOT = PKG.parent
+SOURCES = ["binning.cu", "render_fwd.cu", "render_bwd.cu", "gsr_abi.cu"]
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
+         "--expt-relaxed-constexpr", "-I", str(ROOT / "include")]
+
+
+def _stale(out: Path, deps) -> bool:
+    if not out.exists():
+        return True
+    t = out.stat().st_mtime
+    return any(Path(d).stat().st_mtime > t for d in deps)
+
+
+def build(force: bool = False, verbose: bool = False) -> Path:
+    headers = list(CSRC.glob("*.cuh")) + [ROOT / "include" / "gsr.h"]
+    objdir = PKG / "build"
+    objdir.mkdir(exist_ok=True)
+    objs = []
+    for src in SOURCES:
+        s = CSRC / src
+        o = objdir / (src + ".o")
+        objs.append(o)
+        if force or _stale(o, [s, *headers]):
+            cmd = [NVCC, *ARCH, *FLAGS, "-c", str(s), "-o", str(o)]
+            r = subprocess.run(cmd, capture_output=True, text=True)
+            log = objdir / (src + ".ptxas.txt")
+            log.write_text(r.stdout + r.stderr)
+            if r.returncode != 0:
+                sys.stderr.write(r.stdout + r.stderr)
+                raise RuntimeError(f"nvcc failed for {src}")
+            if verbose:
+                sys.stderr.write(r.stderr)
+    if force or _stale(LIB, objs):
+        tmp = LIB.with_suffix(".so.tmp%d" % os.getpid())
+        cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", str(tmp), *map(str, objs)]
+        subprocess.check_call(cmd)
+        os.replace(tmp, LIB)
+    return LIB
+
+
+if __name__ == "__main__":
+    build(force="--force" in sys.argv, verbose=True)
+    print(LIB)

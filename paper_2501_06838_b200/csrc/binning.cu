@@ -1,0 +1,464 @@
+// binning.cu -- K1 (window rect + cell key), stable LSD radix sort, cell starts, K1b (records),
+// pair count and the debug introspection kernels.
+//
+// Binning: every Gaussian's window has the same size (Alg. 1 window
+// r*W x r*H in LR px, P:1385 / reading R1-R2), so a render tile's candidates are the Gaussians
+// whose unclipped rect origin (x0u, y0u) lies in [Tx0 - wmax + 1, Tx1] x [Ty0 - hmax + 1, Ty1].
+// Sorting Gaussians by the CELL x CELL cell of that origin turns each tile's candidate set into
+// one contiguous record span per cell row -- no per-(Gaussian, tile) key duplication.
+#include <utility>
+
+#include "gsr_internal.cuh"
+
+namespace gsr {
+
+namespace {
+
+constexpr int RS_WARPS = 8;
+constexpr int RS_THREADS = RS_WARPS * 32;
+constexpr int RS_SEG = 256;                      // items per warp segment
+constexpr int RS_BLOCK = RS_WARPS * RS_SEG;      // 2048 items per block
+constexpr int SCAN_THREADS = 1024;
+constexpr int SCAN_ITEMS = 4;
+constexpr int SCAN_BLOCK = SCAN_THREADS * SCAN_ITEMS;
+
+inline size_t align256(size_t b) { return (b + 255) & ~size_t(255); }
+
+long long rs_blocks(long long n) { return (n + RS_BLOCK - 1) / RS_BLOCK; }
+long long scan_blocks(long long n) { return (n + SCAN_BLOCK - 1) / SCAN_BLOCK; }
+
+// ---- K1: keys ----------------------------------------------------------------------------
+__global__ void k_keys(const float* __restrict__ alpha, const float* __restrict__ mu,
+                       const float* __restrict__ sigma, const float* __restrict__ rho,
+                       const float* __restrict__ color, long long n, ImgTable tab,
+                       uint32_t* __restrict__ keys, int* __restrict__ vals) {
+    long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    uint32_t key = (uint32_t)tab.total_cells;
+    int k = find_image_by_gauss(tab, i);
+    if (k >= 0) {
+        const DevImg& im = tab.img[k];
+        float mx = mu[2 * i], my = mu[2 * i + 1];
+        if (gaussian_valid(alpha[i], mx, my, sigma[2 * i], sigma[2 * i + 1], rho[i],
+                           color[3 * i], color[3 * i + 1], color[3 * i + 2])) {
+            Rect r = window_rect(mx, my, im);
+            if (r.nonempty) {
+                int cx = (r.x0u + im.offx) / CELL;
+                int cy = (r.y0u - im.row_begin + im.offy) / CELL;
+                key = (uint32_t)(im.cell_base + cy * im.ncx + cx);
+            }
+        }
+    }
+    keys[i] = key;
+    vals[i] = (int)i;
+}
+
+// ---- stable LSD radix sort, 8-bit digits -----------------------------------------------
+__global__ void __launch_bounds__(RS_THREADS) k_rs_hist(const uint32_t* __restrict__ keys,
+                                                        long long n, int shift,
+                                                        int* __restrict__ hist, int nblocks) {
+    __shared__ int cnt[256];
+    for (int d = threadIdx.x; d < 256; d += RS_THREADS) cnt[d] = 0;
+    __syncthreads();
+    long long b0 = (long long)blockIdx.x * RS_BLOCK;
+    long long b1 = min(b0 + RS_BLOCK, n);
+    for (long long i = b0 + threadIdx.x; i < b1; i += RS_THREADS)
+        atomicAdd(&cnt[(keys[i] >> shift) & 255u], 1);
+    __syncthreads();
+    for (int d = threadIdx.x; d < 256; d += RS_THREADS)
+        hist[(long long)d * nblocks + blockIdx.x] = cnt[d];
+}
+
+__global__ void __launch_bounds__(RS_THREADS) k_rs_scatter(
+    const uint32_t* __restrict__ keys_in, const int* __restrict__ vals_in, long long n, int shift,
+    const int* __restrict__ offs, int nblocks, uint32_t* __restrict__ keys_out,
+    int* __restrict__ vals_out) {
+    __shared__ int wcnt[RS_WARPS][256];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int d = threadIdx.x; d < RS_WARPS * 256; d += RS_THREADS) (&wcnt[0][0])[d] = 0;
+    __syncthreads();
+    const long long seg = (long long)blockIdx.x * RS_BLOCK + (long long)warp * RS_SEG;
+    const unsigned lt = (1u << lane) - 1u;
+    // pass 1: per-warp digit counts
+    for (int c = 0; c < RS_SEG; c += 32) {
+        long long i = seg + c + lane;
+        bool valid = i < n;
+        unsigned vm = __ballot_sync(0xffffffffu, valid);
+        if (vm == 0) break;
+        if (valid) {
+            unsigned d = (keys_in[i] >> shift) & 255u;
+            unsigned peers = __match_any_sync(vm, d);
+            if ((peers & lt) == 0) wcnt[warp][d] += __popc(peers);
+        }
+        __syncwarp();
+    }
+    __syncthreads();
+    // per digit: exclusive prefix over warps + global (digit, block) offset
+    for (int d = threadIdx.x; d < 256; d += RS_THREADS) {
+        int run = offs[(long long)d * nblocks + blockIdx.x];
+        for (int w = 0; w < RS_WARPS; ++w) {
+            int t = wcnt[w][d];
+            wcnt[w][d] = run;
+            run += t;
+        }
+    }
+    __syncthreads();
+    // pass 2: stable ranks and scatter
+    for (int c = 0; c < RS_SEG; c += 32) {
+        long long i = seg + c + lane;
+        bool valid = i < n;
+        unsigned vm = __ballot_sync(0xffffffffu, valid);
+        if (vm == 0) break;
+        uint32_t key = 0; int val = 0; unsigned d = 0, peers = 0; int pos = 0;
+        if (valid) {
+            key = keys_in[i];
+            val = vals_in[i];
+            d = (key >> shift) & 255u;
+            peers = __match_any_sync(vm, d);
+            pos = wcnt[warp][d] + __popc(peers & lt);
+        }
+        __syncwarp();
+        if (valid) {
+            if ((peers & lt) == 0) wcnt[warp][d] += __popc(peers);
+            keys_out[pos] = key;
+            vals_out[pos] = val;
+        }
+        __syncwarp();
+    }
+}
+
+// ---- exclusive scan (int32), reduce-then-scan ----------------------------------------------
+__device__ __forceinline__ int block_incl_scan(int v, int* sh) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        int t = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += t;
+    }
+    if (lane == 31) sh[warp] = v;
+    __syncthreads();
+    if (warp == 0) {
+        int w = (lane < (int)(blockDim.x >> 5)) ? sh[lane] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            int t = __shfl_up_sync(0xffffffffu, w, o);
+            if (lane >= o) w += t;
+        }
+        sh[lane] = w;
+    }
+    __syncthreads();
+    int r = v + (warp > 0 ? sh[warp - 1] : 0);
+    __syncthreads();
+    return r;
+}
+
+__global__ void __launch_bounds__(SCAN_THREADS) k_scan_reduce(const int* __restrict__ in,
+                                                              long long n,
+                                                              int* __restrict__ sums) {
+    __shared__ int sh[32];
+    long long base = (long long)blockIdx.x * SCAN_BLOCK + (long long)threadIdx.x * SCAN_ITEMS;
+    int v = 0;
+#pragma unroll
+    for (int j = 0; j < SCAN_ITEMS; ++j)
+        if (base + j < n) v += in[base + j];
+    int incl = block_incl_scan(v, sh);
+    if (threadIdx.x == SCAN_THREADS - 1) sums[blockIdx.x] = incl;
+}
+
+// single block: exclusive scan of the block sums in place (any count, sequential chunks)
+__global__ void __launch_bounds__(SCAN_THREADS) k_scan_sums(int* __restrict__ sums,
+                                                            long long nb) {
+    __shared__ int sh[32];
+    __shared__ int last;
+    int carry = 0;
+    for (long long c = 0; c < nb; c += SCAN_THREADS) {
+        long long i = c + threadIdx.x;
+        int v = i < nb ? sums[i] : 0;
+        int incl = block_incl_scan(v, sh);
+        if (i < nb) sums[i] = carry + incl - v;
+        if (threadIdx.x == SCAN_THREADS - 1) last = incl;
+        __syncthreads();
+        carry += last;
+        __syncthreads();
+    }
+}
+
+__global__ void __launch_bounds__(SCAN_THREADS) k_scan_down(const int* __restrict__ in,
+                                                            long long n,
+                                                            const int* __restrict__ sums,
+                                                            int* __restrict__ out) {
+    __shared__ int sh[32];
+    long long base = (long long)blockIdx.x * SCAN_BLOCK + (long long)threadIdx.x * SCAN_ITEMS;
+    int v[SCAN_ITEMS];
+    int t = 0;
+#pragma unroll
+    for (int j = 0; j < SCAN_ITEMS; ++j) {
+        v[j] = (base + j < n) ? in[base + j] : 0;
+        t += v[j];
+    }
+    int incl = block_incl_scan(t, sh);
+    int run = sums[blockIdx.x] + incl - t;
+#pragma unroll
+    for (int j = 0; j < SCAN_ITEMS; ++j) {
+        if (base + j < n) out[base + j] = run;
+        run += v[j];
+    }
+}
+
+// ---- cell starts from sorted keys --------------------------------------------------------
+__global__ void k_cell_start(const uint32_t* __restrict__ keys, long long n, int total_cells,
+                             int* __restrict__ cell_start) {
+    long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p > n) return;
+    long long prev = p == 0 ? -1 : (long long)keys[p - 1];
+    long long cur = p == n ? (long long)total_cells : (long long)keys[p];
+    if (cur > total_cells) cur = total_cells;
+    for (long long c = prev + 1; c <= cur; ++c) cell_start[c] = (int)p;
+}
+
+// ---- K1b: records in sorted order ---------------------------------------------------------
+__global__ void k_records(const float* __restrict__ alpha, const float* __restrict__ mu,
+                          const float* __restrict__ sigma, const float* __restrict__ rho,
+                          const float* __restrict__ color, long long n, ImgTable tab,
+                          const uint32_t* __restrict__ keys, const int* __restrict__ perm,
+                          float4* __restrict__ rec) {
+    long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= n) return;
+    if (keys[p] >= (uint32_t)tab.total_cells) return;
+    long long i = perm[p];
+    int k = find_image_by_gauss(tab, i);
+    const DevImg& im = tab.img[k];
+    float mxf = mu[2 * i], myf = mu[2 * i + 1];
+    Rect r = window_rect(mxf, myf, im);
+    double mx = mxf, my = myf;
+    double sx = sigma[2 * i], sy = sigma[2 * i + 1], rh = rho[i], al = alpha[i];
+    double D = (1.0 - rh) * (1.0 + rh);
+    // exponent in factored form (no cancellation):
+    //   q = -Q/2 log2 e = -(w'^2 + v'^2),  w' = a1 dx + b1 dy,  v' = c1 dy
+    //   a1 = sqrt(k/D)/sx, b1 = -rho sqrt(k/D)/sy, c1 = sqrt(k)/sy,  k = log2(e)/2
+    double kd = sqrt(HALF_LOG2E / D);
+    double a1 = kd / sx, b1 = -rh * kd / sy, c1 = sqrt(HALF_LOG2E) / sy;
+    double K = 1.0 / (TWO_PI * sx * sy * sqrt(D));
+    double axd = rint(im.s * mx), ayd = rint(im.s * my);   // anchor: nearest HR pixel
+    double dlx = mx - axd / im.s, dly = my - ayd / im.s;
+    double w = al * K;
+    float4 r0 = make_float4((float)axd, (float)ayd, (float)dlx, (float)dly);
+    float4 r1 = make_float4((float)a1, (float)b1, (float)c1, (float)(w * color[3 * i]));
+    unsigned xs = (unsigned)r.x0 | ((unsigned)r.x1 << 16);
+    unsigned ys = (unsigned)r.y0 | ((unsigned)r.y1 << 16);
+    float4 r2 = make_float4((float)(w * color[3 * i + 1]), (float)(w * color[3 * i + 2]),
+                            __uint_as_float(xs), __uint_as_float(ys));
+    rec[3 * p + 0] = r0;
+    rec[3 * p + 1] = r1;
+    rec[3 * p + 2] = r2;
+}
+
+// ---- pair count ---------------------------------------------------------------------------
+__global__ void k_pair_count(const float* __restrict__ alpha, const float* __restrict__ mu,
+                             const float* __restrict__ sigma, const float* __restrict__ rho,
+                             const float* __restrict__ color, long long n, ImgTable tab,
+                             unsigned long long* __restrict__ out) {
+    long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    unsigned long long v = 0;
+    if (i < n) {
+        int k = find_image_by_gauss(tab, i);
+        if (k >= 0) {
+            const DevImg& im = tab.img[k];
+            float mx = mu[2 * i], my = mu[2 * i + 1];
+            if (gaussian_valid(alpha[i], mx, my, sigma[2 * i], sigma[2 * i + 1], rho[i],
+                               color[3 * i], color[3 * i + 1], color[3 * i + 2])) {
+                Rect r = window_rect(mx, my, im);
+                if (r.nonempty)
+                    v = (unsigned long long)(r.x1 - r.x0 + 1) * (unsigned long long)(r.y1 - r.y0 + 1);
+            }
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0 && v) atomicAdd(out, v);
+}
+
+__global__ void k_debug_rects(const float* __restrict__ alpha, const float* __restrict__ mu,
+                              const float* __restrict__ sigma, const float* __restrict__ rho,
+                              const float* __restrict__ color, long long n, ImgTable tab,
+                              int4* __restrict__ rects) {
+    long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    int4 o = make_int4(1, 0, 1, 0);
+    int k = find_image_by_gauss(tab, i);
+    if (k >= 0) {
+        const DevImg& im = tab.img[k];
+        float mx = mu[2 * i], my = mu[2 * i + 1];
+        if (gaussian_valid(alpha[i], mx, my, sigma[2 * i], sigma[2 * i + 1], rho[i],
+                           color[3 * i], color[3 * i + 1], color[3 * i + 2])) {
+            Rect r = window_rect(mx, my, im);
+            if (r.nonempty) o = make_int4(r.x0, r.x1, r.y0, r.y1);
+        }
+    }
+    rects[i] = o;
+}
+
+// Materialised per-tile candidate lists, walking the same cell spans as the render kernels and
+// keeping the candidates whose rect intersects the tile. One thread per tile (test-only).
+__global__ void k_debug_tile_lists(ImgTable tab, const int* __restrict__ cell_start,
+                                   const float4* __restrict__ rec, const int* __restrict__ perm,
+                                   const uint32_t* __restrict__ keys,
+                                   const int* __restrict__ tile_off, int* __restrict__ counts,
+                                   int* __restrict__ ids, int* __restrict__ cells) {
+    int tile = blockIdx.x * blockDim.x + threadIdx.x;
+    if (tile >= tab.total_tiles) return;
+    const DevImg& im = tab.img[find_image_by_tile(tab, tile)];
+    int t = tile - im.tile_base;
+    int Tx0 = (t % im.ntx) * TILE_W, Ty0 = im.row_begin + (t / im.ntx) * TILE_H;
+    int Tx1 = min(Tx0 + TILE_W - 1, im.Ws - 1), Ty1 = min(Ty0 + TILE_H - 1, im.row_end - 1);
+    int cx_lo = (Tx0 - im.wmax + 1 + im.offx) / CELL;
+    int cx_hi = min(im.ncx - 1, (Tx1 + im.offx) / CELL);
+    int cy_lo = (Ty0 - im.row_begin - im.hmax + 1 + im.offy) / CELL;
+    int cy_hi = min(im.ncy - 1, (Ty1 - im.row_begin + im.offy) / CELL);
+    int c = 0;
+    int base = ids ? tile_off[tile] : 0;
+    for (int cy = cy_lo; cy <= cy_hi; ++cy) {
+        int row = im.cell_base + cy * im.ncx;
+        for (int p = cell_start[row + cx_lo]; p < cell_start[row + cx_hi + 1]; ++p) {
+            float4 r2 = rec[3 * p + 2];
+            unsigned xs = __float_as_uint(r2.z), ys = __float_as_uint(r2.w);
+            int x0 = xs & 0xffff, x1 = xs >> 16, y0 = ys & 0xffff, y1 = ys >> 16;
+            if (x1 < Tx0 || x0 > Tx1 || y1 < Ty0 || y0 > Ty1) continue;
+            if (ids) {
+                ids[base + c] = perm[p];
+                cells[base + c] = (int)keys[p];
+            }
+            ++c;
+        }
+    }
+    if (!ids) counts[tile] = c;
+}
+
+inline unsigned grid1d(long long n, int t) { return (unsigned)((n + t - 1) / t); }
+
+}  // namespace
+
+size_t binning_bytes(long long n, int total_cells, int total_tiles) {
+    size_t b = 0;
+    long long nb = rs_blocks(n);
+    long long hist = 256 * nb;
+    long long scan_src = hist > (long long)total_tiles + 1 ? hist : (long long)total_tiles + 1;
+    b += 2 * align256(sizeof(uint32_t) * (size_t)n);            // keys a/b
+    b += 2 * align256(sizeof(int) * (size_t)n);                 // vals a/b
+    b += align256(sizeof(int) * (size_t)(hist + 1));            // hist
+    b += align256(sizeof(int) * (size_t)(scan_blocks(scan_src) + 1));  // scan tmp
+    b += align256(sizeof(int) * (size_t)(total_cells + 1));     // cell_start
+    b += align256(sizeof(float4) * 3 * (size_t)n);              // records
+    b += align256(sizeof(double) * 8 * (size_t)n);              // moments
+    b += align256(sizeof(unsigned long long) * 4);              // counters
+    b += align256(sizeof(int) * (size_t)(total_tiles + 1));     // debug tile offsets
+    return b + 256;
+}
+
+void carve_workspace(void* base, long long n, int total_cells, int total_tiles, Workspace* ws) {
+    char* p = (char*)(((uintptr_t)base + 255) & ~uintptr_t(255));
+    auto take = [&](size_t bytes) { char* r = p; p += align256(bytes); return (void*)r; };
+    long long nb = rs_blocks(n);
+    long long hist = 256 * nb;
+    long long scan_src = hist > (long long)total_tiles + 1 ? hist : (long long)total_tiles + 1;
+    ws->keys_a = (uint32_t*)take(sizeof(uint32_t) * (size_t)n);
+    ws->keys_b = (uint32_t*)take(sizeof(uint32_t) * (size_t)n);
+    ws->vals_a = (int*)take(sizeof(int) * (size_t)n);
+    ws->vals_b = (int*)take(sizeof(int) * (size_t)n);
+    ws->hist = (int*)take(sizeof(int) * (size_t)(hist + 1));
+    ws->scan_tmp = (int*)take(sizeof(int) * (size_t)(scan_blocks(scan_src) + 1));
+    ws->cell_start = (int*)take(sizeof(int) * (size_t)(total_cells + 1));
+    ws->rec = (float4*)take(sizeof(float4) * 3 * (size_t)n);
+    ws->moments = (double*)take(sizeof(double) * 8 * (size_t)n);
+    ws->counter = (unsigned long long*)take(sizeof(unsigned long long) * 4);
+    ws->tile_off = (int*)take(sizeof(int) * (size_t)(total_tiles + 1));
+}
+
+cudaError_t exclusive_scan_i32(const int* in, int* out, long long n, int* tmp, cudaStream_t st) {
+    if (n <= 0) return cudaSuccess;
+    long long nb = scan_blocks(n);
+    k_scan_reduce<<<(unsigned)nb, SCAN_THREADS, 0, st>>>(in, n, tmp);
+    k_scan_sums<<<1, SCAN_THREADS, 0, st>>>(tmp, nb);
+    k_scan_down<<<(unsigned)nb, SCAN_THREADS, 0, st>>>(in, n, tmp, out);
+    return cudaGetLastError();
+}
+
+cudaError_t bin_gaussians(const float* alpha, const float* mu, const float* sigma,
+                          const float* rho, const float* color, long long n,
+                          const ImgTable& tab, Workspace& ws, int** perm_out,
+                          uint32_t** keys_sorted_out, cudaStream_t st) {
+    if (n > 0) {
+        k_keys<<<grid1d(n, 256), 256, 0, st>>>(alpha, mu, sigma, rho, color, n, tab, ws.keys_a,
+                                               ws.vals_a);
+        int bits = 32 - __builtin_clz((unsigned)tab.total_cells | 1u);
+        int passes = (bits + 7) / 8;
+        long long nb = rs_blocks(n);
+        uint32_t* kin = ws.keys_a; uint32_t* kout = ws.keys_b;
+        int* vin = ws.vals_a; int* vout = ws.vals_b;
+        for (int ps = 0; ps < passes; ++ps) {
+            int shift = 8 * ps;
+            k_rs_hist<<<(unsigned)nb, RS_THREADS, 0, st>>>(kin, n, shift, ws.hist, (int)nb);
+            cudaError_t e = exclusive_scan_i32(ws.hist, ws.hist, 256 * nb, ws.scan_tmp, st);
+            if (e != cudaSuccess) return e;
+            k_rs_scatter<<<(unsigned)nb, RS_THREADS, 0, st>>>(kin, vin, n, shift, ws.hist,
+                                                             (int)nb, kout, vout);
+            std::swap(kin, kout);
+            std::swap(vin, vout);
+        }
+        k_cell_start<<<grid1d(n + 1, 256), 256, 0, st>>>(kin, n, tab.total_cells,
+                                                         ws.cell_start);
+        k_records<<<grid1d(n, 256), 256, 0, st>>>(alpha, mu, sigma, rho, color, n, tab, kin, vin,
+                                                   ws.rec);
+        *perm_out = vin;
+        *keys_sorted_out = kin;
+    } else {
+        // no Gaussians: every cell is empty
+        cudaMemsetAsync(ws.cell_start, 0, sizeof(int) * (size_t)(tab.total_cells + 1), st);
+        *perm_out = ws.vals_a;
+        *keys_sorted_out = ws.keys_a;
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_pair_count(const float* alpha, const float* mu, const float* sigma,
+                              const float* rho, const float* color, long long n,
+                              const ImgTable& tab, long long* d_pairs, cudaStream_t st) {
+    cudaMemsetAsync(d_pairs, 0, sizeof(long long), st);
+    if (n > 0)
+        k_pair_count<<<grid1d(n, 256), 256, 0, st>>>(alpha, mu, sigma, rho, color, n, tab,
+                                                     (unsigned long long*)d_pairs);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_debug_rects(const float* alpha, const float* mu, const float* sigma,
+                               const float* rho, const float* color, long long n,
+                               const ImgTable& tab, int* rects, cudaStream_t st) {
+    if (n > 0)
+        k_debug_rects<<<grid1d(n, 256), 256, 0, st>>>(alpha, mu, sigma, rho, color, n, tab,
+                                                      (int4*)rects);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_debug_tile_lists(const ImgTable& tab, const Workspace& ws, const int* perm,
+                                    const uint32_t* keys_sorted, int* counts, int* ids,
+                                    int* cells, cudaStream_t st) {
+    int nt = tab.total_tiles;
+    if (nt <= 0) return cudaSuccess;
+    if (!ids) {
+        k_debug_tile_lists<<<grid1d(nt, 64), 64, 0, st>>>(tab, ws.cell_start, ws.rec, perm,
+                                                          keys_sorted, nullptr, counts, nullptr,
+                                                          nullptr);
+    } else {
+        k_debug_tile_lists<<<grid1d(nt, 64), 64, 0, st>>>(tab, ws.cell_start, ws.rec, perm,
+                                                          keys_sorted, nullptr, ws.tile_off,
+                                                          nullptr, nullptr);
+        cudaError_t e = exclusive_scan_i32(ws.tile_off, ws.tile_off, nt, ws.scan_tmp, st);
+        if (e != cudaSuccess) return e;
+        k_debug_tile_lists<<<grid1d(nt, 64), 64, 0, st>>>(tab, ws.cell_start, ws.rec, perm,
+                                                          keys_sorted, ws.tile_off, counts, ids,
+                                                          cells);
+    }
+    return cudaGetLastError();
+}
+
+}  // namespace gsr

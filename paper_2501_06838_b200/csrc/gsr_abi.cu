@@ -1,0 +1,274 @@
+// gsr_abi.cu -- the C-ABI of include/gsr.h: argument validation, per-image geometry (fp64,
+// host), workspace carving and launch orchestration. No allocation, no stream sync.
+#include <cmath>
+#include <cstring>
+
+#include "../../include/gsr.h"
+#include "gsr_internal.cuh"
+
+using namespace gsr;
+
+namespace {
+
+constexpr int MAX_DIM = 65535;
+
+inline int ceil_div(long long a, long long b) { return (int)((a + b - 1) / b); }
+
+// Builds the per-image table; returns GSR_EINVAL on any host-checkable argument error.
+gsr_status build_table(const gsr_image* imgs, int32_t n_imgs, int64_t n_total, double ratio,
+                       ImgTable* tab) {
+    if (!imgs || n_imgs < 1 || n_imgs > GSR_MAX_IMAGES) return GSR_EINVAL;
+    if (n_total < 0 || n_total >= (1LL << 31)) return GSR_EINVAL;
+    if (!std::isfinite(ratio) || !(ratio > 0.0) || ratio > 1.0) return GSR_EINVAL;
+    std::memset(tab, 0, sizeof(*tab));
+    tab->n_imgs = n_imgs;
+    long long cells = 0, tiles = 0, prev_end = 0;
+    for (int k = 0; k < n_imgs; ++k) {
+        const gsr_image& g = imgs[k];
+        if (g.lr_h < 1 || g.lr_w < 1) return GSR_EINVAL;
+        if (!std::isfinite(g.scale) || !(g.scale >= 1.0)) return GSR_EINVAL;
+        if (g.g_off < prev_end || g.g_cnt < 0 || g.g_off + g.g_cnt > n_total) return GSR_EINVAL;
+        if (g.out_off < 0) return GSR_EINVAL;
+        prev_end = g.g_off + g.g_cnt;
+        double hsd = std::floor(g.scale * (double)g.lr_h);   // reading R4
+        double wsd = std::floor(g.scale * (double)g.lr_w);
+        if (hsd > MAX_DIM || wsd > MAX_DIM || hsd < 1 || wsd < 1) return GSR_EINVAL;
+        DevImg& d = tab->img[k];
+        d.s = g.scale;
+        d.hx = ratio * (double)g.lr_w;    // reading R1: x <-> W
+        d.hy = ratio * (double)g.lr_h;
+        d.g_off = g.g_off;
+        d.g_cnt = g.g_cnt;
+        d.out_off = g.out_off;
+        d.invs = (float)(1.0 / g.scale);
+        d.H = g.lr_h; d.W = g.lr_w; d.Hs = (int)hsd; d.Ws = (int)wsd;
+        int rb = g.row_begin, re = g.row_end < 0 ? d.Hs : g.row_end;
+        if (rb < 0 || re > d.Hs || rb > re) return GSR_EINVAL;
+        d.row_begin = rb; d.row_end = re;
+        // bounds on the unclipped rect extent: width <= 2 s r W + 1 (+ fp64 rounding)
+        d.wmax = (int)std::ceil(2.0 * g.scale * d.hx) + 2;
+        d.hmax = (int)std::ceil(2.0 * g.scale * d.hy) + 2;
+        d.offx = CELL * ceil_div(d.wmax, CELL);
+        d.offy = CELL * ceil_div(d.hmax, CELL);
+        int nrows = re - rb;
+        if (nrows > 0) {
+            d.ncx = (d.Ws - 1 + d.offx) / CELL + 1;
+            d.ncy = (nrows - 1 + d.offy) / CELL + 1;
+            d.ntx = ceil_div(d.Ws, TILE_W);
+            d.nty = ceil_div(nrows, TILE_H);
+        } else {
+            d.ncx = d.ncy = d.ntx = d.nty = 0;
+        }
+        d.cell_base = (int)cells;
+        d.tile_base = (int)tiles;
+        cells += (long long)d.ncx * d.ncy;
+        tiles += (long long)d.ntx * d.nty;
+        if (cells >= (1LL << 30) || tiles >= (1LL << 30)) return GSR_EINVAL;
+    }
+    tab->total_cells = (int)cells;
+    tab->total_tiles = (int)tiles;
+    return GSR_OK;
+}
+
+gsr_image single(int64_t n, int32_t h, int32_t w, double s) {
+    gsr_image g;
+    g.lr_h = h; g.lr_w = w; g.scale = s;
+    g.g_off = 0; g.g_cnt = n; g.out_off = 0; g.row_begin = 0; g.row_end = -1;
+    return g;
+}
+
+bool params_ok(const float* a, const float* m, const float* s, const float* r, const float* c,
+               int64_t n) {
+    return n == 0 || (a && m && s && r && c);
+}
+
+size_t ws_bytes(const ImgTable& t, int64_t n) {
+    return binning_bytes(n, t.total_cells, t.total_tiles);
+}
+
+gsr_status finish(cudaError_t e) {
+    if (e != cudaSuccess) return GSR_ECUDA;
+    return cudaGetLastError() == cudaSuccess ? GSR_OK : GSR_ECUDA;
+}
+
+struct Prepared {
+    ImgTable tab;
+    Workspace ws;
+    int* perm = nullptr;
+    uint32_t* keys = nullptr;
+};
+
+gsr_status prepare(const float* alpha, const float* mu, const float* sigma, const float* rho,
+                   const float* color, int64_t n_total, const gsr_image* imgs, int32_t n_imgs,
+                   double ratio, void* workspace, size_t workspace_bytes, cudaStream_t st,
+                   Prepared* P, bool bin) {
+    gsr_status s = build_table(imgs, n_imgs, n_total, ratio, &P->tab);
+    if (s != GSR_OK) return s;
+    if (!params_ok(alpha, mu, sigma, rho, color, n_total)) return GSR_EINVAL;
+    if (!workspace || workspace_bytes < ws_bytes(P->tab, n_total)) return GSR_EWORKSPACE;
+    carve_workspace(workspace, n_total, P->tab.total_cells, P->tab.total_tiles, &P->ws);
+    if (!bin) return GSR_OK;
+    cudaError_t e = bin_gaussians(alpha, mu, sigma, rho, color, n_total, P->tab, P->ws, &P->perm,
+                                  &P->keys, st);
+    return e == cudaSuccess ? GSR_OK : GSR_ECUDA;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* gsr_version(void) { return "gsr-b200 0.1 (sm_100a; fwd tile 32x32, cell 16)"; }
+
+void gsr_tile_shape(int32_t* tile_w, int32_t* tile_h, int32_t* cell_w, int32_t* cell_h) {
+    if (tile_w) *tile_w = TILE_W;
+    if (tile_h) *tile_h = TILE_H;
+    if (cell_w) *cell_w = CELL;
+    if (cell_h) *cell_h = CELL;
+}
+
+gsr_status gsr_out_dims(int32_t lr_h, int32_t lr_w, double scale, int32_t* out_h,
+                        int32_t* out_w) {
+    if (lr_h < 1 || lr_w < 1 || !std::isfinite(scale) || !(scale >= 1.0)) return GSR_EINVAL;
+    double h = std::floor(scale * (double)lr_h), w = std::floor(scale * (double)lr_w);
+    if (h > MAX_DIM || w > MAX_DIM) return GSR_EINVAL;
+    if (out_h) *out_h = (int32_t)h;
+    if (out_w) *out_w = (int32_t)w;
+    return GSR_OK;
+}
+
+size_t gsr_workspace_bytes_batched(const gsr_image* imgs, int32_t n_imgs, int64_t n_total,
+                                   double ratio) {
+    ImgTable local;
+    if (build_table(imgs, n_imgs, n_total, ratio, &local) != GSR_OK) return 0;
+    return ws_bytes(local, n_total);
+}
+
+size_t gsr_workspace_bytes(int64_t n, int32_t lr_h, int32_t lr_w, double scale, double ratio) {
+    gsr_image g = single(n, lr_h, lr_w, scale);
+    return gsr_workspace_bytes_batched(&g, 1, n, ratio);
+}
+
+gsr_status gsr_render_fwd_batched(const float* alpha, const float* mu, const float* sigma,
+                                  const float* rho, const float* color, int64_t n_total,
+                                  const gsr_image* imgs, int32_t n_imgs, double ratio, float* out,
+                                  void* workspace, size_t workspace_bytes, void* stream) {
+    if (!out) return GSR_EINVAL;
+    cudaStream_t st = (cudaStream_t)stream;
+    Prepared P;
+    gsr_status s = prepare(alpha, mu, sigma, rho, color, n_total, imgs, n_imgs, ratio, workspace,
+                           workspace_bytes, st, &P, true);
+    if (s != GSR_OK) return s;
+    return finish(launch_render_fwd(P.tab, P.ws, out, st));
+}
+
+gsr_status gsr_render_fwd(const float* alpha, const float* mu, const float* sigma,
+                          const float* rho, const float* color, int64_t n, int32_t lr_h,
+                          int32_t lr_w, double scale, double ratio, float* out, void* workspace,
+                          size_t workspace_bytes, void* stream) {
+    gsr_image g = single(n, lr_h, lr_w, scale);
+    return gsr_render_fwd_batched(alpha, mu, sigma, rho, color, n, &g, 1, ratio, out, workspace,
+                                  workspace_bytes, stream);
+}
+
+gsr_status gsr_render_bwd_moments_batched(const float* alpha, const float* mu, const float* sigma,
+                                          const float* rho, const float* color, int64_t n_total,
+                                          const gsr_image* imgs, int32_t n_imgs, double ratio,
+                                          const float* grad_out, double* moments, void* workspace,
+                                          size_t workspace_bytes, void* stream) {
+    if (!grad_out || (!moments && n_total > 0)) return GSR_EINVAL;
+    cudaStream_t st = (cudaStream_t)stream;
+    Prepared P;
+    gsr_status s = prepare(alpha, mu, sigma, rho, color, n_total, imgs, n_imgs, ratio, workspace,
+                           workspace_bytes, st, &P, true);
+    if (s != GSR_OK) return s;
+    return finish(launch_render_bwd_moments(P.tab, P.ws, P.perm, grad_out, moments, st));
+}
+
+gsr_status gsr_finalize_grads(const float* alpha, const float* mu, const float* sigma,
+                              const float* rho, const float* color, int64_t n_total,
+                              const double* moments, float* d_alpha, float* d_mu, float* d_sigma,
+                              float* d_rho, float* d_color, void* stream) {
+    if (n_total < 0) return GSR_EINVAL;
+    if (n_total > 0 && (!params_ok(alpha, mu, sigma, rho, color, n_total) || !moments ||
+                        !d_alpha || !d_mu || !d_sigma || !d_rho || !d_color))
+        return GSR_EINVAL;
+    return finish(launch_finalize(alpha, mu, sigma, rho, color, n_total, moments, d_alpha, d_mu,
+                                  d_sigma, d_rho, d_color, (cudaStream_t)stream));
+}
+
+gsr_status gsr_render_bwd_batched(const float* alpha, const float* mu, const float* sigma,
+                                  const float* rho, const float* color, int64_t n_total,
+                                  const gsr_image* imgs, int32_t n_imgs, double ratio,
+                                  const float* grad_out, float* d_alpha, float* d_mu,
+                                  float* d_sigma, float* d_rho, float* d_color, void* workspace,
+                                  size_t workspace_bytes, void* stream) {
+    if (!grad_out) return GSR_EINVAL;
+    if (n_total > 0 && (!d_alpha || !d_mu || !d_sigma || !d_rho || !d_color)) return GSR_EINVAL;
+    cudaStream_t st = (cudaStream_t)stream;
+    Prepared P;
+    gsr_status s = prepare(alpha, mu, sigma, rho, color, n_total, imgs, n_imgs, ratio, workspace,
+                           workspace_bytes, st, &P, true);
+    if (s != GSR_OK) return s;
+    if (n_total == 0) return GSR_OK;
+    cudaMemsetAsync(P.ws.moments, 0, sizeof(double) * 8 * (size_t)n_total, st);
+    cudaError_t e = launch_render_bwd_moments(P.tab, P.ws, P.perm, grad_out, P.ws.moments, st);
+    if (e != cudaSuccess) return GSR_ECUDA;
+    return finish(launch_finalize(alpha, mu, sigma, rho, color, n_total, P.ws.moments, d_alpha,
+                                  d_mu, d_sigma, d_rho, d_color, st));
+}
+
+gsr_status gsr_render_bwd(const float* alpha, const float* mu, const float* sigma,
+                          const float* rho, const float* color, int64_t n, int32_t lr_h,
+                          int32_t lr_w, double scale, double ratio, const float* grad_out,
+                          float* d_alpha, float* d_mu, float* d_sigma, float* d_rho,
+                          float* d_color, void* workspace, size_t workspace_bytes, void* stream) {
+    gsr_image g = single(n, lr_h, lr_w, scale);
+    return gsr_render_bwd_batched(alpha, mu, sigma, rho, color, n, &g, 1, ratio, grad_out,
+                                  d_alpha, d_mu, d_sigma, d_rho, d_color, workspace,
+                                  workspace_bytes, stream);
+}
+
+gsr_status gsr_pair_count_batched(const float* alpha, const float* mu, const float* sigma,
+                                  const float* rho, const float* color, int64_t n_total,
+                                  const gsr_image* imgs, int32_t n_imgs, double ratio,
+                                  int64_t* d_pairs, void* workspace, size_t workspace_bytes,
+                                  void* stream) {
+    if (!d_pairs) return GSR_EINVAL;
+    Prepared P;
+    gsr_status s = prepare(alpha, mu, sigma, rho, color, n_total, imgs, n_imgs, ratio, workspace,
+                           workspace_bytes, (cudaStream_t)stream, &P, false);
+    if (s != GSR_OK) return s;
+    return finish(launch_pair_count(alpha, mu, sigma, rho, color, n_total, P.tab,
+                                    (long long*)d_pairs, (cudaStream_t)stream));
+}
+
+gsr_status gsr_debug_rects(const float* alpha, const float* mu, const float* sigma,
+                           const float* rho, const float* color, int64_t n, int32_t lr_h,
+                           int32_t lr_w, double scale, double ratio, int32_t* rects,
+                           void* stream) {
+    gsr_image g = single(n, lr_h, lr_w, scale);
+    ImgTable tab;
+    gsr_status s = build_table(&g, 1, n, ratio, &tab);
+    if (s != GSR_OK) return s;
+    if (!params_ok(alpha, mu, sigma, rho, color, n) || (n > 0 && !rects)) return GSR_EINVAL;
+    return finish(launch_debug_rects(alpha, mu, sigma, rho, color, n, tab, rects,
+                                     (cudaStream_t)stream));
+}
+
+gsr_status gsr_debug_tile_lists(const float* alpha, const float* mu, const float* sigma,
+                                const float* rho, const float* color, int64_t n, int32_t lr_h,
+                                int32_t lr_w, double scale, double ratio, int32_t* counts,
+                                int32_t* ids, int32_t* cells, void* workspace,
+                                size_t workspace_bytes, void* stream) {
+    if (!counts && !ids) return GSR_EINVAL;
+    if (ids && !cells) return GSR_EINVAL;
+    gsr_image g = single(n, lr_h, lr_w, scale);
+    cudaStream_t st = (cudaStream_t)stream;
+    Prepared P;
+    gsr_status s = prepare(alpha, mu, sigma, rho, color, n, &g, 1, ratio, workspace,
+                           workspace_bytes, st, &P, true);
+    if (s != GSR_OK) return s;
+    return finish(launch_debug_tile_lists(P.tab, P.ws, P.perm, P.keys, counts, ids, cells, st));
+}
+
+}  // extern "C"

@@ -1,0 +1,217 @@
+// gsr_internal.cuh -- shared definitions of the sm_100a kernels behind include/gsr.h.
+//
+// Data layout in HBM:
+//   params      float32 SoA from the caller (alpha, mu, sigma, rho, color), read by K1/K1b/K6.
+//   keys/vals   uint32 cell key + int32 Gaussian index, radix-sorted (stable) -> perm.
+//   cell_start  int32[total_cells+1]: first sorted position of each cell (CSR over cells).
+//   rec         3 x float4 per sorted position (48 B record, see Rec below).
+//   moments     float64[n][8], original Gaussian order (backward only).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace gsr {
+
+// ---- compile-time geometry -------------------------------------------------------------
+constexpr int CELL = 16;       // cell edge (HR px): binning granularity (sort key)
+constexpr int TILE_W = 32;     // render tile (HR px), forward and backward
+constexpr int TILE_H = 32;
+constexpr int FWD_STRIP = 8;   // forward: each lane owns a 1 x 8 horizontal pixel strip
+constexpr int FWD_WARPS = TILE_W / FWD_STRIP;    // 4 warps side by side, lane = tile row
+constexpr int FWD_THREADS = FWD_WARPS * 32;      // 128
+constexpr int FWD_CHUNK = 128;                   // records per TMA bulk stage
+constexpr int FWD_STAGES = 4;
+constexpr int BWD_WARPS = 4;
+constexpr int BWD_THREADS = BWD_WARPS * 32;
+constexpr int MAX_IMAGES = 64;
+constexpr uint32_t KEY_SENTINEL_FLAG = 0xffffffffu;
+
+// log2(e)/2: exp(-Q/2) = 2^(-HALF_LOG2E * Q)
+constexpr double HALF_LOG2E = 0.72134752044448170368;
+constexpr double TWO_PI = 6.28318530717958647693;
+
+// Per-image constants, computed on the host in fp64, passed by value in ImgTable.
+struct DevImg {
+    double s;           // scale
+    double hx, hy;      // window half-extents r*W, r*H (LR px, fp64)
+    long long g_off, g_cnt, out_off;
+    float invs;         // fp32(1/s)
+    int H, W, Hs, Ws;
+    int row_begin, row_end;   // HR row band
+    int offx, offy;           // cell-grid offsets (multiples of CELL, >= max rect extent)
+    int ncx, ncy, cell_base;  // cells of this image: [cell_base, cell_base + ncx*ncy)
+    int ntx, nty, tile_base;  // render tiles of this image
+    int wmax, hmax;           // upper bounds on the unclipped rect width/height
+};
+
+struct ImgTable {
+    int n_imgs;
+    int total_cells;          // key of an unbinned Gaussian (sorts last)
+    int total_tiles;
+    int pad;
+    DevImg img[MAX_IMAGES];
+};
+
+// Sorted record (48 B = 3 x float4), one per binned Gaussian, in cell order:
+//   r0 = {ax, ay, dlx, dly}        anchor (integer HR px, as float) and fp32 residual
+//                                  dl = mu - a/s  (LR px, |dl| <= 0.5/s)
+//   r1 = {a1, b1, c1, cr}          factored exponent: q = -Q/2 log2 e = -(w^2 + v^2),
+//                                  w = a1 dx + b1 dy, v = c1 dy
+//   r2 = {cg, cb, x0|x1<<16, y0|y1<<16}  c' = alpha c K (rgb), clipped rect (int bits)
+
+__host__ __device__ inline int find_image_by_tile(const ImgTable& t, int tile) {
+    int lo = 0, hi = t.n_imgs - 1;
+    while (lo < hi) {
+        int mid = (lo + hi + 1) >> 1;
+        if (t.img[mid].tile_base <= tile) lo = mid; else hi = mid - 1;
+    }
+    return lo;
+}
+
+__host__ __device__ inline int find_image_by_gauss(const ImgTable& t, long long i) {
+    // images sorted by g_off; returns -1 if i is not owned by any image
+    int lo = 0, hi = t.n_imgs - 1;
+    while (lo < hi) {
+        int mid = (lo + hi + 1) >> 1;
+        if (t.img[mid].g_off <= i) lo = mid; else hi = mid - 1;
+    }
+    if (t.n_imgs == 0) return -1;
+    const DevImg& im = t.img[lo];
+    if (i < im.g_off || i >= im.g_off + im.g_cnt) return -1;
+    return lo;
+}
+
+// ---- the normative window rect (reading R2), fp64, fixed op order, no FMA ---------------
+struct Rect { int x0u, y0u, x0, x1, y0, y1; bool nonempty; };
+
+__device__ __forceinline__ double clamp_bound(double v) {
+    const double lim = 1073741824.0;  // 2^30
+    return v < -lim ? -lim : (v > lim ? lim : v);
+}
+
+__device__ __forceinline__ Rect window_rect(float mux, float muy, const DevImg& im) {
+    Rect r;
+    double mx = (double)mux, my = (double)muy;
+    double lx = __dmul_rn(im.s, __dsub_rn(mx, im.hx));
+    double ux = __dmul_rn(im.s, __dadd_rn(mx, im.hx));
+    double ly = __dmul_rn(im.s, __dsub_rn(my, im.hy));
+    double uy = __dmul_rn(im.s, __dadd_rn(my, im.hy));
+    long long ax0 = (long long)floor(clamp_bound(lx)) + 1;
+    long long ax1 = (long long)ceil(clamp_bound(ux)) - 1;
+    long long ay0 = (long long)floor(clamp_bound(ly)) + 1;
+    long long ay1 = (long long)ceil(clamp_bound(uy)) - 1;
+    r.x0u = (int)ax0;
+    r.y0u = (int)ay0;
+    long long cx0 = ax0 < 0 ? 0 : ax0;
+    long long cx1 = ax1 > im.Ws - 1 ? im.Ws - 1 : ax1;
+    long long cy0 = ay0 < im.row_begin ? im.row_begin : ay0;          // band clip
+    long long cy1 = ay1 > im.row_end - 1 ? im.row_end - 1 : ay1;
+    r.x0 = (int)cx0; r.x1 = (int)cx1; r.y0 = (int)cy0; r.y1 = (int)cy1;
+    r.nonempty = (cx0 <= cx1) && (cy0 <= cy1) && !isnan(lx) && !isnan(ux) && !isnan(ly) &&
+                 !isnan(uy);
+    return r;
+}
+
+__device__ __forceinline__ bool gaussian_valid(float a, float mx, float my, float sx, float sy,
+                                               float rh, float cr, float cg, float cb) {
+    bool fin = isfinite(a) && isfinite(mx) && isfinite(my) && isfinite(sx) && isfinite(sy) &&
+               isfinite(rh) && isfinite(cr) && isfinite(cg) && isfinite(cb);
+    return fin && sx > 0.f && sy > 0.f && fabsf(rh) < 1.f;
+}
+
+// ---- PTX helpers ------------------------------------------------------------------------
+__device__ __forceinline__ float ex2_approx(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void fence_barrier_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(
+                     smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+// 1-D TMA bulk copy global -> shared, completion counted on an mbarrier (bytes % 16 == 0).
+__device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                             uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+// ---- host-side launchers (defined in the .cu files) --------------------------------------
+struct Workspace {
+    uint32_t* keys_a; uint32_t* keys_b;
+    int* vals_a; int* vals_b;
+    int* hist;               // radix histograms [256 * nblocks]
+    int* scan_tmp;           // block sums for the scan
+    int* cell_start;         // [total_cells + 1]
+    float4* rec;             // [3 * n]
+    double* moments;         // [8 * n] (backward)
+    unsigned long long* counter;  // scratch counters
+    int* tile_off;           // debug tile lists: [total_tiles + 1]
+};
+
+// binning.cu
+size_t binning_bytes(long long n, int total_cells, int total_tiles);
+void carve_workspace(void* base, long long n, int total_cells, int total_tiles, Workspace* ws);
+// Runs K1 (keys) + stable radix sort + cell starts + K1b (records). Returns sorted perm in
+// *perm_out (points into ws).
+cudaError_t bin_gaussians(const float* alpha, const float* mu, const float* sigma,
+                          const float* rho, const float* color, long long n,
+                          const ImgTable& tab, Workspace& ws, int** perm_out,
+                          uint32_t** keys_sorted_out, cudaStream_t st);
+cudaError_t launch_pair_count(const float* alpha, const float* mu, const float* sigma,
+                              const float* rho, const float* color, long long n,
+                              const ImgTable& tab, long long* d_pairs, cudaStream_t st);
+cudaError_t launch_debug_rects(const float* alpha, const float* mu, const float* sigma,
+                               const float* rho, const float* color, long long n,
+                               const ImgTable& tab, int* rects, cudaStream_t st);
+cudaError_t launch_debug_tile_lists(const ImgTable& tab, const Workspace& ws, const int* perm,
+                                    const uint32_t* keys_sorted, int* counts, int* ids,
+                                    int* cells, cudaStream_t st);
+cudaError_t exclusive_scan_i32(const int* in, int* out, long long n, int* tmp, cudaStream_t st);
+
+// render_fwd.cu
+cudaError_t launch_render_fwd(const ImgTable& tab, const Workspace& ws, float* out,
+                              cudaStream_t st);
+// render_bwd.cu
+cudaError_t launch_render_bwd_moments(const ImgTable& tab, const Workspace& ws, const int* perm,
+                                      const float* grad_out, double* moments, cudaStream_t st);
+cudaError_t launch_finalize(const float* alpha, const float* mu, const float* sigma,
+                            const float* rho, const float* color, long long n,
+                            const double* moments, float* d_alpha, float* d_mu, float* d_sigma,
+                            float* d_rho, float* d_color, cudaStream_t st);
+
+}  // namespace gsr

@@ -1,0 +1,240 @@
+// render_bwd.cu -- K5 (backward pair pass -> per-Gaussian moments) and K6 (finalize).
+//
+// For L with upstream gradient g = dL/dI, every pair (Gaussian i, pixel (x,y)) inside the window
+// contributes, with e = 2^q = exp(-Q/2), c' = alpha c K, w = e (g . c'):
+//   m0..2 += e g_k,  m3 += w dx,  m4 += w dy,  m5 += w dx^2,  m6 += w dx dy,  m7 += w dy^2.
+// K6 turns the moments into the gradients of Eq. 1-2:
+//   d alpha = K (c . m012),  d c_k = alpha K m_k,  M0 = alpha K (c . m012)
+//   d mu_x = a m3 + b m4,  d mu_y = b m3 + c m4            (a, b, c: conic of Eq. 2)
+//   d sx = ((m5/sx^2 - rho m6/(sx sy))/D - M0)/sx,  d sy = ((m7/sy^2 - rho m6/(sx sy))/D - M0)/sy
+//   d rho = (rho M0 - rho (a m5 + 2 b m6 + c m7) + m6/(sx sy))/D
+//
+// Layout of K5: one CTA per 32 x 32 HR tile (the forward's tiles) with the tile's dL/dI staged in
+// shared memory as column pairs. Lanes own Gaussians: each warp takes 32 consecutive candidates
+// of a cell-row span, and all 32 lanes walk the same pixels (warp-uniform loop bounds from the
+// union of their rects), reading dL/dI as shared-memory broadcasts. Per-pair work is paired over
+// two pixels with FFMA2. Within a row the dy-dependent moments are factored out
+// (sum_row w dy = dy sum_row w, ...), so a pair costs 14 FP32 lane-ops + 1 ex2. Each lane's
+// (Gaussian, tile) partial moments are reduced in registers (row partials, then the tile) and
+// leave the CTA as 8 fp64 atomics -- the only global atomics of the backward.
+#include "gsr_internal.cuh"
+
+namespace gsr {
+
+namespace {
+
+__device__ __forceinline__ float2 f2(float a) { return make_float2(a, a); }
+
+struct LaneG {        // per-lane Gaussian constants
+    float2 A2, u2, t2, inv2, ndl, cr, cg, cb;
+    int x0, x1;
+};
+
+template <bool MASKED>
+__device__ __forceinline__ void row_pairs(int c_begin, int c_end, const float4* __restrict__ gArow,
+                                          const float2* __restrict__ gBrow, float kT,
+                                          const LaneG& L, int Tx0, float2& FR, float2& FG,
+                                          float2& FB, float2& W1, float2& W2) {
+    float2 kx = make_float2(kT + (float)c_begin, kT + (float)(c_begin + 1));
+    const float2 two = f2(2.0f);
+    for (int c = c_begin; c < c_end; c += 2) {
+        const float4 ga = gArow[c >> 1];     // {gr0, gr1, gg0, gg1}
+        const float2 gb = gBrow[c >> 1];     // {gb0, gb1}
+        float2 dx = __ffma2_rn(kx, L.inv2, L.ndl);
+        float2 w = __ffma2_rn(L.A2, dx, L.t2);                   // a1 dx + b1 dy
+        float2 q = __ffma2_rn(make_float2(-w.x, -w.y), w, L.u2); // -(w^2) - v^2
+        if (MASKED) {
+            int xa = Tx0 + c;
+            q.x = (xa >= L.x0 && xa <= L.x1) ? q.x : -INFINITY;
+            q.y = (xa + 1 >= L.x0 && xa + 1 <= L.x1) ? q.y : -INFINITY;
+        }
+        float2 e = make_float2(ex2_approx(q.x), ex2_approx(q.y));
+        const float2 gr = make_float2(ga.x, ga.y), gg = make_float2(ga.z, ga.w);
+        FR = __ffma2_rn(e, gr, FR);
+        FG = __ffma2_rn(e, gg, FG);
+        FB = __ffma2_rn(e, gb, FB);
+        float2 gc = __fmul2_rn(gr, L.cr);
+        gc = __ffma2_rn(gg, L.cg, gc);
+        gc = __ffma2_rn(gb, L.cb, gc);
+        float2 ed = __fmul2_rn(e, dx);
+        W1 = __ffma2_rn(gc, ed, W1);
+        float2 edd = __fmul2_rn(ed, dx);
+        W2 = __ffma2_rn(gc, edd, W2);
+        kx = __fadd2_rn(kx, two);
+    }
+}
+
+__global__ void __launch_bounds__(BWD_THREADS) k_render_bwd(
+    const ImgTable tab, const float4* __restrict__ rec, const int* __restrict__ cell_start,
+    const int* __restrict__ perm, const float* __restrict__ grad_out,
+    double* __restrict__ moments) {
+    __shared__ __align__(16) float4 gA[TILE_H][TILE_W / 2];
+    __shared__ __align__(16) float2 gB[TILE_H][TILE_W / 2];
+
+    const int tile = blockIdx.x;
+    const DevImg& im = tab.img[find_image_by_tile(tab, tile)];
+    const int t = tile - im.tile_base;
+    const int Tx0 = (t % im.ntx) * TILE_W;
+    const int Ty0 = im.row_begin + (t / im.ntx) * TILE_H;
+    const int Tx1 = min(Tx0 + TILE_W - 1, im.Ws - 1);
+    const int Ty1 = min(Ty0 + TILE_H - 1, im.row_end - 1);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+    // stage dL/dI of the tile (zeros outside the image / band)
+    for (int pp = threadIdx.x; pp < TILE_H * (TILE_W / 2); pp += BWD_THREADS) {
+        int ry = pp / (TILE_W / 2), cp = pp % (TILE_W / 2);
+        int y = Ty0 + ry, x = Tx0 + 2 * cp;
+        float v[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        if (y <= Ty1) {
+            const float* g = grad_out + im.out_off + ((long long)(y - im.row_begin) * im.Ws) * 3;
+            if (x <= Tx1) { v[0] = g[3 * x]; v[1] = g[3 * x + 1]; v[2] = g[3 * x + 2]; }
+            if (x + 1 <= Tx1) { v[3] = g[3 * x + 3]; v[4] = g[3 * x + 4]; v[5] = g[3 * x + 5]; }
+        }
+        gA[ry][cp] = make_float4(v[0], v[3], v[1], v[4]);
+        gB[ry][cp] = make_float2(v[2], v[5]);
+    }
+    __syncthreads();
+
+    const int cx_lo = (Tx0 - im.wmax + 1 + im.offx) / CELL;
+    const int cx_hi = min(im.ncx - 1, (Tx1 + im.offx) / CELL);
+    const int cy_lo = (Ty0 - im.row_begin - im.hmax + 1 + im.offy) / CELL;
+    const int cy_hi = min(im.ncy - 1, (Ty1 - im.row_begin + im.offy) / CELL);
+    const float invs = im.invs;
+
+    for (int cy = cy_lo; cy <= cy_hi; ++cy) {
+        const int row = im.cell_base + cy * im.ncx;
+        const int sp0 = cell_start[row + cx_lo], sp1 = cell_start[row + cx_hi + 1];
+        for (int p0 = sp0 + warp * 32; p0 < sp1; p0 += BWD_WARPS * 32) {
+            const int p = p0 + lane;
+            bool act = p < sp1;
+            float4 r0 = make_float4(0.f, 0.f, 0.f, 0.f), r1 = r0, r2 = r0;
+            int x0 = 1, x1 = 0, y0 = 1, y1 = 0;
+            if (act) {
+                r0 = __ldg(rec + 3LL * p);
+                r1 = __ldg(rec + 3LL * p + 1);
+                r2 = __ldg(rec + 3LL * p + 2);
+                unsigned xs = __float_as_uint(r2.z), ys = __float_as_uint(r2.w);
+                x0 = (int)(xs & 0xffffu); x1 = (int)(xs >> 16);
+                y0 = (int)(ys & 0xffffu); y1 = (int)(ys >> 16);
+                act = !(x1 < Tx0 || x0 > Tx1 || y1 < Ty0 || y0 > Ty1);
+                if (!act) { x0 = 1; x1 = 0; y0 = 1; y1 = 0; }
+            }
+            if (__ballot_sync(0xffffffffu, act) == 0) continue;
+            // warp-uniform loop bounds: union of the active rects (rows and columns), and the
+            // column range covered by every active lane (no per-pixel x mask needed there)
+            const int ya = max(Ty0, (int)__reduce_min_sync(0xffffffffu, act ? y0 : 0x7fffffff));
+            const int yb = min(Ty1, (int)__reduce_max_sync(0xffffffffu, act ? y1 : -1));
+            const int xa = max(Tx0, (int)__reduce_min_sync(0xffffffffu, act ? x0 : 0x7fffffff));
+            const int xb = min(Tx1, (int)__reduce_max_sync(0xffffffffu, act ? x1 : -1));
+            const int xia = (int)__reduce_max_sync(0xffffffffu, act ? x0 : -1);
+            const int xib = (int)__reduce_min_sync(0xffffffffu, act ? x1 : 0x7fffffff);
+            // column pairs relative to Tx0
+            const int ca = (xa - Tx0) & ~1;
+            const int ce = ((xb - Tx0) | 1) + 1;                  // exclusive, even
+            int ma = ((xia - Tx0) + 1) & ~1;                      // first pair fully >= xia
+            int mb = ((xib - Tx0) + 1) & ~1;                      // pairs [ma, mb) fully <= xib
+            ma = min(max(ma, ca), ce);
+            mb = min(max(mb, ma), ce);
+
+            LaneG L;
+            L.A2 = f2(r1.x); L.inv2 = f2(invs); L.ndl = f2(-r0.z);
+            L.cr = f2(r1.w); L.cg = f2(r2.x); L.cb = f2(r2.y);
+            L.x0 = x0; L.x1 = x1;
+            const float kT = (float)Tx0 - r0.x;
+            float m[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) m[k] = 0.f;
+            for (int y = ya; y <= yb; ++y) {
+                const float dy = fmaf((float)y - r0.y, invs, -r0.w);
+                const float v = r1.z * dy;
+                const float u = (y >= y0 && y <= y1) ? -(v * v) : -INFINITY;
+                L.t2 = f2(r1.y * dy);
+                L.u2 = f2(u);
+                const float4* gAr = &gA[y - Ty0][0];
+                const float2* gBr = &gB[y - Ty0][0];
+                float2 FR = f2(0.f), FG = FR, FB = FR, W1 = FR, W2 = FR;
+                row_pairs<true>(ca, ma, gAr, gBr, kT, L, Tx0, FR, FG, FB, W1, W2);
+                row_pairs<false>(ma, mb, gAr, gBr, kT, L, Tx0, FR, FG, FB, W1, W2);
+                row_pairs<true>(mb, ce, gAr, gBr, kT, L, Tx0, FR, FG, FB, W1, W2);
+                const float fr = FR.x + FR.y, fg = FG.x + FG.y, fb = FB.x + FB.y;
+                const float w0 = fmaf(r1.w, fr, fmaf(r2.x, fg, r2.y * fb));
+                const float w1 = W1.x + W1.y, w2 = W2.x + W2.y;
+                m[0] += fr; m[1] += fg; m[2] += fb;
+                m[3] += w1;
+                m[4] = fmaf(dy, w0, m[4]);
+                m[5] += w2;
+                m[6] = fmaf(dy, w1, m[6]);
+                m[7] = fmaf(dy * dy, w0, m[7]);
+            }
+            if (act) {
+                double* dst = moments + 8LL * perm[p];
+#pragma unroll
+                for (int k = 0; k < 8; ++k) atomicAdd(dst + k, (double)m[k]);
+            }
+        }
+    }
+}
+
+__global__ void k_finalize(const float* __restrict__ alpha, const float* __restrict__ mu,
+                           const float* __restrict__ sigma, const float* __restrict__ rho,
+                           const float* __restrict__ color, long long n,
+                           const double* __restrict__ moments, float* __restrict__ d_alpha,
+                           float* __restrict__ d_mu, float* __restrict__ d_sigma,
+                           float* __restrict__ d_rho, float* __restrict__ d_color) {
+    long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    float o[9] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    if (gaussian_valid(alpha[i], mu[2 * i], mu[2 * i + 1], sigma[2 * i], sigma[2 * i + 1], rho[i],
+                       color[3 * i], color[3 * i + 1], color[3 * i + 2])) {
+        const double* m = moments + 8 * i;
+        double sx = sigma[2 * i], sy = sigma[2 * i + 1], rh = rho[i], al = alpha[i];
+        double c0 = color[3 * i], c1 = color[3 * i + 1], c2 = color[3 * i + 2];
+        double D = (1.0 - rh) * (1.0 + rh);
+        double a = 1.0 / (sx * sx * D), b = -rh / (sx * sy * D), c = 1.0 / (sy * sy * D);
+        double K = 1.0 / (TWO_PI * sx * sy * sqrt(D));
+        double cf = c0 * m[0] + c1 * m[1] + c2 * m[2];
+        double M0 = al * K * cf;
+        double sxy = sx * sy;
+        o[0] = (float)(K * cf);
+        o[1] = (float)(a * m[3] + b * m[4]);
+        o[2] = (float)(b * m[3] + c * m[4]);
+        o[3] = (float)(((m[5] / (sx * sx) - rh * m[6] / sxy) / D - M0) / sx);
+        o[4] = (float)(((m[7] / (sy * sy) - rh * m[6] / sxy) / D - M0) / sy);
+        o[5] = (float)((rh * M0 - rh * (a * m[5] + 2.0 * b * m[6] + c * m[7]) + m[6] / sxy) / D);
+        o[6] = (float)(al * K * m[0]);
+        o[7] = (float)(al * K * m[1]);
+        o[8] = (float)(al * K * m[2]);
+    }
+    d_alpha[i] = o[0];
+    d_mu[2 * i] = o[1];
+    d_mu[2 * i + 1] = o[2];
+    d_sigma[2 * i] = o[3];
+    d_sigma[2 * i + 1] = o[4];
+    d_rho[i] = o[5];
+    d_color[3 * i] = o[6];
+    d_color[3 * i + 1] = o[7];
+    d_color[3 * i + 2] = o[8];
+}
+
+}  // namespace
+
+cudaError_t launch_render_bwd_moments(const ImgTable& tab, const Workspace& ws, const int* perm,
+                                      const float* grad_out, double* moments, cudaStream_t st) {
+    if (tab.total_tiles <= 0) return cudaSuccess;
+    k_render_bwd<<<tab.total_tiles, BWD_THREADS, 0, st>>>(tab, ws.rec, ws.cell_start, perm,
+                                                          grad_out, moments);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_finalize(const float* alpha, const float* mu, const float* sigma,
+                            const float* rho, const float* color, long long n,
+                            const double* moments, float* d_alpha, float* d_mu, float* d_sigma,
+                            float* d_rho, float* d_color, cudaStream_t st) {
+    if (n <= 0) return cudaSuccess;
+    k_finalize<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(alpha, mu, sigma, rho, color, n,
+                                                            moments, d_alpha, d_mu, d_sigma,
+                                                            d_rho, d_color);
+    return cudaGetLastError();
+}
+
+}  // namespace gsr

@@ -1,0 +1,283 @@
+"""PyTorch binding over the C-ABI (include/gsr.h): argument marshalling only.
+
+Every step of the rasterization runs in libgsr.so's sm_100a kernels; PyTorch provides device
+memory (caching allocator), the current CUDA stream and autograd plumbing. There is no CPU or
+PyTorch fallback: CPU tensors, a missing library or a launch failure raise.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+from typing import List, Optional, Sequence, Tuple
+
+import torch
+
+from . import _lib
+from ._lib import check
+
+PARAMS = ("alpha", "mu", "sigma", "rho", "color")
+WIDTH = {"alpha": 1, "mu": 2, "sigma": 2, "rho": 1, "color": 3}
+
+
+def _stream_ptr(device) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def _check_param(t: torch.Tensor, name: str, n: Optional[int] = None) -> torch.Tensor:
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise TypeError(f"{name} must be a CUDA tensor (no CPU fallback)")
+    if t.dtype != torch.float32:
+        raise TypeError(f"{name} must be float32, got {t.dtype}")
+    t = t.contiguous()
+    w = WIDTH.get(name, None)
+    if w is not None:
+        if (w == 1 and t.dim() != 1) or (w > 1 and (t.dim() != 2 or t.shape[1] != w)):
+            raise ValueError(f"{name} must have shape [n]" + ("" if w == 1 else f"x{w}"))
+        if n is not None and t.shape[0] != n:
+            raise ValueError(f"{name} has {t.shape[0]} rows, expected {n}")
+    return t
+
+
+def _params(alpha, mu, sigma, rho, color):
+    n = alpha.shape[0] if isinstance(alpha, torch.Tensor) else None
+    ts = [_check_param(t, k, n) for t, k in zip((alpha, mu, sigma, rho, color), PARAMS)]
+    dev = ts[0].device
+    for t in ts:
+        if t.device != dev:
+            raise ValueError("all parameters must live on the same device")
+    return ts, n
+
+
+def _ptr(t: torch.Tensor, offset_elems: int = 0) -> int:
+    return t.data_ptr() + offset_elems * t.element_size()
+
+
+@dataclass
+class Image:
+    """One image of a batch: LR size (H, W), scale s, its Gaussians [g_off, g_off+g_cnt) and the
+    HR row band [row_begin, row_end) (row_end = -1: all Hs rows)."""
+    H: int
+    W: int
+    s: float
+    g_off: int
+    g_cnt: int
+    row_begin: int = 0
+    row_end: int = -1
+
+
+@dataclass
+class Layout:
+    images: List[Image]
+    dims: List[Tuple[int, int]]          # (Hs, Ws)
+    rows: List[Tuple[int, int]]          # resolved band per image
+    out_off: List[int]                   # float offsets into the flat output
+    out_numel: int
+
+    def view(self, flat: torch.Tensor, k: int) -> torch.Tensor:
+        rb, re = self.rows[k]
+        Ws = self.dims[k][1]
+        o = self.out_off[k]
+        return flat[o:o + (re - rb) * Ws * 3].view(re - rb, Ws, 3)
+
+
+def layout(images: Sequence[Image]) -> Layout:
+    dims, rows, offs = [], [], []
+    off = 0
+    for im in images:
+        Hs, Ws = _lib.out_dims(im.H, im.W, im.s)
+        rb = im.row_begin
+        re = Hs if im.row_end is None or im.row_end < 0 else im.row_end
+        dims.append((Hs, Ws))
+        rows.append((rb, re))
+        offs.append(off)
+        off += (re - rb) * Ws * 3
+    return Layout(list(images), dims, rows, offs, off)
+
+
+def _chunks(lay: Layout):
+    """Split a batch into ABI calls of <= GSR_MAX_IMAGES images; each call sees its own
+    contiguous Gaussian range and output range (pointer offsets, g_off/out_off rebased)."""
+    ims = lay.images
+    for c0 in range(0, len(ims), _lib.MAX_IMAGES):
+        sel = list(range(c0, min(c0 + _lib.MAX_IMAGES, len(ims))))
+        g0 = min(ims[k].g_off for k in sel)
+        g1 = max(ims[k].g_off + ims[k].g_cnt for k in sel)
+        o0 = lay.out_off[sel[0]]
+        recs = []
+        for k in sel:
+            im = ims[k]
+            rb, re = lay.rows[k]
+            recs.append((im.H, im.W, im.s, im.g_off - g0, im.g_cnt, lay.out_off[k] - o0, rb, re))
+        yield g0, g1, o0, _lib.images_array(recs), len(sel)
+
+
+class Workspace:
+    """Grow-only device workspace from the caching allocator (the library allocates nothing)."""
+
+    def __init__(self):
+        self.buf: Optional[torch.Tensor] = None
+
+    def get(self, nbytes: int, device) -> torch.Tensor:
+        if self.buf is None or self.buf.numel() < nbytes or self.buf.device != torch.device(device):
+            self.buf = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=device)
+        return self.buf
+
+
+_WS = {}
+
+
+def _workspace(device, nbytes: int) -> torch.Tensor:
+    key = torch.device(device).index
+    ws = _WS.setdefault(key, Workspace())
+    return ws.get(nbytes, device)
+
+
+def _ws_bytes(arr, n_imgs, n_total, ratio) -> int:
+    b = _lib.load().gsr_workspace_bytes_batched(arr, n_imgs, n_total, float(ratio))
+    if b == 0:
+        raise _lib.GsrError("gsr_workspace_bytes_batched: invalid arguments")
+    return b
+
+
+def render_fwd_batched(alpha, mu, sigma, rho, color, lay: Layout, ratio: float = 0.1,
+                       out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """Forward render of every image of `lay` into one flat float32 buffer (HWC blocks)."""
+    (alpha, mu, sigma, rho, color), n = _params(alpha, mu, sigma, rho, color)
+    dev = alpha.device
+    if out is None:
+        out = torch.empty(lay.out_numel, dtype=torch.float32, device=dev)
+    lib = _lib.load()
+    st = _stream_ptr(dev)
+    for g0, g1, o0, arr, m in _chunks(lay):
+        nb = _ws_bytes(arr, m, g1 - g0, ratio)
+        ws = _workspace(dev, nb)
+        check(lib.gsr_render_fwd_batched(_ptr(alpha, g0), _ptr(mu, 2 * g0), _ptr(sigma, 2 * g0),
+                                         _ptr(rho, g0), _ptr(color, 3 * g0), g1 - g0, arr, m,
+                                         float(ratio), _ptr(out, o0), ws.data_ptr(), ws.numel(),
+                                         st), "gsr_render_fwd_batched")
+    return out
+
+
+def render_bwd_moments_batched(alpha, mu, sigma, rho, color, lay: Layout, grad_out: torch.Tensor,
+                               moments: torch.Tensor, ratio: float = 0.1) -> torch.Tensor:
+    """Accumulate (+=) the backward moments [n, 8] (float64) of every image band of `lay`."""
+    (alpha, mu, sigma, rho, color), n = _params(alpha, mu, sigma, rho, color)
+    dev = alpha.device
+    grad_out = _check_param(grad_out, "grad_out")
+    if moments.dtype != torch.float64 or not moments.is_contiguous() or moments.numel() != 8 * n:
+        raise ValueError("moments must be a contiguous float64 [n, 8] tensor")
+    lib = _lib.load()
+    st = _stream_ptr(dev)
+    for g0, g1, o0, arr, m in _chunks(lay):
+        nb = _ws_bytes(arr, m, g1 - g0, ratio)
+        ws = _workspace(dev, nb)
+        check(lib.gsr_render_bwd_moments_batched(
+            _ptr(alpha, g0), _ptr(mu, 2 * g0), _ptr(sigma, 2 * g0), _ptr(rho, g0),
+            _ptr(color, 3 * g0), g1 - g0, arr, m, float(ratio), _ptr(grad_out, o0),
+            _ptr(moments, 8 * g0), ws.data_ptr(), ws.numel(), st),
+            "gsr_render_bwd_moments_batched")
+    return moments
+
+
+def finalize_grads(alpha, mu, sigma, rho, color, moments: torch.Tensor):
+    """Moments [n, 8] (float64) -> (d_alpha, d_mu, d_sigma, d_rho, d_color)."""
+    (alpha, mu, sigma, rho, color), n = _params(alpha, mu, sigma, rho, color)
+    dev = alpha.device
+    grads = [torch.empty_like(t) for t in (alpha, mu, sigma, rho, color)]
+    check(_lib.load().gsr_finalize_grads(*[_ptr(t) for t in (alpha, mu, sigma, rho, color)], n,
+                                         _ptr(moments), *[_ptr(g) for g in grads],
+                                         _stream_ptr(dev)), "gsr_finalize_grads")
+    return tuple(grads)
+
+
+def render_bwd_batched(alpha, mu, sigma, rho, color, lay: Layout, grad_out: torch.Tensor,
+                       ratio: float = 0.1):
+    """Gradients of sum(grad_out * I) wrt every parameter (float32, input layouts)."""
+    (alpha, mu, sigma, rho, color), n = _params(alpha, mu, sigma, rho, color)
+    dev = alpha.device
+    grad_out = _check_param(grad_out, "grad_out")
+    grads = [torch.zeros_like(t) for t in (alpha, mu, sigma, rho, color)]
+    lib = _lib.load()
+    st = _stream_ptr(dev)
+    for g0, g1, o0, arr, m in _chunks(lay):
+        nb = _ws_bytes(arr, m, g1 - g0, ratio)
+        ws = _workspace(dev, nb)
+        ga, gm, gs, gr, gc = grads
+        check(lib.gsr_render_bwd_batched(
+            _ptr(alpha, g0), _ptr(mu, 2 * g0), _ptr(sigma, 2 * g0), _ptr(rho, g0),
+            _ptr(color, 3 * g0), g1 - g0, arr, m, float(ratio), _ptr(grad_out, o0),
+            _ptr(ga, g0), _ptr(gm, 2 * g0), _ptr(gs, 2 * g0), _ptr(gr, g0), _ptr(gc, 3 * g0),
+            ws.data_ptr(), ws.numel(), st), "gsr_render_bwd_batched")
+    return tuple(grads)
+
+
+def pair_count(alpha, mu, sigma, rho, color, lay: Layout, ratio: float = 0.1) -> int:
+    """P = number of (Gaussian, pixel) pairs inside the windows (synchronises)."""
+    (alpha, mu, sigma, rho, color), n = _params(alpha, mu, sigma, rho, color)
+    dev = alpha.device
+    lib = _lib.load()
+    st = _stream_ptr(dev)
+    total = torch.zeros(1, dtype=torch.int64, device=dev)
+    tmp = torch.zeros(1, dtype=torch.int64, device=dev)
+    for g0, g1, o0, arr, m in _chunks(lay):
+        nb = _ws_bytes(arr, m, g1 - g0, ratio)
+        ws = _workspace(dev, nb)
+        check(lib.gsr_pair_count_batched(_ptr(alpha, g0), _ptr(mu, 2 * g0), _ptr(sigma, 2 * g0),
+                                         _ptr(rho, g0), _ptr(color, 3 * g0), g1 - g0, arr, m,
+                                         float(ratio), tmp.data_ptr(), ws.data_ptr(), ws.numel(),
+                                         st), "gsr_pair_count_batched")
+        total += tmp
+    return int(total.item())
+
+
+# ------------------------------------------------------------------ single image + autograd
+def _single(n, H, W, s):
+    return layout([Image(int(H), int(W), float(s), 0, int(n))])
+
+
+def render_fwd(alpha, mu, sigma, rho, color, H: int, W: int, scale: float,
+               ratio: float = 0.1) -> torch.Tensor:
+    lay = _single(alpha.shape[0], H, W, scale)
+    return lay.view(render_fwd_batched(alpha, mu, sigma, rho, color, lay, ratio), 0)
+
+
+def render_bwd(alpha, mu, sigma, rho, color, H: int, W: int, scale: float,
+               grad_out: torch.Tensor, ratio: float = 0.1):
+    lay = _single(alpha.shape[0], H, W, scale)
+    return render_bwd_batched(alpha, mu, sigma, rho, color, lay, grad_out.reshape(-1), ratio)
+
+
+class _RenderFn(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, alpha, mu, sigma, rho, color, lay, ratio):
+        ctx.lay, ctx.ratio = lay, ratio
+        ctx.save_for_backward(alpha, mu, sigma, rho, color)
+        return render_fwd_batched(alpha.detach(), mu.detach(), sigma.detach(), rho.detach(),
+                                  color.detach(), lay, ratio)
+
+    @staticmethod
+    def backward(ctx, g):
+        alpha, mu, sigma, rho, color = ctx.saved_tensors
+        grads = render_bwd_batched(alpha, mu, sigma, rho, color, ctx.lay, g.contiguous(),
+                                   ctx.ratio)
+        return (*grads, None, None)
+
+
+def render_batch(alpha, mu, sigma, rho, color, images: Sequence[Tuple[int, int, float]],
+                 counts: Sequence[int], ratio: float = 0.1):
+    """Differentiable ragged batch render. images[k] = (H, W, s) owns counts[k] consecutive
+    Gaussians. Returns (flat output, Layout); Layout.view(flat, k) is image k as [Hs, Ws, 3]."""
+    ims, off = [], 0
+    for (H, W, s), c in zip(images, counts):
+        ims.append(Image(int(H), int(W), float(s), off, int(c)))
+        off += int(c)
+    lay = layout(ims)
+    return _RenderFn.apply(alpha, mu, sigma, rho, color, lay, float(ratio)), lay
+
+
+def render(alpha, mu, sigma, rho, color, H: int, W: int, scale: float,
+           ratio: float = 0.1) -> torch.Tensor:
+    """I_SR = Eq. 4 / Alg. 1 as a differentiable op: [floor(sH), floor(sW), 3] float32."""
+    lay = _single(alpha.shape[0], H, W, scale)
+    flat = _RenderFn.apply(alpha, mu, sigma, rho, color, lay, float(ratio))
+    return lay.view(flat, 0)

@@ -1,0 +1,52 @@
+"""Shared helpers for the GPU parity tests (no method arithmetic here)."""
+import numpy as np
+
+KEYS = ("alpha", "mu", "sigma", "rho", "color")
+
+
+def to_dev(cloud, device="cuda"):
+    import torch
+    return [torch.from_numpy(np.ascontiguousarray(cloud[k], np.float32)).to(device) for k in KEYS]
+
+
+def cat(clouds):
+    return {k: np.concatenate([c[k] for c in clouds], axis=0) for k in KEYS}
+
+
+def grad_dict(grads):
+    return {k: g.detach().cpu().numpy().astype(np.float64) for k, g in zip(KEYS, grads)}
+
+
+def flat9(d):
+    """alpha, mu_x, mu_y, sigma_x, sigma_y, rho, c_r, c_g, c_b columns (oracle absmass order)."""
+    return np.concatenate([np.asarray(d["alpha"]).reshape(-1, 1), np.asarray(d["mu"]).reshape(-1, 2),
+                           np.asarray(d["sigma"]).reshape(-1, 2), np.asarray(d["rho"]).reshape(-1, 1),
+                           np.asarray(d["color"]).reshape(-1, 3)], axis=1)
+
+
+def assert_fwd_close(got, want, dist="image", atol=1e-5):
+    """Forward gate (R18): image-like max-abs <= 1e-5; stress: 1e-5 * max(1, |I|)."""
+    got = np.asarray(got, np.float64)
+    err = np.abs(got - want)
+    if dist == "image":
+        bound = atol
+    else:
+        bound = atol * np.maximum(1.0, np.abs(want))
+    bad = err > bound
+    assert not bad.any(), (f"fwd mismatch: {bad.sum()} of {err.size} elements, max err "
+                           f"{err.max():.3e}, max |I| {np.abs(want).max():.3e}")
+    return float(err.max())
+
+
+def assert_bwd_close(got, want, absmass, rtol=1e-4, mass_floor=1e-2):
+    """Backward gate (R18): |g_gpu - g| <= rtol * max(|g|, mass_floor * S), S = sum of
+    |terms| for that gradient entry (the fp32 rounding scale of the sum)."""
+    g = flat9(got)
+    w = flat9(want)
+    bound = rtol * np.maximum(np.abs(w), mass_floor * absmass)
+    err = np.abs(g - w)
+    bad = err > bound + 1e-30
+    assert not bad.any(), (f"bwd mismatch: {bad.sum()} of {err.size}; worst ratio "
+                           f"{(err / (bound + 1e-30)).max():.3f}; cols {np.nonzero(bad.any(0))[0]}")
+    rel = err / np.maximum(np.abs(w), 1e-30)
+    return float(np.quantile(rel, 0.5)), float(np.quantile(rel, 0.99)), float((err / (bound + 1e-30)).max())

@@ -1,0 +1,143 @@
+// Pipe-throughput microbenchmarks for the roofline denominators (SFU ex2, FP32 FFMA/FFMA2).
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o microbench microbench.cu
+// Each kernel runs ITERS iterations of UNROLL independent chains per thread; the SM-cycle count
+// comes from clock64() around the loop (per CTA, max over CTAs), so results are per SM clock.
+#include <cstdio>
+#include <cuda_runtime.h>
+
+#define ITERS 4096
+
+__device__ __forceinline__ float ex2f(float x) { float y; asm volatile("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x)); return y; }
+
+__global__ void k_ex2(float* out, long long* cyc, float seed) {
+  float a[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) a[j] = seed * (threadIdx.x + j) * 1e-9f - 0.5f;
+  __syncthreads();
+  long long t0 = clock64();
+  for (int it = 0; it < ITERS; ++it) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) a[j] = ex2f(a[j]) - 1.0f;   // ex2 + FADD per element
+  }
+  __syncthreads();
+  long long t1 = clock64();
+  float s = 0; for (int j = 0; j < 8; ++j) s += a[j];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+  if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+}
+
+__global__ void k_ex2_pure(float* out, long long* cyc, float seed) {
+  float a[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) a[j] = seed * (threadIdx.x + j) * 1e-9f - 0.5f;
+  __syncthreads();
+  long long t0 = clock64();
+  for (int it = 0; it < ITERS; ++it) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) a[j] = ex2f(a[j]);   // chained ex2 (value converges to ~0.64)
+  }
+  __syncthreads();
+  long long t1 = clock64();
+  float s = 0; for (int j = 0; j < 8; ++j) s += a[j];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+  if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+}
+
+__global__ void k_ffma(float* out, long long* cyc, float seed) {
+  float a[8], b = seed * 1e-7f + 0.999f, c = seed * 1e-8f;
+  float b2 = b * 0.5f, c2 = c + 1.0f;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) a[j] = threadIdx.x + j;
+  __syncthreads();
+  long long t0 = clock64();
+  for (int it = 0; it < ITERS; ++it) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) { a[j] = fmaf(a[j], b, c); a[j] = fmaf(a[j], b2, c2); }
+  }
+  __syncthreads();
+  long long t1 = clock64();
+  float s = 0; for (int j = 0; j < 8; ++j) s += a[j];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+  if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+}
+
+__global__ void k_ffma2(float* out, long long* cyc, float seed) {
+  float2 a[8], b = make_float2(seed * 1e-7f + 0.999f, 0.998f), c = make_float2(seed * 1e-8f, 1e-3f);
+  float2 b2 = make_float2(0.5f, 0.25f), c2 = make_float2(1.0f, 2.0f);
+#pragma unroll
+  for (int j = 0; j < 8; ++j) a[j] = make_float2(threadIdx.x + j, j);
+  __syncthreads();
+  long long t0 = clock64();
+  for (int it = 0; it < ITERS; ++it) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) { a[j] = __ffma2_rn(a[j], b, c); a[j] = __ffma2_rn(a[j], b2, c2); }
+  }
+  __syncthreads();
+  long long t1 = clock64();
+  float s = 0; for (int j = 0; j < 8; ++j) s += a[j].x + a[j].y;
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+  if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+}
+
+// forward-like mix per element: 2 FFMA (q), 1 MUFU, 3 FFMA (rgb accumulate)
+__global__ void k_mix(float* out, long long* cyc, float seed) {
+  float d[8], ar[8], ag[8], ab[8];
+  float A = -0.7f, t = seed * 1e-9f, u = -0.1f, cr = 0.3f, cg = 0.2f, cb = 0.1f;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) { d[j] = (threadIdx.x & 7) * 0.01f + j * 0.125f; ar[j] = ag[j] = ab[j] = 0.f; }
+  __syncthreads();
+  long long t0 = clock64();
+  for (int it = 0; it < ITERS; ++it) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      float q = fmaf(fmaf(A, d[j], t), d[j], u);
+      float e = ex2f(q);
+      ar[j] = fmaf(cr, e, ar[j]); ag[j] = fmaf(cg, e, ag[j]); ab[j] = fmaf(cb, e, ab[j]);
+    }
+    t += 1e-7f;
+  }
+  __syncthreads();
+  long long t1 = clock64();
+  float s = 0; for (int j = 0; j < 8; ++j) s += ar[j] + ag[j] + ab[j];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+  if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+}
+
+typedef void (*kfn)(float*, long long*, float);
+
+static void run(const char* name, kfn k, double ops_per_elem_iter, int threads, int blocks_per_sm) {
+  int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  int blocks = sms * blocks_per_sm;
+  float* out; long long* cyc;
+  cudaMalloc(&out, sizeof(float) * blocks * threads);
+  cudaMalloc(&cyc, sizeof(long long) * blocks);
+  k<<<blocks, threads>>>(out, cyc, 1.0f);
+  cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+  cudaEventRecord(e0);
+  k<<<blocks, threads>>>(out, cyc, 2.0f);
+  cudaEventRecord(e1); cudaEventSynchronize(e1);
+  float ms; cudaEventElapsedTime(&ms, e0, e1);
+  long long* h = new long long[blocks];
+  cudaMemcpy(h, cyc, sizeof(long long) * blocks, cudaMemcpyDeviceToHost);
+  long long mx = 0; for (int i = 0; i < blocks; ++i) if (h[i] > mx) mx = h[i];
+  double elems = (double)blocks * threads * 8.0 * ITERS;           // element-iterations
+  double per_clk_sm = elems * ops_per_elem_iter / (double)mx / sms * blocks_per_sm / blocks_per_sm;
+  // all CTAs of an SM run concurrently (blocks_per_sm resident), so per-SM work = elems/sms
+  per_clk_sm = elems * ops_per_elem_iter / sms / (double)mx;
+  printf("%-10s threads=%d ctas/SM=%d  cycles=%lld  ms=%.3f  => %.2f ops/clk/SM  (implied clock %.0f MHz)\n",
+         name, threads, blocks_per_sm, mx, ms, per_clk_sm, mx / (ms * 1e3));
+  cudaFree(out); cudaFree(cyc); delete[] h;
+}
+
+int main() {
+  cudaDeviceProp p; cudaGetDeviceProperties(&p, 0);
+  printf("%s SMs=%d cc=%d.%d\n", p.name, p.multiProcessorCount, p.major, p.minor);
+  for (int bps : {2, 4, 8}) {
+    run("ex2+fadd", k_ex2, 1.0, 256, bps);       // counts ex2 per clk
+    run("ex2", k_ex2_pure, 1.0, 256, bps);
+    run("ffma", k_ffma, 2.0, 256, bps);          // FFMA lanes per clk
+    run("ffma2", k_ffma2, 4.0, 256, bps);        // FP32 FMA lanes per clk (2 per FFMA2)
+    run("fwdmix", k_mix, 1.0, 256, bps);         // elements (pairs) per clk
+  }
+  return 0;
+}
