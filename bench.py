@@ -1,0 +1,439 @@
+#!/usr/bin/env python
+"""Headline benchmark: fwd+bwd scale-aware 2D Gaussian rasterization (GSASR, arXiv 2501.06838).
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl gsr|reference] [--workload C5]
+
+One step = one pass of the whole hot path over one batch: binning (K1 + radix sort + records),
+forward render (K4), backward pair pass (K5) and finalize (K6), for every image of the workload
+(default C5 = BASELINE.json configs[4]: 64 DIV2K-size 255x170 LR images at x8 -> 2040x1360,
+the configuration the metric "... at 1/2/4/8 B200" is quoted on). Under torchrun (N > 1) every
+rank renders a pair-balanced HR row band of every image, then the output bands are all-gathered
+and the backward moments all-reduced over NCCL (paper_2501_06838_b200/dist.py).
+
+Rank 0 prints ONE JSON line. value = HR Mpix/s of the whole job (fwd+bwd: output pixels of the
+batch per step / step time); gpairs_per_s = Gaussian-pixel evaluations per second (the work unit,
+P pairs per pass, counted twice per step). `--impl reference` times the float64 CPU oracle
+(oracle/, test infrastructure) on a bounded sample of the same workload on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import csv
+import io
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+import numpy as np  # noqa: E402
+
+import gsr_synth as S  # noqa: E402
+
+METRIC = "HR Mpix/s & Gaussian-pixel evals/s fwd+bwd at 1/2/4/8 B200; % of roofline"
+UNIT = "HR Mpix/s (fwd+bwd)"
+RATIO = 0.1
+SM_COUNT = 148
+# Roofline per pair: forward = 1 ex2 on the SFU (16/clk/SM, measured);
+# backward = 14 FP32 lane-ops on the FMA pipe (128 lanes/clk/SM).
+FWD_PAIRS_PER_CLK_SM = 16.0
+BWD_PAIRS_PER_CLK_SM = 128.0 / 14.0
+
+
+def peaks():
+    p = {"sm_max_mhz": 1965.0, "source": "fallback (B200_PROFILING.md)"}
+    f = ROOT / "MEASURED_PEAKS.json"
+    if f.exists():
+        try:
+            d = json.loads(f.read_text())
+            p["sm_max_mhz"] = float(d.get("sm_max_mhz", 1965.0))
+            p["hbm_gbs"] = float(d.get("hbm_gbs", 0.0))
+            p["source"] = "MEASURED_PEAKS.json (sm_max_mhz) + tools/microbench.cu (pipe rates)"
+        except Exception:
+            pass
+    return p
+
+
+def workload(name: str, n_images: int | None):
+    cfg = S.CONFIGS[name]
+    imgs = list(cfg["images"])
+    if n_images:
+        imgs = imgs[:n_images]
+    return cfg, imgs
+
+
+def make_inputs(imgs, seed0=1000):
+    clouds = [S.gaussians(H, W, seed=seed0 + k) for k, (H, W, s) in enumerate(imgs)]
+    host = {k: np.ascontiguousarray(np.concatenate([c[k] for c in clouds])) for k in
+            ("alpha", "mu", "sigma", "rho", "color")}
+    counts = [c["alpha"].shape[0] for c in clouds]
+    return host, counts, clouds
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        try:
+            out, _ = self.p.communicate(timeout=5)
+        except Exception:
+            self.p.kill()
+            out = ""
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for row in csv.reader(io.StringIO(out)):
+            if len(row) < 9:
+                continue
+            try:
+                sm.append(float(row[1])); mx.append(float(row[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, row[5:9]):
+                if v.strip().lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "samples": len(sm),
+                "reasons": sorted(reasons)}
+
+
+def ncu_traffic(workload_name: str, kernel: str):
+    """dram bytes per launch of `kernel` from the committed ncu --set full capture, if it was
+    taken on this workload (profiles/ncu_traffic.json), else None."""
+    f = ROOT / "profiles" / "ncu_traffic.json"
+    if not f.exists():
+        return None
+    try:
+        d = json.loads(f.read_text())
+        e = d.get(workload_name, {}).get(kernel)
+        return None if e is None else float(e["dram_bytes_per_launch"])
+    except Exception:
+        return None
+
+
+# ----------------------------------------------------------------------------- CPU oracle
+def oracle_sample(imgs, clouds, host_grad_img0, budget_s: float, max_threads=None):
+    """Time the float64 oracle (as it stands) on a bounded sample of the workload: forward
+    (rect mode) on a band of HR rows of image 0 and backward on a set of Gaussians of image 0.
+    Returns (pairs/s fwd, pairs/s bwd, cores, sample description)."""
+    import oracle as O
+    if max_threads:
+        O.oracle.set_threads(max_threads)
+    cores = O.oracle.max_threads()
+    H, W, s = imgs[0]
+    c = clouds[0]
+    Hs, Ws = O.out_dims(H, W, s)
+    mid = Hs // 2
+    # calibrate with one row, then size the sample to ~budget/2 per pass
+    t0 = time.perf_counter()
+    O.render_fwd(c, H, W, s, RATIO, mode="rect", rows=(mid, mid + 1))
+    t1 = time.perf_counter() - t0
+    p1 = O.pair_count(c, H, W, s, RATIO, rows=(mid, mid + 1))
+    rows = int(max(1, min(Hs - mid, (budget_s / 2) / max(t1, 1e-3))))
+    t0 = time.perf_counter()
+    O.render_fwd(c, H, W, s, RATIO, mode="rect", rows=(mid, mid + rows))
+    tf = time.perf_counter() - t0
+    pf = O.pair_count(c, H, W, s, RATIO, rows=(mid, mid + rows))
+    R = O.rects(c, H, W, s, RATIO)
+    area = np.maximum(R[:, 3] - R[:, 2] + 1, 0) * np.maximum(R[:, 5] - R[:, 4] + 1, 0)
+    rate_f = pf / tf
+    target = int(rate_f * budget_s / 2)
+    order = np.argsort(np.abs(c["mu"][:, 1] - H / 2) + np.abs(c["mu"][:, 0] - W / 2))
+    cum = np.cumsum(area[order])
+    k = int(max(1, min(len(order), np.searchsorted(cum, target) + 1)))
+    idx = np.sort(order[:k])
+    t0 = time.perf_counter()
+    O.render_bwd(c, H, W, s, RATIO, host_grad_img0, idx=idx)
+    tb = time.perf_counter() - t0
+    pb = int(area[idx].sum())
+    desc = (f"image 0 of the workload: forward rect-mode on HR rows [{mid},{mid + rows}) "
+            f"({pf:.3e} pairs, {tf:.1f} s), backward of {k} Gaussians nearest the centre "
+            f"({pb:.3e} pairs, {tb:.1f} s); extrapolated to the full step by pairs/s")
+    return pf / tf, pb / tb, cores, desc, (tf + tb)
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    cfg, imgs = workload(args.workload, args.images)
+    host, counts, clouds = make_inputs(imgs[:1])
+    import oracle as O
+    H, W, s = imgs[0]
+    Hs, Ws = O.out_dims(H, W, s)
+    P_img = O.pair_count(clouds[0], H, W, s, RATIO)
+    P = P_img * len(imgs)                      # images of the workload are i.i.d. draws
+    pix = sum(O.out_dims(h, w, sc)[0] * O.out_dims(h, w, sc)[1] for h, w, sc in imgs)
+    g0 = S.grad_out((Hs, Ws, 3), seed=2000).astype(np.float64)
+    times = []
+    desc = cores = None
+    for it in range(args.warmup + args.steps):
+        rf, rb, cores, desc, _ = oracle_sample(imgs, clouds, g0, args.ref_budget)
+        t_step = P / rf + P / rb
+        if it >= args.warmup:
+            times.append(t_step)
+    t = float(np.median(times))
+    value = pix / t / 1e6
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (gsr_synth image-like recipe)",
+            "config": {"workload": f"{args.workload}: {cfg['desc']}", "images": len(imgs),
+                       "ratio": RATIO, "pairs_per_pass": P},
+            "gpairs_per_s": 2 * P / t / 1e9,
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                             "sample": desc},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------------------- GPU arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["gsr", "reference"], default="gsr")
+    ap.add_argument("--workload", default="C5", choices=list(S.CONFIGS))
+    ap.add_argument("--images", type=int, default=None, help="dev only: first N images")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=12.0, help="seconds of oracle work")
+    ap.add_argument("--ref-budget", type=float, default=6.0, help="oracle seconds per ref step")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2501_06838_b200 as gsr
+    from paper_2501_06838_b200 import _lib
+    from paper_2501_06838_b200 import dist as gdist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    gsr.load()
+
+    cfg, imgs = workload(args.workload, args.images)
+    host, counts, clouds = make_inputs(imgs)
+    n = int(host["alpha"].shape[0])
+    params = [torch.from_numpy(host[k]).to(dev) for k in ("alpha", "mu", "sigma", "rho", "color")]
+
+    # ---- row-band plan (identical on every rank; deterministic from the inputs)
+    dims = [gsr.out_dims(H, W, s) for H, W, s in imgs]
+    widths3 = [Ws * 3 for _, Ws in dims]
+    offs = np.concatenate([[0], np.cumsum(counts)])
+    bounds = []
+    for k, (H, W, s) in enumerate(imgs):
+        if world == 1:
+            bounds.append([0, dims[k][0]])
+        else:
+            rc = gdist.row_pair_counts(host["mu"][offs[k]:offs[k + 1]],
+                                       np.ones(counts[k], bool), H, W, s, RATIO)
+            bounds.append(gdist.plan_bands(rc, world))
+    band_imgs = [gsr.Image(H, W, s, int(offs[k]), counts[k], bounds[k][rank], bounds[k][rank + 1])
+                 for k, (H, W, s) in enumerate(imgs)]
+    lay = gsr.layout(band_imgs)
+    full_pix = sum(h * w for h, w in dims)
+    P_rank = gsr.pair_count(*params, lay, RATIO)
+    Pt = torch.tensor([P_rank], dtype=torch.int64, device=dev)
+    if world > 1:
+        dist.all_reduce(Pt)
+    P_total = int(Pt.item())
+
+    # grad_out for this rank's bands (the upstream gradient of the step, synthetic)
+    g_band = torch.empty(lay.out_numel, dtype=torch.float32, device=dev)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(2000 + rank)
+    g_band.uniform_(-1.0, 1.0, generator=gen)
+
+    def step():
+        out = gsr.render_fwd_batched(*params, lay, RATIO)
+        gathered = out
+        if world > 1:
+            gathered = gdist.gather_bands(out, gdist.rank_numels(bounds, widths3, world))
+        moments = torch.zeros((n, 8), dtype=torch.float64, device=dev)
+        gsr.render_bwd_moments_batched(*params, lay, g_band, moments, RATIO)
+        if world > 1:
+            gdist.reduce_moments(moments)
+        grads = gsr.finalize_grads(*params, moments)
+        return gathered, grads
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+
+    _lib.profile_collect(reset=True)
+    _lib.profile_enable(True)
+    sampler = ClockSampler(local if "CUDA_VISIBLE_DEVICES" not in os.environ else
+                           int(os.environ["CUDA_VISIBLE_DEVICES"].split(",")[local]))
+    sampler.start()
+    time.sleep(0.3)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        step()
+    e1.record()
+    torch.cuda.synchronize()
+    barrier()
+    clocks = sampler.stop()
+    _lib.profile_enable(False)
+    phase_ms, phase_calls, launches = _lib.profile_collect(reset=True)
+    ms = e0.elapsed_time(e1)
+    tt = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    ms_total = float(tt.item())
+    ms_step = ms_total / args.steps
+
+    # ---- e2e: host (pinned) buffers through the public API, copies inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        hp = [torch.from_numpy(host[k]).pin_memory() for k in ("alpha", "mu", "sigma", "rho", "color")]
+        hg = g_band.cpu().pin_memory()
+        h_out = torch.empty(lay.out_numel, dtype=torch.float32).pin_memory()
+        h_grads = [torch.empty_like(t).pin_memory() for t in hp]
+        h2d = sum(t.numel() * t.element_size() for t in hp) + hg.numel() * 4
+        d2h = h_out.numel() * 4 + sum(t.numel() * t.element_size() for t in h_grads)
+
+        def e2e_step():
+            dp = [t.to(dev, non_blocking=True) for t in hp]
+            dg = hg.to(dev, non_blocking=True)
+            out = gsr.render_fwd_batched(*dp, lay, RATIO)
+            mom = torch.zeros((n, 8), dtype=torch.float64, device=dev)
+            gsr.render_bwd_moments_batched(*dp, lay, dg, mom, RATIO)
+            if world > 1:
+                gdist.reduce_moments(mom)
+            gr = gsr.finalize_grads(*dp, mom)
+            h_out.copy_(out, non_blocking=True)
+            for h, d in zip(h_grads, gr):
+                h.copy_(d, non_blocking=True)
+
+        e2e_step()
+        torch.cuda.synchronize()
+        barrier()
+        e0.record()
+        for _ in range(args.steps):
+            e2e_step()
+        e1.record()
+        torch.cuda.synchronize()
+        barrier()
+        te = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e_ms = float(te.item()) / args.steps
+        e2e = {"value": full_pix / (e2e_ms * 1e-3) / 1e6, "unit": UNIT,
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "ms_per_step": e2e_ms}
+
+    # ---- roofline of the dominant kernel (per launch, this rank)
+    pk = peaks()
+    f_clk = pk["sm_max_mhz"] * 1e6
+    kern = max(("render_fwd", "render_bwd"), key=lambda k: phase_ms.get(k, 0.0))
+    ncall = max(phase_calls.get(kern, 0), 1)
+    t_launch = phase_ms[kern] / ncall * 1e-3
+    per_clk = FWD_PAIRS_PER_CLK_SM if kern == "render_fwd" else BWD_PAIRS_PER_CLK_SM
+    peak = per_clk * SM_COUNT * f_clk / 1e9           # Gpair/s
+    achieved = P_rank / t_launch / 1e9
+    roof = {"bound": "alu", "pipe": "SFU ex2" if kern == "render_fwd" else "FP32 FMA",
+            "kernel": kern, "achieved": achieved, "peak": peak, "unit": "Gpair/s",
+            "frac": achieved / peak, "traffic": ncu_traffic(args.workload, kern),
+            "peak_basis": f"{per_clk:.3f} pairs/clk/SM x {SM_COUNT} SMs x {pk['sm_max_mhz']:.0f} MHz "
+                          f"({pk['source']})",
+            "frac_at_sampled_clock": (achieved / (per_clk * SM_COUNT * clocks["sm_mhz"] * 1e6 / 1e9)
+                                      if clocks.get("sm_mhz") else None),
+            "pairs_per_launch": P_rank}
+    other = "render_bwd" if kern == "render_fwd" else "render_fwd"
+    if phase_calls.get(other):
+        t_o = phase_ms[other] / phase_calls[other] * 1e-3
+        pc = FWD_PAIRS_PER_CLK_SM if other == "render_fwd" else BWD_PAIRS_PER_CLK_SM
+        pko = pc * SM_COUNT * f_clk / 1e9
+        roof["other_kernel"] = {"kernel": other, "achieved": P_rank / t_o / 1e9, "peak": pko,
+                                "frac": P_rank / t_o / 1e9 / pko}
+    share = {k: v / max(ms_total if world == 1 else ms, 1e-9) for k, v in phase_ms.items()}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        Hs0, Ws0 = dims[0]
+        g0 = g_band[:Hs0 * Ws0 * 3].view(Hs0, Ws0, 3).double().cpu().numpy()
+        rf, rb, cores, desc, spent = oracle_sample(imgs, clouds, g0, args.cpu_budget)
+        t_cpu = P_total / rf + P_total / rb
+        cpu = {"value": full_pix / t_cpu / 1e6, "unit": UNIT, "cores": cores, "kind": "oracle",
+               "sample": desc, "oracle_gpairs_per_s_fwd": rf / 1e9,
+               "oracle_gpairs_per_s_bwd": rb / 1e9}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC,
+            "value": full_pix / (ms_step * 1e-3) / 1e6,
+            "unit": UNIT,
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": ms_step,
+            "higher_is_better": True,
+            "scaling": "strong",
+            "vs_baseline": None,
+            "dtype": "f32",
+            "data": "synthetic (gsr_synth image-like recipe, seeded; DESIGN.md)",
+            "config": {"workload": f"{args.workload}: {cfg['desc']}", "images": len(imgs),
+                       "lr_hw": [imgs[0][0], imgs[0][1]], "scale": imgs[0][2], "ratio": RATIO,
+                       "m": 16, "gaussians": n, "pairs_per_pass": P_total,
+                       "parallelism": f"row-band x{world}" if world > 1 else "single GPU",
+                       "l2": "working set > 126 MB L2 (params 1.6 GB, image 2.1 GB); no flush"},
+            "gpairs_per_s": 2 * P_total / (ms_step * 1e-3) / 1e9,
+            "gpu_launches": int(launches),
+            "phase_ms_per_step": {k: v / args.steps for k, v in phase_ms.items()},
+            "phase_share": share,
+            "clocks": clocks,
+            "roofline": roof,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+            "lib": gsr.version(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

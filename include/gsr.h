@@ -30,7 +30,8 @@
  *   - Images are HWC float32: out[y][x][k], k = r,g,b (Alg. 1 l.1 "(sH, sW, 3)").
  *   - ratio r is passed as double (0.1 is not an fp32-exact value); 0 < r <= 1.
  *   - Ownership: the caller allocates every buffer (inputs, outputs, workspace). The library
- *     allocates nothing, keeps no state between calls and never synchronises the stream.
+ *     allocates nothing, keeps no state between calls (apart from the opt-in profiler and a
+ *     launch counter, see gsr_profile_*) and never synchronises the stream.
  *   - Asynchrony: every compute entry point enqueues its kernels on `stream` (a cudaStream_t
  *     passed as void*; NULL = legacy default stream) and returns immediately.
  *   - Errors: GSR_EINVAL for host-checkable argument errors (nothing is launched);
@@ -122,11 +123,12 @@ gsr_status gsr_render_bwd_batched(const float* alpha, const float* mu, const flo
 
 /* Backward split in two for row-band sharding:
  * gsr_render_bwd_moments_batched ACCUMULATES (+=) into moments[n_total][8] (float64, caller
- * zeroes it first) the per-Gaussian pair sums over the pixels of each image's row band, with
- * e = exp(-Q/2), g = dL/dI at the pixel, c' = alpha c K, K = (2 pi sx sy sqrt(1-rho^2))^-1,
- * w = e (g . c'), (dx, dy) = (x/s - mu_x, y/s - mu_y):
- *   m[0..2] = sum e g_k,  m[3] = sum w dx,  m[4] = sum w dy,
- *   m[5] = sum w dx^2,    m[6] = sum w dx dy,  m[7] = sum w dy^2.
+ * zeroes it first) the per-Gaussian pair sums over the pixels of each image's row band. With
+ * u = dx/sx, v = dy/sy, (dx, dy) = (x/s - mu_x, y/s - mu_y), D = 1 - rho^2, k = log2(e)/2,
+ * wq = sqrt(k/D) (u - rho v), vq = sqrt(k) v, e = exp(-Q/2) = 2^-(wq^2 + vq^2),
+ * g = dL/dI at the pixel, c' = alpha c K, K = (2 pi sx sy sqrt(D))^-1, w = e (g . c'):
+ *   m[0..2] = sum e g_k,  m[3] = sum w wq,  m[4] = sum w vq,
+ *   m[5] = sum w wq^2,    m[6] = sum w wq vq,  m[7] = sum w vq^2.
  * Sums of moments over bands (e.g. an all-reduce across ranks) are moments of the union.
  * gsr_finalize_grads turns moments into the gradients (closed forms in DESIGN.md). */
 gsr_status gsr_render_bwd_moments_batched(const float* alpha, const float* mu, const float* sigma,
@@ -167,6 +169,20 @@ gsr_status gsr_debug_tile_lists(const float* alpha, const float* mu, const float
                                 int32_t lr_w, double scale, double ratio, int32_t* counts,
                                 int32_t* ids, int32_t* cells, void* workspace,
                                 size_t workspace_bytes, void* stream);
+
+/* ---- measurement ------------------------------------------------------------------------ */
+
+/* Phase timing for benchmarks (process-global, not thread-safe; off by default). While enabled,
+ * every compute call records a pair of CUDA events on its stream around each phase:
+ *   0 = binning (K1 keys + stable radix sort + cell starts + K1b records),
+ *   1 = forward render kernel (K4), 2 = backward pair pass (K5), 3 = finalize (K6).
+ * gsr_profile_collect synchronises the recorded events, returns the accumulated milliseconds
+ * ms[4] and call counts calls[4] since the last reset, and the number of kernels libgsr
+ * launched (*kernel_launches, counted whether or not profiling is enabled). reset != 0 clears
+ * them. Any argument may be NULL. */
+gsr_status gsr_profile_enable(int32_t on);
+gsr_status gsr_profile_collect(double* ms, int64_t* calls, int64_t* kernel_launches,
+                               int32_t reset);
 
 /* Render-tile and cell geometry used by the kernels (compile-time constants). */
 void gsr_tile_shape(int32_t* tile_w, int32_t* tile_h, int32_t* cell_w, int32_t* cell_h);

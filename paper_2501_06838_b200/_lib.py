@@ -20,7 +20,8 @@ MAX_IMAGES = 64
 EXPORTS = ["gsr_version", "gsr_out_dims", "gsr_workspace_bytes_batched", "gsr_workspace_bytes",
            "gsr_render_fwd", "gsr_render_bwd", "gsr_render_fwd_batched", "gsr_render_bwd_batched",
            "gsr_render_bwd_moments_batched", "gsr_finalize_grads", "gsr_pair_count_batched",
-           "gsr_debug_rects", "gsr_debug_tile_lists", "gsr_tile_shape"]
+           "gsr_debug_rects", "gsr_debug_tile_lists", "gsr_tile_shape", "gsr_profile_enable",
+           "gsr_profile_collect"]
 
 
 class GsrImage(ctypes.Structure):
@@ -74,6 +75,8 @@ def load(path: Path | str | None = None):
     lib.gsr_debug_tile_lists.argtypes = par + [_I64, _I32, _I32, _D, _D, _P, _P, _P, _P, _SZ, _P]
     lib.gsr_tile_shape.argtypes = [ctypes.POINTER(_I32)] * 4
     lib.gsr_tile_shape.restype = None
+    lib.gsr_profile_enable.argtypes = [_I32]
+    lib.gsr_profile_collect.argtypes = [_P, _P, _P, _I32]
     _lib = lib
     return lib
 
@@ -103,6 +106,24 @@ def tile_shape():
     v = [_I32() for _ in range(4)]
     load().gsr_tile_shape(*[ctypes.byref(x) for x in v])
     return tuple(x.value for x in v)
+
+
+PHASES = ("binning", "render_fwd", "render_bwd", "finalize")
+
+
+def profile_enable(on: bool = True) -> None:
+    check(load().gsr_profile_enable(1 if on else 0), "gsr_profile_enable")
+
+
+def profile_collect(reset: bool = True):
+    """-> ({phase: ms}, {phase: calls}, kernel_launches); synchronises the recorded events."""
+    ms = (ctypes.c_double * 4)()
+    calls = (ctypes.c_int64 * 4)()
+    nl = ctypes.c_int64()
+    check(load().gsr_profile_collect(ctypes.cast(ms, _P), ctypes.cast(calls, _P),
+                                     ctypes.cast(ctypes.byref(nl), _P), 1 if reset else 0),
+          "gsr_profile_collect")
+    return dict(zip(PHASES, list(ms))), dict(zip(PHASES, list(calls))), nl.value
 
 
 def version() -> str:

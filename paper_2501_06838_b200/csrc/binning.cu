@@ -377,6 +377,7 @@ void carve_workspace(void* base, long long n, int total_cells, int total_tiles, 
 cudaError_t exclusive_scan_i32(const int* in, int* out, long long n, int* tmp, cudaStream_t st) {
     if (n <= 0) return cudaSuccess;
     long long nb = scan_blocks(n);
+    count_launches(3);
     k_scan_reduce<<<(unsigned)nb, SCAN_THREADS, 0, st>>>(in, n, tmp);
     k_scan_sums<<<1, SCAN_THREADS, 0, st>>>(tmp, nb);
     k_scan_down<<<(unsigned)nb, SCAN_THREADS, 0, st>>>(in, n, tmp, out);
@@ -388,6 +389,7 @@ cudaError_t bin_gaussians(const float* alpha, const float* mu, const float* sigm
                           const ImgTable& tab, Workspace& ws, int** perm_out,
                           uint32_t** keys_sorted_out, cudaStream_t st) {
     if (n > 0) {
+        count_launches(1);
         k_keys<<<grid1d(n, 256), 256, 0, st>>>(alpha, mu, sigma, rho, color, n, tab, ws.keys_a,
                                                ws.vals_a);
         int bits = 32 - __builtin_clz((unsigned)tab.total_cells | 1u);
@@ -397,6 +399,7 @@ cudaError_t bin_gaussians(const float* alpha, const float* mu, const float* sigm
         int* vin = ws.vals_a; int* vout = ws.vals_b;
         for (int ps = 0; ps < passes; ++ps) {
             int shift = 8 * ps;
+            count_launches(2);
             k_rs_hist<<<(unsigned)nb, RS_THREADS, 0, st>>>(kin, n, shift, ws.hist, (int)nb);
             cudaError_t e = exclusive_scan_i32(ws.hist, ws.hist, 256 * nb, ws.scan_tmp, st);
             if (e != cudaSuccess) return e;
@@ -405,6 +408,7 @@ cudaError_t bin_gaussians(const float* alpha, const float* mu, const float* sigm
             std::swap(kin, kout);
             std::swap(vin, vout);
         }
+        count_launches(2);
         k_cell_start<<<grid1d(n + 1, 256), 256, 0, st>>>(kin, n, tab.total_cells,
                                                          ws.cell_start);
         k_records<<<grid1d(n, 256), 256, 0, st>>>(alpha, mu, sigma, rho, color, n, tab, kin, vin,
@@ -424,9 +428,11 @@ cudaError_t launch_pair_count(const float* alpha, const float* mu, const float* 
                               const float* rho, const float* color, long long n,
                               const ImgTable& tab, long long* d_pairs, cudaStream_t st) {
     cudaMemsetAsync(d_pairs, 0, sizeof(long long), st);
-    if (n > 0)
+    if (n > 0) {
+        count_launches(1);
         k_pair_count<<<grid1d(n, 256), 256, 0, st>>>(alpha, mu, sigma, rho, color, n, tab,
                                                      (unsigned long long*)d_pairs);
+    }
     return cudaGetLastError();
 }
 

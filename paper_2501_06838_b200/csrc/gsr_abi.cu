@@ -1,12 +1,59 @@
 // gsr_abi.cu -- the C-ABI of include/gsr.h: argument validation, per-image geometry (fp64,
 // host), workspace carving and launch orchestration. No allocation, no stream sync.
+#include <atomic>
 #include <cmath>
 #include <cstring>
+#include <mutex>
+#include <vector>
 
 #include "../../include/gsr.h"
 #include "gsr_internal.cuh"
 
 using namespace gsr;
+
+// ---- launch accounting / phase profiler ----------------------------------------------------
+namespace {
+std::atomic<long long> g_launches{0};
+struct Profiler {
+    std::mutex mu;
+    bool on = false;
+    std::vector<cudaEvent_t> pool;
+    struct Rec { int phase; cudaEvent_t a, b; };
+    std::vector<Rec> open_, done;
+    double ms[4] = {0, 0, 0, 0};
+    long long calls[4] = {0, 0, 0, 0};
+    cudaEvent_t get() {
+        if (!pool.empty()) { cudaEvent_t e = pool.back(); pool.pop_back(); return e; }
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        return e;
+    }
+} g_prof;
+}  // namespace
+
+namespace gsr {
+void count_launches(long long k) { g_launches += k; }
+int prof_begin(int phase, cudaStream_t st) {
+    std::lock_guard<std::mutex> lk(g_prof.mu);
+    if (!g_prof.on) return -1;
+    Profiler::Rec r{phase, g_prof.get(), g_prof.get()};
+    cudaEventRecord(r.a, st);
+    g_prof.open_.push_back(r);
+    return (int)g_prof.open_.size() - 1;
+}
+void prof_end(int handle, cudaStream_t st) {
+    if (handle < 0) return;
+    std::lock_guard<std::mutex> lk(g_prof.mu);
+    if (handle >= (int)g_prof.open_.size()) return;
+    Profiler::Rec r = g_prof.open_[handle];
+    cudaEventRecord(r.b, st);
+    g_prof.done.push_back(r);
+    g_prof.open_[handle].phase = -1;
+    bool all_closed = true;
+    for (auto& o : g_prof.open_) all_closed &= (o.phase < 0);
+    if (all_closed) g_prof.open_.clear();
+}
+}  // namespace gsr
 
 namespace {
 
@@ -108,8 +155,10 @@ gsr_status prepare(const float* alpha, const float* mu, const float* sigma, cons
     if (!workspace || workspace_bytes < ws_bytes(P->tab, n_total)) return GSR_EWORKSPACE;
     carve_workspace(workspace, n_total, P->tab.total_cells, P->tab.total_tiles, &P->ws);
     if (!bin) return GSR_OK;
+    int h = prof_begin(0, st);
     cudaError_t e = bin_gaussians(alpha, mu, sigma, rho, color, n_total, P->tab, P->ws, &P->perm,
                                   &P->keys, st);
+    prof_end(h, st);
     return e == cudaSuccess ? GSR_OK : GSR_ECUDA;
 }
 
@@ -118,6 +167,37 @@ gsr_status prepare(const float* alpha, const float* mu, const float* sigma, cons
 extern "C" {
 
 const char* gsr_version(void) { return "gsr-b200 0.1 (sm_100a; fwd tile 32x32, cell 16)"; }
+
+gsr_status gsr_profile_enable(int32_t on) {
+    std::lock_guard<std::mutex> lk(g_prof.mu);
+    g_prof.on = on != 0;
+    return GSR_OK;
+}
+
+gsr_status gsr_profile_collect(double* ms, int64_t* calls, int64_t* kernel_launches,
+                               int32_t reset) {
+    std::lock_guard<std::mutex> lk(g_prof.mu);
+    for (auto& r : g_prof.done) {
+        float t = 0.f;
+        if (cudaEventSynchronize(r.b) != cudaSuccess) return GSR_ECUDA;
+        cudaEventElapsedTime(&t, r.a, r.b);
+        g_prof.ms[r.phase] += t;
+        g_prof.calls[r.phase] += 1;
+        g_prof.pool.push_back(r.a);
+        g_prof.pool.push_back(r.b);
+    }
+    g_prof.done.clear();
+    for (int k = 0; k < 4; ++k) {
+        if (ms) ms[k] = g_prof.ms[k];
+        if (calls) calls[k] = g_prof.calls[k];
+    }
+    if (kernel_launches) *kernel_launches = g_launches.load();
+    if (reset) {
+        for (int k = 0; k < 4; ++k) { g_prof.ms[k] = 0; g_prof.calls[k] = 0; }
+        g_launches = 0;
+    }
+    return GSR_OK;
+}
 
 void gsr_tile_shape(int32_t* tile_w, int32_t* tile_h, int32_t* cell_w, int32_t* cell_h) {
     if (tile_w) *tile_w = TILE_W;

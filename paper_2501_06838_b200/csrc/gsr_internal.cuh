@@ -170,6 +170,11 @@ __device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, uint32_
         : "memory");
 }
 
+// ---- host-side launch accounting (gsr_profile_*) --------------------------------------------
+void count_launches(long long k);          // kernels launched by libgsr (all phases)
+int prof_begin(int phase, cudaStream_t st);  // returns a handle (-1 when profiling is off)
+void prof_end(int handle, cudaStream_t st);
+
 // ---- host-side launchers (defined in the .cu files) --------------------------------------
 struct Workspace {
     uint32_t* keys_a; uint32_t* keys_b;

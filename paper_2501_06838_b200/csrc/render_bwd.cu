@@ -1,21 +1,27 @@
 // render_bwd.cu -- K5 (backward pair pass -> per-Gaussian moments) and K6 (finalize).
 //
-// For L with upstream gradient g = dL/dI, every pair (Gaussian i, pixel (x,y)) inside the window
-// contributes, with e = 2^q = exp(-Q/2), c' = alpha c K, w = e (g . c'):
-//   m0..2 += e g_k,  m3 += w dx,  m4 += w dy,  m5 += w dx^2,  m6 += w dx dy,  m7 += w dy^2.
-// K6 turns the moments into the gradients of Eq. 1-2:
-//   d alpha = K (c . m012),  d c_k = alpha K m_k,  M0 = alpha K (c . m012)
-//   d mu_x = a m3 + b m4,  d mu_y = b m3 + c m4            (a, b, c: conic of Eq. 2)
-//   d sx = ((m5/sx^2 - rho m6/(sx sy))/D - M0)/sx,  d sy = ((m7/sy^2 - rho m6/(sx sy))/D - M0)/sy
-//   d rho = (rho M0 - rho (a m5 + 2 b m6 + c m7) + m6/(sx sy))/D
+// Notation (Eq. 2): u = dx/sx, v = dy/sy, D = 1 - rho^2, Q = (u^2 - 2 rho u v +
+// v^2)/D = p^2/D + v^2 with p = u - rho v. The kernels work in the scaled coordinates of the
+// factored exponent, wq = sqrt(k/D) p and vq = sqrt(k) v (k = log2(e)/2), so 2^(-(wq^2+vq^2))
+// = exp(-Q/2). For L with upstream gradient g = dL/dI every pair (Gaussian i, pixel (x,y))
+// inside the window contributes, with e = exp(-Q/2), c' = alpha c K, w = e (g . c'):
+//   m0..2 += e g_k,  m3 += w wq,  m4 += w vq,  m5 += w wq^2,  m6 += w wq vq,  m7 += w vq^2.
+// The (p, v) basis keeps the finalize well conditioned as |rho| -> 1 (the (dx, dy) basis loses
+// 1/sqrt(D) digits there). K6 (fp64), with S0 = sum w = alpha K (c . m012), Sp = m3/kp,
+// Sv = m4/sqrt(k), Spp = m5/kp^2, Spv = m6/(kp sqrt(k)), Svv = m7/k, kp = sqrt(k/D):
+//   d alpha = K (c . m012),  d c_k = alpha K m_k
+//   d mu_x = Sp/(sx D),  d mu_y = (Sv - rho Sp/D)/sy
+//   d sx = ((Spp + rho Spv)/D - S0)/sx,  d sy = (Svv - rho Spv/D - S0)/sy
+//   d rho = (rho S0 + Spv - rho Spp/D)/D
+// (derivation in DESIGN.md "Backward"; the oracle uses direct per-pair derivatives instead).
 //
 // Layout of K5: one CTA per 32 x 32 HR tile (the forward's tiles) with the tile's dL/dI staged in
 // shared memory as column pairs. Lanes own Gaussians: each warp takes 32 consecutive candidates
 // of a cell-row span, and all 32 lanes walk the same pixels (warp-uniform loop bounds from the
 // union of their rects), reading dL/dI as shared-memory broadcasts. Per-pair work is paired over
-// two pixels with FFMA2. Within a row the dy-dependent moments are factored out
-// (sum_row w dy = dy sum_row w, ...), so a pair costs 14 FP32 lane-ops + 1 ex2. Each lane's
-// (Gaussian, tile) partial moments are reduced in registers (row partials, then the tile) and
+// two pixels with FFMA2. Within a row the vq-dependent moments are factored out
+// (sum_row w vq = vq sum_row w, ...), so a pair costs 14 FP32 lane-ops + 1 ex2. Row partials
+// (fp32, <= 16 terms per lane half) are folded into fp64 per-(Gaussian, tile) accumulators, which
 // leave the CTA as 8 fp64 atomics -- the only global atomics of the backward.
 #include "gsr_internal.cuh"
 
@@ -56,9 +62,9 @@ __device__ __forceinline__ void row_pairs(int c_begin, int c_end, const float4* 
         float2 gc = __fmul2_rn(gr, L.cr);
         gc = __ffma2_rn(gg, L.cg, gc);
         gc = __ffma2_rn(gb, L.cb, gc);
-        float2 ed = __fmul2_rn(e, dx);
+        float2 ed = __fmul2_rn(e, w);                            // e wq
         W1 = __ffma2_rn(gc, ed, W1);
-        float2 edd = __fmul2_rn(ed, dx);
+        float2 edd = __fmul2_rn(ed, w);                          // e wq^2
         W2 = __ffma2_rn(gc, edd, W2);
         kx = __fadd2_rn(kx, two);
     }
@@ -141,9 +147,9 @@ __global__ void __launch_bounds__(BWD_THREADS) k_render_bwd(
             L.cr = f2(r1.w); L.cg = f2(r2.x); L.cb = f2(r2.y);
             L.x0 = x0; L.x1 = x1;
             const float kT = (float)Tx0 - r0.x;
-            float m[8];
+            double m[8];
 #pragma unroll
-            for (int k = 0; k < 8; ++k) m[k] = 0.f;
+            for (int k = 0; k < 8; ++k) m[k] = 0.0;
             for (int y = ya; y <= yb; ++y) {
                 const float dy = fmaf((float)y - r0.y, invs, -r0.w);
                 const float v = r1.z * dy;
@@ -157,19 +163,20 @@ __global__ void __launch_bounds__(BWD_THREADS) k_render_bwd(
                 row_pairs<false>(ma, mb, gAr, gBr, kT, L, Tx0, FR, FG, FB, W1, W2);
                 row_pairs<true>(mb, ce, gAr, gBr, kT, L, Tx0, FR, FG, FB, W1, W2);
                 const float fr = FR.x + FR.y, fg = FG.x + FG.y, fb = FB.x + FB.y;
-                const float w0 = fmaf(r1.w, fr, fmaf(r2.x, fg, r2.y * fb));
-                const float w1 = W1.x + W1.y, w2 = W2.x + W2.y;
+                const double w0 = (double)fmaf(r1.w, fr, fmaf(r2.x, fg, r2.y * fb));
+                const double w1 = (double)W1.x + (double)W1.y, w2 = (double)W2.x + (double)W2.y;
+                const double vq = (double)v;
                 m[0] += fr; m[1] += fg; m[2] += fb;
                 m[3] += w1;
-                m[4] = fmaf(dy, w0, m[4]);
+                m[4] = fma(vq, w0, m[4]);
                 m[5] += w2;
-                m[6] = fmaf(dy, w1, m[6]);
-                m[7] = fmaf(dy * dy, w0, m[7]);
+                m[6] = fma(vq, w1, m[6]);
+                m[7] = fma(vq * vq, w0, m[7]);
             }
             if (act) {
                 double* dst = moments + 8LL * perm[p];
 #pragma unroll
-                for (int k = 0; k < 8; ++k) atomicAdd(dst + k, (double)m[k]);
+                for (int k = 0; k < 8; ++k) atomicAdd(dst + k, m[k]);
             }
         }
     }
@@ -190,17 +197,18 @@ __global__ void k_finalize(const float* __restrict__ alpha, const float* __restr
         double sx = sigma[2 * i], sy = sigma[2 * i + 1], rh = rho[i], al = alpha[i];
         double c0 = color[3 * i], c1 = color[3 * i + 1], c2 = color[3 * i + 2];
         double D = (1.0 - rh) * (1.0 + rh);
-        double a = 1.0 / (sx * sx * D), b = -rh / (sx * sy * D), c = 1.0 / (sy * sy * D);
         double K = 1.0 / (TWO_PI * sx * sy * sqrt(D));
+        double kp = sqrt(HALF_LOG2E / D), kv = sqrt(HALF_LOG2E);
         double cf = c0 * m[0] + c1 * m[1] + c2 * m[2];
-        double M0 = al * K * cf;
-        double sxy = sx * sy;
+        double S0 = al * K * cf;
+        double Sp = m[3] / kp, Sv = m[4] / kv;
+        double Spp = m[5] / (kp * kp), Spv = m[6] / (kp * kv), Svv = m[7] / HALF_LOG2E;
         o[0] = (float)(K * cf);
-        o[1] = (float)(a * m[3] + b * m[4]);
-        o[2] = (float)(b * m[3] + c * m[4]);
-        o[3] = (float)(((m[5] / (sx * sx) - rh * m[6] / sxy) / D - M0) / sx);
-        o[4] = (float)(((m[7] / (sy * sy) - rh * m[6] / sxy) / D - M0) / sy);
-        o[5] = (float)((rh * M0 - rh * (a * m[5] + 2.0 * b * m[6] + c * m[7]) + m[6] / sxy) / D);
+        o[1] = (float)(Sp / (sx * D));
+        o[2] = (float)((Sv - rh * Sp / D) / sy);
+        o[3] = (float)(((Spp + rh * Spv) / D - S0) / sx);
+        o[4] = (float)((Svv - rh * Spv / D - S0) / sy);
+        o[5] = (float)((rh * S0 + Spv - rh * Spp / D) / D);
         o[6] = (float)(al * K * m[0]);
         o[7] = (float)(al * K * m[1]);
         o[8] = (float)(al * K * m[2]);
@@ -221,8 +229,11 @@ __global__ void k_finalize(const float* __restrict__ alpha, const float* __restr
 cudaError_t launch_render_bwd_moments(const ImgTable& tab, const Workspace& ws, const int* perm,
                                       const float* grad_out, double* moments, cudaStream_t st) {
     if (tab.total_tiles <= 0) return cudaSuccess;
+    count_launches(1);
+    int h = prof_begin(2, st);
     k_render_bwd<<<tab.total_tiles, BWD_THREADS, 0, st>>>(tab, ws.rec, ws.cell_start, perm,
                                                           grad_out, moments);
+    prof_end(h, st);
     return cudaGetLastError();
 }
 
@@ -231,9 +242,12 @@ cudaError_t launch_finalize(const float* alpha, const float* mu, const float* si
                             const double* moments, float* d_alpha, float* d_mu, float* d_sigma,
                             float* d_rho, float* d_color, cudaStream_t st) {
     if (n <= 0) return cudaSuccess;
+    count_launches(1);
+    int h = prof_begin(3, st);
     k_finalize<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(alpha, mu, sigma, rho, color, n,
                                                             moments, d_alpha, d_mu, d_sigma,
                                                             d_rho, d_color);
+    prof_end(h, st);
     return cudaGetLastError();
 }
 

@@ -174,7 +174,10 @@ __global__ void __launch_bounds__(FWD_THREADS) k_render_fwd(const ImgTable tab,
 cudaError_t launch_render_fwd(const ImgTable& tab, const Workspace& ws, float* out,
                               cudaStream_t st) {
     if (tab.total_tiles <= 0) return cudaSuccess;
+    count_launches(1);
+    int h = prof_begin(1, st);
     k_render_fwd<<<tab.total_tiles, FWD_THREADS, 0, st>>>(tab, ws.rec, ws.cell_start, out);
+    prof_end(h, st);
     return cudaGetLastError();
 }
 

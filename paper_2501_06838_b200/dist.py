@@ -1,0 +1,143 @@
+"""Multi-GPU row-band sharding: one process per GPU, torch.distributed (NCCL over
+NVLink on B200; gloo in the CPU tests) for the two exchange steps of the path.
+
+Partition: every rank renders HR rows [b_r, b_{r+1}) of every image, with the Gaussians whose
+window meets those rows (the halo) -- the library bins only band-intersecting Gaussians, so the
+replicated parameters cost O(N) preprocessing per rank and nothing else. Boundaries equalise the
+per-row pair counts (the work unit), not the row counts.
+
+Exchange steps (the only collectives):
+  forward : all-gather of the output bands (each rank's bands padded to the largest) -> every
+            rank holds every band, `assemble_image` views/copies out a full image;
+  backward: every rank accumulates the pair moments [n, 8] (float64) of its bands; Gaussians
+            whose window spans a seam have partial moments on several ranks, so the moments are
+            sum-reduced (all-reduce) before the closed-form finalize (gsr_finalize_grads).
+
+The band renderer is injected (`render_band` / `moments_band` / `finalize`), so this host logic
+is tested on CPU with gloo and a CPU stand-in, and runs on B200 with the CUDA path.
+"""
+from __future__ import annotations
+
+import math
+from typing import Callable, List, Sequence
+
+import numpy as np
+
+
+def out_size(n: int, s: float) -> int:
+    return int(math.floor(s * n))
+
+
+def row_pair_counts(mu: np.ndarray, valid: np.ndarray, H: int, W: int, s: float, ratio: float
+                    ) -> np.ndarray:
+    """Exact pairs per HR row of one image: rowpairs[y] = sum_i [y0_i <= y <= y1_i] (x1_i-x0_i+1),
+    with the integer window rect of reading R2 (fp64, same operation order as the kernels)."""
+    Hs, Ws = out_size(H, s), out_size(W, s)
+    mx = mu[:, 0].astype(np.float64)
+    my = mu[:, 1].astype(np.float64)
+    hx, hy = ratio * W, ratio * H
+    lim = float(2 ** 30)
+    with np.errstate(invalid="ignore"):
+        x0 = np.floor(np.clip(s * (mx - hx), -lim, lim)) + 1
+        x1 = np.ceil(np.clip(s * (mx + hx), -lim, lim)) - 1
+        y0 = np.floor(np.clip(s * (my - hy), -lim, lim)) + 1
+        y1 = np.ceil(np.clip(s * (my + hy), -lim, lim)) - 1
+        x0 = np.maximum(x0, 0); x1 = np.minimum(x1, Ws - 1)
+        y0 = np.maximum(y0, 0); y1 = np.minimum(y1, Hs - 1)
+        ok = valid & (x0 <= x1) & (y0 <= y1)
+    w = (x1 - x0 + 1)[ok].astype(np.int64)
+    d = np.zeros(Hs + 1, np.int64)
+    np.add.at(d, y0[ok].astype(np.int64), w)
+    np.add.at(d, y1[ok].astype(np.int64) + 1, -w)
+    return np.cumsum(d[:-1])
+
+
+def plan_bands(row_counts: np.ndarray, G: int) -> List[int]:
+    """Boundaries b_0 = 0 <= ... <= b_G = Hs splitting the rows into G contiguous bands of
+    (nearly) equal pair count; every band gets at least one row when Hs >= G."""
+    Hs = int(row_counts.shape[0])
+    if G <= 1:
+        return [0, Hs]
+    cum = np.cumsum(row_counts.astype(np.float64))
+    total = float(cum[-1]) if Hs else 0.0
+    b = [0]
+    for g in range(1, G):
+        if total <= 0:
+            y = (g * Hs) // G
+        else:
+            target = g * total / G
+            hi = int(np.searchsorted(cum, target, side="left")) + 1   # cum[hi-1] >= target
+            lo = hi - 1
+            c_lo = cum[lo - 1] if lo >= 1 else 0.0
+            y = lo if abs(c_lo - target) <= abs(cum[hi - 1] - target) else hi
+        if Hs >= G:
+            y = min(max(y, b[-1] + 1), Hs - (G - g))
+        else:
+            y = min(max(y, b[-1]), Hs)
+        b.append(y)
+    b.append(Hs)
+    return b
+
+
+def band_imbalance(row_counts: np.ndarray, bounds: Sequence[int]) -> float:
+    """max band work / mean band work (1.0 = perfect balance)."""
+    w = [float(row_counts[bounds[g]:bounds[g + 1]].sum()) for g in range(len(bounds) - 1)]
+    m = float(np.mean(w)) if w else 0.0
+    return max(w) / m if m > 0 else 1.0
+
+
+def rank_numels(bounds: Sequence[Sequence[int]], widths3: Sequence[int], world: int) -> List[int]:
+    """Floats of rank r's output: the concatenation of its band of every image."""
+    return [sum((b[r + 1] - b[r]) * w3 for b, w3 in zip(bounds, widths3)) for r in range(world)]
+
+
+def gather_bands(out, numels: Sequence[int], group=None):
+    """All-gather every rank's flat band buffer, padded to the largest: -> [world, max]."""
+    import torch
+    import torch.distributed as dist
+    world = len(numels)
+    mx = max(numels)
+    send = out if out.numel() == mx else torch.cat(
+        [out.reshape(-1), out.new_zeros(mx - out.numel())])
+    recv = out.new_empty(world * mx)
+    dist.all_gather_into_tensor(recv, send.contiguous(), group=group)
+    return recv.view(world, mx)
+
+
+def assemble_image(gathered, bounds: Sequence[Sequence[int]], widths3: Sequence[int], k: int):
+    """Full image k ([Hs_k, Ws_k*3]) from the gathered bands of every rank."""
+    import torch
+    world = gathered.shape[0]
+    parts = []
+    for r in range(world):
+        off = sum((b[r + 1] - b[r]) * w3 for b, w3 in zip(bounds[:k], widths3[:k]))
+        rows = bounds[k][r + 1] - bounds[k][r]
+        parts.append(gathered[r, off:off + rows * widths3[k]].view(rows, widths3[k]))
+    return torch.cat(parts, 0)
+
+
+def reduce_moments(moments, group=None):
+    """Seam reduce: sum the per-rank partial moments [n, 8] (float64) in place."""
+    import torch.distributed as dist
+    dist.all_reduce(moments, op=dist.ReduceOp.SUM, group=group)
+    return moments
+
+
+def sharded_step(rank: int, world: int, bounds: Sequence[Sequence[int]], widths3: Sequence[int],
+                 render_band: Callable, moments_band: Callable, finalize: Callable, n: int,
+                 device, group=None, moment_cols: int = 8):
+    """One fwd+bwd step of a batch under row-band sharding. render_band(rows) -> this rank's flat
+    bands (images in order); moments_band(rows, moments) accumulates its band moments;
+    finalize(moments) -> gradients. Returns (gathered bands [world, max] or the local bands,
+    gradients)."""
+    import torch
+    rows = [(b[rank], b[rank + 1]) for b in bounds]
+    out = render_band(rows)
+    gathered = out
+    if world > 1:
+        gathered = gather_bands(out, rank_numels(bounds, widths3, world), group)
+    moments = torch.zeros((n, moment_cols), dtype=torch.float64, device=device)
+    moments_band(rows, moments)
+    if world > 1:
+        reduce_moments(moments, group)
+    return gathered, finalize(moments)

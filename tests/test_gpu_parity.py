@@ -265,8 +265,8 @@ def test_row_bands_equal_full(gsr):
         gsr.render_bwd_moments_batched(*dev, lay, g[rb:re].reshape(-1).contiguous(), mom)
     grads_b = gsr.finalize_grads(*dev, mom)
     grads_f = gsr.render_bwd(*dev, H, W, s, g)
-    for a, b in zip(grads_b, grads_f):
-        assert torch.allclose(a, b, rtol=1e-5, atol=1e-7)
+    for a, b in zip(grads_b, grads_f):       # same sums, different fp32 grouping
+        assert torch.allclose(a, b, rtol=1e-4, atol=1e-6 * b.abs().max().item())
 
 
 def test_autograd_matches_abi(gsr):
