@@ -307,7 +307,8 @@ int gsr_oracle_field(int64_t n, const double* alpha, const double* mu, const dou
 /* Backward: direct per-pair derivatives of Eq. 1-2 (no moment formulas).     */
 /* grad_out holds rows [row_begin,row_end) of dL/dI.  Gradients are written   */
 /* (overwritten) for the Gaussians listed in idx (or all if idx == NULL).     */
-/* absmass (optional, [n,9]) = sum over pairs of |term| per output:           */
+/* absmass (optional, [n,9]) = sum over pairs of the monomial magnitudes of   */
+/* each term (its fp32 rounding scale, R18), per output:            */
 /*   alpha, mu_x, mu_y, sigma_x, sigma_y, rho, c_r, c_g, c_b                  */
 /* mode 0 brute (literal predicate over all pixels), mode 1 rect.             */
 /* Per-pair derivatives (u = dx/sx, v = dy/sy, D = 1-rho^2, w = alpha f g.c): */
@@ -361,7 +362,7 @@ int gsr_oracle_render_bwd(int64_t n, const double* alpha, const double* mu, cons
                         double u = dx / sx, v = dy / sy;
                         double gc = g[0] * c[0] + g[1] * c[1] + g[2] * c[2];
                         double w = al * f * gc;
-                        double term[9];
+                        double term[9], mono[9];
                         term[0] = f * gc;
                         term[1] = w * (u - rh * v) / (sx * D);
                         term[2] = w * (v - rh * u) / (sy * D);
@@ -371,9 +372,22 @@ int gsr_oracle_render_bwd(int64_t n, const double* alpha, const double* mu, cons
                         term[6] = al * f * g[0];
                         term[7] = al * f * g[1];
                         term[8] = al * f * g[2];
+                        /* rounding scale of each term (R18): the sum of the absolute
+                         * values of its monomials, with |g.c| -> sum_k |g_k c_k| */
+                        double gca = fabs(g[0] * c[0]) + fabs(g[1] * c[1]) + fabs(g[2] * c[2]);
+                        double wa = al * f * gca;
+                        mono[0] = f * gca;
+                        mono[1] = wa * (fabs(u) + fabs(rh * v)) / (sx * D);
+                        mono[2] = wa * (fabs(v) + fabs(rh * u)) / (sy * D);
+                        mono[3] = wa * ((u * u + fabs(rh * u * v)) / D + 1.0) / sx;
+                        mono[4] = wa * ((v * v + fabs(rh * u * v)) / D + 1.0) / sy;
+                        mono[5] = wa * (fabs(rh) + fabs(u * v) + fabs(rh) * Q) / D;
+                        mono[6] = fabs(term[6]);
+                        mono[7] = fabs(term[7]);
+                        mono[8] = fabs(term[8]);
                         for (int k = 0; k < 9; ++k) {
                             g9[k] += term[k];
-                            a9[k] += fabs(term[k]);
+                            a9[k] += mono[k];
                         }
                     }
                 }

@@ -69,7 +69,7 @@ gsr_status build_table(const gsr_image* imgs, int32_t n_imgs, int64_t n_total, d
     if (!std::isfinite(ratio) || !(ratio > 0.0) || ratio > 1.0) return GSR_EINVAL;
     std::memset(tab, 0, sizeof(*tab));
     tab->n_imgs = n_imgs;
-    long long cells = 0, tiles = 0, prev_end = 0;
+    long long cells = 0, tiles = 0, ftiles = 0, prev_end = 0;
     for (int k = 0; k < n_imgs; ++k) {
         const gsr_image& g = imgs[k];
         if (g.lr_h < 1 || g.lr_w < 1) return GSR_EINVAL;
@@ -103,17 +103,22 @@ gsr_status build_table(const gsr_image* imgs, int32_t n_imgs, int64_t n_total, d
             d.ncy = (nrows - 1 + d.offy) / CELL + 1;
             d.ntx = ceil_div(d.Ws, TILE_W);
             d.nty = ceil_div(nrows, TILE_H);
+            d.fntx = ceil_div(d.Ws, FTILE_W);
+            d.fnty = ceil_div(nrows, FTILE_H);
         } else {
-            d.ncx = d.ncy = d.ntx = d.nty = 0;
+            d.ncx = d.ncy = d.ntx = d.nty = d.fntx = d.fnty = 0;
         }
         d.cell_base = (int)cells;
         d.tile_base = (int)tiles;
+        d.ftile_base = (int)ftiles;
         cells += (long long)d.ncx * d.ncy;
         tiles += (long long)d.ntx * d.nty;
+        ftiles += (long long)d.fntx * d.fnty;
         if (cells >= (1LL << 30) || tiles >= (1LL << 30)) return GSR_EINVAL;
     }
     tab->total_cells = (int)cells;
     tab->total_tiles = (int)tiles;
+    tab->total_ftiles = (int)ftiles;
     return GSR_OK;
 }
 

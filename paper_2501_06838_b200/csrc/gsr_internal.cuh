@@ -14,11 +14,16 @@ namespace gsr {
 
 // ---- compile-time geometry -------------------------------------------------------------
 constexpr int CELL = 16;       // cell edge (HR px): binning granularity (sort key)
-constexpr int TILE_W = 32;     // render tile (HR px), forward and backward
+constexpr int TILE_W = 32;     // backward render tile (HR px); also the debug tile-list tile
 constexpr int TILE_H = 32;
-constexpr int FWD_STRIP = 8;   // forward: each lane owns a 1 x 8 horizontal pixel strip
-constexpr int FWD_WARPS = TILE_W / FWD_STRIP;    // 4 warps side by side, lane = tile row
-constexpr int FWD_THREADS = FWD_WARPS * 32;      // 128
+// forward: a CTA renders a 32 x 64 tile with 4 consumer warps stacked vertically (each warp a
+// 32 x 16 footprint); a lane owns 2 rows x 8 columns; one extra warp is the TMA producer.
+constexpr int FTILE_W = 32;
+constexpr int FTILE_H = 64;
+constexpr int FWD_STRIP = 8;                     // columns per lane
+constexpr int FWD_ROWS = 2;                      // rows per lane
+constexpr int FWD_CWARPS = 4;                    // consumer warps
+constexpr int FWD_THREADS = (FWD_CWARPS + 1) * 32;
 constexpr int FWD_CHUNK = 128;                   // records per TMA bulk stage
 constexpr int FWD_STAGES = 4;
 constexpr int BWD_WARPS = 4;
@@ -40,15 +45,16 @@ struct DevImg {
     int row_begin, row_end;   // HR row band
     int offx, offy;           // cell-grid offsets (multiples of CELL, >= max rect extent)
     int ncx, ncy, cell_base;  // cells of this image: [cell_base, cell_base + ncx*ncy)
-    int ntx, nty, tile_base;  // render tiles of this image
+    int ntx, nty, tile_base;  // backward tiles (TILE_W x TILE_H) of this image
+    int fntx, fnty, ftile_base;  // forward tiles (FTILE_W x FTILE_H)
     int wmax, hmax;           // upper bounds on the unclipped rect width/height
 };
 
 struct ImgTable {
     int n_imgs;
     int total_cells;          // key of an unbinned Gaussian (sorts last)
-    int total_tiles;
-    int pad;
+    int total_tiles;          // backward tiles
+    int total_ftiles;         // forward tiles
     DevImg img[MAX_IMAGES];
 };
 
@@ -64,6 +70,15 @@ __host__ __device__ inline int find_image_by_tile(const ImgTable& t, int tile) {
     while (lo < hi) {
         int mid = (lo + hi + 1) >> 1;
         if (t.img[mid].tile_base <= tile) lo = mid; else hi = mid - 1;
+    }
+    return lo;
+}
+
+__host__ __device__ inline int find_image_by_ftile(const ImgTable& t, int tile) {
+    int lo = 0, hi = t.n_imgs - 1;
+    while (lo < hi) {
+        int mid = (lo + hi + 1) >> 1;
+        if (t.img[mid].ftile_base <= tile) lo = mid; else hi = mid - 1;
     }
     return lo;
 }
@@ -168,6 +183,14 @@ __device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, uint32_
             smem_u32(dst)),
         "l"(src), "r"(bytes), "r"(smem_u32(bar))
         : "memory");
+}
+
+// split-K factor for small problems: keep >= ~4 CTAs per SM (148 SMs); 1, 2, 4 or 8
+inline int split_k_factor(int tiles) {
+    const int target = 4 * 148;
+    int ks = 1;
+    while (ks < 8 && tiles * ks * 2 <= target) ks *= 2;
+    return ks;
 }
 
 // ---- host-side launch accounting (gsr_profile_*) --------------------------------------------

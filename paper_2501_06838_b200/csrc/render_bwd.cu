@@ -20,7 +20,7 @@
 // of a cell-row span, and all 32 lanes walk the same pixels (warp-uniform loop bounds from the
 // union of their rects), reading dL/dI as shared-memory broadcasts. Per-pair work is paired over
 // two pixels with FFMA2. Within a row the vq-dependent moments are factored out
-// (sum_row w vq = vq sum_row w, ...), so a pair costs 14 FP32 lane-ops + 1 ex2. Row partials
+// (sum_row w vq = vq sum_row w, ...), so a pair costs 13 FP32 lane-ops + 1 ex2 (kx, w, q, 3 e g, 3 g.c', 4 moments). Row partials
 // (fp32, <= 16 terms per lane half) are folded into fp64 per-(Gaussian, tile) accumulators, which
 // leave the CTA as 8 fp64 atomics -- the only global atomics of the backward.
 #include "gsr_internal.cuh"
@@ -32,7 +32,7 @@ namespace {
 __device__ __forceinline__ float2 f2(float a) { return make_float2(a, a); }
 
 struct LaneG {        // per-lane Gaussian constants
-    float2 A2, u2, t2, inv2, ndl, cr, cg, cb;
+    float2 D2, u2, T2, cr, cg, cb;   // w = D kx + T (D = a1/s, T = b1 dy - a1 dl_x), u = -v^2
     int x0, x1;
 };
 
@@ -46,8 +46,7 @@ __device__ __forceinline__ void row_pairs(int c_begin, int c_end, const float4* 
     for (int c = c_begin; c < c_end; c += 2) {
         const float4 ga = gArow[c >> 1];     // {gr0, gr1, gg0, gg1}
         const float2 gb = gBrow[c >> 1];     // {gb0, gb1}
-        float2 dx = __ffma2_rn(kx, L.inv2, L.ndl);
-        float2 w = __ffma2_rn(L.A2, dx, L.t2);                   // a1 dx + b1 dy
+        float2 w = __ffma2_rn(L.D2, kx, L.T2);                   // a1 dx + b1 dy
         float2 q = __ffma2_rn(make_float2(-w.x, -w.y), w, L.u2); // -(w^2) - v^2
         if (MASKED) {
             int xa = Tx0 + c;
@@ -73,11 +72,12 @@ __device__ __forceinline__ void row_pairs(int c_begin, int c_end, const float4* 
 __global__ void __launch_bounds__(BWD_THREADS) k_render_bwd(
     const ImgTable tab, const float4* __restrict__ rec, const int* __restrict__ cell_start,
     const int* __restrict__ perm, const float* __restrict__ grad_out,
-    double* __restrict__ moments) {
+    double* __restrict__ moments, int ks) {
     __shared__ __align__(16) float4 gA[TILE_H][TILE_W / 2];
     __shared__ __align__(16) float2 gB[TILE_H][TILE_W / 2];
 
-    const int tile = blockIdx.x;
+    const int tile = blockIdx.x / ks;
+    const int kpart = blockIdx.x % ks;    // split: this CTA takes every ks-th candidate group
     const DevImg& im = tab.img[find_image_by_tile(tab, tile)];
     const int t = tile - im.tile_base;
     const int Tx0 = (t % im.ntx) * TILE_W;
@@ -110,7 +110,8 @@ __global__ void __launch_bounds__(BWD_THREADS) k_render_bwd(
     for (int cy = cy_lo; cy <= cy_hi; ++cy) {
         const int row = im.cell_base + cy * im.ncx;
         const int sp0 = cell_start[row + cx_lo], sp1 = cell_start[row + cx_hi + 1];
-        for (int p0 = sp0 + warp * 32; p0 < sp1; p0 += BWD_WARPS * 32) {
+        for (int p0 = sp0 + (kpart * BWD_WARPS + warp) * 32; p0 < sp1;
+             p0 += ks * BWD_WARPS * 32) {
             const int p = p0 + lane;
             bool act = p < sp1;
             float4 r0 = make_float4(0.f, 0.f, 0.f, 0.f), r1 = r0, r2 = r0;
@@ -143,7 +144,7 @@ __global__ void __launch_bounds__(BWD_THREADS) k_render_bwd(
             mb = min(max(mb, ma), ce);
 
             LaneG L;
-            L.A2 = f2(r1.x); L.inv2 = f2(invs); L.ndl = f2(-r0.z);
+            L.D2 = f2(r1.x * invs);
             L.cr = f2(r1.w); L.cg = f2(r2.x); L.cb = f2(r2.y);
             L.x0 = x0; L.x1 = x1;
             const float kT = (float)Tx0 - r0.x;
@@ -154,7 +155,7 @@ __global__ void __launch_bounds__(BWD_THREADS) k_render_bwd(
                 const float dy = fmaf((float)y - r0.y, invs, -r0.w);
                 const float v = r1.z * dy;
                 const float u = (y >= y0 && y <= y1) ? -(v * v) : -INFINITY;
-                L.t2 = f2(r1.y * dy);
+                L.T2 = f2(fmaf(-r1.x, r0.z, r1.y * dy));
                 L.u2 = f2(u);
                 const float4* gAr = &gA[y - Ty0][0];
                 const float2* gBr = &gB[y - Ty0][0];
@@ -231,8 +232,9 @@ cudaError_t launch_render_bwd_moments(const ImgTable& tab, const Workspace& ws, 
     if (tab.total_tiles <= 0) return cudaSuccess;
     count_launches(1);
     int h = prof_begin(2, st);
-    k_render_bwd<<<tab.total_tiles, BWD_THREADS, 0, st>>>(tab, ws.rec, ws.cell_start, perm,
-                                                          grad_out, moments);
+    int ks = split_k_factor(tab.total_tiles);
+    k_render_bwd<<<tab.total_tiles * ks, BWD_THREADS, 0, st>>>(tab, ws.rec, ws.cell_start, perm,
+                                                               grad_out, moments, ks);
     prof_end(h, st);
     return cudaGetLastError();
 }

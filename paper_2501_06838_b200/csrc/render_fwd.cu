@@ -1,17 +1,26 @@
-// render_fwd.cu -- K4: forward render (Eq. 4 / Alg. 1).
+// render_fwd.cu -- K4: forward render (Eq. 4 / Alg. 1, P:1368-1401).
 //
-//   I[y][x][:] = sum over sorted records i with x0_i <= x <= x1_i, y0_i <= y <= y1_i of
-//                c'_i * 2^(q_i(x,y)),  q = -(w^2 + v^2), w = a1 dx + b1 dy, v = c1 dy,
-//                dx = (x - ax_i)/s - dl_x,  dy = (y - ay_i)/s - dl_y     (= x/s - mu_x, y/s - mu_y)
+//   I[y][x][:] = sum over records i with x0_i <= x <= x1_i, y0_i <= y <= y1_i of
+//                c'_i * 2^(q_i(x,y)),   q = -(w^2 + v^2),  w = a1 dx + b1 dy,  v = c1 dy,
+//                dx = (x - ax_i)/s - dl_x,  dy = (y - ay_i)/s - dl_y   (= x/s - mu_x, y/s - mu_y)
 //
-// Layout: one CTA per 32 x 32 HR tile, 4 warps side by side; warp w owns columns
-// [Tx0 + 8w, Tx0 + 8w + 8) and lane l owns row Ty0 + l, i.e. every lane accumulates a 1 x 8
-// pixel strip in registers. The x-window test is therefore warp-uniform per Gaussian (skip /
-// full cover / partial), the y test is per lane and folded into the quadratic's constant term
-// (u = -inf -> 2^q = 0). Candidate records (contiguous cell-row spans, binning.cu) are staged
-// through shared memory by 1-D TMA bulk copies (cp.async.bulk + mbarrier, FWD_STAGES deep) and
-// read as warp broadcasts. exp runs on the SFU (ex2.approx.ftz); the FP32 work is paired over
-// neighbouring pixels with sm_100 FFMA2. Sums are two-level (per staged chunk, then total).
+// CTA = one FTILE_W x FTILE_H (32 x 64) HR tile, 4 consumer warps + 1 TMA producer warp.
+// Consumer warp w owns the 32 x 16 footprint rows [Ty0 + 16w, Ty0 + 16w + 16); lane l owns the
+// 2 x 8 block at columns Tx0 + 8 (l & 3) .. + 7 and rows Ty0 + 16w + 2 (l >> 2) + {0, 1}.
+//   * per Gaussian, warp-uniform: skip if its rect misses the footprint; "full" if it covers all
+//     32 columns (no per-pixel x mask), otherwise masked.
+//   * per lane: kx = x - ax (exact small integers, one FADD2 per column pair, shared by the two
+//     rows), per row w = (a1/s) kx + (b1 dy - a1 dl_x) (one FFMA2 per pixel pair), q = -w^2 - v^2
+//     (one FFMA2; the y test folds into -v^2 -> -inf), 2^q on the SFU (ex2.approx.ftz ->
+//     MUFU.EX2), colour += c' 2^q (3 FFMA2). 5.5 FP32 lane-ops + 1 ex2 per pair.
+//   * candidate records (contiguous cell-row spans, binning.cu) stream through a FWD_STAGES-deep
+//     shared-memory ring filled by 1-D TMA bulk copies (cp.async.bulk, mbarrier complete_tx)
+//     issued by the producer warp; consumers release stages through per-stage "empty" mbarriers
+//     (no CTA-wide barrier in the main loop).
+//   * two-level sums: per-chunk partials in registers, folded into per-thread totals in shared
+//     memory after every chunk (<= 128 Gaussians).
+//   * split-K for small problems: KS CTAs of a cluster share a tile, take every KS-th chunk, and
+//     reduce their totals through DSMEM in cluster-rank order (deterministic, no atomics).
 #include "gsr_internal.cuh"
 
 namespace gsr {
@@ -21,7 +30,7 @@ namespace {
 struct FwdProducer {
     int cy, cy_hi, row_stride, row0, cx_lo, cx_hi, cur, end;
     const int* cs;
-    __device__ int next(int* start) {
+    __device__ int raw_next(int* start) {
         while (cur >= end) {
             if (++cy > cy_hi) return 0;
             int row = row0 + cy * row_stride;
@@ -33,151 +42,269 @@ struct FwdProducer {
         cur += n;
         return n;
     }
+    __device__ int next(int* start, int skip) {   // drop `skip` chunks, then take one
+        for (int k = 0; k < skip; ++k)
+            if (raw_next(start) == 0) return 0;
+        return raw_next(start);
+    }
 };
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;"
+                 ::: "memory");
+}
+__device__ __forceinline__ float2 ld_dsmem_f2(const float2* local_addr, uint32_t rank) {
+    uint32_t a = smem_u32(local_addr), ra;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(rank));
+    float2 v;
+    asm volatile("ld.shared::cluster.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(ra)
+                 : "memory");
+    return v;
+}
 
 __device__ __forceinline__ float2 f2(float a) { return make_float2(a, a); }
 
+constexpr int NACC = FWD_ROWS * (FWD_STRIP / 2) * 3;   // float2 accumulators per thread (24)
+constexpr int NCONS = FWD_CWARPS * 32;                  // consumer threads (128)
+
+struct FwdSmem {
+    float4 rec[FWD_STAGES][FWD_CHUNK * 3];
+    float2 tot[NACC][NCONS];
+    uint64_t full_bar[FWD_STAGES];
+    uint64_t empty_bar[FWD_STAGES];
+    int count[FWD_STAGES];
+};
+
 template <bool FULL>
 __device__ __forceinline__ void fwd_gauss(const float4 r0, const float4 r1, const float4 r2,
-                                          float yf, int y, float xw0f, int xw0, float invs,
-                                          int x0, int x1, float2 (&pr)[4], float2 (&pg)[4],
-                                          float2 (&pb)[4]) {
-    unsigned ys = __float_as_uint(r2.w);
-    int y0 = (int)(ys & 0xffffu), y1 = (int)(ys >> 16);
-    float dy = fmaf(yf - r0.y, invs, -r0.w);
-    float t = r1.y * dy;                 // b1 dy
-    float v = r1.z * dy;                 // c1 dy
-    float u = -(v * v);
-    u = (y >= y0 && y <= y1) ? u : -INFINITY;
-    const float kx0 = xw0f - r0.x;
-    const float2 A2 = f2(r1.x), t2 = f2(t), u2 = f2(u), inv2 = f2(invs), ndl = f2(-r0.z);
-    const float2 cr = f2(r1.w), cg = f2(r2.x), cb = f2(r2.y);
-    const float2 k2 = f2(kx0);
+                                          const float (&yf)[FWD_ROWS], const int (&yi)[FWD_ROWS],
+                                          float xl0f, int xl0, float invs, int x0, int x1,
+                                          float2 (&acc)[NACC]) {
+    const unsigned ys = __float_as_uint(r2.w);
+    const int y0 = (int)(ys & 0xffffu), y1 = (int)(ys >> 16);
+    const float delta = r1.x * invs;                         // a1 / s
+    const float2 D2 = f2(delta);
+    const float2 k2 = f2(xl0f - r0.x);
+    float2 kx[FWD_STRIP / 2];
 #pragma unroll
-    for (int jp = 0; jp < FWD_STRIP / 2; ++jp) {
-        float2 kx = __fadd2_rn(k2, make_float2((float)(2 * jp), (float)(2 * jp + 1)));
-        float2 dx = __ffma2_rn(kx, inv2, ndl);
-        float2 w = __ffma2_rn(A2, dx, t2);                       // a1 dx + b1 dy
-        float2 q = __ffma2_rn(make_float2(-w.x, -w.y), w, u2);   // -(w^2) - v^2
-        if (!FULL) {
-            int xa = xw0 + 2 * jp;
-            q.x = (xa >= x0 && xa <= x1) ? q.x : -INFINITY;
-            q.y = (xa + 1 >= x0 && xa + 1 <= x1) ? q.y : -INFINITY;
+    for (int jp = 0; jp < FWD_STRIP / 2; ++jp)
+        kx[jp] = __fadd2_rn(k2, make_float2((float)(2 * jp), (float)(2 * jp + 1)));
+    bool cin[FWD_STRIP];
+    if (!FULL) {
+#pragma unroll
+        for (int j = 0; j < FWD_STRIP; ++j) cin[j] = (xl0 + j >= x0) && (xl0 + j <= x1);
+    }
+    const float2 cr = f2(r1.w), cg = f2(r2.x), cb = f2(r2.y);
+#pragma unroll
+    for (int r = 0; r < FWD_ROWS; ++r) {
+        const float dy = fmaf(yf[r] - r0.y, invs, -r0.w);
+        const float v = r1.z * dy;                           // c1 dy
+        const float u = (yi[r] >= y0 && yi[r] <= y1) ? -(v * v) : -INFINITY;
+        const float tau = fmaf(-r1.x, r0.z, r1.y * dy);      // b1 dy - a1 dl_x
+        const float2 T2 = f2(tau), U2 = f2(u);
+#pragma unroll
+        for (int jp = 0; jp < FWD_STRIP / 2; ++jp) {
+            float2 w = __ffma2_rn(D2, kx[jp], T2);
+            float2 q = __ffma2_rn(make_float2(-w.x, -w.y), w, U2);
+            if (!FULL) {
+                q.x = cin[2 * jp] ? q.x : -INFINITY;
+                q.y = cin[2 * jp + 1] ? q.y : -INFINITY;
+            }
+            const float2 e = make_float2(ex2_approx(q.x), ex2_approx(q.y));
+            const int a = (r * (FWD_STRIP / 2) + jp) * 3;
+            acc[a + 0] = __ffma2_rn(cr, e, acc[a + 0]);
+            acc[a + 1] = __ffma2_rn(cg, e, acc[a + 1]);
+            acc[a + 2] = __ffma2_rn(cb, e, acc[a + 2]);
         }
-        float2 e = make_float2(ex2_approx(q.x), ex2_approx(q.y));
-        pr[jp] = __ffma2_rn(cr, e, pr[jp]);
-        pg[jp] = __ffma2_rn(cg, e, pg[jp]);
-        pb[jp] = __ffma2_rn(cb, e, pb[jp]);
     }
 }
 
+template <int KS>
 __global__ void __launch_bounds__(FWD_THREADS) k_render_fwd(const ImgTable tab,
                                                             const float4* __restrict__ rec,
                                                             const int* __restrict__ cell_start,
                                                             float* __restrict__ out) {
-    __shared__ __align__(128) float4 srec[FWD_STAGES][FWD_CHUNK * 3];
-    __shared__ __align__(8) uint64_t full_bar[FWD_STAGES];
-    __shared__ int scount[FWD_STAGES];
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    FwdSmem& sm = *reinterpret_cast<FwdSmem*>(smem_raw);
 
-    const int tile = blockIdx.x;
-    const DevImg& im = tab.img[find_image_by_tile(tab, tile)];
-    const int t = tile - im.tile_base;
-    const int Tx0 = (t % im.ntx) * TILE_W;
-    const int Ty0 = im.row_begin + (t / im.ntx) * TILE_H;
+    const int tile = blockIdx.x / KS;
+    const int krank = KS > 1 ? (int)cluster_rank() : 0;
+    const DevImg& im = tab.img[find_image_by_ftile(tab, tile)];
+    const int t = tile - im.ftile_base;
+    const int Tx0 = (t % im.fntx) * FTILE_W;
+    const int Ty0 = im.row_begin + (t / im.fntx) * FTILE_H;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int xw0 = Tx0 + warp * FWD_STRIP;
-    const int xwl = min(xw0 + FWD_STRIP - 1, im.Ws - 1);
-    const int y = Ty0 + lane;
-    const float yf = (float)y, xw0f = (float)xw0, invs = im.invs;
 
-    FwdProducer prod;
     if (threadIdx.x == 0) {
-        const int Tx1 = Tx0 + TILE_W - 1, Ty1 = Ty0 + TILE_H - 1;
-        prod.cs = cell_start;
-        prod.row0 = im.cell_base;
-        prod.row_stride = im.ncx;
-        prod.cx_lo = (Tx0 - im.wmax + 1 + im.offx) / CELL;
-        prod.cx_hi = min(im.ncx - 1, (min(Tx1, im.Ws - 1) + im.offx) / CELL);
-        prod.cy = (Ty0 - im.row_begin - im.hmax + 1 + im.offy) / CELL - 1;
-        prod.cy_hi = min(im.ncy - 1, (min(Ty1, im.row_end - 1) - im.row_begin + im.offy) / CELL);
-        prod.cur = prod.end = 0;
-        for (int s = 0; s < FWD_STAGES; ++s) mbar_init(&full_bar[s], 1);
+        for (int s = 0; s < FWD_STAGES; ++s) {
+            mbar_init(&sm.full_bar[s], 1);
+            mbar_init(&sm.empty_bar[s], FWD_CWARPS);
+        }
         fence_barrier_init();
     }
+    for (int i = threadIdx.x; i < NACC * NCONS; i += FWD_THREADS)
+        (&sm.tot[0][0])[i] = make_float2(0.f, 0.f);
     __syncthreads();
-    auto issue = [&](int s) {
-        int start = 0;
-        int n = prod.next(&start);
-        scount[s] = n;
-        if (n > 0) {
-            uint32_t bytes = (uint32_t)n * 48u;
-            mbar_arrive_expect_tx(&full_bar[s], bytes);
-            tma_bulk_g2s(&srec[s][0], rec + 3LL * start, bytes, &full_bar[s]);
-        } else {
-            mbar_arrive(&full_bar[s]);
-        }
-    };
-    if (threadIdx.x == 0)
-        for (int s = 0; s < FWD_STAGES; ++s) issue(s);
 
-    float2 tr[4], tg[4], tb[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) tr[j] = tg[j] = tb[j] = make_float2(0.f, 0.f);
-
-    for (int k = 0;; ++k) {
-        const int s = k % FWD_STAGES;
-        mbar_wait(&full_bar[s], (uint32_t)((k / FWD_STAGES) & 1));
-        const int n = scount[s];
-        if (n == 0) break;
-        float2 pr[4], pg[4], pb[4];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) pr[j] = pg[j] = pb[j] = make_float2(0.f, 0.f);
-        const float4* sr = &srec[s][0];
-        for (int g = 0; g < n; ++g) {
-            const float4 r2 = sr[3 * g + 2];
-            const unsigned xs = __float_as_uint(r2.z);
-            const int x0 = (int)(xs & 0xffffu), x1 = (int)(xs >> 16);
-            if (x1 < xw0 || x0 > xwl) continue;             // warp-uniform
-            const float4 r0 = sr[3 * g], r1 = sr[3 * g + 1];
-            if (x0 <= xw0 && x1 >= xwl)
-                fwd_gauss<true>(r0, r1, r2, yf, y, xw0f, xw0, invs, x0, x1, pr, pg, pb);
-            else
-                fwd_gauss<false>(r0, r1, r2, yf, y, xw0f, xw0, invs, x0, x1, pr, pg, pb);
-        }
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            tr[j] = __fadd2_rn(tr[j], pr[j]);
-            tg[j] = __fadd2_rn(tg[j], pg[j]);
-            tb[j] = __fadd2_rn(tb[j], pb[j]);
-        }
-        __syncthreads();                       // every warp is done with stage s
-        if (threadIdx.x == 0) issue(s);        // refill it with chunk k + FWD_STAGES
-    }
-
-    if (y < im.row_end) {
-        float* o = out + im.out_off + ((long long)(y - im.row_begin) * im.Ws) * 3;
-#pragma unroll
-        for (int j = 0; j < FWD_STRIP; ++j) {
-            int x = xw0 + j;
-            if (x < im.Ws) {
-                float2 r = tr[j >> 1], g = tg[j >> 1], b = tb[j >> 1];
-                o[3 * x + 0] = (j & 1) ? r.y : r.x;
-                o[3 * x + 1] = (j & 1) ? g.y : g.x;
-                o[3 * x + 2] = (j & 1) ? b.y : b.x;
+    if (warp == FWD_CWARPS) {
+        // ---------------- producer warp: one elected lane walks the chunk list ----------------
+        if (lane == 0) {
+            FwdProducer prod;
+            const int Tx1 = min(Tx0 + FTILE_W - 1, im.Ws - 1);
+            const int Ty1 = min(Ty0 + FTILE_H - 1, im.row_end - 1);
+            prod.cs = cell_start;
+            prod.row0 = im.cell_base;
+            prod.row_stride = im.ncx;
+            prod.cx_lo = (Tx0 - im.wmax + 1 + im.offx) / CELL;
+            prod.cx_hi = min(im.ncx - 1, (Tx1 + im.offx) / CELL);
+            prod.cy = (Ty0 - im.row_begin - im.hmax + 1 + im.offy) / CELL - 1;
+            prod.cy_hi = min(im.ncy - 1, (Ty1 - im.row_begin + im.offy) / CELL);
+            prod.cur = prod.end = 0;
+            for (int k = 0;; ++k) {
+                const int s = k % FWD_STAGES;
+                if (k >= FWD_STAGES)
+                    mbar_wait(&sm.empty_bar[s], (uint32_t)((k / FWD_STAGES - 1) & 1));
+                int start = 0;
+                const int n = prod.next(&start, k == 0 ? krank : KS - 1);
+                sm.count[s] = n;
+                if (n > 0) {
+                    const uint32_t bytes = (uint32_t)n * 48u;
+                    mbar_arrive_expect_tx(&sm.full_bar[s], bytes);
+                    tma_bulk_g2s(&sm.rec[s][0], rec + 3LL * start, bytes, &sm.full_bar[s]);
+                } else {
+                    mbar_arrive(&sm.full_bar[s]);    // end marker
+                    break;
+                }
             }
         }
+    } else {
+        // ---------------- consumer warps ------------------------------------------------------
+        const int xl0 = Tx0 + FWD_STRIP * (lane & 3);
+        const int yl0 = Ty0 + 16 * warp + FWD_ROWS * (lane >> 2);
+        const int fx0 = Tx0, fx1 = min(Tx0 + FTILE_W - 1, im.Ws - 1);   // warp footprint
+        const int fy0 = Ty0 + 16 * warp, fy1 = min(fy0 + 15, im.row_end - 1);
+        const float invs = im.invs, xl0f = (float)xl0;
+        float yf[FWD_ROWS];
+        int yi[FWD_ROWS];
+#pragma unroll
+        for (int r = 0; r < FWD_ROWS; ++r) { yi[r] = yl0 + r; yf[r] = (float)(yl0 + r); }
+
+        for (int k = 0;; ++k) {
+            const int s = k % FWD_STAGES;
+            mbar_wait(&sm.full_bar[s], (uint32_t)((k / FWD_STAGES) & 1));
+            const int n = sm.count[s];
+            if (n == 0) break;
+            float2 acc[NACC];
+#pragma unroll
+            for (int a = 0; a < NACC; ++a) acc[a] = make_float2(0.f, 0.f);
+            const float4* sr = &sm.rec[s][0];
+            if (fy0 <= fy1) {
+                for (int g = 0; g < n; ++g) {
+                    const float4 r2 = sr[3 * g + 2];
+                    const unsigned xs = __float_as_uint(r2.z), ys = __float_as_uint(r2.w);
+                    const int x0 = (int)(xs & 0xffffu), x1 = (int)(xs >> 16);
+                    const int y0 = (int)(ys & 0xffffu), y1 = (int)(ys >> 16);
+                    if (x1 < fx0 || x0 > fx1 || y1 < fy0 || y0 > fy1) continue;   // warp-uniform
+                    const float4 r0 = sr[3 * g], r1 = sr[3 * g + 1];
+                    if (x0 <= fx0 && x1 >= fx1)
+                        fwd_gauss<true>(r0, r1, r2, yf, yi, xl0f, xl0, invs, x0, x1, acc);
+                    else
+                        fwd_gauss<false>(r0, r1, r2, yf, yi, xl0f, xl0, invs, x0, x1, acc);
+                }
+            }
+            // fold the chunk partials into the per-thread totals (second accumulation level)
+#pragma unroll
+            for (int a = 0; a < NACC; ++a)
+                sm.tot[a][threadIdx.x] = __fadd2_rn(sm.tot[a][threadIdx.x], acc[a]);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&sm.empty_bar[s]);
+        }
     }
+
+    if (KS > 1) {
+        cluster_sync_all();                    // every CTA's totals are final
+        if (krank == 0 && warp < FWD_CWARPS) {
+            for (int a = 0; a < NACC; ++a) {
+                float2 v = make_float2(0.f, 0.f);
+                for (int q = 0; q < KS; ++q)
+                    v = __fadd2_rn(v, ld_dsmem_f2(&sm.tot[a][threadIdx.x], q));
+                sm.tot[a][threadIdx.x] = v;    // only this thread reads its own slot afterwards
+            }
+        }
+        cluster_sync_all();                    // keep every CTA's smem alive until read
+        if (krank != 0) return;
+    }
+    if (warp >= FWD_CWARPS) return;
+
+    const int xl0 = Tx0 + FWD_STRIP * (lane & 3);
+    const int yl0 = Ty0 + 16 * warp + FWD_ROWS * (lane >> 2);
+#pragma unroll
+    for (int r = 0; r < FWD_ROWS; ++r) {
+        const int y = yl0 + r;
+        if (y >= im.row_end) continue;
+        float* o = out + im.out_off + ((long long)(y - im.row_begin) * im.Ws) * 3;
+#pragma unroll
+        for (int jp = 0; jp < FWD_STRIP / 2; ++jp) {
+            const int a = (r * (FWD_STRIP / 2) + jp) * 3;
+            const float2 R = sm.tot[a][threadIdx.x], G = sm.tot[a + 1][threadIdx.x],
+                         B = sm.tot[a + 2][threadIdx.x];
+            const int x = xl0 + 2 * jp;
+            if (x < im.Ws) { o[3 * x] = R.x; o[3 * x + 1] = G.x; o[3 * x + 2] = B.x; }
+            if (x + 1 < im.Ws) { o[3 * x + 3] = R.y; o[3 * x + 4] = G.y; o[3 * x + 5] = B.y; }
+        }
+    }
+}
+
+template <int KS>
+cudaError_t launch_ks(const ImgTable& tab, const Workspace& ws, float* out, cudaStream_t st) {
+    static bool attr_set = false;
+    const size_t smem = sizeof(FwdSmem);
+    if (!attr_set) {
+        cudaError_t e = cudaFuncSetAttribute(k_render_fwd<KS>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+        if (e != cudaSuccess) return e;
+        attr_set = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)tab.total_ftiles * KS);
+    cfg.blockDim = dim3(FWD_THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = KS;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, k_render_fwd<KS>, tab, (const float4*)ws.rec,
+                              (const int*)ws.cell_start, out);
 }
 
 }  // namespace
 
 cudaError_t launch_render_fwd(const ImgTable& tab, const Workspace& ws, float* out,
                               cudaStream_t st) {
-    if (tab.total_tiles <= 0) return cudaSuccess;
+    if (tab.total_ftiles <= 0) return cudaSuccess;
     count_launches(1);
     int h = prof_begin(1, st);
-    k_render_fwd<<<tab.total_tiles, FWD_THREADS, 0, st>>>(tab, ws.rec, ws.cell_start, out);
+    // split-K so that small problems still fill the 148 SMs (>= ~4 CTAs per SM)
+    const int ks = split_k_factor(tab.total_ftiles);
+    cudaError_t e;
+    switch (ks) {
+        case 8: e = launch_ks<8>(tab, ws, out, st); break;
+        case 4: e = launch_ks<4>(tab, ws, out, st); break;
+        case 2: e = launch_ks<2>(tab, ws, out, st); break;
+        default: e = launch_ks<1>(tab, ws, out, st); break;
+    }
     prof_end(h, st);
+    if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
 

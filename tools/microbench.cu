@@ -103,6 +103,20 @@ __global__ void k_mix(float* out, long long* cyc, float seed) {
   if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
 }
 
+// accuracy of ex2.approx.ftz.f32 (MUFU.EX2) against exp2 in fp64, over x in [lo, hi]
+__global__ void k_ex2_acc(double lo, double hi, long long n, double* worst) {
+  double w = 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    float x = (float)(lo + (hi - lo) * (double)i / (double)n);
+    double ref = exp2((double)x);
+    double rel = fabs((double)ex2f(x) - ref) / ref;
+    w = rel > w ? rel : w;
+  }
+  for (int o = 16; o > 0; o >>= 1) { double t = __shfl_xor_sync(0xffffffffu, w, o); w = t > w ? t : w; }
+  if ((threadIdx.x & 31) == 0) atomicMax((unsigned long long*)worst, __double_as_longlong(w));
+}
+
 typedef void (*kfn)(float*, long long*, float);
 
 static void run(const char* name, kfn k, double ops_per_elem_iter, int threads, int blocks_per_sm) {
@@ -132,6 +146,17 @@ static void run(const char* name, kfn k, double ops_per_elem_iter, int threads, 
 int main() {
   cudaDeviceProp p; cudaGetDeviceProperties(&p, 0);
   printf("%s SMs=%d cc=%d.%d\n", p.name, p.multiProcessorCount, p.major, p.minor);
+  {
+    double* d; cudaMalloc(&d, sizeof(double));
+    const double rng[][2] = {{-1.0, 0.0}, {-30.0, 0.0}, {-126.0, -30.0}};
+    for (auto& r : rng) {
+      cudaMemset(d, 0, sizeof(double));
+      k_ex2_acc<<<1184, 256>>>(r[0], r[1], 1LL << 26, d);
+      double h; cudaMemcpy(&h, d, sizeof(double), cudaMemcpyDeviceToHost);
+      printf("ex2.approx.ftz.f32 max rel err on [%g, %g]: %.3e (= 2^%.2f)\n", r[0], r[1], h, log2(h));
+    }
+    cudaFree(d);
+  }
   for (int bps : {2, 4, 8}) {
     run("ex2+fadd", k_ex2, 1.0, 256, bps);       // counts ex2 per clk
     run("ex2", k_ex2_pure, 1.0, 256, bps);
