@@ -20,7 +20,8 @@
 // of a cell-row span, and all 32 lanes walk the same pixels (warp-uniform loop bounds from the
 // union of their rects), reading dL/dI as shared-memory broadcasts. Per-pair work is paired over
 // two pixels with FFMA2. Within a row the vq-dependent moments are factored out
-// (sum_row w vq = vq sum_row w, ...), so a pair costs 13 FP32 lane-ops + 1 ex2 (kx, w, q, 3 e g, 3 g.c', 4 moments). Row partials
+// (sum_row w vq = vq sum_row w, ...), so a pair costs 12.5 FP32 lane-ops + 1 ex2 (kx shared by a row pair, w, q, 3 e g, 3 g.c',
+// 4 moments); lanes process two rows at once for two independent accumulation chains. Row partials
 // (fp32, <= 16 terms per lane half) are folded into fp64 per-(Gaussian, tile) accumulators, which
 // leave the CTA as 8 fp64 atomics -- the only global atomics of the backward.
 #include "gsr_internal.cuh"
@@ -32,41 +33,79 @@ namespace {
 __device__ __forceinline__ float2 f2(float a) { return make_float2(a, a); }
 
 struct LaneG {        // per-lane Gaussian constants
-    float2 D2, u2, T2, cr, cg, cb;   // w = D kx + T (D = a1/s, T = b1 dy - a1 dl_x), u = -v^2
+    float2 D2, cr, cg, cb;           // w = D kx + T_row (D = a1/s, T = b1 dy - a1 dl_x)
     int x0, x1;
 };
 
+struct RowAcc {       // per-row partial sums of a lane (register pairs = two pixels)
+    float2 FR, FG, FB, W1, W2;
+};
+
+// One pixel pair (columns c, c+1) of one row: 1 FFMA2 (w) + 1 FFMA2 (q) + 2 ex2 + 3 FFMA2 (e g)
+// + 3 (g . c') + 4 (moments) -- all paired over the two pixels.
 template <bool MASKED>
-__device__ __forceinline__ void row_pairs(int c_begin, int c_end, const float4* __restrict__ gArow,
-                                          const float2* __restrict__ gBrow, float kT,
-                                          const LaneG& L, int Tx0, float2& FR, float2& FG,
-                                          float2& FB, float2& W1, float2& W2) {
+__device__ __forceinline__ void pix_pair(const float4 ga, const float2 gb, const float2 kx,
+                                         const float2 T2, const float2 U2, const LaneG& L,
+                                         bool in0, bool in1, RowAcc& A) {
+    const float2 w = __ffma2_rn(L.D2, kx, T2);                       // a1 dx + b1 dy
+    float2 q = __ffma2_rn(make_float2(-w.x, -w.y), w, U2);           // -(w^2) - v^2
+    if (MASKED) {
+        q.x = in0 ? q.x : -INFINITY;
+        q.y = in1 ? q.y : -INFINITY;
+    }
+    const float2 e = make_float2(ex2_approx(q.x), ex2_approx(q.y));
+    const float2 gr = make_float2(ga.x, ga.y), gg = make_float2(ga.z, ga.w);
+    A.FR = __ffma2_rn(e, gr, A.FR);
+    A.FG = __ffma2_rn(e, gg, A.FG);
+    A.FB = __ffma2_rn(e, gb, A.FB);
+    float2 gc = __fmul2_rn(gr, L.cr);
+    gc = __ffma2_rn(gg, L.cg, gc);
+    gc = __ffma2_rn(gb, L.cb, gc);
+    const float2 ed = __fmul2_rn(e, w);                              // e wq
+    A.W1 = __ffma2_rn(gc, ed, A.W1);
+    const float2 edd = __fmul2_rn(ed, w);                            // e wq^2
+    A.W2 = __ffma2_rn(gc, edd, A.W2);
+}
+
+// Columns [c_begin, c_end) (pairs) of two rows at once: the column part (kx, masks, dL/dI
+// addresses) is shared, and the two rows give two independent accumulation chains.
+template <bool MASKED>
+__device__ __forceinline__ void row2_pairs(int c_begin, int c_end, const float4* __restrict__ gA0,
+                                           const float2* __restrict__ gB0,
+                                           const float4* __restrict__ gA1,
+                                           const float2* __restrict__ gB1, float kT,
+                                           const LaneG& L, int Tx0, const float2 T0,
+                                           const float2 U0, const float2 T1, const float2 U1,
+                                           RowAcc& A0, RowAcc& A1) {
     float2 kx = make_float2(kT + (float)c_begin, kT + (float)(c_begin + 1));
     const float2 two = f2(2.0f);
     for (int c = c_begin; c < c_end; c += 2) {
-        const float4 ga = gArow[c >> 1];     // {gr0, gr1, gg0, gg1}
-        const float2 gb = gBrow[c >> 1];     // {gb0, gb1}
-        float2 w = __ffma2_rn(L.D2, kx, L.T2);                   // a1 dx + b1 dy
-        float2 q = __ffma2_rn(make_float2(-w.x, -w.y), w, L.u2); // -(w^2) - v^2
+        const int cp = c >> 1;
+        bool in0 = true, in1 = true;
         if (MASKED) {
-            int xa = Tx0 + c;
-            q.x = (xa >= L.x0 && xa <= L.x1) ? q.x : -INFINITY;
-            q.y = (xa + 1 >= L.x0 && xa + 1 <= L.x1) ? q.y : -INFINITY;
+            const int xa = Tx0 + c;
+            in0 = xa >= L.x0 && xa <= L.x1;
+            in1 = xa + 1 >= L.x0 && xa + 1 <= L.x1;
         }
-        float2 e = make_float2(ex2_approx(q.x), ex2_approx(q.y));
-        const float2 gr = make_float2(ga.x, ga.y), gg = make_float2(ga.z, ga.w);
-        FR = __ffma2_rn(e, gr, FR);
-        FG = __ffma2_rn(e, gg, FG);
-        FB = __ffma2_rn(e, gb, FB);
-        float2 gc = __fmul2_rn(gr, L.cr);
-        gc = __ffma2_rn(gg, L.cg, gc);
-        gc = __ffma2_rn(gb, L.cb, gc);
-        float2 ed = __fmul2_rn(e, w);                            // e wq
-        W1 = __ffma2_rn(gc, ed, W1);
-        float2 edd = __fmul2_rn(ed, w);                          // e wq^2
-        W2 = __ffma2_rn(gc, edd, W2);
+        pix_pair<MASKED>(gA0[cp], gB0[cp], kx, T0, U0, L, in0, in1, A0);
+        pix_pair<MASKED>(gA1[cp], gB1[cp], kx, T1, U1, L, in0, in1, A1);
         kx = __fadd2_rn(kx, two);
     }
+}
+
+// fold one row's partials into the fp64 per-(Gaussian, tile) moments
+__device__ __forceinline__ void fold_row(const RowAcc& A, float v, const float4 r1, const float4 r2,
+                                         double (&m)[8]) {
+    const float fr = A.FR.x + A.FR.y, fg = A.FG.x + A.FG.y, fb = A.FB.x + A.FB.y;
+    const double w0 = (double)fmaf(r1.w, fr, fmaf(r2.x, fg, r2.y * fb));
+    const double w1 = (double)A.W1.x + (double)A.W1.y, w2 = (double)A.W2.x + (double)A.W2.y;
+    const double vq = (double)v;
+    m[0] += fr; m[1] += fg; m[2] += fb;
+    m[3] += w1;
+    m[4] = fma(vq, w0, m[4]);
+    m[5] += w2;
+    m[6] = fma(vq, w1, m[6]);
+    m[7] = fma(vq * vq, w0, m[7]);
 }
 
 __global__ void __launch_bounds__(BWD_THREADS) k_render_bwd(
@@ -148,31 +187,34 @@ __global__ void __launch_bounds__(BWD_THREADS) k_render_bwd(
             L.cr = f2(r1.w); L.cg = f2(r2.x); L.cb = f2(r2.y);
             L.x0 = x0; L.x1 = x1;
             const float kT = (float)Tx0 - r0.x;
+            const float tdl = -r1.x * r0.z;                        // -a1 dl_x
             double m[8];
 #pragma unroll
             for (int k = 0; k < 8; ++k) m[k] = 0.0;
-            for (int y = ya; y <= yb; ++y) {
-                const float dy = fmaf((float)y - r0.y, invs, -r0.w);
-                const float v = r1.z * dy;
-                const float u = (y >= y0 && y <= y1) ? -(v * v) : -INFINITY;
-                L.T2 = f2(fmaf(-r1.x, r0.z, r1.y * dy));
-                L.u2 = f2(u);
-                const float4* gAr = &gA[y - Ty0][0];
-                const float2* gBr = &gB[y - Ty0][0];
-                float2 FR = f2(0.f), FG = FR, FB = FR, W1 = FR, W2 = FR;
-                row_pairs<true>(ca, ma, gAr, gBr, kT, L, Tx0, FR, FG, FB, W1, W2);
-                row_pairs<false>(ma, mb, gAr, gBr, kT, L, Tx0, FR, FG, FB, W1, W2);
-                row_pairs<true>(mb, ce, gAr, gBr, kT, L, Tx0, FR, FG, FB, W1, W2);
-                const float fr = FR.x + FR.y, fg = FG.x + FG.y, fb = FB.x + FB.y;
-                const double w0 = (double)fmaf(r1.w, fr, fmaf(r2.x, fg, r2.y * fb));
-                const double w1 = (double)W1.x + (double)W1.y, w2 = (double)W2.x + (double)W2.y;
-                const double vq = (double)v;
-                m[0] += fr; m[1] += fg; m[2] += fb;
-                m[3] += w1;
-                m[4] = fma(vq, w0, m[4]);
-                m[5] += w2;
-                m[6] = fma(vq, w1, m[6]);
-                m[7] = fma(vq * vq, w0, m[7]);
+            for (int y = ya; y <= yb; y += 2) {
+                // rows y and y + 1 (the second one is a phantom when y == yb: u = -inf)
+                const int y1r = y + 1;
+                const bool has1 = y1r <= yb;
+                const float dy0 = fmaf((float)y - r0.y, invs, -r0.w);
+                const float dy1 = fmaf((float)y1r - r0.y, invs, -r0.w);
+                const float v0 = r1.z * dy0, v1 = r1.z * dy1;
+                const float u0 = (y >= y0 && y <= y1) ? -(v0 * v0) : -INFINITY;
+                const float u1 = (has1 && y1r >= y0 && y1r <= y1) ? -(v1 * v1) : -INFINITY;
+                const float2 T0 = f2(fmaf(r1.y, dy0, tdl)), T1 = f2(fmaf(r1.y, dy1, tdl));
+                const float2 U0 = f2(u0), U1 = f2(u1);
+                const int ry0 = y - Ty0, ry1 = has1 ? ry0 + 1 : ry0;
+                const float4* gA0 = &gA[ry0][0];
+                const float2* gB0 = &gB[ry0][0];
+                const float4* gA1 = &gA[ry1][0];
+                const float2* gB1 = &gB[ry1][0];
+                RowAcc A0, A1;
+                A0.FR = A0.FG = A0.FB = A0.W1 = A0.W2 = f2(0.f);
+                A1 = A0;
+                row2_pairs<true>(ca, ma, gA0, gB0, gA1, gB1, kT, L, Tx0, T0, U0, T1, U1, A0, A1);
+                row2_pairs<false>(ma, mb, gA0, gB0, gA1, gB1, kT, L, Tx0, T0, U0, T1, U1, A0, A1);
+                row2_pairs<true>(mb, ce, gA0, gB0, gA1, gB1, kT, L, Tx0, T0, U0, T1, U1, A0, A1);
+                fold_row(A0, v0, r1, r2, m);
+                if (has1) fold_row(A1, v1, r1, r2, m);
             }
             if (act) {
                 double* dst = moments + 8LL * perm[p];
