@@ -16,10 +16,11 @@ namespace gsr {
 constexpr int CELL = 16;       // cell edge (HR px): binning granularity (sort key)
 constexpr int TILE_W = 32;     // backward render tile (HR px); also the debug tile-list tile
 constexpr int TILE_H = 32;
-// forward: a CTA renders a 32 x 64 tile with 4 consumer warps stacked vertically (each warp a
-// 32 x 16 footprint); a lane owns 2 rows x 8 columns; one extra warp is the TMA producer.
+// forward: a CTA renders a 32 x 16 tile; each of the 4 consumer warps covers the whole tile
+// (a lane owns 2 rows x 8 columns) and takes every 4th Gaussian of each staged chunk, so the
+// warps' work is balanced by construction; one extra warp is the TMA producer.
 constexpr int FTILE_W = 32;
-constexpr int FTILE_H = 64;
+constexpr int FTILE_H = 16;
 constexpr int FWD_STRIP = 8;                     // columns per lane
 constexpr int FWD_ROWS = 2;                      // rows per lane
 constexpr int FWD_CWARPS = 4;                    // consumer warps

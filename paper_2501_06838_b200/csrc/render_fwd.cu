@@ -4,10 +4,13 @@
 //                c'_i * 2^(q_i(x,y)),   q = -(w^2 + v^2),  w = a1 dx + b1 dy,  v = c1 dy,
 //                dx = (x - ax_i)/s - dl_x,  dy = (y - ay_i)/s - dl_y   (= x/s - mu_x, y/s - mu_y)
 //
-// CTA = one FTILE_W x FTILE_H (32 x 64) HR tile, 4 consumer warps + 1 TMA producer warp.
-// Consumer warp w owns the 32 x 16 footprint rows [Ty0 + 16w, Ty0 + 16w + 16); lane l owns the
-// 2 x 8 block at columns Tx0 + 8 (l & 3) .. + 7 and rows Ty0 + 16w + 2 (l >> 2) + {0, 1}.
-//   * per Gaussian, warp-uniform: skip if its rect misses the footprint; "full" if it covers all
+// CTA = one FTILE_W x FTILE_H (32 x 16) HR tile, 4 consumer warps + 1 TMA producer warp.
+// Every consumer warp covers the whole tile -- lane l owns the 2 x 8 block at columns
+// Tx0 + 8 (l & 3) .. + 7 and rows Ty0 + 2 (l >> 2) + {0, 1} -- and takes the Gaussians
+// g = w, w + 4, w + 8, ... of each staged chunk: the warps' loads are identical by construction
+// (a vertical split of the tile would give each warp a different, order-dependent share of every
+// chunk and serialise the ring). The 4 partial images are summed in warp order at the end.
+//   * per Gaussian, warp-uniform: skip if its rect misses the tile; "full" if it covers all
 //     32 columns (no per-pixel x mask), otherwise masked.
 //   * per lane: kx = x - ax (exact small integers, one FADD2 per column pair, shared by the two
 //     rows), per row w = (a1/s) kx + (b1 dy - a1 dl_x) (one FFMA2 per pixel pair), q = -w^2 - v^2
@@ -74,7 +77,7 @@ constexpr int NCONS = FWD_CWARPS * 32;                  // consumer threads (128
 
 struct FwdSmem {
     float4 rec[FWD_STAGES][FWD_CHUNK * 3];
-    float2 tot[NACC][NCONS];
+    float2 tot[FWD_CWARPS][NACC][32];        // per-warp totals (second accumulation level)
     uint64_t full_bar[FWD_STAGES];
     uint64_t empty_bar[FWD_STAGES];
     int count[FWD_STAGES];
@@ -147,8 +150,8 @@ __global__ void __launch_bounds__(FWD_THREADS) k_render_fwd(const ImgTable tab,
         }
         fence_barrier_init();
     }
-    for (int i = threadIdx.x; i < NACC * NCONS; i += FWD_THREADS)
-        (&sm.tot[0][0])[i] = make_float2(0.f, 0.f);
+    for (int i = threadIdx.x; i < FWD_CWARPS * NACC * 32; i += FWD_THREADS)
+        (&sm.tot[0][0][0])[i] = make_float2(0.f, 0.f);
     __syncthreads();
 
     if (warp == FWD_CWARPS) {
@@ -185,9 +188,9 @@ __global__ void __launch_bounds__(FWD_THREADS) k_render_fwd(const ImgTable tab,
     } else {
         // ---------------- consumer warps ------------------------------------------------------
         const int xl0 = Tx0 + FWD_STRIP * (lane & 3);
-        const int yl0 = Ty0 + 16 * warp + FWD_ROWS * (lane >> 2);
-        const int fx0 = Tx0, fx1 = min(Tx0 + FTILE_W - 1, im.Ws - 1);   // warp footprint
-        const int fy0 = Ty0 + 16 * warp, fy1 = min(fy0 + 15, im.row_end - 1);
+        const int yl0 = Ty0 + FWD_ROWS * (lane >> 2);
+        const int fx0 = Tx0, fx1 = min(Tx0 + FTILE_W - 1, im.Ws - 1);   // tile footprint
+        const int fy0 = Ty0, fy1 = min(Ty0 + FTILE_H - 1, im.row_end - 1);
         const float invs = im.invs, xl0f = (float)xl0;
         float yf[FWD_ROWS];
         int yi[FWD_ROWS];
@@ -204,7 +207,7 @@ __global__ void __launch_bounds__(FWD_THREADS) k_render_fwd(const ImgTable tab,
             for (int a = 0; a < NACC; ++a) acc[a] = make_float2(0.f, 0.f);
             const float4* sr = &sm.rec[s][0];
             if (fy0 <= fy1) {
-                for (int g = 0; g < n; ++g) {
+                for (int g = warp; g < n; g += FWD_CWARPS) {
                     const float4 r2 = sr[3 * g + 2];
                     const unsigned xs = __float_as_uint(r2.z), ys = __float_as_uint(r2.w);
                     const int x0 = (int)(xs & 0xffffu), x1 = (int)(xs >> 16);
@@ -220,29 +223,38 @@ __global__ void __launch_bounds__(FWD_THREADS) k_render_fwd(const ImgTable tab,
             // fold the chunk partials into the per-thread totals (second accumulation level)
 #pragma unroll
             for (int a = 0; a < NACC; ++a)
-                sm.tot[a][threadIdx.x] = __fadd2_rn(sm.tot[a][threadIdx.x], acc[a]);
+                sm.tot[warp][a][lane] = __fadd2_rn(sm.tot[warp][a][lane], acc[a]);
             __syncwarp();
             if (lane == 0) mbar_arrive(&sm.empty_bar[s]);
         }
     }
 
+    // sum the 4 warps' partial images in warp order (deterministic) into tot[0]
+    __syncthreads();
+    if (warp == 0) {
+#pragma unroll 4
+        for (int a = 0; a < NACC; ++a) {
+            float2 v = sm.tot[0][a][lane];
+            for (int q = 1; q < FWD_CWARPS; ++q) v = __fadd2_rn(v, sm.tot[q][a][lane]);
+            sm.tot[0][a][lane] = v;
+        }
+    }
     if (KS > 1) {
-        cluster_sync_all();                    // every CTA's totals are final
-        if (krank == 0 && warp < FWD_CWARPS) {
+        cluster_sync_all();                    // every CTA's tile sum is final
+        if (krank == 0 && warp == 0) {
             for (int a = 0; a < NACC; ++a) {
                 float2 v = make_float2(0.f, 0.f);
-                for (int q = 0; q < KS; ++q)
-                    v = __fadd2_rn(v, ld_dsmem_f2(&sm.tot[a][threadIdx.x], q));
-                sm.tot[a][threadIdx.x] = v;    // only this thread reads its own slot afterwards
+                for (int q = 0; q < KS; ++q) v = __fadd2_rn(v, ld_dsmem_f2(&sm.tot[0][a][lane], q));
+                sm.tot[0][a][lane] = v;        // only this thread reads its own slot afterwards
             }
         }
         cluster_sync_all();                    // keep every CTA's smem alive until read
         if (krank != 0) return;
     }
-    if (warp >= FWD_CWARPS) return;
+    if (warp != 0) return;
 
     const int xl0 = Tx0 + FWD_STRIP * (lane & 3);
-    const int yl0 = Ty0 + 16 * warp + FWD_ROWS * (lane >> 2);
+    const int yl0 = Ty0 + FWD_ROWS * (lane >> 2);
 #pragma unroll
     for (int r = 0; r < FWD_ROWS; ++r) {
         const int y = yl0 + r;
@@ -251,8 +263,8 @@ __global__ void __launch_bounds__(FWD_THREADS) k_render_fwd(const ImgTable tab,
 #pragma unroll
         for (int jp = 0; jp < FWD_STRIP / 2; ++jp) {
             const int a = (r * (FWD_STRIP / 2) + jp) * 3;
-            const float2 R = sm.tot[a][threadIdx.x], G = sm.tot[a + 1][threadIdx.x],
-                         B = sm.tot[a + 2][threadIdx.x];
+            const float2 R = sm.tot[0][a][lane], G = sm.tot[0][a + 1][lane],
+                         B = sm.tot[0][a + 2][lane];
             const int x = xl0 + 2 * jp;
             if (x < im.Ws) { o[3 * x] = R.x; o[3 * x + 1] = G.x; o[3 * x + 2] = B.x; }
             if (x + 1 < im.Ws) { o[3 * x + 3] = R.y; o[3 * x + 4] = G.y; o[3 * x + 5] = B.y; }
