@@ -18,8 +18,9 @@
 //     MUFU.EX2), colour += c' 2^q (3 FFMA2). 5.5 FP32 lane-ops + 1 ex2 per pair.
 //   * candidate records (contiguous cell-row spans, binning.cu) stream through a FWD_STAGES-deep
 //     shared-memory ring filled by 1-D TMA bulk copies (cp.async.bulk, mbarrier complete_tx)
-//     issued by the producer warp; consumers release stages through per-stage "empty" mbarriers
-//     (no CTA-wide barrier in the main loop).
+//     issued by the producer warp, which also filters every landed chunk against the tile,
+//     compacts the kept indices and pre-transforms the kept records (full / ready / empty
+//     mbarriers per stage; no CTA-wide barrier in the main loop).
 //   * two-level sums: per-chunk partials in registers, folded into per-thread totals in shared
 //     memory after every chunk (<= 128 Gaussians).
 //   * split-K for small problems: KS CTAs of a cluster share a tile, take every KS-th chunk, and
@@ -78,37 +79,43 @@ constexpr int NCONS = FWD_CWARPS * 32;                  // consumer threads (128
 struct FwdSmem {
     float4 rec[FWD_STAGES][FWD_CHUNK * 3];
     float2 tot[FWD_CWARPS][NACC][32];        // per-warp totals (second accumulation level)
-    uint64_t full_bar[FWD_STAGES];
-    uint64_t empty_bar[FWD_STAGES];
-    int count[FWD_STAGES];
+    uint8_t idx[FWD_STAGES][FWD_CHUNK];      // kept records of a chunk: index | (full-x << 7)
+    uint64_t full_bar[FWD_STAGES];           // TMA bytes landed
+    uint64_t ready_bar[FWD_STAGES];          // producer warp filtered + transformed the chunk
+    uint64_t empty_bar[FWD_STAGES];          // consumer warps done with the stage
+    int count[FWD_STAGES];                   // records in the chunk (0 = end of the list)
+    int kept[FWD_STAGES];                    // records kept by the filter (-1 = end)
 };
 
+// Transformed record (written in shared memory by the producer warp, see k_render_fwd):
+//   r0 = {-ax, ay, dl_y, a1/s},  r1 = {-a1 dl_x, b1, c1, c'_r},  r2 = {c'_g, c'_b, x0|x1, y0|y1}
 template <bool FULL>
 __device__ __forceinline__ void fwd_gauss(const float4 r0, const float4 r1, const float4 r2,
-                                          const float (&yf)[FWD_ROWS], const int (&yi)[FWD_ROWS],
-                                          float xl0f, int xl0, float invs, int x0, int x1,
+                                          const float2 (&xj)[FWD_STRIP / 2], float yf0,
+                                          const int (&yi)[FWD_ROWS], int xl0, float invs,
                                           float2 (&acc)[NACC]) {
     const unsigned ys = __float_as_uint(r2.w);
     const int y0 = (int)(ys & 0xffffu), y1 = (int)(ys >> 16);
-    const float delta = r1.x * invs;                         // a1 / s
-    const float2 D2 = f2(delta);
-    const float2 k2 = f2(xl0f - r0.x);
+    const float2 D2 = f2(r0.w);
+    const float2 nax = f2(r0.x);
     float2 kx[FWD_STRIP / 2];
 #pragma unroll
-    for (int jp = 0; jp < FWD_STRIP / 2; ++jp)
-        kx[jp] = __fadd2_rn(k2, make_float2((float)(2 * jp), (float)(2 * jp + 1)));
+    for (int jp = 0; jp < FWD_STRIP / 2; ++jp) kx[jp] = __fadd2_rn(xj[jp], nax);   // x - ax
     bool cin[FWD_STRIP];
     if (!FULL) {
+        const unsigned xs = __float_as_uint(r2.z);
+        const int x0 = (int)(xs & 0xffffu), x1 = (int)(xs >> 16);
 #pragma unroll
         for (int j = 0; j < FWD_STRIP; ++j) cin[j] = (xl0 + j >= x0) && (xl0 + j <= x1);
     }
     const float2 cr = f2(r1.w), cg = f2(r2.x), cb = f2(r2.y);
+    float dy = fmaf(yf0 - r0.y, invs, -r0.z);
 #pragma unroll
     for (int r = 0; r < FWD_ROWS; ++r) {
-        const float dy = fmaf(yf[r] - r0.y, invs, -r0.w);
+        if (r > 0) dy += invs;                               // consecutive rows: exact to 1 ulp(1/s)
         const float v = r1.z * dy;                           // c1 dy
         const float u = (yi[r] >= y0 && yi[r] <= y1) ? -(v * v) : -INFINITY;
-        const float tau = fmaf(-r1.x, r0.z, r1.y * dy);      // b1 dy - a1 dl_x
+        const float tau = fmaf(r1.y, dy, r1.x);              // b1 dy - a1 dl_x
         const float2 T2 = f2(tau), U2 = f2(u);
 #pragma unroll
         for (int jp = 0; jp < FWD_STRIP / 2; ++jp) {
@@ -146,6 +153,7 @@ __global__ void __launch_bounds__(FWD_THREADS) k_render_fwd(const ImgTable tab,
     if (threadIdx.x == 0) {
         for (int s = 0; s < FWD_STAGES; ++s) {
             mbar_init(&sm.full_bar[s], 1);
+            mbar_init(&sm.ready_bar[s], 32);
             mbar_init(&sm.empty_bar[s], FWD_CWARPS);
         }
         fence_barrier_init();
@@ -154,73 +162,118 @@ __global__ void __launch_bounds__(FWD_THREADS) k_render_fwd(const ImgTable tab,
         (&sm.tot[0][0][0])[i] = make_float2(0.f, 0.f);
     __syncthreads();
 
+    const int fx0 = Tx0, fx1 = min(Tx0 + FTILE_W - 1, im.Ws - 1);   // tile footprint
+    const int fy0 = Ty0, fy1 = min(Ty0 + FTILE_H - 1, im.row_end - 1);
+    const float invs = im.invs;
+
     if (warp == FWD_CWARPS) {
-        // ---------------- producer warp: one elected lane walks the chunk list ----------------
-        if (lane == 0) {
-            FwdProducer prod;
-            const int Tx1 = min(Tx0 + FTILE_W - 1, im.Ws - 1);
-            const int Ty1 = min(Ty0 + FTILE_H - 1, im.row_end - 1);
-            prod.cs = cell_start;
-            prod.row0 = im.cell_base;
-            prod.row_stride = im.ncx;
-            prod.cx_lo = (Tx0 - im.wmax + 1 + im.offx) / CELL;
-            prod.cx_hi = min(im.ncx - 1, (Tx1 + im.offx) / CELL);
-            prod.cy = (Ty0 - im.row_begin - im.hmax + 1 + im.offy) / CELL - 1;
-            prod.cy_hi = min(im.ncy - 1, (Ty1 - im.row_begin + im.offy) / CELL);
-            prod.cur = prod.end = 0;
-            for (int k = 0;; ++k) {
-                const int s = k % FWD_STAGES;
-                if (k >= FWD_STAGES)
-                    mbar_wait(&sm.empty_bar[s], (uint32_t)((k / FWD_STAGES - 1) & 1));
-                int start = 0;
-                const int n = prod.next(&start, k == 0 ? krank : KS - 1);
-                sm.count[s] = n;
-                if (n > 0) {
-                    const uint32_t bytes = (uint32_t)n * 48u;
-                    mbar_arrive_expect_tx(&sm.full_bar[s], bytes);
-                    tma_bulk_g2s(&sm.rec[s][0], rec + 3LL * start, bytes, &sm.full_bar[s]);
-                } else {
-                    mbar_arrive(&sm.full_bar[s]);    // end marker
-                    break;
+        // ---------------- producer warp --------------------------------------------------------
+        // lane 0 walks the chunk list and issues the TMA bulk copies FWD_STAGES chunks ahead; the
+        // whole warp then filters each landed chunk against the tile (rect intersection, full-x
+        // flag), compacts the kept indices and rewrites the kept records in place into the
+        // consumers' form, so the consumer warps never see a Gaussian that misses the tile.
+        FwdProducer prod;
+        prod.cs = cell_start;
+        prod.row0 = im.cell_base;
+        prod.row_stride = im.ncx;
+        prod.cx_lo = (Tx0 - im.wmax + 1 + im.offx) / CELL;
+        prod.cx_hi = min(im.ncx - 1, (fx1 + im.offx) / CELL);
+        prod.cy = (Ty0 - im.row_begin - im.hmax + 1 + im.offy) / CELL - 1;
+        prod.cy_hi = min(im.ncy - 1, (fy1 - im.row_begin + im.offy) / CELL);
+        prod.cur = prod.end = 0;
+        auto issue = [&](int k) -> int {          // lane 0 only
+            const int s = k % FWD_STAGES;
+            int start = 0;
+            const int n = prod.next(&start, k == 0 ? krank : KS - 1);
+            sm.count[s] = n;
+            if (n > 0) {
+                const uint32_t bytes = (uint32_t)n * 48u;
+                mbar_arrive_expect_tx(&sm.full_bar[s], bytes);
+                tma_bulk_g2s(&sm.rec[s][0], rec + 3LL * start, bytes, &sm.full_bar[s]);
+            } else {
+                mbar_arrive(&sm.full_bar[s]);      // end marker
+            }
+            return n;
+        };
+        int ended = 0;
+        if (lane == 0)
+            for (int k = 0; k < FWD_STAGES && !ended; ++k) ended = issue(k) == 0;
+        ended = __shfl_sync(0xffffffffu, ended, 0);
+        const unsigned lt = (1u << lane) - 1u;
+        for (int k = 0;; ++k) {
+            const int s = k % FWD_STAGES;
+            mbar_wait(&sm.full_bar[s], (uint32_t)((k / FWD_STAGES) & 1));
+            const int n = sm.count[s];
+            if (n == 0) {
+                if (lane == 0) sm.kept[s] = -1;
+                mbar_arrive(&sm.ready_bar[s]);
+                break;
+            }
+            int base = 0;
+            float4* sr = &sm.rec[s][0];
+            for (int g0 = 0; g0 < n; g0 += 32) {
+                const int g = g0 + lane;
+                bool keep = false, full = false;
+                if (g < n) {
+                    const float4 r2 = sr[3 * g + 2];
+                    const unsigned xs = __float_as_uint(r2.z), ys = __float_as_uint(r2.w);
+                    const int x0 = (int)(xs & 0xffffu), x1 = (int)(xs >> 16);
+                    const int y0 = (int)(ys & 0xffffu), y1 = (int)(ys >> 16);
+                    keep = fy0 <= fy1 && !(x1 < fx0 || x0 > fx1 || y1 < fy0 || y0 > fy1);
+                    full = x0 <= fx0 && x1 >= fx1;
+                    if (keep) {
+                        const float4 r0 = sr[3 * g], r1 = sr[3 * g + 1];
+                        sr[3 * g] = make_float4(-r0.x, r0.y, r0.w, r1.x * invs);
+                        sr[3 * g + 1] = make_float4(-r1.x * r0.z, r1.y, r1.z, r1.w);
+                    }
                 }
+                const unsigned m = __ballot_sync(0xffffffffu, keep);
+                if (keep) sm.idx[s][base + __popc(m & lt)] = (uint8_t)(g | (full ? 0x80 : 0));
+                base += __popc(m);
+            }
+            if (lane == 0) sm.kept[s] = base;
+            mbar_arrive(&sm.ready_bar[s]);         // each lane releases its own smem writes
+            // refill the previous stage once the consumers are done with it
+            if (k >= 1 && !ended) {
+                const int kp = k - 1, sp = kp % FWD_STAGES;
+                mbar_wait(&sm.empty_bar[sp], (uint32_t)((kp / FWD_STAGES) & 1));
+                if (lane == 0) ended = issue(kp + FWD_STAGES) == 0;
+                ended = __shfl_sync(0xffffffffu, ended, 0);
             }
         }
     } else {
         // ---------------- consumer warps ------------------------------------------------------
         const int xl0 = Tx0 + FWD_STRIP * (lane & 3);
         const int yl0 = Ty0 + FWD_ROWS * (lane >> 2);
-        const int fx0 = Tx0, fx1 = min(Tx0 + FTILE_W - 1, im.Ws - 1);   // tile footprint
-        const int fy0 = Ty0, fy1 = min(Ty0 + FTILE_H - 1, im.row_end - 1);
-        const float invs = im.invs, xl0f = (float)xl0;
-        float yf[FWD_ROWS];
+        float2 xj[FWD_STRIP / 2];
+#pragma unroll
+        for (int jp = 0; jp < FWD_STRIP / 2; ++jp)
+            xj[jp] = make_float2((float)(xl0 + 2 * jp), (float)(xl0 + 2 * jp + 1));
         int yi[FWD_ROWS];
 #pragma unroll
-        for (int r = 0; r < FWD_ROWS; ++r) { yi[r] = yl0 + r; yf[r] = (float)(yl0 + r); }
+        for (int r = 0; r < FWD_ROWS; ++r) yi[r] = yl0 + r;
+        const float yf0 = (float)yl0;
 
         for (int k = 0;; ++k) {
             const int s = k % FWD_STAGES;
-            mbar_wait(&sm.full_bar[s], (uint32_t)((k / FWD_STAGES) & 1));
-            const int n = sm.count[s];
-            if (n == 0) break;
+            mbar_wait(&sm.ready_bar[s], (uint32_t)((k / FWD_STAGES) & 1));
+            const int nk = sm.kept[s];
+            if (nk < 0) break;
             float2 acc[NACC];
 #pragma unroll
             for (int a = 0; a < NACC; ++a) acc[a] = make_float2(0.f, 0.f);
             const float4* sr = &sm.rec[s][0];
-            if (fy0 <= fy1) {
-                for (int g = warp; g < n; g += FWD_CWARPS) {
-                    const float4 r2 = sr[3 * g + 2];
-                    const unsigned xs = __float_as_uint(r2.z), ys = __float_as_uint(r2.w);
-                    const int x0 = (int)(xs & 0xffffu), x1 = (int)(xs >> 16);
-                    const int y0 = (int)(ys & 0xffffu), y1 = (int)(ys >> 16);
-                    if (x1 < fx0 || x0 > fx1 || y1 < fy0 || y0 > fy1) continue;   // warp-uniform
-                    const float4 r0 = sr[3 * g], r1 = sr[3 * g + 1];
-                    if (x0 <= fx0 && x1 >= fx1)
-                        fwd_gauss<true>(r0, r1, r2, yf, yi, xl0f, xl0, invs, x0, x1, acc);
-                    else
-                        fwd_gauss<false>(r0, r1, r2, yf, yi, xl0f, xl0, invs, x0, x1, acc);
-                }
+            const uint8_t* ix = &sm.idx[s][0];
+            for (int i = warp; i < nk; i += FWD_CWARPS) {
+                const int e = ix[i];
+                const int g = e & 0x7f;
+                const float4 r0 = sr[3 * g], r1 = sr[3 * g + 1], r2 = sr[3 * g + 2];
+                if (e & 0x80)
+                    fwd_gauss<true>(r0, r1, r2, xj, yf0, yi, xl0, invs, acc);
+                else
+                    fwd_gauss<false>(r0, r1, r2, xj, yf0, yi, xl0, invs, acc);
             }
-            // fold the chunk partials into the per-thread totals (second accumulation level)
+            // fold the chunk partials into the per-warp totals (second accumulation level)
 #pragma unroll
             for (int a = 0; a < NACC; ++a)
                 sm.tot[warp][a][lane] = __fadd2_rn(sm.tot[warp][a][lane], acc[a]);
