@@ -79,6 +79,7 @@ __device__ __forceinline__ void row2_pairs(int c_begin, int c_end, const float4*
                                            RowAcc& A0, RowAcc& A1) {
     float2 kx = make_float2(kT + (float)c_begin, kT + (float)(c_begin + 1));
     const float2 two = f2(2.0f);
+#pragma unroll 2
     for (int c = c_begin; c < c_end; c += 2) {
         const int cp = c >> 1;
         bool in0 = true, in1 = true;

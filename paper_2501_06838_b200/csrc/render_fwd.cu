@@ -98,9 +98,10 @@ __device__ __forceinline__ void fwd_gauss(const float4 r0, const float4 r1, cons
     const int y0 = (int)(ys & 0xffffu), y1 = (int)(ys >> 16);
     const float2 D2 = f2(r0.w);
     const float2 nax = f2(r0.x);
+    // kx = x - ax for the lane's 8 columns: exact small integers (one FADD2 per column pair)
     float2 kx[FWD_STRIP / 2];
 #pragma unroll
-    for (int jp = 0; jp < FWD_STRIP / 2; ++jp) kx[jp] = __fadd2_rn(xj[jp], nax);   // x - ax
+    for (int jp = 0; jp < FWD_STRIP / 2; ++jp) kx[jp] = __fadd2_rn(xj[jp], nax);
     bool cin[FWD_STRIP];
     if (!FULL) {
         const unsigned xs = __float_as_uint(r2.z);
@@ -200,46 +201,60 @@ __global__ void __launch_bounds__(FWD_THREADS) k_render_fwd(const ImgTable tab,
             for (int k = 0; k < FWD_STAGES && !ended; ++k) ended = issue(k) == 0;
         ended = __shfl_sync(0xffffffffu, ended, 0);
         const unsigned lt = (1u << lane) - 1u;
-        for (int k = 0;; ++k) {
-            const int s = k % FWD_STAGES;
-            mbar_wait(&sm.full_bar[s], (uint32_t)((k / FWD_STAGES) & 1));
-            const int n = sm.count[s];
-            if (n == 0) {
-                if (lane == 0) sm.kept[s] = -1;
-                mbar_arrive(&sm.ready_bar[s]);
-                break;
-            }
-            int base = 0;
-            float4* sr = &sm.rec[s][0];
-            for (int g0 = 0; g0 < n; g0 += 32) {
-                const int g = g0 + lane;
-                bool keep = false, full = false;
-                if (g < n) {
-                    const float4 r2 = sr[3 * g + 2];
-                    const unsigned xs = __float_as_uint(r2.z), ys = __float_as_uint(r2.w);
-                    const int x0 = (int)(xs & 0xffffu), x1 = (int)(xs >> 16);
-                    const int y0 = (int)(ys & 0xffffu), y1 = (int)(ys >> 16);
-                    keep = fy0 <= fy1 && !(x1 < fx0 || x0 > fx1 || y1 < fy0 || y0 > fy1);
-                    full = x0 <= fx0 && x1 >= fx1;
-                    if (keep) {
-                        const float4 r0 = sr[3 * g], r1 = sr[3 * g + 1];
-                        sr[3 * g] = make_float4(-r0.x, r0.y, r0.w, r1.x * invs);
-                        sr[3 * g + 1] = make_float4(-r1.x * r0.z, r1.y, r1.z, r1.w);
-                    }
+        // Two independent jobs, polled without blocking one on the other: filter chunk kf as soon
+        // as its bytes land, refill the stage of chunk kr once the consumers released it. When
+        // neither is ready the warp sleeps (it shares an SM sub-partition with consumer warps).
+        int kf = 0, kr = 0;
+        bool done = false;
+        while (!done) {
+            bool worked = false;
+            const int sf = kf % FWD_STAGES;
+            if (kf < kr + FWD_STAGES && mbar_test(&sm.full_bar[sf], (uint32_t)((kf / FWD_STAGES) & 1))) {
+                worked = true;
+                const int n = sm.count[sf];
+                if (n == 0) {
+                    if (lane == 0) sm.kept[sf] = -1;
+                    mbar_arrive(&sm.ready_bar[sf]);
+                    done = true;
+                    break;
                 }
-                const unsigned m = __ballot_sync(0xffffffffu, keep);
-                if (keep) sm.idx[s][base + __popc(m & lt)] = (uint8_t)(g | (full ? 0x80 : 0));
-                base += __popc(m);
+                int base = 0;
+                float4* sr = &sm.rec[sf][0];
+                for (int g0 = 0; g0 < n; g0 += 32) {
+                    const int g = g0 + lane;
+                    bool keep = false, full = false;
+                    if (g < n) {
+                        const float4 r2 = sr[3 * g + 2];
+                        const unsigned xs = __float_as_uint(r2.z), ys = __float_as_uint(r2.w);
+                        const int x0 = (int)(xs & 0xffffu), x1 = (int)(xs >> 16);
+                        const int y0 = (int)(ys & 0xffffu), y1 = (int)(ys >> 16);
+                        keep = fy0 <= fy1 && !(x1 < fx0 || x0 > fx1 || y1 < fy0 || y0 > fy1);
+                        full = x0 <= fx0 && x1 >= fx1;
+                        if (keep) {
+                            const float4 r0 = sr[3 * g], r1 = sr[3 * g + 1];
+                            sr[3 * g] = make_float4(-r0.x, r0.y, r0.w, r1.x * invs);
+                            sr[3 * g + 1] = make_float4(-r1.x * r0.z, r1.y, r1.z, r1.w);
+                        }
+                    }
+                    const unsigned m = __ballot_sync(0xffffffffu, keep);
+                    if (keep) sm.idx[sf][base + __popc(m & lt)] = (uint8_t)(g | (full ? 0x80 : 0));
+                    base += __popc(m);
+                }
+                if (lane == 0) sm.kept[sf] = base;
+                mbar_arrive(&sm.ready_bar[sf]);    // each lane releases its own smem writes
+                ++kf;
             }
-            if (lane == 0) sm.kept[s] = base;
-            mbar_arrive(&sm.ready_bar[s]);         // each lane releases its own smem writes
-            // refill the previous stage once the consumers are done with it
-            if (k >= 1 && !ended) {
-                const int kp = k - 1, sp = kp % FWD_STAGES;
-                mbar_wait(&sm.empty_bar[sp], (uint32_t)((kp / FWD_STAGES) & 1));
-                if (lane == 0) ended = issue(kp + FWD_STAGES) == 0;
-                ended = __shfl_sync(0xffffffffu, ended, 0);
+            // refill: chunk kr's stage gets chunk kr + FWD_STAGES once consumers are done with kr
+            if (!ended && kr < kf) {
+                const int sr_ = kr % FWD_STAGES;
+                if (mbar_test(&sm.empty_bar[sr_], (uint32_t)((kr / FWD_STAGES) & 1))) {
+                    worked = true;
+                    if (lane == 0) ended = issue(kr + FWD_STAGES) == 0;
+                    ended = __shfl_sync(0xffffffffu, ended, 0);
+                    ++kr;
+                }
             }
+            if (!worked) __nanosleep(256);
         }
     } else {
         // ---------------- consumer warps ------------------------------------------------------
