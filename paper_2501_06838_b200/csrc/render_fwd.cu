@@ -10,8 +10,9 @@
 // g = w, w + 4, w + 8, ... of each staged chunk: the warps' loads are identical by construction
 // (a vertical split of the tile would give each warp a different, order-dependent share of every
 // chunk and serialise the ring). The 4 partial images are summed in warp order at the end.
-//   * per Gaussian, warp-uniform: skip if its rect misses the tile; "full" if it covers all
-//     32 columns (no per-pixel x mask), otherwise masked.
+//   * per Gaussian, warp-uniform: the producer drops it if its rect misses the tile and flags
+//     it "full" if the rect covers all 32 columns and 16 rows (no x mask, no y test);
+//     otherwise the masked path.
 //   * per lane: kx = x - ax (exact small integers, one FADD2 per column pair, shared by the two
 //     rows), per row w = (a1/s) kx + (b1 dy - a1 dl_x) (one FFMA2 per pixel pair), q = -w^2 - v^2
 //     (one FFMA2; the y test folds into -v^2 -> -inf), 2^q on the SFU (ex2.approx.ftz ->
@@ -79,7 +80,7 @@ constexpr int NCONS = FWD_CWARPS * 32;                  // consumer threads (128
 struct FwdSmem {
     float4 rec[FWD_STAGES][FWD_CHUNK * 3];
     float2 tot[FWD_CWARPS][NACC][32];        // per-warp totals (second accumulation level)
-    uint8_t idx[FWD_STAGES][FWD_CHUNK];      // kept records of a chunk: index | (full-x << 7)
+    uint16_t idx[FWD_STAGES][FWD_CHUNK];     // kept records: index | full-x << 8 | full-y << 9
     uint64_t full_bar[FWD_STAGES];           // TMA bytes landed
     uint64_t ready_bar[FWD_STAGES];          // producer warp filtered + transformed the chunk
     uint64_t empty_bar[FWD_STAGES];          // consumer warps done with the stage
@@ -94,8 +95,6 @@ __device__ __forceinline__ void fwd_gauss(const float4 r0, const float4 r1, cons
                                           const float2 (&xj)[FWD_STRIP / 2], float yf0,
                                           const int (&yi)[FWD_ROWS], int xl0, float invs,
                                           float2 (&acc)[NACC]) {
-    const unsigned ys = __float_as_uint(r2.w);
-    const int y0 = (int)(ys & 0xffffu), y1 = (int)(ys >> 16);
     const float2 D2 = f2(r0.w);
     const float2 nax = f2(r0.x);
     // kx = x - ax for the lane's 8 columns: exact small integers (one FADD2 per column pair)
@@ -115,7 +114,12 @@ __device__ __forceinline__ void fwd_gauss(const float4 r0, const float4 r1, cons
     for (int r = 0; r < FWD_ROWS; ++r) {
         if (r > 0) dy += invs;                               // consecutive rows: exact to 1 ulp(1/s)
         const float v = r1.z * dy;                           // c1 dy
-        const float u = (yi[r] >= y0 && yi[r] <= y1) ? -(v * v) : -INFINITY;
+        float u = -(v * v);
+        if (!FULL) {                                         // lane's row outside [y0, y1]
+            const unsigned ys = __float_as_uint(r2.w);
+            const int y0 = (int)(ys & 0xffffu), y1 = (int)(ys >> 16);
+            u = (yi[r] >= y0 && yi[r] <= y1) ? u : -INFINITY;
+        }
         const float tau = fmaf(r1.y, dy, r1.x);              // b1 dy - a1 dl_x
         const float2 T2 = f2(tau), U2 = f2(u);
 #pragma unroll
@@ -237,7 +241,7 @@ __global__ void __launch_bounds__(FWD_THREADS) k_render_fwd(const ImgTable tab,
                         }
                     }
                     const unsigned m = __ballot_sync(0xffffffffu, keep);
-                    if (keep) sm.idx[sf][base + __popc(m & lt)] = (uint8_t)(g | (full ? 0x80 : 0));
+                    if (keep) sm.idx[sf][base + __popc(m & lt)] = (uint16_t)(g | (full ? 0x100 : 0));
                     base += __popc(m);
                 }
                 if (lane == 0) sm.kept[sf] = base;
@@ -278,12 +282,12 @@ __global__ void __launch_bounds__(FWD_THREADS) k_render_fwd(const ImgTable tab,
 #pragma unroll
             for (int a = 0; a < NACC; ++a) acc[a] = make_float2(0.f, 0.f);
             const float4* sr = &sm.rec[s][0];
-            const uint8_t* ix = &sm.idx[s][0];
+            const uint16_t* ix = &sm.idx[s][0];
             for (int i = warp; i < nk; i += FWD_CWARPS) {
                 const int e = ix[i];
-                const int g = e & 0x7f;
+                const int g = e & 0xff;
                 const float4 r0 = sr[3 * g], r1 = sr[3 * g + 1], r2 = sr[3 * g + 2];
-                if (e & 0x80)
+                if (e & 0x100)
                     fwd_gauss<true>(r0, r1, r2, xj, yf0, yi, xl0, invs, acc);
                 else
                     fwd_gauss<false>(r0, r1, r2, xj, yf0, yi, xl0, invs, acc);

@@ -79,6 +79,31 @@ __global__ void k_ffma2(float* out, long long* cyc, float seed) {
   if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
 }
 
+// FFMA2 with three distinct register pairs per instruction (no operand reuse between
+// consecutive instructions): exposes register-file bank limits on the paired FMA path
+__global__ void k_ffma2_norreuse(float* out, long long* cyc, float seed) {
+  float2 a[8], x[8], y[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    a[j] = make_float2(threadIdx.x + j, j);
+    x[j] = make_float2(0.999f + j * 1e-4f + seed * 1e-9f + threadIdx.x * 1e-10f, 0.998f - j * 1e-4f);
+    y[j] = make_float2(1e-3f * j + threadIdx.x * 1e-10f, 2e-3f * j + seed * 1e-9f);
+  }
+  __syncthreads();
+  long long t0 = clock64();
+  for (int it = 0; it < ITERS; ++it) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) a[j] = __ffma2_rn(x[j], a[j], y[(j + 3) & 7]);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) a[j] = __ffma2_rn(y[j], a[j], x[(j + 5) & 7]);
+  }
+  __syncthreads();
+  long long t1 = clock64();
+  float s = 0; for (int j = 0; j < 8; ++j) s += a[j].x + a[j].y;
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+  if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+}
+
 // forward-like mix per element: 2 FFMA (q), 1 MUFU, 3 FFMA (rgb accumulate)
 __global__ void k_mix(float* out, long long* cyc, float seed) {
   float d[8], ar[8], ag[8], ab[8];
@@ -162,6 +187,7 @@ int main() {
     run("ex2", k_ex2_pure, 1.0, 256, bps);
     run("ffma", k_ffma, 2.0, 256, bps);          // FFMA lanes per clk
     run("ffma2", k_ffma2, 4.0, 256, bps);        // FP32 FMA lanes per clk (2 per FFMA2)
+    run("ffma2_nr", k_ffma2_norreuse, 4.0, 256, bps);
     run("fwdmix", k_mix, 1.0, 256, bps);         // elements (pairs) per clk
   }
   return 0;

@@ -77,7 +77,10 @@ def main():
         for r in csv.DictReader(io.StringIO("".join(lines))):
             if r.get("Metric Name") != "gpu__time_duration.sum":
                 continue
-            name = r["Kernel Name"].split("(")[0].split("<")[0].replace("void ", "")
+            name = r["Kernel Name"].replace("void ", "").split("(")[0]
+            name = name.replace("(anonymous namespace)", "").replace("<unnamed>", "")
+            base = name.split("<")[0]
+            name = base.split("::")[-1] + (("<" + name.split("<", 1)[1]) if "<" in name else "")
             v = float(r["Metric Value"].replace(",", ""))
             unit = r.get("Metric Unit", "ns")
             ns = v * {"ns": 1, "us": 1e3, "usecond": 1e3, "ms": 1e6, "msecond": 1e6,

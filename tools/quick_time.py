@@ -33,7 +33,7 @@ def run(name, nimg_override=None, iters=3):
     tf, tb = min(tf), min(tb)
     peak = 16 * 148 * 1.965e9
     print(f"{name} imgs={len(imgs)} P={P:.3e} fwd {tf:.3f} ms ({P/tf/1e9:.3f} Tpair/s, {P/tf*1e3/peak:.1%} of SFU) "
-          f"bwd {tb:.3f} ms ({P/tb/1e9:.3f} Tpair/s, {P/tb*1e3/(128/14*148*1.965e9):.1%} of FP32)", flush=True)
+          f"bwd {tb:.3f} ms ({P/tb/1e9:.3f} Tpair/s, {P/tb*1e3/(128/12.5*148*1.965e9):.1%} of FP32)", flush=True)
 
 
 if __name__ == "__main__":
