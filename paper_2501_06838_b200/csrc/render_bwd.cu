@@ -55,15 +55,19 @@ __device__ __forceinline__ void pix_pair(const float4 ga, const float2 gb, const
     }
     const float2 e = make_float2(ex2_approx(q.x), ex2_approx(q.y));
     const float2 gr = make_float2(ga.x, ga.y), gg = make_float2(ga.z, ga.w);
-    A.FR = __ffma2_rn(e, gr, A.FR);
-    A.FG = __ffma2_rn(e, gg, A.FG);
-    A.FB = __ffma2_rn(e, gb, A.FB);
+    // g . c' first (scalar-broadcast operands), then the accumulations grouped by their shared
+    // operand (e for the three channel sums, g.c' for the two moments) so that consecutive FFMA2s
+    // can hit the operand reuse cache: an FFMA2 that reads three fresh register pairs costs 3
+    // issue cycles instead of 2 (register-file bandwidth; tools/microbench.cu "ffma2_nr").
     float2 gc = __fmul2_rn(gr, L.cr);
     gc = __ffma2_rn(gg, L.cg, gc);
     gc = __ffma2_rn(gb, L.cb, gc);
     const float2 ed = __fmul2_rn(e, w);                              // e wq
-    A.W1 = __ffma2_rn(gc, ed, A.W1);
     const float2 edd = __fmul2_rn(ed, w);                            // e wq^2
+    A.FR = __ffma2_rn(e, gr, A.FR);
+    A.FG = __ffma2_rn(e, gg, A.FG);
+    A.FB = __ffma2_rn(e, gb, A.FB);
+    A.W1 = __ffma2_rn(gc, ed, A.W1);
     A.W2 = __ffma2_rn(gc, edd, A.W2);
 }
 

@@ -233,7 +233,8 @@ __global__ void __launch_bounds__(FWD_THREADS) k_render_fwd(const ImgTable tab,
                         const int x0 = (int)(xs & 0xffffu), x1 = (int)(xs >> 16);
                         const int y0 = (int)(ys & 0xffffu), y1 = (int)(ys >> 16);
                         keep = fy0 <= fy1 && !(x1 < fx0 || x0 > fx1 || y1 < fy0 || y0 > fy1);
-                        full = x0 <= fx0 && x1 >= fx1;
+                        // "full": the rect covers every column and every lane row of the tile
+                        full = x0 <= fx0 && x1 >= fx1 && y0 <= fy0 && y1 >= fy0 + FTILE_H - 1;
                         if (keep) {
                             const float4 r0 = sr[3 * g], r1 = sr[3 * g + 1];
                             sr[3 * g] = make_float4(-r0.x, r0.y, r0.w, r1.x * invs);
