@@ -14,7 +14,7 @@ namespace gsr {
 
 // ---- compile-time geometry -------------------------------------------------------------
 constexpr int CELL = 16;       // cell edge (HR px): binning granularity (sort key)
-constexpr int TILE_W = 32;     // backward render tile (HR px); also the debug tile-list tile
+constexpr int TILE_W = 64;     // backward render tile (HR px); also the debug tile-list tile
 constexpr int TILE_H = 32;
 // forward: a CTA renders a 32 x 16 tile; each of the 4 consumer warps covers the whole tile
 // (a lane owns 2 rows x 8 columns) and takes every 4th Gaussian of each staged chunk, so the
