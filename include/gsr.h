@@ -141,6 +141,27 @@ gsr_status gsr_finalize_grads(const float* alpha, const float* mu, const float* 
                               const double* moments, float* d_alpha, float* d_mu, float* d_sigma,
                               float* d_rho, float* d_color, void* stream);
 
+/* Variants of the two backward entry points with flags.
+ * GSR_REUSE_BINNING: the workspace still holds the binning (sorted keys, permutation, cell
+ * starts, records) computed by the immediately preceding call on the SAME parameter arrays,
+ * images and ratio (typically this step's forward), enqueued on the same stream; the binning
+ * stage (K1, radix sort, K1b) is skipped. Results are undefined if that precondition is false. */
+#define GSR_REUSE_BINNING 0x1u
+gsr_status gsr_render_bwd_batched_ex(const float* alpha, const float* mu, const float* sigma,
+                                     const float* rho, const float* color, int64_t n_total,
+                                     const gsr_image* imgs, int32_t n_imgs, double ratio,
+                                     const float* grad_out, float* d_alpha, float* d_mu,
+                                     float* d_sigma, float* d_rho, float* d_color,
+                                     void* workspace, size_t workspace_bytes, uint32_t flags,
+                                     void* stream);
+gsr_status gsr_render_bwd_moments_batched_ex(const float* alpha, const float* mu,
+                                             const float* sigma, const float* rho,
+                                             const float* color, int64_t n_total,
+                                             const gsr_image* imgs, int32_t n_imgs, double ratio,
+                                             const float* grad_out, double* moments,
+                                             void* workspace, size_t workspace_bytes,
+                                             uint32_t flags, void* stream);
+
 /* Number of (Gaussian, pixel) pairs inside the windows, P = sum_i |rect_i| restricted to each
  * image's row band (the work unit of the roofline). Writes one int64 to *d_pairs
  * (device pointer). Uses the workspace. */

@@ -424,6 +424,16 @@ cudaError_t bin_gaussians(const float* alpha, const float* mu, const float* sigm
     return cudaGetLastError();
 }
 
+void binned_pointers(const ImgTable& tab, long long n, const Workspace& ws, int** perm,
+                     uint32_t** keys_sorted) {
+    if (n <= 0) { *perm = ws.vals_a; *keys_sorted = ws.keys_a; return; }
+    int bits = 32 - __builtin_clz((unsigned)tab.total_cells | 1u);
+    int passes = (bits + 7) / 8;
+    bool odd = passes & 1;
+    *perm = odd ? ws.vals_b : ws.vals_a;
+    *keys_sorted = odd ? ws.keys_b : ws.keys_a;
+}
+
 cudaError_t launch_pair_count(const float* alpha, const float* mu, const float* sigma,
                               const float* rho, const float* color, long long n,
                               const ImgTable& tab, long long* d_pairs, cudaStream_t st) {

@@ -159,7 +159,10 @@ gsr_status prepare(const float* alpha, const float* mu, const float* sigma, cons
     if (!params_ok(alpha, mu, sigma, rho, color, n_total)) return GSR_EINVAL;
     if (!workspace || workspace_bytes < ws_bytes(P->tab, n_total)) return GSR_EWORKSPACE;
     carve_workspace(workspace, n_total, P->tab.total_cells, P->tab.total_tiles, &P->ws);
-    if (!bin) return GSR_OK;
+    if (!bin) {
+        binned_pointers(P->tab, n_total, P->ws, &P->perm, &P->keys);
+        return GSR_OK;
+    }
     int h = prof_begin(0, st);
     cudaError_t e = bin_gaussians(alpha, mu, sigma, rho, color, n_total, P->tab, P->ws, &P->perm,
                                   &P->keys, st);
@@ -255,18 +258,31 @@ gsr_status gsr_render_fwd(const float* alpha, const float* mu, const float* sigm
                                   workspace_bytes, stream);
 }
 
+gsr_status gsr_render_bwd_moments_batched_ex(const float* alpha, const float* mu,
+                                             const float* sigma, const float* rho,
+                                             const float* color, int64_t n_total,
+                                             const gsr_image* imgs, int32_t n_imgs, double ratio,
+                                             const float* grad_out, double* moments,
+                                             void* workspace, size_t workspace_bytes,
+                                             uint32_t flags, void* stream) {
+    if (!grad_out || (!moments && n_total > 0)) return GSR_EINVAL;
+    if (flags & ~GSR_REUSE_BINNING) return GSR_EINVAL;
+    cudaStream_t st = (cudaStream_t)stream;
+    Prepared P;
+    gsr_status s = prepare(alpha, mu, sigma, rho, color, n_total, imgs, n_imgs, ratio, workspace,
+                           workspace_bytes, st, &P, !(flags & GSR_REUSE_BINNING));
+    if (s != GSR_OK) return s;
+    return finish(launch_render_bwd_moments(P.tab, P.ws, P.perm, grad_out, moments, st));
+}
+
 gsr_status gsr_render_bwd_moments_batched(const float* alpha, const float* mu, const float* sigma,
                                           const float* rho, const float* color, int64_t n_total,
                                           const gsr_image* imgs, int32_t n_imgs, double ratio,
                                           const float* grad_out, double* moments, void* workspace,
                                           size_t workspace_bytes, void* stream) {
-    if (!grad_out || (!moments && n_total > 0)) return GSR_EINVAL;
-    cudaStream_t st = (cudaStream_t)stream;
-    Prepared P;
-    gsr_status s = prepare(alpha, mu, sigma, rho, color, n_total, imgs, n_imgs, ratio, workspace,
-                           workspace_bytes, st, &P, true);
-    if (s != GSR_OK) return s;
-    return finish(launch_render_bwd_moments(P.tab, P.ws, P.perm, grad_out, moments, st));
+    return gsr_render_bwd_moments_batched_ex(alpha, mu, sigma, rho, color, n_total, imgs, n_imgs,
+                                             ratio, grad_out, moments, workspace,
+                                             workspace_bytes, 0u, stream);
 }
 
 gsr_status gsr_finalize_grads(const float* alpha, const float* mu, const float* sigma,
@@ -281,18 +297,20 @@ gsr_status gsr_finalize_grads(const float* alpha, const float* mu, const float* 
                                   d_sigma, d_rho, d_color, (cudaStream_t)stream));
 }
 
-gsr_status gsr_render_bwd_batched(const float* alpha, const float* mu, const float* sigma,
-                                  const float* rho, const float* color, int64_t n_total,
-                                  const gsr_image* imgs, int32_t n_imgs, double ratio,
-                                  const float* grad_out, float* d_alpha, float* d_mu,
-                                  float* d_sigma, float* d_rho, float* d_color, void* workspace,
-                                  size_t workspace_bytes, void* stream) {
+gsr_status gsr_render_bwd_batched_ex(const float* alpha, const float* mu, const float* sigma,
+                                     const float* rho, const float* color, int64_t n_total,
+                                     const gsr_image* imgs, int32_t n_imgs, double ratio,
+                                     const float* grad_out, float* d_alpha, float* d_mu,
+                                     float* d_sigma, float* d_rho, float* d_color,
+                                     void* workspace, size_t workspace_bytes, uint32_t flags,
+                                     void* stream) {
     if (!grad_out) return GSR_EINVAL;
+    if (flags & ~GSR_REUSE_BINNING) return GSR_EINVAL;
     if (n_total > 0 && (!d_alpha || !d_mu || !d_sigma || !d_rho || !d_color)) return GSR_EINVAL;
     cudaStream_t st = (cudaStream_t)stream;
     Prepared P;
     gsr_status s = prepare(alpha, mu, sigma, rho, color, n_total, imgs, n_imgs, ratio, workspace,
-                           workspace_bytes, st, &P, true);
+                           workspace_bytes, st, &P, !(flags & GSR_REUSE_BINNING));
     if (s != GSR_OK) return s;
     if (n_total == 0) return GSR_OK;
     cudaMemsetAsync(P.ws.moments, 0, sizeof(double) * 8 * (size_t)n_total, st);
@@ -300,6 +318,17 @@ gsr_status gsr_render_bwd_batched(const float* alpha, const float* mu, const flo
     if (e != cudaSuccess) return GSR_ECUDA;
     return finish(launch_finalize(alpha, mu, sigma, rho, color, n_total, P.ws.moments, d_alpha,
                                   d_mu, d_sigma, d_rho, d_color, st));
+}
+
+gsr_status gsr_render_bwd_batched(const float* alpha, const float* mu, const float* sigma,
+                                  const float* rho, const float* color, int64_t n_total,
+                                  const gsr_image* imgs, int32_t n_imgs, double ratio,
+                                  const float* grad_out, float* d_alpha, float* d_mu,
+                                  float* d_sigma, float* d_rho, float* d_color, void* workspace,
+                                  size_t workspace_bytes, void* stream) {
+    return gsr_render_bwd_batched_ex(alpha, mu, sigma, rho, color, n_total, imgs, n_imgs, ratio,
+                                     grad_out, d_alpha, d_mu, d_sigma, d_rho, d_color, workspace,
+                                     workspace_bytes, 0u, stream);
 }
 
 gsr_status gsr_render_bwd(const float* alpha, const float* mu, const float* sigma,

@@ -243,6 +243,9 @@ cudaError_t bin_gaussians(const float* alpha, const float* mu, const float* sigm
                           const float* rho, const float* color, long long n,
                           const ImgTable& tab, Workspace& ws, int** perm_out,
                           uint32_t** keys_sorted_out, cudaStream_t st);
+// Where a previous bin_gaussians() on the same table left perm / sorted keys in the workspace.
+void binned_pointers(const ImgTable& tab, long long n, const Workspace& ws, int** perm,
+                     uint32_t** keys_sorted);
 cudaError_t launch_pair_count(const float* alpha, const float* mu, const float* sigma,
                               const float* rho, const float* color, long long n,
                               const ImgTable& tab, long long* d_pairs, cudaStream_t st);

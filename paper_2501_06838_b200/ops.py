@@ -139,8 +139,28 @@ def _ws_bytes(arr, n_imgs, n_total, ratio) -> int:
     return b
 
 
+def single_chunk(lay: Layout) -> bool:
+    return len(lay.images) <= _lib.MAX_IMAGES
+
+
+def workspace_for(alpha, lay: Layout, ratio: float = 0.1) -> torch.Tensor:
+    """A private workspace for a single-chunk layout (lets a backward reuse the forward's
+    binning: GSR_REUSE_BINNING)."""
+    g0, g1, o0, arr, m = next(_chunks(lay))
+    return torch.empty(_ws_bytes(arr, m, g1 - g0, ratio), dtype=torch.uint8, device=alpha.device)
+
+
+def _ws_for(dev, nb, workspace):
+    if workspace is not None:
+        if workspace.numel() < nb:
+            raise ValueError("workspace too small")
+        return workspace
+    return _workspace(dev, nb)
+
+
 def render_fwd_batched(alpha, mu, sigma, rho, color, lay: Layout, ratio: float = 0.1,
-                       out: Optional[torch.Tensor] = None) -> torch.Tensor:
+                       out: Optional[torch.Tensor] = None,
+                       workspace: Optional[torch.Tensor] = None) -> torch.Tensor:
     """Forward render of every image of `lay` into one flat float32 buffer (HWC blocks)."""
     (alpha, mu, sigma, rho, color), n = _params(alpha, mu, sigma, rho, color)
     dev = alpha.device
@@ -150,7 +170,7 @@ def render_fwd_batched(alpha, mu, sigma, rho, color, lay: Layout, ratio: float =
     st = _stream_ptr(dev)
     for g0, g1, o0, arr, m in _chunks(lay):
         nb = _ws_bytes(arr, m, g1 - g0, ratio)
-        ws = _workspace(dev, nb)
+        ws = _ws_for(dev, nb, workspace)
         check(lib.gsr_render_fwd_batched(_ptr(alpha, g0), _ptr(mu, 2 * g0), _ptr(sigma, 2 * g0),
                                          _ptr(rho, g0), _ptr(color, 3 * g0), g1 - g0, arr, m,
                                          float(ratio), _ptr(out, o0), ws.data_ptr(), ws.numel(),
@@ -159,8 +179,11 @@ def render_fwd_batched(alpha, mu, sigma, rho, color, lay: Layout, ratio: float =
 
 
 def render_bwd_moments_batched(alpha, mu, sigma, rho, color, lay: Layout, grad_out: torch.Tensor,
-                               moments: torch.Tensor, ratio: float = 0.1) -> torch.Tensor:
-    """Accumulate (+=) the backward moments [n, 8] (float64) of every image band of `lay`."""
+                               moments: torch.Tensor, ratio: float = 0.1,
+                               workspace: Optional[torch.Tensor] = None,
+                               reuse_binning: bool = False) -> torch.Tensor:
+    """Accumulate (+=) the backward moments [n, 8] (float64) of every image band of `lay`.
+    reuse_binning: `workspace` holds this layout's binning from the preceding forward."""
     (alpha, mu, sigma, rho, color), n = _params(alpha, mu, sigma, rho, color)
     dev = alpha.device
     grad_out = _check_param(grad_out, "grad_out")
@@ -168,14 +191,16 @@ def render_bwd_moments_batched(alpha, mu, sigma, rho, color, lay: Layout, grad_o
         raise ValueError("moments must be a contiguous float64 [n, 8] tensor")
     lib = _lib.load()
     st = _stream_ptr(dev)
+    flags = _lib.GSR_REUSE_BINNING if (reuse_binning and workspace is not None and
+                                       single_chunk(lay)) else 0
     for g0, g1, o0, arr, m in _chunks(lay):
         nb = _ws_bytes(arr, m, g1 - g0, ratio)
-        ws = _workspace(dev, nb)
-        check(lib.gsr_render_bwd_moments_batched(
+        ws = _ws_for(dev, nb, workspace)
+        check(lib.gsr_render_bwd_moments_batched_ex(
             _ptr(alpha, g0), _ptr(mu, 2 * g0), _ptr(sigma, 2 * g0), _ptr(rho, g0),
             _ptr(color, 3 * g0), g1 - g0, arr, m, float(ratio), _ptr(grad_out, o0),
-            _ptr(moments, 8 * g0), ws.data_ptr(), ws.numel(), st),
-            "gsr_render_bwd_moments_batched")
+            _ptr(moments, 8 * g0), ws.data_ptr(), ws.numel(), flags, st),
+            "gsr_render_bwd_moments_batched_ex")
     return moments
 
 
@@ -191,23 +216,27 @@ def finalize_grads(alpha, mu, sigma, rho, color, moments: torch.Tensor):
 
 
 def render_bwd_batched(alpha, mu, sigma, rho, color, lay: Layout, grad_out: torch.Tensor,
-                       ratio: float = 0.1):
-    """Gradients of sum(grad_out * I) wrt every parameter (float32, input layouts)."""
+                       ratio: float = 0.1, workspace: Optional[torch.Tensor] = None,
+                       reuse_binning: bool = False):
+    """Gradients of sum(grad_out * I) wrt every parameter (float32, input layouts).
+    reuse_binning: `workspace` holds this layout's binning from the preceding forward."""
     (alpha, mu, sigma, rho, color), n = _params(alpha, mu, sigma, rho, color)
     dev = alpha.device
     grad_out = _check_param(grad_out, "grad_out")
     grads = [torch.zeros_like(t) for t in (alpha, mu, sigma, rho, color)]
     lib = _lib.load()
     st = _stream_ptr(dev)
+    flags = _lib.GSR_REUSE_BINNING if (reuse_binning and workspace is not None and
+                                       single_chunk(lay)) else 0
     for g0, g1, o0, arr, m in _chunks(lay):
         nb = _ws_bytes(arr, m, g1 - g0, ratio)
-        ws = _workspace(dev, nb)
+        ws = _ws_for(dev, nb, workspace)
         ga, gm, gs, gr, gc = grads
-        check(lib.gsr_render_bwd_batched(
+        check(lib.gsr_render_bwd_batched_ex(
             _ptr(alpha, g0), _ptr(mu, 2 * g0), _ptr(sigma, 2 * g0), _ptr(rho, g0),
             _ptr(color, 3 * g0), g1 - g0, arr, m, float(ratio), _ptr(grad_out, o0),
             _ptr(ga, g0), _ptr(gm, 2 * g0), _ptr(gs, 2 * g0), _ptr(gr, g0), _ptr(gc, 3 * g0),
-            ws.data_ptr(), ws.numel(), st), "gsr_render_bwd_batched")
+            ws.data_ptr(), ws.numel(), flags, st), "gsr_render_bwd_batched_ex")
     return tuple(grads)
 
 
@@ -248,18 +277,24 @@ def render_bwd(alpha, mu, sigma, rho, color, H: int, W: int, scale: float,
 
 
 class _RenderFn(torch.autograd.Function):
+    """Forward keeps its private workspace so the backward reuses the forward's binning
+    (GSR_REUSE_BINNING) -- valid because autograd saves the very same parameter tensors."""
+
     @staticmethod
     def forward(ctx, alpha, mu, sigma, rho, color, lay, ratio):
         ctx.lay, ctx.ratio = lay, ratio
         ctx.save_for_backward(alpha, mu, sigma, rho, color)
+        ws = workspace_for(alpha, lay, ratio) if single_chunk(lay) else None
+        ctx.ws = ws
         return render_fwd_batched(alpha.detach(), mu.detach(), sigma.detach(), rho.detach(),
-                                  color.detach(), lay, ratio)
+                                  color.detach(), lay, ratio, workspace=ws)
 
     @staticmethod
     def backward(ctx, g):
         alpha, mu, sigma, rho, color = ctx.saved_tensors
         grads = render_bwd_batched(alpha, mu, sigma, rho, color, ctx.lay, g.contiguous(),
-                                   ctx.ratio)
+                                   ctx.ratio, workspace=ctx.ws, reuse_binning=ctx.ws is not None)
+        ctx.ws = None
         return (*grads, None, None)
 
 
