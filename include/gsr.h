@@ -162,6 +162,31 @@ gsr_status gsr_render_bwd_moments_batched_ex(const float* alpha, const float* mu
                                              void* workspace, size_t workspace_bytes,
                                              uint32_t flags, void* stream);
 
+/* ---- training-step adjacency ------------------------------------------
+ * One fused training step of the rasterizer for the paper's L1 objective, from the RAW
+ * outputs of the Gaussian Primary Head:
+ *   alpha = sigmoid(raw_alpha), c = sigmoid(raw_color), sigma = sigmoid(raw_sigma),
+ *   rho = rho_scale * tanh(raw_rho)  (paper: rho_scale = 1; SPEC's rho_eps: 1 - 1e-4),
+ *   mu = ref + offset               (reference position p + predicted offset o)
+ * then the forward render (as gsr_render_fwd_batched, written to `out`), the loss
+ *   *loss = inv_numel * sum |out - gt|   (float64 device scalar, overwritten; gt has out's layout)
+ * and the gradients of *loss with respect to every raw input (float32, input layouts,
+ * overwritten; d_offset is also dL/d mu). The L1 subgradient is sign(out - gt) (0 at ties).
+ * inv_numel <= 0 means 1 / (number of output elements of this call); pass the global value when
+ * the batch is sharded. All arrays are device pointers; workspace from
+ * gsr_train_workspace_bytes_batched. Errors as for the render entry points. */
+size_t gsr_train_workspace_bytes_batched(const gsr_image* imgs, int32_t n_imgs, int64_t n_total,
+                                         double ratio);
+gsr_status gsr_train_step_l1_batched(const float* raw_alpha, const float* offset, const float* ref,
+                                     const float* raw_sigma, const float* raw_rho,
+                                     const float* raw_color, int64_t n_total,
+                                     const gsr_image* imgs, int32_t n_imgs, double ratio,
+                                     float rho_scale, double inv_numel, const float* gt,
+                                     float* out, double* loss, float* d_raw_alpha,
+                                     float* d_offset, float* d_raw_sigma, float* d_raw_rho,
+                                     float* d_raw_color, void* workspace, size_t workspace_bytes,
+                                     void* stream);
+
 /* Number of (Gaussian, pixel) pairs inside the windows, P = sum_i |rect_i| restricted to each
  * image's row band (the work unit of the roofline). Writes one int64 to *d_pairs
  * (device pointer). Uses the workspace. */

@@ -21,7 +21,8 @@ EXPORTS = ["gsr_version", "gsr_out_dims", "gsr_workspace_bytes_batched", "gsr_wo
            "gsr_render_fwd", "gsr_render_bwd", "gsr_render_fwd_batched", "gsr_render_bwd_batched",
            "gsr_render_bwd_moments_batched", "gsr_finalize_grads", "gsr_pair_count_batched",
            "gsr_debug_rects", "gsr_debug_tile_lists", "gsr_tile_shape", "gsr_profile_enable",
-           "gsr_profile_collect", "gsr_render_bwd_batched_ex", "gsr_render_bwd_moments_batched_ex"]
+           "gsr_profile_collect", "gsr_render_bwd_batched_ex", "gsr_render_bwd_moments_batched_ex",
+           "gsr_train_workspace_bytes_batched", "gsr_train_step_l1_batched"]
 GSR_REUSE_BINNING = 0x1
 
 
@@ -75,6 +76,11 @@ def load(path: Path | str | None = None):
     lib.gsr_render_bwd_moments_batched_ex.argtypes = par + [_I64, _IMGP, _I32, _D, _P, _P, _P,
                                                             _SZ, ctypes.c_uint32, _P]
     lib.gsr_finalize_grads.argtypes = par + [_I64, _P, _P, _P, _P, _P, _P, _P]
+    lib.gsr_train_workspace_bytes_batched.argtypes = [_IMGP, _I32, _I64, _D]
+    lib.gsr_train_workspace_bytes_batched.restype = _SZ
+    lib.gsr_train_step_l1_batched.argtypes = [_P] * 6 + [_I64, _IMGP, _I32, _D, ctypes.c_float,
+                                                         _D, _P, _P, _P, _P, _P, _P, _P, _P, _P,
+                                                         _SZ, _P]
     lib.gsr_pair_count_batched.argtypes = par + [_I64, _IMGP, _I32, _D, _P, _P, _SZ, _P]
     lib.gsr_debug_rects.argtypes = par + [_I64, _I32, _I32, _D, _D, _P, _P]
     lib.gsr_debug_tile_lists.argtypes = par + [_I64, _I32, _I32, _D, _D, _P, _P, _P, _P, _SZ, _P]

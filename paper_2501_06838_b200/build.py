@@ -10,7 +10,7 @@ PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libgsr.so"
 ROOT = PKG.parent
-SOURCES = ["binning.cu", "render_fwd.cu", "render_bwd.cu", "gsr_abi.cu"]
+SOURCES = ["binning.cu", "render_fwd.cu", "render_bwd.cu", "train.cu", "gsr_abi.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xptxas", "-v",

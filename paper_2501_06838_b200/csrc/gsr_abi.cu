@@ -342,6 +342,77 @@ gsr_status gsr_render_bwd(const float* alpha, const float* mu, const float* sigm
                                   workspace_bytes, stream);
 }
 
+size_t gsr_train_workspace_bytes_batched(const gsr_image* imgs, int32_t n_imgs, int64_t n_total,
+                                         double ratio) {
+    size_t b = gsr_workspace_bytes_batched(imgs, n_imgs, n_total, ratio);
+    if (b == 0) return 0;
+    return b + (((size_t)n_total * 9 * sizeof(float) + 255) & ~(size_t)255) + 512;
+}
+
+gsr_status gsr_train_step_l1_batched(const float* raw_alpha, const float* offset, const float* ref,
+                                     const float* raw_sigma, const float* raw_rho,
+                                     const float* raw_color, int64_t n_total,
+                                     const gsr_image* imgs, int32_t n_imgs, double ratio,
+                                     float rho_scale, double inv_numel, const float* gt,
+                                     float* out, double* loss, float* d_raw_alpha,
+                                     float* d_offset, float* d_raw_sigma, float* d_raw_rho,
+                                     float* d_raw_color, void* workspace, size_t workspace_bytes,
+                                     void* stream) {
+    if (!gt || !out || !loss) return GSR_EINVAL;
+    if (!std::isfinite(rho_scale) || !(rho_scale > 0.f) || rho_scale > 1.f) return GSR_EINVAL;
+    if (!std::isfinite(inv_numel)) return GSR_EINVAL;
+    if (n_total > 0 && (!raw_alpha || !offset || !ref || !raw_sigma || !raw_rho || !raw_color ||
+                        !d_raw_alpha || !d_offset || !d_raw_sigma || !d_raw_rho || !d_raw_color))
+        return GSR_EINVAL;
+    cudaStream_t st = (cudaStream_t)stream;
+    ImgTable tab;
+    gsr_status s = build_table(imgs, n_imgs, n_total, ratio, &tab);
+    if (s != GSR_OK) return s;
+    const size_t act_bytes = (((size_t)n_total * 9 * sizeof(float) + 255) & ~(size_t)255);
+    if (!workspace || workspace_bytes < gsr_train_workspace_bytes_batched(imgs, n_imgs, n_total,
+                                                                          ratio))
+        return GSR_EWORKSPACE;
+    char* base = (char*)(((uintptr_t)workspace + 255) & ~uintptr_t(255));
+    double* loss_acc = (double*)base;                    // 256 B slot
+    float* act = (float*)(base + 256);
+    float* a_alpha = act;
+    float* a_mu = act + n_total;
+    float* a_sigma = act + 3 * n_total;
+    float* a_rho = act + 5 * n_total;
+    float* a_color = act + 6 * n_total;
+    void* rws = base + 256 + act_bytes;
+    size_t rws_bytes = workspace_bytes - (size_t)((char*)rws - (char*)workspace);
+    long long numel = 0;
+    for (int k = 0; k < tab.n_imgs; ++k)
+        numel += (long long)(tab.img[k].row_end - tab.img[k].row_begin) * tab.img[k].Ws * 3;
+    const double inv = inv_numel > 0.0 ? inv_numel : (numel > 0 ? 1.0 / (double)numel : 0.0);
+
+    cudaError_t e = launch_activate(raw_alpha, offset, ref, raw_sigma, raw_rho, raw_color,
+                                    n_total, rho_scale, a_alpha, a_mu, a_sigma, a_rho, a_color, st);
+    if (e != cudaSuccess) return GSR_ECUDA;
+    Prepared P;
+    s = prepare(a_alpha, a_mu, a_sigma, a_rho, a_color, n_total, imgs, n_imgs, ratio, rws,
+                rws_bytes, st, &P, true);
+    if (s != GSR_OK) return s;
+    cudaMemsetAsync(loss_acc, 0, sizeof(double), st);
+    e = launch_render_fwd(P.tab, P.ws, out, st, gt, loss_acc);
+    if (e != cudaSuccess) return GSR_ECUDA;
+    if (n_total > 0) {
+        cudaMemsetAsync(P.ws.moments, 0, sizeof(double) * 8 * (size_t)n_total, st);
+        e = launch_render_bwd_moments(P.tab, P.ws, P.perm, nullptr, P.ws.moments, st, out, gt,
+                                      (float)inv);
+        if (e != cudaSuccess) return GSR_ECUDA;
+        RawParams raw{raw_alpha, raw_sigma, raw_rho, raw_color, rho_scale};
+        e = launch_finalize(a_alpha, a_mu, a_sigma, a_rho, a_color, n_total, P.ws.moments,
+                            d_raw_alpha, d_offset, d_raw_sigma, d_raw_rho, d_raw_color, st, &raw);
+        if (e != cudaSuccess) return GSR_ECUDA;
+    }
+    e = launch_scale_loss(loss_acc, inv, st);
+    if (e != cudaSuccess) return GSR_ECUDA;
+    cudaMemcpyAsync(loss, loss_acc, sizeof(double), cudaMemcpyDeviceToDevice, st);
+    return finish(cudaSuccess);
+}
+
 gsr_status gsr_pair_count_batched(const float* alpha, const float* mu, const float* sigma,
                                   const float* rho, const float* color, int64_t n_total,
                                   const gsr_image* imgs, int32_t n_imgs, double ratio,

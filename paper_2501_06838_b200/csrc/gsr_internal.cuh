@@ -259,13 +259,31 @@ cudaError_t exclusive_scan_i32(const int* in, int* out, long long n, int* tmp, c
 
 // render_fwd.cu
 cudaError_t launch_render_fwd(const ImgTable& tab, const Workspace& ws, float* out,
-                              cudaStream_t st);
+                              cudaStream_t st, const float* gt = nullptr,
+                              double* loss_acc = nullptr);
 // render_bwd.cu
+// grad_out = dL/dI, or (img, gt != nullptr) the fused L1 gradient sign(img - gt) * inv_numel
 cudaError_t launch_render_bwd_moments(const ImgTable& tab, const Workspace& ws, const int* perm,
-                                      const float* grad_out, double* moments, cudaStream_t st);
+                                      const float* grad_out, double* moments, cudaStream_t st,
+                                      const float* img = nullptr, const float* gt = nullptr,
+                                      float inv_numel = 0.f);
+// Raw-parameter mode of the finalize (NEXT-1 activation layer): when raw != nullptr the
+// gradients are chained through alpha = sigmoid, c = sigmoid, sigma = sigmoid,
+// rho = rho_scale tanh, mu = p + o, using the raw inputs for the Jacobians.
+struct RawParams {
+    const float* raw_alpha; const float* raw_sigma; const float* raw_rho; const float* raw_color;
+    float rho_scale;
+};
 cudaError_t launch_finalize(const float* alpha, const float* mu, const float* sigma,
                             const float* rho, const float* color, long long n,
                             const double* moments, float* d_alpha, float* d_mu, float* d_sigma,
-                            float* d_rho, float* d_color, cudaStream_t st);
+                            float* d_rho, float* d_color, cudaStream_t st,
+                            const RawParams* raw = nullptr);
+// train.cu
+cudaError_t launch_activate(const float* raw_alpha, const float* offset, const float* ref,
+                            const float* raw_sigma, const float* raw_rho, const float* raw_color,
+                            long long n, float rho_scale, float* alpha, float* mu, float* sigma,
+                            float* rho, float* color, cudaStream_t st);
+cudaError_t launch_scale_loss(double* loss, double scale, cudaStream_t st);
 
 }  // namespace gsr

@@ -116,7 +116,8 @@ __device__ __forceinline__ void fold_row(const RowAcc& A, float v, const float4 
 __global__ void __launch_bounds__(BWD_THREADS) k_render_bwd(
     const ImgTable tab, const float4* __restrict__ rec, const int* __restrict__ cell_start,
     const int* __restrict__ perm, const float* __restrict__ grad_out,
-    double* __restrict__ moments, int ks) {
+    double* __restrict__ moments, int ks, const float* __restrict__ img,
+    const float* __restrict__ gt, float inv_numel) {
     __shared__ __align__(16) float4 gA[TILE_H][TILE_W / 2];
     __shared__ __align__(16) float2 gB[TILE_H][TILE_W / 2];
 
@@ -136,9 +137,18 @@ __global__ void __launch_bounds__(BWD_THREADS) k_render_bwd(
         int y = Ty0 + ry, x = Tx0 + 2 * cp;
         float v[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
         if (y <= Ty1) {
-            const float* g = grad_out + im.out_off + ((long long)(y - im.row_begin) * im.Ws) * 3;
-            if (x <= Tx1) { v[0] = g[3 * x]; v[1] = g[3 * x + 1]; v[2] = g[3 * x + 2]; }
-            if (x + 1 <= Tx1) { v[3] = g[3 * x + 3]; v[4] = g[3 * x + 4]; v[5] = g[3 * x + 5]; }
+            const long long ro = im.out_off + ((long long)(y - im.row_begin) * im.Ws) * 3;
+            const int nv = x + 1 <= Tx1 ? 6 : (x <= Tx1 ? 3 : 0);
+            if (gt) {
+                // fused L1 loss gradient (NEXT-1): dL/dI = sign(I - I_gt) / numel
+                for (int k = 0; k < nv; ++k) {
+                    const float d = img[ro + 3 * x + k] - gt[ro + 3 * x + k];
+                    v[k] = d > 0.f ? inv_numel : (d < 0.f ? -inv_numel : 0.f);
+                }
+            } else {
+                const float* g = grad_out + ro;
+                for (int k = 0; k < nv; ++k) v[k] = g[3 * x + k];
+            }
         }
         gA[ry][cp] = make_float4(v[0], v[3], v[1], v[4]);
         gB[ry][cp] = make_float2(v[2], v[5]);
@@ -235,7 +245,8 @@ __global__ void k_finalize(const float* __restrict__ alpha, const float* __restr
                            const float* __restrict__ color, long long n,
                            const double* __restrict__ moments, float* __restrict__ d_alpha,
                            float* __restrict__ d_mu, float* __restrict__ d_sigma,
-                           float* __restrict__ d_rho, float* __restrict__ d_color) {
+                           float* __restrict__ d_rho, float* __restrict__ d_color, RawParams raw,
+                           int raw_mode) {
     long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     float o[9] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
@@ -251,15 +262,30 @@ __global__ void k_finalize(const float* __restrict__ alpha, const float* __restr
         double S0 = al * K * cf;
         double Sp = m[3] / kp, Sv = m[4] / kv;
         double Spp = m[5] / (kp * kp), Spv = m[6] / (kp * kv), Svv = m[7] / HALF_LOG2E;
-        o[0] = (float)(K * cf);
-        o[1] = (float)(Sp / (sx * D));
-        o[2] = (float)((Sv - rh * Sp / D) / sy);
-        o[3] = (float)(((Spp + rh * Spv) / D - S0) / sx);
-        o[4] = (float)((Svv - rh * Spv / D - S0) / sy);
-        o[5] = (float)((rh * S0 + Spv - rh * Spp / D) / D);
-        o[6] = (float)(al * K * m[0]);
-        o[7] = (float)(al * K * m[1]);
-        o[8] = (float)(al * K * m[2]);
+        double g9[9];
+        g9[0] = K * cf;
+        g9[1] = Sp / (sx * D);
+        g9[2] = (Sv - rh * Sp / D) / sy;
+        g9[3] = ((Spp + rh * Spv) / D - S0) / sx;
+        g9[4] = (Svv - rh * Spv / D - S0) / sy;
+        g9[5] = (rh * S0 + Spv - rh * Spp / D) / D;
+        g9[6] = al * K * m[0];
+        g9[7] = al * K * m[1];
+        g9[8] = al * K * m[2];
+        if (raw_mode) {
+            // chain rule through the Gaussian Primary Head activations: sigmoid' from
+            // the raw input in fp64 (exact also where the fp32 sigmoid saturates), tanh' likewise
+            auto dsig = [](double r) { double e = exp(-fabs(r)); return e / ((1.0 + e) * (1.0 + e)); };
+            auto dtanh = [](double r) { double t = tanh(r); return 1.0 - t * t; };
+            g9[0] *= dsig((double)raw.raw_alpha[i]);
+            g9[3] *= dsig((double)raw.raw_sigma[2 * i]);
+            g9[4] *= dsig((double)raw.raw_sigma[2 * i + 1]);
+            g9[5] *= (double)raw.rho_scale * dtanh((double)raw.raw_rho[i]);
+            g9[6] *= dsig((double)raw.raw_color[3 * i]);
+            g9[7] *= dsig((double)raw.raw_color[3 * i + 1]);
+            g9[8] *= dsig((double)raw.raw_color[3 * i + 2]);
+        }
+        for (int k = 0; k < 9; ++k) o[k] = (float)g9[k];
     }
     d_alpha[i] = o[0];
     d_mu[2 * i] = o[1];
@@ -275,13 +301,14 @@ __global__ void k_finalize(const float* __restrict__ alpha, const float* __restr
 }  // namespace
 
 cudaError_t launch_render_bwd_moments(const ImgTable& tab, const Workspace& ws, const int* perm,
-                                      const float* grad_out, double* moments, cudaStream_t st) {
+                                      const float* grad_out, double* moments, cudaStream_t st,
+                                      const float* img, const float* gt, float inv_numel) {
     if (tab.total_tiles <= 0) return cudaSuccess;
     count_launches(1);
     int h = prof_begin(2, st);
     int ks = split_k_factor(tab.total_tiles);
     k_render_bwd<<<tab.total_tiles * ks, BWD_THREADS, 0, st>>>(tab, ws.rec, ws.cell_start, perm,
-                                                               grad_out, moments, ks);
+                                                               grad_out, moments, ks, img, gt, inv_numel);
     prof_end(h, st);
     return cudaGetLastError();
 }
@@ -289,13 +316,15 @@ cudaError_t launch_render_bwd_moments(const ImgTable& tab, const Workspace& ws, 
 cudaError_t launch_finalize(const float* alpha, const float* mu, const float* sigma,
                             const float* rho, const float* color, long long n,
                             const double* moments, float* d_alpha, float* d_mu, float* d_sigma,
-                            float* d_rho, float* d_color, cudaStream_t st) {
+                            float* d_rho, float* d_color, cudaStream_t st, const RawParams* raw) {
     if (n <= 0) return cudaSuccess;
     count_launches(1);
     int h = prof_begin(3, st);
     k_finalize<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(alpha, mu, sigma, rho, color, n,
                                                             moments, d_alpha, d_mu, d_sigma,
-                                                            d_rho, d_color);
+                                                            d_rho, d_color,
+                                                            raw ? *raw : RawParams{},
+                                                            raw ? 1 : 0);
     prof_end(h, st);
     return cudaGetLastError();
 }

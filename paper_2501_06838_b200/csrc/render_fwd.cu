@@ -75,7 +75,6 @@ __device__ __forceinline__ float2 ld_dsmem_f2(const float2* local_addr, uint32_t
 __device__ __forceinline__ float2 f2(float a) { return make_float2(a, a); }
 
 constexpr int NACC = FWD_ROWS * (FWD_STRIP / 2) * 3;   // float2 accumulators per thread (24)
-constexpr int NCONS = FWD_CWARPS * 32;                  // consumer threads (128)
 
 struct FwdSmem {
     float4 rec[FWD_STAGES][FWD_CHUNK * 3];
@@ -143,7 +142,9 @@ template <int KS>
 __global__ void __launch_bounds__(FWD_THREADS) k_render_fwd(const ImgTable tab,
                                                             const float4* __restrict__ rec,
                                                             const int* __restrict__ cell_start,
-                                                            float* __restrict__ out) {
+                                                            float* __restrict__ out,
+                                                            const float* __restrict__ gt,
+                                                            double* __restrict__ loss_acc) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     FwdSmem& sm = *reinterpret_cast<FwdSmem*>(smem_raw);
 
@@ -328,11 +329,13 @@ __global__ void __launch_bounds__(FWD_THREADS) k_render_fwd(const ImgTable tab,
 
     const int xl0 = Tx0 + FWD_STRIP * (lane & 3);
     const int yl0 = Ty0 + FWD_ROWS * (lane >> 2);
+    float l1 = 0.f;     // fused L1 loss (NEXT-1): sum |I - I_gt| over the stored elements
 #pragma unroll
     for (int r = 0; r < FWD_ROWS; ++r) {
         const int y = yl0 + r;
         if (y >= im.row_end) continue;
-        float* o = out + im.out_off + ((long long)(y - im.row_begin) * im.Ws) * 3;
+        const long long rowoff = im.out_off + ((long long)(y - im.row_begin) * im.Ws) * 3;
+        float* o = out + rowoff;
 #pragma unroll
         for (int jp = 0; jp < FWD_STRIP / 2; ++jp) {
             const int a = (r * (FWD_STRIP / 2) + jp) * 3;
@@ -341,12 +344,28 @@ __global__ void __launch_bounds__(FWD_THREADS) k_render_fwd(const ImgTable tab,
             const int x = xl0 + 2 * jp;
             if (x < im.Ws) { o[3 * x] = R.x; o[3 * x + 1] = G.x; o[3 * x + 2] = B.x; }
             if (x + 1 < im.Ws) { o[3 * x + 3] = R.y; o[3 * x + 4] = G.y; o[3 * x + 5] = B.y; }
+            if (gt) {
+                const float* t = gt + rowoff;
+                if (x < im.Ws)
+                    l1 += fabsf(R.x - t[3 * x]) + fabsf(G.x - t[3 * x + 1]) +
+                          fabsf(B.x - t[3 * x + 2]);
+                if (x + 1 < im.Ws)
+                    l1 += fabsf(R.y - t[3 * x + 3]) + fabsf(G.y - t[3 * x + 4]) +
+                          fabsf(B.y - t[3 * x + 5]);
+            }
         }
+    }
+    if (gt) {
+        double d = (double)l1;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+        if (lane == 0) atomicAdd(loss_acc, d);
     }
 }
 
 template <int KS>
-cudaError_t launch_ks(const ImgTable& tab, const Workspace& ws, float* out, cudaStream_t st) {
+cudaError_t launch_ks(const ImgTable& tab, const Workspace& ws, float* out, const float* gt,
+                      double* loss_acc, cudaStream_t st) {
     static bool attr_set = false;
     const size_t smem = sizeof(FwdSmem);
     if (!attr_set) {
@@ -369,13 +388,13 @@ cudaError_t launch_ks(const ImgTable& tab, const Workspace& ws, float* out, cuda
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, k_render_fwd<KS>, tab, (const float4*)ws.rec,
-                              (const int*)ws.cell_start, out);
+                              (const int*)ws.cell_start, out, gt, loss_acc);
 }
 
 }  // namespace
 
 cudaError_t launch_render_fwd(const ImgTable& tab, const Workspace& ws, float* out,
-                              cudaStream_t st) {
+                              cudaStream_t st, const float* gt, double* loss_acc) {
     if (tab.total_ftiles <= 0) return cudaSuccess;
     count_launches(1);
     int h = prof_begin(1, st);
@@ -383,10 +402,10 @@ cudaError_t launch_render_fwd(const ImgTable& tab, const Workspace& ws, float* o
     const int ks = split_k_factor(tab.total_ftiles);
     cudaError_t e;
     switch (ks) {
-        case 8: e = launch_ks<8>(tab, ws, out, st); break;
-        case 4: e = launch_ks<4>(tab, ws, out, st); break;
-        case 2: e = launch_ks<2>(tab, ws, out, st); break;
-        default: e = launch_ks<1>(tab, ws, out, st); break;
+        case 8: e = launch_ks<8>(tab, ws, out, gt, loss_acc, st); break;
+        case 4: e = launch_ks<4>(tab, ws, out, gt, loss_acc, st); break;
+        case 2: e = launch_ks<2>(tab, ws, out, gt, loss_acc, st); break;
+        default: e = launch_ks<1>(tab, ws, out, gt, loss_acc, st); break;
     }
     prof_end(h, st);
     if (e != cudaSuccess) return e;

@@ -316,3 +316,49 @@ def render(alpha, mu, sigma, rho, color, H: int, W: int, scale: float,
     lay = _single(alpha.shape[0], H, W, scale)
     flat = _RenderFn.apply(alpha, mu, sigma, rho, color, lay, float(ratio))
     return lay.view(flat, 0)
+
+
+# ------------------------------------------------------------------ NEXT-1: fused training step
+RAW = ("raw_alpha", "offset", "raw_sigma", "raw_rho", "raw_color")
+RAW_WIDTH = {"raw_alpha": 1, "offset": 2, "ref": 2, "raw_sigma": 2, "raw_rho": 1, "raw_color": 3}
+
+
+def train_step_l1(raw_alpha, offset, ref, raw_sigma, raw_rho, raw_color, lay: Layout,
+                  gt: torch.Tensor, ratio: float = 0.1, rho_scale: float = 1.0,
+                  inv_numel: float = 0.0, out: Optional[torch.Tensor] = None):
+    """One fused training step of the rasterizer (gsr_train_step_l1_batched): activations of the
+    Gaussian Primary Head, forward render, L1 loss against `gt` and the
+    gradients wrt the raw head outputs. Returns (out, loss[1] float64, grads dict)."""
+    ts = {}
+    n = raw_alpha.shape[0]
+    for name, t in zip(("raw_alpha", "offset", "ref", "raw_sigma", "raw_rho", "raw_color"),
+                       (raw_alpha, offset, ref, raw_sigma, raw_rho, raw_color)):
+        if not isinstance(t, torch.Tensor) or not t.is_cuda or t.dtype != torch.float32:
+            raise TypeError(f"{name} must be a float32 CUDA tensor")
+        t = t.contiguous()
+        w = RAW_WIDTH[name]
+        if t.shape[0] != n or (w == 1 and t.dim() != 1) or (w > 1 and t.shape[1:] != (w,)):
+            raise ValueError(f"{name} has shape {tuple(t.shape)}")
+        ts[name] = t
+    gt = _check_param(gt, "gt")
+    dev = raw_alpha.device
+    if not single_chunk(lay):
+        raise ValueError(f"train_step_l1 takes at most {_lib.MAX_IMAGES} images per call")
+    g0, g1, o0, arr, m = next(_chunks(lay))
+    if g0 != 0 or g1 != n:
+        raise ValueError("the layout's Gaussian ranges must span the parameter arrays")
+    lib = _lib.load()
+    nb = lib.gsr_train_workspace_bytes_batched(arr, m, n, float(ratio))
+    if nb == 0:
+        raise _lib.GsrError("gsr_train_workspace_bytes_batched: invalid arguments")
+    ws = _workspace(dev, nb)
+    if out is None:
+        out = torch.empty(lay.out_numel, dtype=torch.float32, device=dev)
+    loss = torch.empty(1, dtype=torch.float64, device=dev)
+    grads = {k: torch.empty_like(ts[k]) for k in RAW}
+    check(lib.gsr_train_step_l1_batched(
+        *[_ptr(ts[k]) for k in ("raw_alpha", "offset", "ref", "raw_sigma", "raw_rho", "raw_color")],
+        n, arr, m, float(ratio), float(rho_scale), float(inv_numel), _ptr(gt), _ptr(out),
+        _ptr(loss), *[_ptr(grads[k]) for k in RAW], ws.data_ptr(), ws.numel(),
+        _stream_ptr(dev)), "gsr_train_step_l1_batched")
+    return out, loss, grads

@@ -1,0 +1,69 @@
+"""GPU parity of the NEXT-1 fused training step (gsr_train_step_l1_batched) against the float64
+oracle composition (oracle/train.py): activations -> render -> L1 loss -> raw gradients."""
+import numpy as np
+import pytest
+
+import gsr_synth as S
+import oracle as O
+from oracle import train as T
+from _util import assert_fwd_close
+
+pytestmark = pytest.mark.gpu
+
+RAWK = ("raw_alpha", "offset", "raw_sigma", "raw_rho", "raw_color")
+
+
+def raw_cloud(H, W, seed, m=16):
+    """Raw head outputs with the image-like distribution of gsr_synth (before activation)."""
+    rng = np.random.default_rng(seed)
+    n = m * H * W
+    ref = S.reference_grid(H, W, m).astype(np.float32)
+    raw = dict(raw_alpha=rng.normal(-3, 1, n), offset=rng.uniform(-0.5, 0.5, (n, 2)),
+               raw_sigma=rng.normal(-0.5, 0.5, (n, 2)), raw_rho=rng.normal(0, 0.5, n),
+               raw_color=rng.normal(0, 1, (n, 3)))
+    return {k: v.astype(np.float32) for k, v in raw.items()}, ref
+
+
+def gt_near(I, seed, delta=2e-3):
+    """Ground truth offset from the oracle image by +-delta (no sign ties under fp32 error)."""
+    rng = np.random.default_rng(seed)
+    return (I + rng.choice([-delta, delta], size=I.shape)).astype(np.float32)
+
+
+@pytest.mark.parametrize("rho_scale", [1.0, 1 - 1e-4])
+def test_train_step_batch_matches_oracle(rho_scale):
+    import torch
+    import paper_2501_06838_b200 as gsr
+    from paper_2501_06838_b200 import ops
+    scales = [4.0, 2.5, 1.3]
+    raws, refs, imgs, gts = [], [], [], []
+    off = 0
+    for k, s in enumerate(scales):
+        H, W = 20, 24
+        raw, ref = raw_cloud(H, W, seed=50 + k)
+        n = raw["raw_alpha"].shape[0]
+        act = T.activate(raw, ref, rho_scale)
+        gts.append(gt_near(O.render_fwd(act, H, W, s, 0.1), seed=k))
+        raws.append(raw); refs.append(ref); imgs.append((H, W, s, off, n)); off += n
+    raw = {k: np.concatenate([r[k] for r in raws]) for k in RAWK}
+    ref = np.concatenate(refs)
+    outs, loss, g = T.l1_step(raw, ref, imgs, gts, 0.1, rho_scale)
+    lay = gsr.layout([gsr.Image(H, W, s, go, gc) for (H, W, s, go, gc) in imgs])
+    dev = {k: torch.from_numpy(v).cuda() for k, v in raw.items()}
+    gt_flat = torch.from_numpy(np.concatenate([x.reshape(-1) for x in gts])).cuda()
+    out, gl, gg = ops.train_step_l1(dev["raw_alpha"], dev["offset"], torch.from_numpy(ref).cuda(),
+                                    dev["raw_sigma"], dev["raw_rho"], dev["raw_color"], lay, gt_flat,
+                                    0.1, rho_scale)
+    torch.cuda.synchronize()
+    for k, o in enumerate(outs):
+        assert_fwd_close(lay.view(out, k).cpu().numpy(), o)
+    assert float(gl.item()) == pytest.approx(loss, rel=1e-5)
+    cols = [("raw_alpha", [0]), ("offset", [1, 2]), ("raw_sigma", [3, 4]), ("raw_rho", [5]),
+            ("raw_color", [6, 7, 8])]
+    for name, c in cols:
+        got = gg[name].cpu().numpy().astype(np.float64).reshape(len(ref), -1)
+        want = np.asarray(g[name]).reshape(len(ref), -1)
+        S_ = g["absmass"][:, c]
+        bound = 1e-4 * np.maximum(np.abs(want), 0.1 * S_) + 1e-8 * S_.max(axis=0, keepdims=True)
+        err = np.abs(got - want)
+        assert (err <= bound + 1e-30).all(), (name, float((err / (bound + 1e-30)).max()))
