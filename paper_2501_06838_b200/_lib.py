@@ -50,44 +50,50 @@ def load(path: Path | str | None = None):
     global _lib
     if _lib is not None:
         return _lib
-    p = Path(path) if path else LIB_PATH
+    import os
+    p = Path(path) if path else Path(os.environ.get("GSR_LIB_PATH", str(LIB_PATH)))
     if not p.exists():
         raise RuntimeError(f"libgsr.so not built ({p}); run __graft_entry__.build() or "
                            f"python -m paper_2501_06838_b200.build")
     lib = ctypes.CDLL(str(p))
     par = [_P, _P, _P, _P, _P]
-    lib.gsr_version.restype = ctypes.c_char_p
-    lib.gsr_version.argtypes = []
-    lib.gsr_out_dims.argtypes = [_I32, _I32, _D, ctypes.POINTER(_I32), ctypes.POINTER(_I32)]
-    lib.gsr_workspace_bytes_batched.argtypes = [_IMGP, _I32, _I64, _D]
-    lib.gsr_workspace_bytes_batched.restype = _SZ
-    lib.gsr_workspace_bytes.argtypes = [_I64, _I32, _I32, _D, _D]
-    lib.gsr_workspace_bytes.restype = _SZ
-    lib.gsr_render_fwd.argtypes = par + [_I64, _I32, _I32, _D, _D, _P, _P, _SZ, _P]
-    lib.gsr_render_bwd.argtypes = par + [_I64, _I32, _I32, _D, _D, _P, _P, _P, _P, _P, _P, _P,
-                                         _SZ, _P]
-    lib.gsr_render_fwd_batched.argtypes = par + [_I64, _IMGP, _I32, _D, _P, _P, _SZ, _P]
-    lib.gsr_render_bwd_batched.argtypes = par + [_I64, _IMGP, _I32, _D, _P, _P, _P, _P, _P, _P,
-                                                 _P, _SZ, _P]
-    lib.gsr_render_bwd_moments_batched.argtypes = par + [_I64, _IMGP, _I32, _D, _P, _P, _P, _SZ,
-                                                         _P]
-    lib.gsr_render_bwd_batched_ex.argtypes = par + [_I64, _IMGP, _I32, _D, _P, _P, _P, _P, _P,
-                                                    _P, _P, _SZ, ctypes.c_uint32, _P]
-    lib.gsr_render_bwd_moments_batched_ex.argtypes = par + [_I64, _IMGP, _I32, _D, _P, _P, _P,
-                                                            _SZ, ctypes.c_uint32, _P]
-    lib.gsr_finalize_grads.argtypes = par + [_I64, _P, _P, _P, _P, _P, _P, _P]
-    lib.gsr_train_workspace_bytes_batched.argtypes = [_IMGP, _I32, _I64, _D]
-    lib.gsr_train_workspace_bytes_batched.restype = _SZ
-    lib.gsr_train_step_l1_batched.argtypes = [_P] * 6 + [_I64, _IMGP, _I32, _D, ctypes.c_float,
-                                                         _D, _P, _P, _P, _P, _P, _P, _P, _P, _P,
-                                                         _SZ, _P]
-    lib.gsr_pair_count_batched.argtypes = par + [_I64, _IMGP, _I32, _D, _P, _P, _SZ, _P]
-    lib.gsr_debug_rects.argtypes = par + [_I64, _I32, _I32, _D, _D, _P, _P]
-    lib.gsr_debug_tile_lists.argtypes = par + [_I64, _I32, _I32, _D, _D, _P, _P, _P, _P, _SZ, _P]
-    lib.gsr_tile_shape.argtypes = [ctypes.POINTER(_I32)] * 4
-    lib.gsr_tile_shape.restype = None
-    lib.gsr_profile_enable.argtypes = [_I32]
-    lib.gsr_profile_collect.argtypes = [_P, _P, _P, _I32]
+    sig = {
+        "gsr_version": ([], ctypes.c_char_p),
+        "gsr_out_dims": ([_I32, _I32, _D, ctypes.POINTER(_I32), ctypes.POINTER(_I32)], None),
+        "gsr_workspace_bytes_batched": ([_IMGP, _I32, _I64, _D], _SZ),
+        "gsr_workspace_bytes": ([_I64, _I32, _I32, _D, _D], _SZ),
+        "gsr_render_fwd": (par + [_I64, _I32, _I32, _D, _D, _P, _P, _SZ, _P], None),
+        "gsr_render_bwd": (par + [_I64, _I32, _I32, _D, _D, _P, _P, _P, _P, _P, _P, _P, _SZ, _P],
+                           None),
+        "gsr_render_fwd_batched": (par + [_I64, _IMGP, _I32, _D, _P, _P, _SZ, _P], None),
+        "gsr_render_bwd_batched": (par + [_I64, _IMGP, _I32, _D, _P, _P, _P, _P, _P, _P, _P, _SZ,
+                                          _P], None),
+        "gsr_render_bwd_moments_batched": (par + [_I64, _IMGP, _I32, _D, _P, _P, _P, _SZ, _P],
+                                           None),
+        "gsr_render_bwd_batched_ex": (par + [_I64, _IMGP, _I32, _D, _P, _P, _P, _P, _P, _P, _P,
+                                             _SZ, ctypes.c_uint32, _P], None),
+        "gsr_render_bwd_moments_batched_ex": (par + [_I64, _IMGP, _I32, _D, _P, _P, _P, _SZ,
+                                                     ctypes.c_uint32, _P], None),
+        "gsr_finalize_grads": (par + [_I64, _P, _P, _P, _P, _P, _P, _P], None),
+        "gsr_train_workspace_bytes_batched": ([_IMGP, _I32, _I64, _D], _SZ),
+        "gsr_train_step_l1_batched": ([_P] * 6 + [_I64, _IMGP, _I32, _D, ctypes.c_float, _D, _P,
+                                                  _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P], None),
+        "gsr_pair_count_batched": (par + [_I64, _IMGP, _I32, _D, _P, _P, _SZ, _P], None),
+        "gsr_debug_rects": (par + [_I64, _I32, _I32, _D, _D, _P, _P], None),
+        "gsr_debug_tile_lists": (par + [_I64, _I32, _I32, _D, _D, _P, _P, _P, _P, _SZ, _P], None),
+        "gsr_tile_shape": ([ctypes.POINTER(_I32)] * 4, "void"),
+        "gsr_profile_enable": ([_I32], None),
+        "gsr_profile_collect": ([_P, _P, _P, _I32], None),
+    }
+    for name, (args, res) in sig.items():
+        fn = getattr(lib, name, None)
+        if fn is None:                 # an older build (A/B experiments): leave it undeclared
+            continue
+        fn.argtypes = args
+        if res == "void":
+            fn.restype = None
+        elif res is not None:
+            fn.restype = res
     _lib = lib
     return lib
 

@@ -174,7 +174,7 @@ gsr_status prepare(const float* alpha, const float* mu, const float* sigma, cons
 
 extern "C" {
 
-const char* gsr_version(void) { return "gsr-b200 0.1 (sm_100a; fwd tile 32x32, cell 16)"; }
+const char* gsr_version(void) { return "gsr-b200 0.2 (sm_100a; fwd tile 32x16, bwd tile 64x32, cell 16)"; }
 
 gsr_status gsr_profile_enable(int32_t on) {
     std::lock_guard<std::mutex> lk(g_prof.mu);

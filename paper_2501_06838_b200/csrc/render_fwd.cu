@@ -138,7 +138,7 @@ __device__ __forceinline__ void fwd_gauss(const float4 r0, const float4 r1, cons
     }
 }
 
-template <int KS>
+template <int KS, bool LOSS>
 __global__ void __launch_bounds__(FWD_THREADS) k_render_fwd(const ImgTable tab,
                                                             const float4* __restrict__ rec,
                                                             const int* __restrict__ cell_start,
@@ -344,7 +344,7 @@ __global__ void __launch_bounds__(FWD_THREADS) k_render_fwd(const ImgTable tab,
             const int x = xl0 + 2 * jp;
             if (x < im.Ws) { o[3 * x] = R.x; o[3 * x + 1] = G.x; o[3 * x + 2] = B.x; }
             if (x + 1 < im.Ws) { o[3 * x + 3] = R.y; o[3 * x + 4] = G.y; o[3 * x + 5] = B.y; }
-            if (gt) {
+            if (LOSS) {
                 const float* t = gt + rowoff;
                 if (x < im.Ws)
                     l1 += fabsf(R.x - t[3 * x]) + fabsf(G.x - t[3 * x + 1]) +
@@ -355,7 +355,7 @@ __global__ void __launch_bounds__(FWD_THREADS) k_render_fwd(const ImgTable tab,
             }
         }
     }
-    if (gt) {
+    if (LOSS) {
         double d = (double)l1;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
@@ -363,13 +363,13 @@ __global__ void __launch_bounds__(FWD_THREADS) k_render_fwd(const ImgTable tab,
     }
 }
 
-template <int KS>
-cudaError_t launch_ks(const ImgTable& tab, const Workspace& ws, float* out, const float* gt,
-                      double* loss_acc, cudaStream_t st) {
+template <int KS, bool LOSS>
+cudaError_t launch_ks2(const ImgTable& tab, const Workspace& ws, float* out, const float* gt,
+                       double* loss_acc, cudaStream_t st) {
     static bool attr_set = false;
     const size_t smem = sizeof(FwdSmem);
     if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(k_render_fwd<KS>,
+        cudaError_t e = cudaFuncSetAttribute(k_render_fwd<KS, LOSS>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)smem);
         if (e != cudaSuccess) return e;
@@ -387,8 +387,15 @@ cudaError_t launch_ks(const ImgTable& tab, const Workspace& ws, float* out, cons
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, k_render_fwd<KS>, tab, (const float4*)ws.rec,
+    return cudaLaunchKernelEx(&cfg, k_render_fwd<KS, LOSS>, tab, (const float4*)ws.rec,
                               (const int*)ws.cell_start, out, gt, loss_acc);
+}
+
+template <int KS>
+cudaError_t launch_ks(const ImgTable& tab, const Workspace& ws, float* out, const float* gt,
+                      double* loss_acc, cudaStream_t st) {
+    return gt ? launch_ks2<KS, true>(tab, ws, out, gt, loss_acc, st)
+              : launch_ks2<KS, false>(tab, ws, out, gt, loss_acc, st);
 }
 
 }  // namespace

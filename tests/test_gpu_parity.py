@@ -289,3 +289,34 @@ def test_cpu_tensors_rejected(gsr):
     c = S.gaussians(4, 4, seed=0)
     with pytest.raises(TypeError):
         gsr.render_fwd(*[torch.from_numpy(c[k]) for k in KEYS], 4, 4, 2.0)
+
+
+@pytest.mark.parametrize("m,r", [(1, 0.01), (9, 0.01), (9, 0.4), (4, 0.8)])
+def test_sweep_densities_and_ratios(gsr, m, r):
+    """NEXT-3 sweep settings (m in {1,4,9}, r in {0.01 .. 0.8}) at a small size: fwd + bwd."""
+    H, W, s = 18, 20, 4.0
+    c = S.gaussians(H, W, m=m, seed=m * 10 + int(100 * r))
+    Hs, Ws = O.out_dims(H, W, s)
+    assert_fwd_close(fwd(gsr, c, H, W, s, r), O.render_fwd(c, H, W, s, r))
+    g = S.grad_out((Hs, Ws, 3), seed=m)
+    got = bwd(gsr, c, H, W, s, g, r)
+    want = O.render_bwd(c, H, W, s, r, g, want_absmass=True)
+    assert_bwd_close(got, want, want["absmass"])
+
+
+def test_reuse_binning_matches_rebinning(gsr):
+    """GSR_REUSE_BINNING (the forward's workspace) gives exactly the re-binned backward."""
+    import torch
+    H, W, s = 20, 18, 3.0
+    c = S.gaussians(H, W, seed=21)
+    dev = to_dev(c)
+    lay = gsr.layout([gsr.Image(H, W, s, 0, c["alpha"].shape[0])])
+    from paper_2501_06838_b200 import ops
+    ws = ops.workspace_for(dev[0], lay)
+    out = gsr.render_fwd_batched(*dev, lay, workspace=ws)
+    g = torch.from_numpy(S.grad_out((lay.out_numel,), seed=2)).cuda()
+    a = gsr.render_bwd_batched(*dev, lay, g, workspace=ws, reuse_binning=True)
+    b = gsr.render_bwd_batched(*dev, lay, g)
+    torch.cuda.synchronize()
+    for x, y in zip(a, b):
+        assert torch.allclose(x, y, rtol=1e-6, atol=1e-9)
