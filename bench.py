@@ -225,6 +225,9 @@ def main():
     ap.add_argument("--images", type=int, default=None, help="dev only: first N images")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--partition", choices=["band", "image"], default="band",
+                    help="N>1: row bands of every image (NCCL all-gather + moment all-reduce) or "
+                         "whole images per rank (no exchange)")
     ap.add_argument("--cpu-budget", type=float, default=12.0, help="seconds of oracle work")
     ap.add_argument("--ref-budget", type=float, default=6.0, help="oracle seconds per ref step")
     args = ap.parse_args()
@@ -257,15 +260,22 @@ def main():
     widths3 = [Ws * 3 for _, Ws in dims]
     offs = np.concatenate([[0], np.cumsum(counts)])
     bounds = []
+    by_image = world > 1 and args.partition == "image"
     for k, (H, W, s) in enumerate(imgs):
-        if world == 1:
+        if world == 1 or by_image:
             bounds.append([0, dims[k][0]])
         else:
             rc = gdist.row_pair_counts(host["mu"][offs[k]:offs[k + 1]],
                                        np.ones(counts[k], bool), H, W, s, RATIO)
             bounds.append(gdist.plan_bands(rc, world))
-    band_imgs = [gsr.Image(H, W, s, int(offs[k]), counts[k], bounds[k][rank], bounds[k][rank + 1])
-                 for k, (H, W, s) in enumerate(imgs)]
+    if by_image:
+        # whole images per rank: contiguous, equal image counts (the images are i.i.d. draws)
+        k0, k1 = (rank * len(imgs)) // world, ((rank + 1) * len(imgs)) // world
+        band_imgs = [gsr.Image(H, W, s, int(offs[k]), counts[k], 0, dims[k][0])
+                     for k, (H, W, s) in enumerate(imgs) if k0 <= k < k1]
+    else:
+        band_imgs = [gsr.Image(H, W, s, int(offs[k]), counts[k], bounds[k][rank],
+                               bounds[k][rank + 1]) for k, (H, W, s) in enumerate(imgs)]
     lay = gsr.layout(band_imgs)
     full_pix = sum(h * w for h, w in dims)
     P_rank = gsr.pair_count(*params, lay, RATIO)
@@ -280,14 +290,19 @@ def main():
     gen.manual_seed(2000 + rank)
     g_band.uniform_(-1.0, 1.0, generator=gen)
 
+    from paper_2501_06838_b200 import ops as gops
+    step_ws = gops.workspace_for(params[0], lay, RATIO) if gops.single_chunk(lay) else None
+
     def step():
-        out = gsr.render_fwd_batched(*params, lay, RATIO)
+        # one binning per step: the backward reuses the forward's (GSR_REUSE_BINNING)
+        out = gsr.render_fwd_batched(*params, lay, RATIO, workspace=step_ws)
         gathered = out
-        if world > 1:
+        if world > 1 and not by_image:
             gathered = gdist.gather_bands(out, gdist.rank_numels(bounds, widths3, world))
         moments = torch.zeros((n, 8), dtype=torch.float64, device=dev)
-        gsr.render_bwd_moments_batched(*params, lay, g_band, moments, RATIO)
-        if world > 1:
+        gsr.render_bwd_moments_batched(*params, lay, g_band, moments, RATIO, workspace=step_ws,
+                                       reuse_binning=step_ws is not None)
+        if world > 1 and not by_image:
             gdist.reduce_moments(moments)
         grads = gsr.finalize_grads(*params, moments)
         return gathered, grads
@@ -339,10 +354,11 @@ def main():
         def e2e_step():
             dp = [t.to(dev, non_blocking=True) for t in hp]
             dg = hg.to(dev, non_blocking=True)
-            out = gsr.render_fwd_batched(*dp, lay, RATIO)
+            out = gsr.render_fwd_batched(*dp, lay, RATIO, workspace=step_ws)
             mom = torch.zeros((n, 8), dtype=torch.float64, device=dev)
-            gsr.render_bwd_moments_batched(*dp, lay, dg, mom, RATIO)
-            if world > 1:
+            gsr.render_bwd_moments_batched(*dp, lay, dg, mom, RATIO, workspace=step_ws,
+                                           reuse_binning=step_ws is not None)
+            if world > 1 and not by_image:
                 gdist.reduce_moments(mom)
             gr = gsr.finalize_grads(*dp, mom)
             h_out.copy_(out, non_blocking=True)
@@ -419,7 +435,8 @@ def main():
             "config": {"workload": f"{args.workload}: {cfg['desc']}", "images": len(imgs),
                        "lr_hw": [imgs[0][0], imgs[0][1]], "scale": imgs[0][2], "ratio": RATIO,
                        "m": 16, "gaussians": n, "pairs_per_pass": P_total,
-                       "parallelism": f"row-band x{world}" if world > 1 else "single GPU",
+                       "parallelism": (f"{args.partition} x{world}" if world > 1
+                                       else "single GPU"),
                        "l2": "working set > 126 MB L2 (params 1.6 GB, image 2.1 GB); no flush"},
             "gpairs_per_s": 2 * P_total / (ms_step * 1e-3) / 1e9,
             "gpu_launches": int(launches),
