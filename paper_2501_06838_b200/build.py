@@ -15,6 +15,8 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
          "--expt-relaxed-constexpr", "-I", str(ROOT / "include")]
+# experiments only (A/B builds into another directory): extra -D flags
+EXTRA = os.environ.get("GSR_NVCC_EXTRA", "").split()
 
 
 def _stale(out: Path, deps) -> bool:
@@ -24,9 +26,11 @@ def _stale(out: Path, deps) -> bool:
     return any(Path(d).stat().st_mtime > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
+def build(force: bool = False, verbose: bool = False, out: Path | None = None,
+          objdir: Path | None = None) -> Path:
     headers = list(CSRC.glob("*.cuh")) + [ROOT / "include" / "gsr.h"]
-    objdir = PKG / "build"
+    lib = Path(out) if out else LIB
+    objdir = Path(objdir) if objdir else PKG / "build"
     objdir.mkdir(exist_ok=True)
     objs = []
     for src in SOURCES:
@@ -34,7 +38,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         o = objdir / (src + ".o")
         objs.append(o)
         if force or _stale(o, [s, *headers]):
-            cmd = [NVCC, *ARCH, *FLAGS, "-c", str(s), "-o", str(o)]
+            cmd = [NVCC, *ARCH, *FLAGS, *EXTRA, "-c", str(s), "-o", str(o)]
             r = subprocess.run(cmd, capture_output=True, text=True)
             log = objdir / (src + ".ptxas.txt")
             log.write_text(r.stdout + r.stderr)
@@ -43,14 +47,17 @@ def build(force: bool = False, verbose: bool = False) -> Path:
                 raise RuntimeError(f"nvcc failed for {src}")
             if verbose:
                 sys.stderr.write(r.stderr)
-    if force or _stale(LIB, objs):
-        tmp = LIB.with_suffix(".so.tmp%d" % os.getpid())
+    if force or _stale(lib, objs):
+        tmp = lib.with_suffix(".so.tmp%d" % os.getpid())
         cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", str(tmp), *map(str, objs)]
         subprocess.check_call(cmd)
-        os.replace(tmp, LIB)
-    return LIB
+        os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose=True)
-    print(LIB)
+    # python build.py [--force] [--out path.so --objdir dir]  (GSR_NVCC_EXTRA="-D..." for A/B)
+    a = sys.argv
+    out = a[a.index("--out") + 1] if "--out" in a else None
+    od = a[a.index("--objdir") + 1] if "--objdir" in a else None
+    print(build(force="--force" in a, verbose=True, out=out, objdir=od))

@@ -69,6 +69,16 @@ gsr_status build_table(const gsr_image* imgs, int32_t n_imgs, int64_t n_total, d
     if (!std::isfinite(ratio) || !(ratio > 0.0) || ratio > 1.0) return GSR_EINVAL;
     std::memset(tab, 0, sizeof(*tab));
     tab->n_imgs = n_imgs;
+    // forward configuration: small tiles when every window is narrow
+    double max_win = 0.0;
+    for (int k = 0; k < n_imgs; ++k) {
+        const gsr_image& g = imgs[k];
+        double w = 2.0 * ratio * g.scale * (double)(g.lr_h < g.lr_w ? g.lr_h : g.lr_w);
+        if (std::isfinite(w) && w > max_win) max_win = w;
+    }
+    tab->fwd_small = max_win < (double)FWD_SMALL_WINDOW ? 1 : 0;
+    tab->ftile_w = tab->fwd_small ? FwdCfgSmall::TW : FwdCfgLarge::TW;
+    tab->ftile_h = tab->fwd_small ? FwdCfgSmall::TH : FwdCfgLarge::TH;
     long long cells = 0, tiles = 0, ftiles = 0, prev_end = 0;
     for (int k = 0; k < n_imgs; ++k) {
         const gsr_image& g = imgs[k];
@@ -103,8 +113,8 @@ gsr_status build_table(const gsr_image* imgs, int32_t n_imgs, int64_t n_total, d
             d.ncy = (nrows - 1 + d.offy) / CELL + 1;
             d.ntx = ceil_div(d.Ws, TILE_W);
             d.nty = ceil_div(nrows, TILE_H);
-            d.fntx = ceil_div(d.Ws, FTILE_W);
-            d.fnty = ceil_div(nrows, FTILE_H);
+            d.fntx = ceil_div(d.Ws, tab->ftile_w);
+            d.fnty = ceil_div(nrows, tab->ftile_h);
         } else {
             d.ncx = d.ncy = d.ntx = d.nty = d.fntx = d.fnty = 0;
         }

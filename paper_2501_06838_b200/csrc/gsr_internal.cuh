@@ -16,18 +16,26 @@ namespace gsr {
 constexpr int CELL = 16;       // cell edge (HR px): binning granularity (sort key)
 constexpr int TILE_W = 64;     // backward render tile (HR px); also the debug tile-list tile
 constexpr int TILE_H = 32;
-// forward: a CTA renders a 32 x 16 tile; each of the 4 consumer warps covers the whole tile
-// (a lane owns 2 rows x 8 columns) and takes every 4th Gaussian of each staged chunk, so the
-// warps' work is balanced by construction; one extra warp is the TMA producer.
-constexpr int FTILE_W = 32;
-constexpr int FTILE_H = 16;
-constexpr int FWD_STRIP = 8;                     // columns per lane
-constexpr int FWD_ROWS = 2;                      // rows per lane
+// forward: a CTA renders one tile; each of the 4 consumer warps covers the whole tile (lane l
+// owns a FWD_ROWS x FWD_STRIP block at column group l & 3, row group l >> 2) and takes every 4th
+// Gaussian of each staged chunk, so the warps' work is balanced by construction; one extra warp
+// is the TMA producer. Two configurations, chosen per call from the window size:
+//   large (windows >= FWD_SMALL_WINDOW HR px): 2 x 8 px per lane -> 32 x 16 tiles
+//   small (narrow windows, e.g. the x1..x4 training patches): 1 x 4 px per lane -> 16 x 8 tiles,
+//         which wastes far fewer masked evaluations where a window covers only part of a tile.
+struct FwdCfgLarge { static constexpr int ROWS = 2, STRIP = 8, TW = 4 * STRIP, TH = 8 * ROWS; };
+struct FwdCfgSmall { static constexpr int ROWS = 1, STRIP = 4, TW = 4 * STRIP, TH = 8 * ROWS; };
+constexpr int FTILE_W = FwdCfgLarge::TW;          // 32
+constexpr int FTILE_H = FwdCfgLarge::TH;          // 16
+constexpr int FWD_SMALL_WINDOW = 48;             // HR px: below this the small tiles are used
 constexpr int FWD_CWARPS = 4;                    // consumer warps
 constexpr int FWD_THREADS = (FWD_CWARPS + 1) * 32;
 constexpr int FWD_CHUNK = 128;                   // records per TMA bulk stage
 constexpr int FWD_STAGES = 4;
-constexpr int BWD_WARPS = 4;
+#ifndef GSR_BWD_WARPS
+#define GSR_BWD_WARPS 4
+#endif
+constexpr int BWD_WARPS = GSR_BWD_WARPS;
 constexpr int BWD_THREADS = BWD_WARPS * 32;
 constexpr int MAX_IMAGES = 64;
 constexpr uint32_t KEY_SENTINEL_FLAG = 0xffffffffu;
@@ -47,7 +55,7 @@ struct DevImg {
     int offx, offy;           // cell-grid offsets (multiples of CELL, >= max rect extent)
     int ncx, ncy, cell_base;  // cells of this image: [cell_base, cell_base + ncx*ncy)
     int ntx, nty, tile_base;  // backward tiles (TILE_W x TILE_H) of this image
-    int fntx, fnty, ftile_base;  // forward tiles (FTILE_W x FTILE_H)
+    int fntx, fnty, ftile_base;  // forward tiles (ImgTable::ftile_w x ftile_h)
     int wmax, hmax;           // upper bounds on the unclipped rect width/height
 };
 
@@ -56,6 +64,8 @@ struct ImgTable {
     int total_cells;          // key of an unbinned Gaussian (sorts last)
     int total_tiles;          // backward tiles
     int total_ftiles;         // forward tiles
+    int ftile_w, ftile_h;     // forward tile of this call (large or small configuration)
+    int fwd_small;            // 1: FwdCfgSmall
     DevImg img[MAX_IMAGES];
 };
 

@@ -26,9 +26,18 @@
 // leave the CTA as 8 fp64 atomics -- the only global atomics of the backward.
 #include "gsr_internal.cuh"
 
+#ifndef GSR_BWD_UNROLL
+#define GSR_BWD_UNROLL 4
+#endif
+#ifndef GSR_BWD_MACC_T
+#define GSR_BWD_MACC_T float      // per-(Gaussian, tile) accumulator type of the row folds
+#endif
+
 namespace gsr {
 
 namespace {
+
+constexpr int kBwdUnroll = GSR_BWD_UNROLL;
 
 __device__ __forceinline__ float2 f2(float a) { return make_float2(a, a); }
 
@@ -83,7 +92,7 @@ __device__ __forceinline__ void row2_pairs(int c_begin, int c_end, const float4*
                                            RowAcc& A0, RowAcc& A1) {
     float2 kx = make_float2(kT + (float)c_begin, kT + (float)(c_begin + 1));
     const float2 two = f2(2.0f);
-#pragma unroll 2
+#pragma unroll kBwdUnroll
     for (int c = c_begin; c < c_end; c += 2) {
         const int cp = c >> 1;
         bool in0 = true, in1 = true;
@@ -99,12 +108,13 @@ __device__ __forceinline__ void row2_pairs(int c_begin, int c_end, const float4*
 }
 
 // fold one row's partials into the fp64 per-(Gaussian, tile) moments
+typedef GSR_BWD_MACC_T macc_t;
 __device__ __forceinline__ void fold_row(const RowAcc& A, float v, const float4 r1, const float4 r2,
-                                         double (&m)[8]) {
+                                         macc_t (&m)[8]) {
     const float fr = A.FR.x + A.FR.y, fg = A.FG.x + A.FG.y, fb = A.FB.x + A.FB.y;
-    const double w0 = (double)fmaf(r1.w, fr, fmaf(r2.x, fg, r2.y * fb));
-    const double w1 = (double)A.W1.x + (double)A.W1.y, w2 = (double)A.W2.x + (double)A.W2.y;
-    const double vq = (double)v;
+    const macc_t w0 = (macc_t)fmaf(r1.w, fr, fmaf(r2.x, fg, r2.y * fb));
+    const macc_t w1 = (macc_t)A.W1.x + (macc_t)A.W1.y, w2 = (macc_t)A.W2.x + (macc_t)A.W2.y;
+    const macc_t vq = (macc_t)v;
     m[0] += fr; m[1] += fg; m[2] += fb;
     m[3] += w1;
     m[4] = fma(vq, w0, m[4]);
@@ -203,9 +213,9 @@ __global__ void __launch_bounds__(BWD_THREADS) k_render_bwd(
             L.x0 = x0; L.x1 = x1;
             const float kT = (float)Tx0 - r0.x;
             const float tdl = -r1.x * r0.z;                        // -a1 dl_x
-            double m[8];
+            macc_t m[8];
 #pragma unroll
-            for (int k = 0; k < 8; ++k) m[k] = 0.0;
+            for (int k = 0; k < 8; ++k) m[k] = (macc_t)0;
             for (int y = ya; y <= yb; y += 2) {
                 // rows y and y + 1 (the second one is a phantom when y == yb: u = -inf)
                 const int y1r = y + 1;
@@ -234,7 +244,7 @@ __global__ void __launch_bounds__(BWD_THREADS) k_render_bwd(
             if (act) {
                 double* dst = moments + 8LL * perm[p];
 #pragma unroll
-                for (int k = 0; k < 8; ++k) atomicAdd(dst + k, m[k]);
+                for (int k = 0; k < 8; ++k) atomicAdd(dst + k, (double)m[k]);
             }
         }
     }

@@ -24,6 +24,8 @@
 //     mbarriers per stage; no CTA-wide barrier in the main loop).
 //   * two-level sums: per-chunk partials in registers, folded into per-thread totals in shared
 //     memory after every chunk (<= 128 Gaussians).
+//   * two tile configurations (gsr_internal.cuh): 2 x 8 px per lane / 32 x 16 tiles, or for
+//     narrow windows 1 x 4 px per lane / 16 x 8 tiles (fewer masked evaluations).
 //   * split-K for small problems: KS CTAs of a cluster share a tile, take every KS-th chunk, and
 //     reduce their totals through DSMEM in cluster-rank order (deterministic, no atomics).
 #include "gsr_internal.cuh"
@@ -74,9 +76,9 @@ __device__ __forceinline__ float2 ld_dsmem_f2(const float2* local_addr, uint32_t
 
 __device__ __forceinline__ float2 f2(float a) { return make_float2(a, a); }
 
-constexpr int NACC = FWD_ROWS * (FWD_STRIP / 2) * 3;   // float2 accumulators per thread (24)
-
+template <class CFG>
 struct FwdSmem {
+    static constexpr int NACC = CFG::ROWS * (CFG::STRIP / 2) * 3;   // float2 accumulators/thread
     float4 rec[FWD_STAGES][FWD_CHUNK * 3];
     float2 tot[FWD_CWARPS][NACC][32];        // per-warp totals (second accumulation level)
     uint16_t idx[FWD_STAGES][FWD_CHUNK];     // kept records: index | full-x << 8 | full-y << 9
@@ -89,11 +91,12 @@ struct FwdSmem {
 
 // Transformed record (written in shared memory by the producer warp, see k_render_fwd):
 //   r0 = {-ax, ay, dl_y, a1/s},  r1 = {-a1 dl_x, b1, c1, c'_r},  r2 = {c'_g, c'_b, x0|x1, y0|y1}
-template <bool FULL>
+template <class CFG, bool FULL>
 __device__ __forceinline__ void fwd_gauss(const float4 r0, const float4 r1, const float4 r2,
-                                          const float2 (&xj)[FWD_STRIP / 2], float yf0,
-                                          const int (&yi)[FWD_ROWS], int xl0, float invs,
-                                          float2 (&acc)[NACC]) {
+                                          const float2 (&xj)[CFG::STRIP / 2], float yf0,
+                                          const int (&yi)[CFG::ROWS], int xl0, float invs,
+                                          float2 (&acc)[FwdSmem<CFG>::NACC]) {
+    constexpr int FWD_STRIP = CFG::STRIP, FWD_ROWS = CFG::ROWS;
     const float2 D2 = f2(r0.w);
     const float2 nax = f2(r0.x);
     // kx = x - ax for the lane's 8 columns: exact small integers (one FADD2 per column pair)
@@ -138,7 +141,7 @@ __device__ __forceinline__ void fwd_gauss(const float4 r0, const float4 r1, cons
     }
 }
 
-template <int KS, bool LOSS>
+template <int KS, bool LOSS, class CFG>
 __global__ void __launch_bounds__(FWD_THREADS) k_render_fwd(const ImgTable tab,
                                                             const float4* __restrict__ rec,
                                                             const int* __restrict__ cell_start,
@@ -146,7 +149,9 @@ __global__ void __launch_bounds__(FWD_THREADS) k_render_fwd(const ImgTable tab,
                                                             const float* __restrict__ gt,
                                                             double* __restrict__ loss_acc) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    FwdSmem& sm = *reinterpret_cast<FwdSmem*>(smem_raw);
+    FwdSmem<CFG>& sm = *reinterpret_cast<FwdSmem<CFG>*>(smem_raw);
+    constexpr int FTILE_W = CFG::TW, FTILE_H = CFG::TH, FWD_STRIP = CFG::STRIP,
+                  FWD_ROWS = CFG::ROWS, NACC = FwdSmem<CFG>::NACC;
 
     const int tile = blockIdx.x / KS;
     const int krank = KS > 1 ? (int)cluster_rank() : 0;
@@ -290,9 +295,9 @@ __global__ void __launch_bounds__(FWD_THREADS) k_render_fwd(const ImgTable tab,
                 const int g = e & 0xff;
                 const float4 r0 = sr[3 * g], r1 = sr[3 * g + 1], r2 = sr[3 * g + 2];
                 if (e & 0x100)
-                    fwd_gauss<true>(r0, r1, r2, xj, yf0, yi, xl0, invs, acc);
+                    fwd_gauss<CFG, true>(r0, r1, r2, xj, yf0, yi, xl0, invs, acc);
                 else
-                    fwd_gauss<false>(r0, r1, r2, xj, yf0, yi, xl0, invs, acc);
+                    fwd_gauss<CFG, false>(r0, r1, r2, xj, yf0, yi, xl0, invs, acc);
             }
             // fold the chunk partials into the per-warp totals (second accumulation level)
 #pragma unroll
@@ -363,13 +368,13 @@ __global__ void __launch_bounds__(FWD_THREADS) k_render_fwd(const ImgTable tab,
     }
 }
 
-template <int KS, bool LOSS>
-cudaError_t launch_ks2(const ImgTable& tab, const Workspace& ws, float* out, const float* gt,
+template <int KS, bool LOSS, class CFG>
+cudaError_t launch_ks3(const ImgTable& tab, const Workspace& ws, float* out, const float* gt,
                        double* loss_acc, cudaStream_t st) {
     static bool attr_set = false;
-    const size_t smem = sizeof(FwdSmem);
+    const size_t smem = sizeof(FwdSmem<CFG>);
     if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(k_render_fwd<KS, LOSS>,
+        cudaError_t e = cudaFuncSetAttribute(k_render_fwd<KS, LOSS, CFG>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)smem);
         if (e != cudaSuccess) return e;
@@ -387,8 +392,15 @@ cudaError_t launch_ks2(const ImgTable& tab, const Workspace& ws, float* out, con
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, k_render_fwd<KS, LOSS>, tab, (const float4*)ws.rec,
+    return cudaLaunchKernelEx(&cfg, k_render_fwd<KS, LOSS, CFG>, tab, (const float4*)ws.rec,
                               (const int*)ws.cell_start, out, gt, loss_acc);
+}
+
+template <int KS, bool LOSS>
+cudaError_t launch_ks2(const ImgTable& tab, const Workspace& ws, float* out, const float* gt,
+                       double* loss_acc, cudaStream_t st) {
+    return tab.fwd_small ? launch_ks3<KS, LOSS, FwdCfgSmall>(tab, ws, out, gt, loss_acc, st)
+                         : launch_ks3<KS, LOSS, FwdCfgLarge>(tab, ws, out, gt, loss_acc, st);
 }
 
 template <int KS>
