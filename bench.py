@@ -11,8 +11,10 @@ rank renders a pair-balanced HR row band of every image, then the output bands a
 and the backward moments all-reduced over NCCL (paper_2501_06838_b200/dist.py).
 
 Rank 0 prints ONE JSON line. value = HR Mpix/s of the whole job (fwd+bwd: output pixels of the
-batch per step / step time); gpairs_per_s = Gaussian-pixel evaluations per second (the work unit,
-P pairs per pass, counted twice per step). `--impl reference` times the float64 CPU oracle
+batch per step / step time); gpairs_per_s = (Gaussian, pixel) pairs of the windows resolved per
+second (the paper's work unit, P pairs per pass, counted twice per step); gpairs_evaluated_per_s
+and the roofline count the pairs the kernels evaluate, those inside the support rects (DESIGN.md
+reading R21: every pair outside contributes exactly 0 in fp32). `--impl reference` times the float64 CPU oracle
 (oracle/, test infrastructure) on a bounded sample of the same workload on the host cores.
 """
 from __future__ import annotations
@@ -278,11 +280,14 @@ def main():
                                bounds[k][rank + 1]) for k, (H, W, s) in enumerate(imgs)]
     lay = gsr.layout(band_imgs)
     full_pix = sum(h * w for h, w in dims)
+    # P (the paper's work unit): pairs inside the windows; P_eval: pairs inside the support rects,
+    # the pairs the kernels evaluate (reading R21; outside them every term is exactly 0 in fp32)
     P_rank = gsr.pair_count(*params, lay, RATIO)
-    Pt = torch.tensor([P_rank], dtype=torch.int64, device=dev)
+    P_rank_eval = gsr.pair_count(*params, lay, RATIO, support=True)
+    Pt = torch.tensor([P_rank, P_rank_eval], dtype=torch.int64, device=dev)
     if world > 1:
         dist.all_reduce(Pt)
-    P_total = int(Pt.item())
+    P_total, P_total_eval = int(Pt[0].item()), int(Pt[1].item())
 
     # grad_out for this rank's bands (the upstream gradient of the step, synthetic)
     g_band = torch.empty(lay.out_numel, dtype=torch.float32, device=dev)
@@ -390,7 +395,7 @@ def main():
     t_launch = phase_ms[kern] / ncall * 1e-3
     per_clk = FWD_PAIRS_PER_CLK_SM if kern == "render_fwd" else BWD_PAIRS_PER_CLK_SM
     peak = per_clk * SM_COUNT * f_clk / 1e9           # Gpair/s
-    achieved = P_rank / t_launch / 1e9
+    achieved = P_rank_eval / t_launch / 1e9
     roof = {"bound": "alu", "pipe": "SFU ex2" if kern == "render_fwd" else "FP32 FMA",
             "kernel": kern, "achieved": achieved, "peak": peak, "unit": "Gpair/s",
             "frac": achieved / peak, "traffic": ncu_traffic(args.workload, kern),
@@ -398,14 +403,15 @@ def main():
                           f"({pk['source']})",
             "frac_at_sampled_clock": (achieved / (per_clk * SM_COUNT * clocks["sm_mhz"] * 1e6 / 1e9)
                                       if clocks.get("sm_mhz") else None),
-            "pairs_per_launch": P_rank}
+            "pairs_per_launch": P_rank_eval,
+            "work_unit": "evaluated (Gaussian, pixel) pair: inside the support rect (R21)"}
     other = "render_bwd" if kern == "render_fwd" else "render_fwd"
     if phase_calls.get(other):
         t_o = phase_ms[other] / phase_calls[other] * 1e-3
         pc = FWD_PAIRS_PER_CLK_SM if other == "render_fwd" else BWD_PAIRS_PER_CLK_SM
         pko = pc * SM_COUNT * f_clk / 1e9
-        roof["other_kernel"] = {"kernel": other, "achieved": P_rank / t_o / 1e9, "peak": pko,
-                                "frac": P_rank / t_o / 1e9 / pko}
+        roof["other_kernel"] = {"kernel": other, "achieved": P_rank_eval / t_o / 1e9,
+                                "peak": pko, "frac": P_rank_eval / t_o / 1e9 / pko}
     share = {k: v / max(ms_total if world == 1 else ms, 1e-9) for k, v in phase_ms.items()}
 
     cpu = None
@@ -435,10 +441,12 @@ def main():
             "config": {"workload": f"{args.workload}: {cfg['desc']}", "images": len(imgs),
                        "lr_hw": [imgs[0][0], imgs[0][1]], "scale": imgs[0][2], "ratio": RATIO,
                        "m": 16, "gaussians": n, "pairs_per_pass": P_total,
+                       "pairs_evaluated_per_pass": P_total_eval,
                        "parallelism": (f"{args.partition} x{world}" if world > 1
                                        else "single GPU"),
                        "l2": "working set > 126 MB L2 (params 1.6 GB, image 2.1 GB); no flush"},
             "gpairs_per_s": 2 * P_total / (ms_step * 1e-3) / 1e9,
+            "gpairs_evaluated_per_s": 2 * P_total_eval / (ms_step * 1e-3) / 1e9,
             "gpu_launches": int(launches),
             "phase_ms_per_step": {k: v / args.steps for k, v in phase_ms.items()},
             "phase_share": share,

@@ -187,14 +187,30 @@ gsr_status gsr_train_step_l1_batched(const float* raw_alpha, const float* offset
                                      float* d_raw_color, void* workspace, size_t workspace_bytes,
                                      void* stream);
 
+/* Evaluation support (reading R21): a pair with Q >= 13.5^2 has exp(-Q/2) < 2^-131,
+ * exactly 0 in the kernels' fp32 (flush-to-zero) exp, and every pixel outside the box
+ * |x/s - mu_x| <= 13.5 sigma_x, |y/s - mu_y| <= 13.5 sigma_y is such a pair. The render kernels
+ * evaluate each Gaussian over its SUPPORT RECT = window rect (R2) intersected with the integer box
+ * [floor(s (mu - 13.5 sigma)), ceil(s (mu + 13.5 sigma))] (fp64, per axis); the results equal
+ * those of an evaluation over the whole window. GSR_SUPPORT selects the support rect in the
+ * introspection / counting calls below (default: the window rect of Alg. 1). */
+#define GSR_SUPPORT 0x2u
+
 /* Number of (Gaussian, pixel) pairs inside the windows, P = sum_i |rect_i| restricted to each
- * image's row band (the work unit of the roofline). Writes one int64 to *d_pairs
- * (device pointer). Uses the workspace. */
+ * image's row band (the paper's work unit). Writes one int64 to *d_pairs (device
+ * pointer). Uses the workspace. The _ex form with GSR_SUPPORT counts the pairs inside the
+ * support rects instead (the pairs the kernels evaluate; the roofline's work unit). Other flag
+ * bits: GSR_EINVAL. */
 gsr_status gsr_pair_count_batched(const float* alpha, const float* mu, const float* sigma,
                                   const float* rho, const float* color, int64_t n_total,
                                   const gsr_image* imgs, int32_t n_imgs, double ratio,
                                   int64_t* d_pairs, void* workspace, size_t workspace_bytes,
                                   void* stream);
+gsr_status gsr_pair_count_batched_ex(const float* alpha, const float* mu, const float* sigma,
+                                     const float* rho, const float* color, int64_t n_total,
+                                     const gsr_image* imgs, int32_t n_imgs, double ratio,
+                                     uint32_t flags, int64_t* d_pairs, void* workspace,
+                                     size_t workspace_bytes, void* stream);
 
 /* ---- introspection for the parity tests (same kernels as the render path) ---------------- */
 
@@ -203,10 +219,15 @@ gsr_status gsr_pair_count_batched(const float* alpha, const float* mu, const flo
 gsr_status gsr_debug_rects(const float* alpha, const float* mu, const float* sigma,
                            const float* rho, const float* color, int64_t n, int32_t lr_h,
                            int32_t lr_w, double scale, double ratio, int32_t* rects, void* stream);
+/* The same with flags: GSR_SUPPORT returns the support rects (R21) the kernels evaluate. */
+gsr_status gsr_debug_rects_ex(const float* alpha, const float* mu, const float* sigma,
+                              const float* rho, const float* color, int64_t n, int32_t lr_h,
+                              int32_t lr_w, double scale, double ratio, uint32_t flags,
+                              int32_t* rects, void* stream);
 
 /* Tile binning, materialised: for every render tile of the single image (tiles of
  * tile_w x tile_h HR px in row-major tile order, as reported by gsr_tile_shape), the exact list of
- * Gaussians whose rect intersects the tile, in the order the render kernels visit them (cell
+ * Gaussians whose support rect (R21) intersects the tile, in the order the render kernels visit them (cell
  * order, ascending index within a cell). Two calls: first with ids == NULL to fill
  * counts[ntiles] (device int32); then with ids (device int32, sum(counts) entries, CSR by tile)
  * and cells (device int32, same length, the sort key = cell of each entry). */

@@ -32,6 +32,16 @@
  *   R7  |rho| < 1 precondition; no clamping of anything (R8).
  *   R20 invalid Gaussian (non-finite field, sigma<=0, |rho|>=1): contributes 0
  *       and gets zero gradient.
+ *   R21 evaluation support (an implementation reading, not the paper's): every
+ *       pair with Q >= 13.5^2 has exp(-Q/2) < 2^-131 (below the smallest fp32
+ *       normal, i.e. exactly 0 in the fp32 kernels); since Q >= (dx/sx)^2 and
+ *       Q >= (dy/sy)^2, such pairs include every pixel outside the box
+ *       |x/s - mu_x| <= 13.5 sx, |y/s - mu_y| <= 13.5 sy. Integer box:
+ *         bx0 = floor(s*(mu_x - 13.5*sx)),  bx1 = ceil(s*(mu_x + 13.5*sx))
+ *       in IEEE fp64 in exactly this order, clamped to +-2^30. The support
+ *       rect is window rect (R2) intersected with the box; its unclipped
+ *       origin is max(window origin, box origin). Mode "support" renders over
+ *       it; the difference to the window sum is pinned below 1e-30.
  *   Summation order: per pixel, ascending Gaussian index (brute and rect modes
  *   therefore give bit-identical results).
  *
@@ -117,6 +127,42 @@ static int oracle_rect(double mx, double my, int H, int W, double s, double r, i
     return (ax0 <= ax1) && (ay0 <= ay1);
 }
 
+/* R21: window rect intersected with the +-13.5 sigma box (see header). */
+#define ORACLE_SUPPORT_SIGMAS 13.5
+static int oracle_support_rect(double mx, double my, double sx, double sy, int H, int W,
+                               double s, double r, int Hs, int Ws, int64_t* x0u, int64_t* y0u,
+                               int64_t* x0, int64_t* x1, int64_t* y0, int64_t* y1)
+{
+    int64_t wx0u, wy0u;
+    if (!oracle_rect(mx, my, H, W, s, r, Hs, Ws, &wx0u, &wy0u, x0, x1, y0, y1)) return 0;
+    double tx = ORACLE_SUPPORT_SIGMAS * sx, ty = ORACLE_SUPPORT_SIGMAS * sy;
+    double lx = s * (mx - tx), ux = s * (mx + tx);
+    double ly = s * (my - ty), uy = s * (my + ty);
+    if (isnan(lx) || isnan(ux) || isnan(ly) || isnan(uy)) return 0;
+    int64_t bx0 = (int64_t)floor(oracle_clamp_bound(lx));
+    int64_t bx1 = (int64_t)ceil(oracle_clamp_bound(ux));
+    int64_t by0 = (int64_t)floor(oracle_clamp_bound(ly));
+    int64_t by1 = (int64_t)ceil(oracle_clamp_bound(uy));
+    if (x0u) *x0u = wx0u > bx0 ? wx0u : bx0;
+    if (y0u) *y0u = wy0u > by0 ? wy0u : by0;
+    if (*x0 < bx0) *x0 = bx0;
+    if (*x1 > bx1) *x1 = bx1;
+    if (*y0 < by0) *y0 = by0;
+    if (*y1 > by1) *y1 = by1;
+    return (*x0 <= *x1) && (*y0 <= *y1);
+}
+
+/* rect of Gaussian i in the given mode: 0 = window (R2), 1 = support (R21) */
+static int oracle_rect_mode(int support, const double* mu, const double* sigma, int64_t i, int H,
+                            int W, double s, double r, int Hs, int Ws, int64_t* x0u,
+                            int64_t* y0u, int64_t* x0, int64_t* x1, int64_t* y0, int64_t* y1)
+{
+    if (support)
+        return oracle_support_rect(mu[2 * i], mu[2 * i + 1], sigma[2 * i], sigma[2 * i + 1], H,
+                                   W, s, r, Hs, Ws, x0u, y0u, x0, x1, y0, y1);
+    return oracle_rect(mu[2 * i], mu[2 * i + 1], H, W, s, r, Hs, Ws, x0u, y0u, x0, x1, y0, y1);
+}
+
 /* R4 */
 void gsr_oracle_out_dims(int H, int W, double s, int* Hs, int* Ws)
 {
@@ -145,15 +191,15 @@ int gsr_oracle_max_threads(void)
 /* Per-Gaussian rects for tests: out[i*6 + {x0u,y0u,x0,x1,y0,y1}], empty -> x0>x1. */
 void gsr_oracle_rects(int64_t n, const double* alpha, const double* mu, const double* sigma,
                       const double* rho, const double* color, int H, int W, double s, double r,
-                      int64_t* out)
+                      int support, int64_t* out)
 {
     int Hs, Ws;
     gsr_oracle_out_dims(H, W, s, &Hs, &Ws);
     for (int64_t i = 0; i < n; ++i) {
         int64_t x0u = 0, y0u = 0, x0 = 1, x1 = 0, y0 = 1, y1 = 0;
         if (oracle_is_valid(alpha, mu, sigma, rho, color, i))
-            if (!oracle_rect(mu[2 * i], mu[2 * i + 1], H, W, s, r, Hs, Ws, &x0u, &y0u, &x0, &x1,
-                             &y0, &y1)) {
+            if (!oracle_rect_mode(support, mu, sigma, i, H, W, s, r, Hs, Ws, &x0u, &y0u, &x0, &x1,
+                                  &y0, &y1)) {
                 x0 = 1; x1 = 0; y0 = 1; y1 = 0;
             }
         int64_t* o = out + 6 * i;
@@ -165,7 +211,7 @@ void gsr_oracle_rects(int64_t n, const double* alpha, const double* mu, const do
  * to HR rows [row_begin, row_end). */
 int64_t gsr_oracle_pair_count(int64_t n, const double* alpha, const double* mu,
                               const double* sigma, const double* rho, const double* color, int H,
-                              int W, double s, double r, int row_begin, int row_end)
+                              int W, double s, double r, int row_begin, int row_end, int support)
 {
     int Hs, Ws;
     gsr_oracle_out_dims(H, W, s, &Hs, &Ws);
@@ -173,8 +219,8 @@ int64_t gsr_oracle_pair_count(int64_t n, const double* alpha, const double* mu,
     for (int64_t i = 0; i < n; ++i) {
         if (!oracle_is_valid(alpha, mu, sigma, rho, color, i)) continue;
         int64_t x0u, y0u, x0, x1, y0, y1;
-        if (!oracle_rect(mu[2 * i], mu[2 * i + 1], H, W, s, r, Hs, Ws, &x0u, &y0u, &x0, &x1, &y0,
-                         &y1))
+        if (!oracle_rect_mode(support, mu, sigma, i, H, W, s, r, Hs, Ws, &x0u, &y0u, &x0, &x1,
+                              &y0, &y1))
             continue;
         if (y0 < row_begin) y0 = row_begin;
         if (y1 > row_end - 1) y1 = row_end - 1;
@@ -189,6 +235,7 @@ int64_t gsr_oracle_pair_count(int64_t n, const double* alpha, const double* mu,
 /* mode 0 = brute: every Gaussian at every pixel, literal fp64 predicate.     */
 /* mode 1 = rect : every Gaussian over its integer rect (R2).                 */
 /* mode 2 = none : untruncated sum (r ignored), for the truncation bound.     */
+/* mode 3 = support: over the support rect (R21), as the CUDA path does.      */
 /* Output rows [row_begin, row_end) only: out[(y-row_begin)*Ws*3 + x*3 + k].  */
 /* ------------------------------------------------------------------------- */
 int gsr_oracle_render_fwd(int64_t n, const double* alpha, const double* mu, const double* sigma,
@@ -236,7 +283,10 @@ int gsr_oracle_render_fwd(int64_t n, const double* alpha, const double* mu, cons
             if (!oracle_is_valid(alpha, mu, sigma, rho, color, i)) continue;
             double mx = mu[2 * i], my = mu[2 * i + 1];
             int64_t x0u, y0u, x0, x1, y0, y1;
-            if (!oracle_rect(mx, my, H, W, s, r, Hs, Ws, &x0u, &y0u, &x0, &x1, &y0, &y1)) continue;
+            if (!oracle_rect_mode(mode == 3, mu, sigma, i, H, W, s, r, Hs, Ws, &x0u, &y0u, &x0,
+                                  &x1, &y0, &y1))
+                continue;
+            (void)mx; (void)my;
             if (y0 < row_begin) y0 = row_begin;
             if (y1 > row_end - 1) y1 = row_end - 1;
             for (int64_t y = y0; y <= y1; ++y) {
@@ -343,9 +393,10 @@ int gsr_oracle_render_bwd(int64_t n, const double* alpha, const double* mu, cons
             double D = 1.0 - rh * rh;
             int64_t xa = 0, xb = Ws - 1, ya = row_begin, yb = row_end - 1;
             int have = 1;
-            if (mode == 1) {
+            if (mode == 1 || mode == 3) {
                 int64_t x0u, y0u, x0, x1, y0, y1;
-                have = oracle_rect(mx, my, H, W, s, r, Hs, Ws, &x0u, &y0u, &x0, &x1, &y0, &y1);
+                have = oracle_rect_mode(mode == 3, mu, sigma, i, H, W, s, r, Hs, Ws, &x0u, &y0u,
+                                        &x0, &x1, &y0, &y1);
                 xa = x0; xb = x1;
                 ya = y0 > row_begin ? y0 : row_begin;
                 yb = y1 < row_end - 1 ? y1 : row_end - 1;
@@ -419,7 +470,7 @@ int gsr_oracle_render_bwd(int64_t n, const double* alpha, const double* mu, cons
 int64_t gsr_oracle_tile_lists(int64_t n, const double* alpha, const double* mu,
                               const double* sigma, const double* rho, const double* color, int H,
                               int W, double s, double r, int tw, int th, int row_begin,
-                              int row_end, int64_t* counts, int64_t* ids)
+                              int row_end, int support, int64_t* counts, int64_t* ids)
 {
     int Hs, Ws;
     gsr_oracle_out_dims(H, W, s, &Hs, &Ws);
@@ -437,8 +488,8 @@ int64_t gsr_oracle_tile_lists(int64_t n, const double* alpha, const double* mu,
             for (int64_t i = 0; i < n; ++i) {
                 if (!oracle_is_valid(alpha, mu, sigma, rho, color, i)) continue;
                 int64_t x0u, y0u, x0, x1, y0, y1;
-                if (!oracle_rect(mu[2 * i], mu[2 * i + 1], H, W, s, r, Hs, Ws, &x0u, &y0u, &x0,
-                                 &x1, &y0, &y1))
+                if (!oracle_rect_mode(support, mu, sigma, i, H, W, s, r, Hs, Ws, &x0u, &y0u, &x0,
+                                      &x1, &y0, &y1))
                     continue;
                 if (x1 < tx0 || x0 > tx1 || y1 < ty0 || y0 > ty1) continue;
                 if (ids) ids[total] = i;

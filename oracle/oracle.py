@@ -45,15 +45,15 @@ class OracleLib:
         lib.gsr_oracle_set_threads.argtypes = [_i32]
         lib.gsr_oracle_max_threads.restype = _i32
         par = [_i64, _p, _p, _p, _p, _p, _i32, _i32, _dbl, _dbl]
-        lib.gsr_oracle_rects.argtypes = par + [_p]
-        lib.gsr_oracle_pair_count.argtypes = par + [_i32, _i32]
+        lib.gsr_oracle_rects.argtypes = par + [_i32, _p]
+        lib.gsr_oracle_pair_count.argtypes = par + [_i32, _i32, _i32]
         lib.gsr_oracle_pair_count.restype = _i64
         lib.gsr_oracle_render_fwd.argtypes = par + [_i32, _i32, _i32, _p]
         lib.gsr_oracle_render_pixels.argtypes = par + [_i64, _p, _p, _p]
         lib.gsr_oracle_field.argtypes = [_i64, _p, _p, _p, _p, _p, _dbl, _dbl, _i64, _p, _p]
         lib.gsr_oracle_render_bwd.argtypes = par + [_i32, _i32, _i32, _p, _i64, _p, _p, _p, _p,
                                                     _p, _p, _p]
-        lib.gsr_oracle_tile_lists.argtypes = par + [_i32, _i32, _i32, _i32, _p, _p]
+        lib.gsr_oracle_tile_lists.argtypes = par + [_i32, _i32, _i32, _i32, _i32, _p, _p]
         lib.gsr_oracle_tile_lists.restype = _i64
         self.lib = lib
 
@@ -96,7 +96,7 @@ def out_dims(H: int, W: int, s: float):
     return hs.value, ws.value
 
 
-MODES = {"brute": 0, "rect": 1, "none": 2}
+MODES = {"brute": 0, "rect": 1, "none": 2, "support": 3}
 
 
 def render_fwd(cloud, H, W, s, r=0.1, mode="rect", rows=None) -> np.ndarray:
@@ -162,25 +162,27 @@ def render_bwd(cloud, H, W, s, r, grad_out, mode="rect", rows=None, idx=None,
     return res
 
 
-def rects(cloud, H, W, s, r=0.1) -> np.ndarray:
-    """[n,6] int64: x0u, y0u (unclipped starts), x0, x1, y0, y1 (clipped; empty -> x0>x1)."""
+def rects(cloud, H, W, s, r=0.1, support=False) -> np.ndarray:
+    """[n,6] int64: x0u, y0u (unclipped starts), x0, x1, y0, y1 (clipped; empty -> x0>x1).
+    support=True: the window rect intersected with the +-13.5 sigma box (reading R21)."""
     a, mu, sg, rh, c = _params(cloud)
     out = np.zeros((a.shape[0], 6), np.int64)
     load().lib.gsr_oracle_rects(a.shape[0], _ptr(a), _ptr(mu), _ptr(sg), _ptr(rh), _ptr(c),
-                                int(H), int(W), float(s), float(r), _ptr(out))
+                                int(H), int(W), float(s), float(r), int(bool(support)), _ptr(out))
     return out
 
 
-def pair_count(cloud, H, W, s, r=0.1, rows=None) -> int:
+def pair_count(cloud, H, W, s, r=0.1, rows=None, support=False) -> int:
+    """Pairs passing the window predicate (support=True: inside the support rect, R21)."""
     a, mu, sg, rh, c = _params(cloud)
     Hs, _ = out_dims(H, W, s)
     rb, re = (0, Hs) if rows is None else rows
     return int(load().lib.gsr_oracle_pair_count(a.shape[0], _ptr(a), _ptr(mu), _ptr(sg),
                                                 _ptr(rh), _ptr(c), int(H), int(W), float(s),
-                                                float(r), int(rb), int(re)))
+                                                float(r), int(rb), int(re), int(bool(support))))
 
 
-def tile_lists(cloud, H, W, s, r, tw, th, rows=None):
+def tile_lists(cloud, H, W, s, r, tw, th, rows=None, support=False):
     """Brute-force per-tile Gaussian lists: (counts[nty*ntx], ids) CSR, ascending i."""
     a, mu, sg, rh, c = _params(cloud)
     Hs, Ws = out_dims(H, W, s)
@@ -190,7 +192,7 @@ def tile_lists(cloud, H, W, s, r, tw, th, rows=None):
     counts = np.zeros(ntx * nty, np.int64)
     lib = load().lib
     args = (a.shape[0], _ptr(a), _ptr(mu), _ptr(sg), _ptr(rh), _ptr(c), int(H), int(W), float(s),
-            float(r), int(tw), int(th), int(rb), int(re))
+            float(r), int(tw), int(th), int(rb), int(re), int(bool(support)))
     total = lib.gsr_oracle_tile_lists(*args, _ptr(counts), None)
     ids = np.zeros(max(total, 1), np.int64)
     lib.gsr_oracle_tile_lists(*args, _ptr(counts), _ptr(ids))

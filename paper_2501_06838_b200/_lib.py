@@ -22,8 +22,10 @@ EXPORTS = ["gsr_version", "gsr_out_dims", "gsr_workspace_bytes_batched", "gsr_wo
            "gsr_render_bwd_moments_batched", "gsr_finalize_grads", "gsr_pair_count_batched",
            "gsr_debug_rects", "gsr_debug_tile_lists", "gsr_tile_shape", "gsr_profile_enable",
            "gsr_profile_collect", "gsr_render_bwd_batched_ex", "gsr_render_bwd_moments_batched_ex",
-           "gsr_train_workspace_bytes_batched", "gsr_train_step_l1_batched"]
+           "gsr_train_workspace_bytes_batched", "gsr_train_step_l1_batched",
+           "gsr_pair_count_batched_ex", "gsr_debug_rects_ex"]
 GSR_REUSE_BINNING = 0x1
+GSR_SUPPORT = 0x2
 
 
 class GsrImage(ctypes.Structure):
@@ -79,7 +81,10 @@ def load(path: Path | str | None = None):
         "gsr_train_step_l1_batched": ([_P] * 6 + [_I64, _IMGP, _I32, _D, ctypes.c_float, _D, _P,
                                                   _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P], None),
         "gsr_pair_count_batched": (par + [_I64, _IMGP, _I32, _D, _P, _P, _SZ, _P], None),
+        "gsr_pair_count_batched_ex": (par + [_I64, _IMGP, _I32, _D, ctypes.c_uint32, _P, _P, _SZ,
+                                             _P], None),
         "gsr_debug_rects": (par + [_I64, _I32, _I32, _D, _D, _P, _P], None),
+        "gsr_debug_rects_ex": (par + [_I64, _I32, _I32, _D, _D, ctypes.c_uint32, _P, _P], None),
         "gsr_debug_tile_lists": (par + [_I64, _I32, _I32, _D, _D, _P, _P, _P, _P, _SZ, _P], None),
         "gsr_tile_shape": ([ctypes.POINTER(_I32)] * 4, "void"),
         "gsr_profile_enable": ([_I32], None),

@@ -31,26 +31,46 @@ long long scan_blocks(long long n) { return (n + SCAN_BLOCK - 1) / SCAN_BLOCK; }
 __global__ void k_keys(const float* __restrict__ alpha, const float* __restrict__ mu,
                        const float* __restrict__ sigma, const float* __restrict__ rho,
                        const float* __restrict__ color, long long n, ImgTable tab,
-                       uint32_t* __restrict__ keys, int* __restrict__ vals) {
+                       uint32_t* __restrict__ keys, int* __restrict__ vals,
+                       int* __restrict__ ext) {
     long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
     uint32_t key = (uint32_t)tab.total_cells;
-    int k = find_image_by_gauss(tab, i);
-    if (k >= 0) {
-        const DevImg& im = tab.img[k];
-        float mx = mu[2 * i], my = mu[2 * i + 1];
-        if (gaussian_valid(alpha[i], mx, my, sigma[2 * i], sigma[2 * i + 1], rho[i],
-                           color[3 * i], color[3 * i + 1], color[3 * i + 2])) {
-            Rect r = window_rect(mx, my, im);
-            if (r.nonempty) {
-                int cx = (r.x0u + im.offx) / CELL;
-                int cy = (r.y0u - im.row_begin + im.offy) / CELL;
-                key = (uint32_t)(im.cell_base + cy * im.ncx + cx);
+    int k = -1, wx = 0, wy = 0;
+    if (i < n) {
+        k = find_image_by_gauss(tab, i);
+        if (k >= 0) {
+            const DevImg& im = tab.img[k];
+            float mx = mu[2 * i], my = mu[2 * i + 1];
+            if (gaussian_valid(alpha[i], mx, my, sigma[2 * i], sigma[2 * i + 1], rho[i],
+                               color[3 * i], color[3 * i + 1], color[3 * i + 2])) {
+                Rect r = support_rect(mx, my, sigma[2 * i], sigma[2 * i + 1], im);
+                if (r.nonempty) {
+                    // key: cell of the unclipped support origin (>= the window origin, so
+                    // inside the window-sized cell domain)
+                    int cx = (r.x0u + im.offx) / CELL;
+                    int cy = (r.y0u - im.row_begin + im.offy) / CELL;
+                    key = (uint32_t)(im.cell_base + cy * im.ncx + cx);
+                    wx = r.x1u - r.x0u + 1;
+                    wy = r.y1u - r.y0u + 1;
+                }
             }
         }
+        keys[i] = key;
+        vals[i] = (int)i;
     }
-    keys[i] = key;
-    vals[i] = (int)i;
+    // per-image max support extent: warp max over lanes of the same image, one atomic each
+    const unsigned full = 0xffffffffu;
+    const unsigned same = __match_any_sync(full, k);
+    int mwx = wx, mwy = wy;
+    for (unsigned m = same; m; m &= m - 1) {
+        const int l = __ffs(m) - 1;
+        mwx = max(mwx, __shfl_sync(full, wx, l));
+        mwy = max(mwy, __shfl_sync(full, wy, l));
+    }
+    if (k >= 0 && (same & ((1u << (threadIdx.x & 31)) - 1u)) == 0 && (mwx | mwy)) {
+        atomicMax(&ext[2 * k], mwx);
+        atomicMax(&ext[2 * k + 1], mwy);
+    }
 }
 
 // ---- stable LSD radix sort, 8-bit digits -----------------------------------------------
@@ -229,7 +249,7 @@ __global__ void k_records(const float* __restrict__ alpha, const float* __restri
     int k = find_image_by_gauss(tab, i);
     const DevImg& im = tab.img[k];
     float mxf = mu[2 * i], myf = mu[2 * i + 1];
-    Rect r = window_rect(mxf, myf, im);
+    Rect r = support_rect(mxf, myf, sigma[2 * i], sigma[2 * i + 1], im);
     double mx = mxf, my = myf;
     double sx = sigma[2 * i], sy = sigma[2 * i + 1], rh = rho[i], al = alpha[i];
     double D = (1.0 - rh) * (1.0 + rh);
@@ -257,7 +277,7 @@ __global__ void k_records(const float* __restrict__ alpha, const float* __restri
 __global__ void k_pair_count(const float* __restrict__ alpha, const float* __restrict__ mu,
                              const float* __restrict__ sigma, const float* __restrict__ rho,
                              const float* __restrict__ color, long long n, ImgTable tab,
-                             unsigned long long* __restrict__ out) {
+                             bool support, unsigned long long* __restrict__ out) {
     long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     unsigned long long v = 0;
     if (i < n) {
@@ -267,7 +287,8 @@ __global__ void k_pair_count(const float* __restrict__ alpha, const float* __res
             float mx = mu[2 * i], my = mu[2 * i + 1];
             if (gaussian_valid(alpha[i], mx, my, sigma[2 * i], sigma[2 * i + 1], rho[i],
                                color[3 * i], color[3 * i + 1], color[3 * i + 2])) {
-                Rect r = window_rect(mx, my, im);
+                Rect r = support ? support_rect(mx, my, sigma[2 * i], sigma[2 * i + 1], im)
+                                 : window_rect(mx, my, im);
                 if (r.nonempty)
                     v = (unsigned long long)(r.x1 - r.x0 + 1) * (unsigned long long)(r.y1 - r.y0 + 1);
             }
@@ -281,7 +302,7 @@ __global__ void k_pair_count(const float* __restrict__ alpha, const float* __res
 __global__ void k_debug_rects(const float* __restrict__ alpha, const float* __restrict__ mu,
                               const float* __restrict__ sigma, const float* __restrict__ rho,
                               const float* __restrict__ color, long long n, ImgTable tab,
-                              int4* __restrict__ rects) {
+                              bool support, int4* __restrict__ rects) {
     long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     int4 o = make_int4(1, 0, 1, 0);
@@ -291,7 +312,8 @@ __global__ void k_debug_rects(const float* __restrict__ alpha, const float* __re
         float mx = mu[2 * i], my = mu[2 * i + 1];
         if (gaussian_valid(alpha[i], mx, my, sigma[2 * i], sigma[2 * i + 1], rho[i],
                            color[3 * i], color[3 * i + 1], color[3 * i + 2])) {
-            Rect r = window_rect(mx, my, im);
+            Rect r = support ? support_rect(mx, my, sigma[2 * i], sigma[2 * i + 1], im)
+                             : window_rect(mx, my, im);
             if (r.nonempty) o = make_int4(r.x0, r.x1, r.y0, r.y1);
         }
     }
@@ -300,20 +322,22 @@ __global__ void k_debug_rects(const float* __restrict__ alpha, const float* __re
 
 // Materialised per-tile candidate lists, walking the same cell spans as the render kernels and
 // keeping the candidates whose rect intersects the tile. One thread per tile (test-only).
-__global__ void k_debug_tile_lists(ImgTable tab, const int* __restrict__ cell_start,
+__global__ void k_debug_tile_lists(ImgTable tab, const int* __restrict__ ext,
+                                   const int* __restrict__ cell_start,
                                    const float4* __restrict__ rec, const int* __restrict__ perm,
                                    const uint32_t* __restrict__ keys,
                                    const int* __restrict__ tile_off, int* __restrict__ counts,
                                    int* __restrict__ ids, int* __restrict__ cells) {
     int tile = blockIdx.x * blockDim.x + threadIdx.x;
     if (tile >= tab.total_tiles) return;
-    const DevImg& im = tab.img[find_image_by_tile(tab, tile)];
+    const int kimg = find_image_by_tile(tab, tile);
+    const DevImg& im = tab.img[kimg];
     int t = tile - im.tile_base;
     int Tx0 = (t % im.ntx) * TILE_W, Ty0 = im.row_begin + (t / im.ntx) * TILE_H;
     int Tx1 = min(Tx0 + TILE_W - 1, im.Ws - 1), Ty1 = min(Ty0 + TILE_H - 1, im.row_end - 1);
-    int cx_lo = (Tx0 - im.wmax + 1 + im.offx) / CELL;
+    int cx_lo = (Tx0 - query_ext(ext, kimg, 0) + 1 + im.offx) / CELL;
     int cx_hi = min(im.ncx - 1, (Tx1 + im.offx) / CELL);
-    int cy_lo = (Ty0 - im.row_begin - im.hmax + 1 + im.offy) / CELL;
+    int cy_lo = (Ty0 - im.row_begin - query_ext(ext, kimg, 1) + 1 + im.offy) / CELL;
     int cy_hi = min(im.ncy - 1, (Ty1 - im.row_begin + im.offy) / CELL);
     int c = 0;
     int base = ids ? tile_off[tile] : 0;
@@ -352,6 +376,7 @@ size_t binning_bytes(long long n, int total_cells, int total_tiles) {
     b += align256(sizeof(double) * 8 * (size_t)n);              // moments
     b += align256(sizeof(unsigned long long) * 4);              // counters
     b += align256(sizeof(int) * (size_t)(total_tiles + 1));     // debug tile offsets
+    b += align256(sizeof(int) * 2 * MAX_IMAGES);                // support extents
     return b + 256;
 }
 
@@ -372,6 +397,7 @@ void carve_workspace(void* base, long long n, int total_cells, int total_tiles, 
     ws->moments = (double*)take(sizeof(double) * 8 * (size_t)n);
     ws->counter = (unsigned long long*)take(sizeof(unsigned long long) * 4);
     ws->tile_off = (int*)take(sizeof(int) * (size_t)(total_tiles + 1));
+    ws->ext = (int*)take(sizeof(int) * 2 * MAX_IMAGES);
 }
 
 cudaError_t exclusive_scan_i32(const int* in, int* out, long long n, int* tmp, cudaStream_t st) {
@@ -388,10 +414,11 @@ cudaError_t bin_gaussians(const float* alpha, const float* mu, const float* sigm
                           const float* rho, const float* color, long long n,
                           const ImgTable& tab, Workspace& ws, int** perm_out,
                           uint32_t** keys_sorted_out, cudaStream_t st) {
+    cudaMemsetAsync(ws.ext, 0, sizeof(int) * 2 * MAX_IMAGES, st);
     if (n > 0) {
         count_launches(1);
         k_keys<<<grid1d(n, 256), 256, 0, st>>>(alpha, mu, sigma, rho, color, n, tab, ws.keys_a,
-                                               ws.vals_a);
+                                               ws.vals_a, ws.ext);
         int bits = 32 - __builtin_clz((unsigned)tab.total_cells | 1u);
         int passes = (bits + 7) / 8;
         long long nb = rs_blocks(n);
@@ -436,22 +463,24 @@ void binned_pointers(const ImgTable& tab, long long n, const Workspace& ws, int*
 
 cudaError_t launch_pair_count(const float* alpha, const float* mu, const float* sigma,
                               const float* rho, const float* color, long long n,
-                              const ImgTable& tab, long long* d_pairs, cudaStream_t st) {
+                              const ImgTable& tab, bool support, long long* d_pairs,
+                              cudaStream_t st) {
     cudaMemsetAsync(d_pairs, 0, sizeof(long long), st);
     if (n > 0) {
         count_launches(1);
         k_pair_count<<<grid1d(n, 256), 256, 0, st>>>(alpha, mu, sigma, rho, color, n, tab,
-                                                     (unsigned long long*)d_pairs);
+                                                     support, (unsigned long long*)d_pairs);
     }
     return cudaGetLastError();
 }
 
 cudaError_t launch_debug_rects(const float* alpha, const float* mu, const float* sigma,
                                const float* rho, const float* color, long long n,
-                               const ImgTable& tab, int* rects, cudaStream_t st) {
+                               const ImgTable& tab, bool support, int* rects,
+                               cudaStream_t st) {
     if (n > 0)
         k_debug_rects<<<grid1d(n, 256), 256, 0, st>>>(alpha, mu, sigma, rho, color, n, tab,
-                                                      (int4*)rects);
+                                                      support, (int4*)rects);
     return cudaGetLastError();
 }
 
@@ -461,16 +490,16 @@ cudaError_t launch_debug_tile_lists(const ImgTable& tab, const Workspace& ws, co
     int nt = tab.total_tiles;
     if (nt <= 0) return cudaSuccess;
     if (!ids) {
-        k_debug_tile_lists<<<grid1d(nt, 64), 64, 0, st>>>(tab, ws.cell_start, ws.rec, perm,
+        k_debug_tile_lists<<<grid1d(nt, 64), 64, 0, st>>>(tab, ws.ext, ws.cell_start, ws.rec, perm,
                                                           keys_sorted, nullptr, counts, nullptr,
                                                           nullptr);
     } else {
-        k_debug_tile_lists<<<grid1d(nt, 64), 64, 0, st>>>(tab, ws.cell_start, ws.rec, perm,
+        k_debug_tile_lists<<<grid1d(nt, 64), 64, 0, st>>>(tab, ws.ext, ws.cell_start, ws.rec, perm,
                                                           keys_sorted, nullptr, ws.tile_off,
                                                           nullptr, nullptr);
         cudaError_t e = exclusive_scan_i32(ws.tile_off, ws.tile_off, nt, ws.scan_tmp, st);
         if (e != cudaSuccess) return e;
-        k_debug_tile_lists<<<grid1d(nt, 64), 64, 0, st>>>(tab, ws.cell_start, ws.rec, perm,
+        k_debug_tile_lists<<<grid1d(nt, 64), 64, 0, st>>>(tab, ws.ext, ws.cell_start, ws.rec, perm,
                                                           keys_sorted, ws.tile_off, counts, ids,
                                                           cells);
     }

@@ -423,31 +423,50 @@ gsr_status gsr_train_step_l1_batched(const float* raw_alpha, const float* offset
     return finish(cudaSuccess);
 }
 
-gsr_status gsr_pair_count_batched(const float* alpha, const float* mu, const float* sigma,
-                                  const float* rho, const float* color, int64_t n_total,
-                                  const gsr_image* imgs, int32_t n_imgs, double ratio,
-                                  int64_t* d_pairs, void* workspace, size_t workspace_bytes,
-                                  void* stream) {
-    if (!d_pairs) return GSR_EINVAL;
+gsr_status gsr_pair_count_batched_ex(const float* alpha, const float* mu, const float* sigma,
+                                     const float* rho, const float* color, int64_t n_total,
+                                     const gsr_image* imgs, int32_t n_imgs, double ratio,
+                                     uint32_t flags, int64_t* d_pairs, void* workspace,
+                                     size_t workspace_bytes, void* stream) {
+    if (!d_pairs || (flags & ~GSR_SUPPORT)) return GSR_EINVAL;
     Prepared P;
     gsr_status s = prepare(alpha, mu, sigma, rho, color, n_total, imgs, n_imgs, ratio, workspace,
                            workspace_bytes, (cudaStream_t)stream, &P, false);
     if (s != GSR_OK) return s;
     return finish(launch_pair_count(alpha, mu, sigma, rho, color, n_total, P.tab,
-                                    (long long*)d_pairs, (cudaStream_t)stream));
+                                    (flags & GSR_SUPPORT) != 0, (long long*)d_pairs,
+                                    (cudaStream_t)stream));
+}
+
+gsr_status gsr_pair_count_batched(const float* alpha, const float* mu, const float* sigma,
+                                  const float* rho, const float* color, int64_t n_total,
+                                  const gsr_image* imgs, int32_t n_imgs, double ratio,
+                                  int64_t* d_pairs, void* workspace, size_t workspace_bytes,
+                                  void* stream) {
+    return gsr_pair_count_batched_ex(alpha, mu, sigma, rho, color, n_total, imgs, n_imgs, ratio,
+                                     0u, d_pairs, workspace, workspace_bytes, stream);
+}
+
+gsr_status gsr_debug_rects_ex(const float* alpha, const float* mu, const float* sigma,
+                              const float* rho, const float* color, int64_t n, int32_t lr_h,
+                              int32_t lr_w, double scale, double ratio, uint32_t flags,
+                              int32_t* rects, void* stream) {
+    if (flags & ~GSR_SUPPORT) return GSR_EINVAL;
+    gsr_image g = single(n, lr_h, lr_w, scale);
+    ImgTable tab;
+    gsr_status s = build_table(&g, 1, n, ratio, &tab);
+    if (s != GSR_OK) return s;
+    if (!params_ok(alpha, mu, sigma, rho, color, n) || (n > 0 && !rects)) return GSR_EINVAL;
+    return finish(launch_debug_rects(alpha, mu, sigma, rho, color, n, tab,
+                                     (flags & GSR_SUPPORT) != 0, rects, (cudaStream_t)stream));
 }
 
 gsr_status gsr_debug_rects(const float* alpha, const float* mu, const float* sigma,
                            const float* rho, const float* color, int64_t n, int32_t lr_h,
                            int32_t lr_w, double scale, double ratio, int32_t* rects,
                            void* stream) {
-    gsr_image g = single(n, lr_h, lr_w, scale);
-    ImgTable tab;
-    gsr_status s = build_table(&g, 1, n, ratio, &tab);
-    if (s != GSR_OK) return s;
-    if (!params_ok(alpha, mu, sigma, rho, color, n) || (n > 0 && !rects)) return GSR_EINVAL;
-    return finish(launch_debug_rects(alpha, mu, sigma, rho, color, n, tab, rects,
-                                     (cudaStream_t)stream));
+    return gsr_debug_rects_ex(alpha, mu, sigma, rho, color, n, lr_h, lr_w, scale, ratio, 0u,
+                              rects, stream);
 }
 
 gsr_status gsr_debug_tile_lists(const float* alpha, const float* mu, const float* sigma,

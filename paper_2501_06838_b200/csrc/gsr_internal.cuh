@@ -28,6 +28,10 @@ struct FwdCfgSmall { static constexpr int ROWS = 1, STRIP = 4, TW = 4 * STRIP, T
 constexpr int FTILE_W = FwdCfgLarge::TW;          // 32
 constexpr int FTILE_H = FwdCfgLarge::TH;          // 16
 constexpr int FWD_SMALL_WINDOW = 48;             // HR px: below this the small tiles are used
+#ifndef GSR_FWD_REC
+#define GSR_FWD_REC 1
+#endif
+constexpr float FWD_REC_DMAX = GSR_FWD_REC ? 1.0f : -1.0f;            // max a1/s for the forward's exp recurrence
 constexpr int FWD_CWARPS = 4;                    // consumer warps
 constexpr int FWD_THREADS = (FWD_CWARPS + 1) * 32;
 constexpr int FWD_CHUNK = 128;                   // records per TMA bulk stage
@@ -108,7 +112,7 @@ __host__ __device__ inline int find_image_by_gauss(const ImgTable& t, long long 
 }
 
 // ---- the normative window rect (reading R2), fp64, fixed op order, no FMA ---------------
-struct Rect { int x0u, y0u, x0, x1, y0, y1; bool nonempty; };
+struct Rect { int x0u, y0u, x1u, y1u, x0, x1, y0, y1; bool nonempty; };
 
 __device__ __forceinline__ double clamp_bound(double v) {
     const double lim = 1073741824.0;  // 2^30
@@ -128,6 +132,8 @@ __device__ __forceinline__ Rect window_rect(float mux, float muy, const DevImg& 
     long long ay1 = (long long)ceil(clamp_bound(uy)) - 1;
     r.x0u = (int)ax0;
     r.y0u = (int)ay0;
+    r.x1u = (int)ax1;
+    r.y1u = (int)ay1;
     long long cx0 = ax0 < 0 ? 0 : ax0;
     long long cx1 = ax1 > im.Ws - 1 ? im.Ws - 1 : ax1;
     long long cy0 = ay0 < im.row_begin ? im.row_begin : ay0;          // band clip
@@ -135,6 +141,40 @@ __device__ __forceinline__ Rect window_rect(float mux, float muy, const DevImg& 
     r.x0 = (int)cx0; r.x1 = (int)cx1; r.y0 = (int)cy0; r.y1 = (int)cy1;
     r.nonempty = (cx0 <= cx1) && (cy0 <= cy1) && !isnan(lx) && !isnan(ux) && !isnan(ly) &&
                  !isnan(uy);
+    return r;
+}
+
+// Reading R21: the evaluation support. A pair with Q >= 13.5^2 has
+// exp(-Q/2) = 2^(-kappa Q) < 2^-131, below the smallest fp32 normal: the kernels' ex2.approx.ftz
+// returns exactly 0 for it, so it adds nothing to any sum. Q >= (dx/sx)^2 and Q >= (dy/sy)^2 for
+// every rho, hence every pixel outside the box |x/s - mu_x| <= 13.5 sx, |y/s - mu_y| <= 13.5 sy
+// is such a pair. The kernels evaluate the window rect (R2) intersected with the integer box
+//   bx0 = floor(s (mu_x - 13.5 sx)),  bx1 = ceil(s (mu_x + 13.5 sx))   (fp64, this order)
+// and produce the same fp32 results as an evaluation of the whole window.
+constexpr double SUPPORT_SIGMAS = 13.5;
+
+__device__ __forceinline__ Rect support_rect(float mux, float muy, float sxf, float syf,
+                                             const DevImg& im) {
+    Rect r = window_rect(mux, muy, im);
+    const double mx = (double)mux, my = (double)muy;
+    const double tx = __dmul_rn(SUPPORT_SIGMAS, (double)sxf);
+    const double ty = __dmul_rn(SUPPORT_SIGMAS, (double)syf);
+    const double lx = __dmul_rn(im.s, __dsub_rn(mx, tx));
+    const double ux = __dmul_rn(im.s, __dadd_rn(mx, tx));
+    const double ly = __dmul_rn(im.s, __dsub_rn(my, ty));
+    const double uy = __dmul_rn(im.s, __dadd_rn(my, ty));
+    const int bx0 = (int)floor(clamp_bound(lx)), bx1 = (int)ceil(clamp_bound(ux));
+    const int by0 = (int)floor(clamp_bound(ly)), by1 = (int)ceil(clamp_bound(uy));
+    r.x0u = max(r.x0u, bx0);
+    r.y0u = max(r.y0u, by0);
+    r.x1u = min(r.x1u, bx1);
+    r.y1u = min(r.y1u, by1);
+    r.x0 = max(r.x0, bx0);
+    r.x1 = min(r.x1, bx1);
+    r.y0 = max(r.y0, by0);
+    r.y1 = min(r.y1, by1);
+    r.nonempty = r.nonempty && r.x0 <= r.x1 && r.y0 <= r.y1 && !isnan(lx) && !isnan(ux) &&
+                 !isnan(ly) && !isnan(uy);
     return r;
 }
 
@@ -242,7 +282,15 @@ struct Workspace {
     double* moments;         // [8 * n] (backward)
     unsigned long long* counter;  // scratch counters
     int* tile_off;           // debug tile lists: [total_tiles + 1]
+    int* ext;                // [2 * MAX_IMAGES]: per image max unclipped support-rect width,
+                             // height over the binned Gaussians (tile candidate query, K1)
 };
+
+// Tile candidate query over the cell grid (binning.cu): the Gaussians whose unclipped support
+// origin lies in [T0 - ext + 1, T1]; ext >= 1 keeps the cell range non-empty and in bounds.
+__device__ __forceinline__ int query_ext(const int* ext, int k, int axis) {
+    return max(1, ext[2 * k + axis]);
+}
 
 // binning.cu
 size_t binning_bytes(long long n, int total_cells, int total_tiles);
@@ -258,10 +306,11 @@ void binned_pointers(const ImgTable& tab, long long n, const Workspace& ws, int*
                      uint32_t** keys_sorted);
 cudaError_t launch_pair_count(const float* alpha, const float* mu, const float* sigma,
                               const float* rho, const float* color, long long n,
-                              const ImgTable& tab, long long* d_pairs, cudaStream_t st);
+                              const ImgTable& tab, bool support, long long* d_pairs,
+                              cudaStream_t st);
 cudaError_t launch_debug_rects(const float* alpha, const float* mu, const float* sigma,
                                const float* rho, const float* color, long long n,
-                               const ImgTable& tab, int* rects, cudaStream_t st);
+                               const ImgTable& tab, bool support, int* rects, cudaStream_t st);
 cudaError_t launch_debug_tile_lists(const ImgTable& tab, const Workspace& ws, const int* perm,
                                     const uint32_t* keys_sorted, int* counts, int* ids,
                                     int* cells, cudaStream_t st);

@@ -29,6 +29,9 @@
 #ifndef GSR_BWD_UNROLL
 #define GSR_BWD_UNROLL 4
 #endif
+#ifndef GSR_BWD_SNAKE
+#define GSR_BWD_SNAKE 1
+#endif
 #ifndef GSR_BWD_MACC_T
 #define GSR_BWD_MACC_T float      // per-(Gaussian, tile) accumulator type of the row folds
 #endif
@@ -80,6 +83,52 @@ __device__ __forceinline__ void pix_pair(const float4 ga, const float2 gb, const
     A.W2 = __ffma2_rn(gc, edd, A.W2);
 }
 
+// Both rows of a row pair at one column pair, ordered so that every FFMA2 after the first of a
+// group shares an operand register (same slot) with its predecessor: the operand then comes
+// from the reuse cache and the instruction reads two fresh register pairs instead of three
+// (register-file bank bandwidth: 2 instead of 3 issue cycles, tools/microbench.cu "ffma2_nr").
+template <bool MASKED>
+__device__ __forceinline__ void pix_pair2(const float4 gaA, const float2 gbA, const float4 gaB,
+                                          const float2 gbB, const float2 kx, const float2 TA,
+                                          const float2 UA, const float2 TB, const float2 UB,
+                                          const LaneG& L, bool in0, bool in1, RowAcc& A,
+                                          RowAcc& B) {
+    const float2 wA = __ffma2_rn(L.D2, kx, TA);
+    const float2 wB = __ffma2_rn(L.D2, kx, TB);
+    float2 qA = __ffma2_rn(make_float2(-wA.x, -wA.y), wA, UA);
+    float2 qB = __ffma2_rn(make_float2(-wB.x, -wB.y), wB, UB);
+    if (MASKED) {
+        qA.x = in0 ? qA.x : -INFINITY;
+        qA.y = in1 ? qA.y : -INFINITY;
+        qB.x = in0 ? qB.x : -INFINITY;
+        qB.y = in1 ? qB.y : -INFINITY;
+    }
+    const float2 grA = make_float2(gaA.x, gaA.y), ggA = make_float2(gaA.z, gaA.w);
+    const float2 grB = make_float2(gaB.x, gaB.y), ggB = make_float2(gaB.z, gaB.w);
+    // g . c' of both rows, snake order (c' shared between rows, g between channels)
+    float2 gcA = __fmul2_rn(grA, L.cr);
+    float2 gcB = __fmul2_rn(grB, L.cr);
+    gcB = __ffma2_rn(ggB, L.cg, gcB);
+    gcA = __ffma2_rn(ggA, L.cg, gcA);
+    gcA = __ffma2_rn(gbA, L.cb, gcA);
+    gcB = __ffma2_rn(gbB, L.cb, gcB);
+    const float2 eA = make_float2(ex2_approx(qA.x), ex2_approx(qA.y));
+    const float2 eB = make_float2(ex2_approx(qB.x), ex2_approx(qB.y));
+    // channel sums, snake: e shared within a row, g never shared -> e reuse
+    A.FR = __ffma2_rn(eA, grA, A.FR);
+    A.FG = __ffma2_rn(eA, ggA, A.FG);
+    A.FB = __ffma2_rn(eA, gbA, A.FB);
+    B.FB = __ffma2_rn(eB, gbB, B.FB);
+    B.FG = __ffma2_rn(eB, ggB, B.FG);
+    B.FR = __ffma2_rn(eB, grB, B.FR);
+    const float2 edA = __fmul2_rn(eA, wA), edB = __fmul2_rn(eB, wB);
+    const float2 eddA = __fmul2_rn(edA, wA), eddB = __fmul2_rn(edB, wB);
+    A.W1 = __ffma2_rn(gcA, edA, A.W1);
+    A.W2 = __ffma2_rn(gcA, eddA, A.W2);
+    B.W2 = __ffma2_rn(gcB, eddB, B.W2);
+    B.W1 = __ffma2_rn(gcB, edB, B.W1);
+}
+
 // Columns [c_begin, c_end) (pairs) of two rows at once: the column part (kx, masks, dL/dI
 // addresses) is shared, and the two rows give two independent accumulation chains.
 template <bool MASKED>
@@ -101,8 +150,13 @@ __device__ __forceinline__ void row2_pairs(int c_begin, int c_end, const float4*
             in0 = xa >= L.x0 && xa <= L.x1;
             in1 = xa + 1 >= L.x0 && xa + 1 <= L.x1;
         }
+#if GSR_BWD_SNAKE
+        pix_pair2<MASKED>(gA0[cp], gB0[cp], gA1[cp], gB1[cp], kx, T0, U0, T1, U1, L, in0, in1, A0,
+                          A1);
+#else
         pix_pair<MASKED>(gA0[cp], gB0[cp], kx, T0, U0, L, in0, in1, A0);
         pix_pair<MASKED>(gA1[cp], gB1[cp], kx, T1, U1, L, in0, in1, A1);
+#endif
         kx = __fadd2_rn(kx, two);
     }
 }
@@ -125,7 +179,7 @@ __device__ __forceinline__ void fold_row(const RowAcc& A, float v, const float4 
 
 __global__ void __launch_bounds__(BWD_THREADS) k_render_bwd(
     const ImgTable tab, const float4* __restrict__ rec, const int* __restrict__ cell_start,
-    const int* __restrict__ perm, const float* __restrict__ grad_out,
+    const int* __restrict__ ext, const int* __restrict__ perm, const float* __restrict__ grad_out,
     double* __restrict__ moments, int ks, const float* __restrict__ img,
     const float* __restrict__ gt, float inv_numel) {
     __shared__ __align__(16) float4 gA[TILE_H][TILE_W / 2];
@@ -133,7 +187,8 @@ __global__ void __launch_bounds__(BWD_THREADS) k_render_bwd(
 
     const int tile = blockIdx.x / ks;
     const int kpart = blockIdx.x % ks;    // split: this CTA takes every ks-th candidate group
-    const DevImg& im = tab.img[find_image_by_tile(tab, tile)];
+    const int kimg = find_image_by_tile(tab, tile);
+    const DevImg& im = tab.img[kimg];
     const int t = tile - im.tile_base;
     const int Tx0 = (t % im.ntx) * TILE_W;
     const int Ty0 = im.row_begin + (t / im.ntx) * TILE_H;
@@ -165,9 +220,9 @@ __global__ void __launch_bounds__(BWD_THREADS) k_render_bwd(
     }
     __syncthreads();
 
-    const int cx_lo = (Tx0 - im.wmax + 1 + im.offx) / CELL;
+    const int cx_lo = (Tx0 - query_ext(ext, kimg, 0) + 1 + im.offx) / CELL;
     const int cx_hi = min(im.ncx - 1, (Tx1 + im.offx) / CELL);
-    const int cy_lo = (Ty0 - im.row_begin - im.hmax + 1 + im.offy) / CELL;
+    const int cy_lo = (Ty0 - im.row_begin - query_ext(ext, kimg, 1) + 1 + im.offy) / CELL;
     const int cy_hi = min(im.ncy - 1, (Ty1 - im.row_begin + im.offy) / CELL);
     const float invs = im.invs;
 
@@ -317,8 +372,9 @@ cudaError_t launch_render_bwd_moments(const ImgTable& tab, const Workspace& ws, 
     count_launches(1);
     int h = prof_begin(2, st);
     int ks = split_k_factor(tab.total_tiles);
-    k_render_bwd<<<tab.total_tiles * ks, BWD_THREADS, 0, st>>>(tab, ws.rec, ws.cell_start, perm,
-                                                               grad_out, moments, ks, img, gt, inv_numel);
+    k_render_bwd<<<tab.total_tiles * ks, BWD_THREADS, 0, st>>>(tab, ws.rec, ws.cell_start, ws.ext,
+                                                               perm, grad_out, moments, ks, img,
+                                                               gt, inv_numel);
     prof_end(h, st);
     return cudaGetLastError();
 }

@@ -81,7 +81,8 @@ struct FwdSmem {
     static constexpr int NACC = CFG::ROWS * (CFG::STRIP / 2) * 3;   // float2 accumulators/thread
     float4 rec[FWD_STAGES][FWD_CHUNK * 3];
     float2 tot[FWD_CWARPS][NACC][32];        // per-warp totals (second accumulation level)
-    uint16_t idx[FWD_STAGES][FWD_CHUNK];     // kept records: index | full-x << 8 | full-y << 9
+    float g3[FWD_STAGES][FWD_CHUNK];         // 2^(-9 D^2) of recurrence-path records
+    uint16_t idx[FWD_STAGES][FWD_CHUNK];     // kept records: index | full << 8 | recurrence << 9
     uint64_t full_bar[FWD_STAGES];           // TMA bytes landed
     uint64_t ready_bar[FWD_STAGES];          // producer warp filtered + transformed the chunk
     uint64_t empty_bar[FWD_STAGES];          // consumer warps done with the stage
@@ -141,10 +142,87 @@ __device__ __forceinline__ void fwd_gauss(const float4 r0, const float4 r1, cons
     }
 }
 
+// Two-row lane block (FwdCfgLarge): accumulators pair the lane's two rows of one column,
+// acc[3 j + k] = (row 0, row 1) of column j, channel k. Three per-Gaussian variants:
+//   MODE 0  masked:  per column, w = D kx + tau, q = -w^2 + u (x / y masks -> -inf), 2^q
+//   MODE 1  full, direct: the same without masks
+//   MODE 2  full, exponential recurrence (producer-flagged when D = a1/s <= FWD_REC_DMAX):
+//           along a row w(kx + t) = w_a + t D, so
+//             2^q(kx_a + t) = 2^q_a * B^t * G_t,  B = 2^(-2 D w_a),  G_t = 2^(-D^2 t^2),
+//           evaluated at anchors j = 0, 4 (t = 1..3 from products): 2 ex2 per 4 pairs instead
+//           of 4, the FMA-pipe work unchanged (w, q, -2Dw, 3 B products, 3 G products per
+//           anchor vs w, q per pair). G_t come from the producer. The exponent -2 D w_a is
+//           clamped to <= 40: with D <= 1 a clamped anchor has |w_a| > 20, so 2^q_a = 0 and all
+//           four values are exactly 0 (B^3 <= 2^120 stays finite, no 0 * inf); an anchor whose
+//           2^q_a flushes to zero (q_a < -126) has q(kx_a + 3) < -67 (|w_a| > 11.2, D <= 1),
+//           i.e. only values below 2^-67 are lost; products never overflow (q <= 0 and
+//           D^2 t^2 <= 9). Error: the exponent of B^t carries t * 2 D |w_a| * 2^-24 relative.
+template <int MODE>
+__device__ __forceinline__ void fwd_gauss_r2(const float4 r0, const float4 r1, const float4 r2,
+                                             float g3, float xlf, float yf0, const int (&yi)[2],
+                                             int xl0, float invs, float2 (&acc)[24]) {
+    const float D = r0.w;
+    const float2 D2 = f2(D);
+    const float kx0 = xlf + r0.x;                           // x - ax of column 0 (exact)
+    const float dy0 = fmaf(yf0 - r0.y, invs, -r0.z);
+    const float dy1 = dy0 + invs;                           // consecutive rows: exact to 1 ulp(1/s)
+    const float v0 = r1.z * dy0, v1 = r1.z * dy1;
+    float2 U = make_float2(-(v0 * v0), -(v1 * v1));
+    if (MODE == 0) {                                        // lane rows outside [y0, y1]
+        const unsigned ys = __float_as_uint(r2.w);
+        const int y0 = (int)(ys & 0xffffu), y1 = (int)(ys >> 16);
+        U.x = (yi[0] >= y0 && yi[0] <= y1) ? U.x : -INFINITY;
+        U.y = (yi[1] >= y0 && yi[1] <= y1) ? U.y : -INFINITY;
+    }
+    const float2 T = make_float2(fmaf(r1.y, dy0, r1.x), fmaf(r1.y, dy1, r1.x));  // b1 dy - a1 dl_x
+    const float2 cr = f2(r1.w), cg = f2(r2.x), cb = f2(r2.y);
+    auto accum = [&](int j, float2 e) {
+        acc[3 * j + 0] = __ffma2_rn(cr, e, acc[3 * j + 0]);
+        acc[3 * j + 1] = __ffma2_rn(cg, e, acc[3 * j + 1]);
+        acc[3 * j + 2] = __ffma2_rn(cb, e, acc[3 * j + 2]);
+    };
+    if (MODE == 2) {
+        const float2 G1 = f2(r2.z), G2 = f2(r2.w), G3 = f2(g3), M2D = f2(-2.f * D);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const float2 w = __ffma2_rn(D2, f2(kx0 + 4.f * h), T);
+            const float2 q = __ffma2_rn(make_float2(-w.x, -w.y), w, U);
+            float2 b = __fmul2_rn(w, M2D);
+            b.x = fminf(b.x, 40.f);
+            b.y = fminf(b.y, 40.f);
+            const float2 A = make_float2(ex2_approx(q.x), ex2_approx(q.y));
+            const float2 B = make_float2(ex2_approx(b.x), ex2_approx(b.y));
+            const float2 AB1 = __fmul2_rn(A, B);
+            const float2 AB2 = __fmul2_rn(AB1, B);
+            const float2 AB3 = __fmul2_rn(AB2, B);
+            accum(4 * h + 0, A);
+            accum(4 * h + 1, __fmul2_rn(AB1, G1));
+            accum(4 * h + 2, __fmul2_rn(AB2, G2));
+            accum(4 * h + 3, __fmul2_rn(AB3, G3));
+        }
+    } else {
+        unsigned xs = 0;
+        int x0 = 0, x1 = 0;
+        if (MODE == 0) {
+            xs = __float_as_uint(r2.z);
+            x0 = (int)(xs & 0xffffu);
+            x1 = (int)(xs >> 16);
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const float2 w = __ffma2_rn(D2, f2(kx0 + (float)j), T);
+            float2 q = __ffma2_rn(make_float2(-w.x, -w.y), w, U);
+            if (MODE == 0 && !(xl0 + j >= x0 && xl0 + j <= x1)) q = f2(-INFINITY);
+            accum(j, make_float2(ex2_approx(q.x), ex2_approx(q.y)));
+        }
+    }
+}
+
 template <int KS, bool LOSS, class CFG>
 __global__ void __launch_bounds__(FWD_THREADS) k_render_fwd(const ImgTable tab,
                                                             const float4* __restrict__ rec,
                                                             const int* __restrict__ cell_start,
+                                                            const int* __restrict__ ext,
                                                             float* __restrict__ out,
                                                             const float* __restrict__ gt,
                                                             double* __restrict__ loss_acc) {
@@ -155,7 +233,8 @@ __global__ void __launch_bounds__(FWD_THREADS) k_render_fwd(const ImgTable tab,
 
     const int tile = blockIdx.x / KS;
     const int krank = KS > 1 ? (int)cluster_rank() : 0;
-    const DevImg& im = tab.img[find_image_by_ftile(tab, tile)];
+    const int kimg = find_image_by_ftile(tab, tile);
+    const DevImg& im = tab.img[kimg];
     const int t = tile - im.ftile_base;
     const int Tx0 = (t % im.fntx) * FTILE_W;
     const int Ty0 = im.row_begin + (t / im.fntx) * FTILE_H;
@@ -187,9 +266,9 @@ __global__ void __launch_bounds__(FWD_THREADS) k_render_fwd(const ImgTable tab,
         prod.cs = cell_start;
         prod.row0 = im.cell_base;
         prod.row_stride = im.ncx;
-        prod.cx_lo = (Tx0 - im.wmax + 1 + im.offx) / CELL;
+        prod.cx_lo = (Tx0 - query_ext(ext, kimg, 0) + 1 + im.offx) / CELL;
         prod.cx_hi = min(im.ncx - 1, (fx1 + im.offx) / CELL);
-        prod.cy = (Ty0 - im.row_begin - im.hmax + 1 + im.offy) / CELL - 1;
+        prod.cy = (Ty0 - im.row_begin - query_ext(ext, kimg, 1) + 1 + im.offy) / CELL - 1;
         prod.cy_hi = min(im.ncy - 1, (fy1 - im.row_begin + im.offy) / CELL);
         prod.cur = prod.end = 0;
         auto issue = [&](int k) -> int {          // lane 0 only
@@ -232,7 +311,7 @@ __global__ void __launch_bounds__(FWD_THREADS) k_render_fwd(const ImgTable tab,
                 float4* sr = &sm.rec[sf][0];
                 for (int g0 = 0; g0 < n; g0 += 32) {
                     const int g = g0 + lane;
-                    bool keep = false, full = false;
+                    bool keep = false, full = false, rec_ok = false;
                     if (g < n) {
                         const float4 r2 = sr[3 * g + 2];
                         const unsigned xs = __float_as_uint(r2.z), ys = __float_as_uint(r2.w);
@@ -243,12 +322,22 @@ __global__ void __launch_bounds__(FWD_THREADS) k_render_fwd(const ImgTable tab,
                         full = x0 <= fx0 && x1 >= fx1 && y0 <= fy0 && y1 >= fy0 + FTILE_H - 1;
                         if (keep) {
                             const float4 r0 = sr[3 * g], r1 = sr[3 * g + 1];
-                            sr[3 * g] = make_float4(-r0.x, r0.y, r0.w, r1.x * invs);
+                            const float D = r1.x * invs;
+                            sr[3 * g] = make_float4(-r0.x, r0.y, r0.w, D);
                             sr[3 * g + 1] = make_float4(-r1.x * r0.z, r1.y, r1.z, r1.w);
+                            // exponential recurrence (2-row lane blocks): G_t = 2^(-D^2 t^2)
+                            rec_ok = CFG::ROWS == 2 && full && D <= FWD_REC_DMAX;
+                            if (rec_ok) {
+                                const float d2 = D * D;
+                                sr[3 * g + 2] = make_float4(r2.x, r2.y, exp2f(-d2), exp2f(-4.f * d2));
+                                sm.g3[sf][g] = exp2f(-9.f * d2);
+                            }
                         }
                     }
                     const unsigned m = __ballot_sync(0xffffffffu, keep);
-                    if (keep) sm.idx[sf][base + __popc(m & lt)] = (uint16_t)(g | (full ? 0x100 : 0));
+                    if (keep)
+                        sm.idx[sf][base + __popc(m & lt)] =
+                            (uint16_t)(g | (full ? 0x100 : 0) | (rec_ok ? 0x200 : 0));
                     base += __popc(m);
                 }
                 if (lane == 0) sm.kept[sf] = base;
@@ -275,6 +364,7 @@ __global__ void __launch_bounds__(FWD_THREADS) k_render_fwd(const ImgTable tab,
 #pragma unroll
         for (int jp = 0; jp < FWD_STRIP / 2; ++jp)
             xj[jp] = make_float2((float)(xl0 + 2 * jp), (float)(xl0 + 2 * jp + 1));
+        const float xlf = (float)xl0;
         int yi[FWD_ROWS];
 #pragma unroll
         for (int r = 0; r < FWD_ROWS; ++r) yi[r] = yl0 + r;
@@ -294,10 +384,19 @@ __global__ void __launch_bounds__(FWD_THREADS) k_render_fwd(const ImgTable tab,
                 const int e = ix[i];
                 const int g = e & 0xff;
                 const float4 r0 = sr[3 * g], r1 = sr[3 * g + 1], r2 = sr[3 * g + 2];
-                if (e & 0x100)
-                    fwd_gauss<CFG, true>(r0, r1, r2, xj, yf0, yi, xl0, invs, acc);
-                else
-                    fwd_gauss<CFG, false>(r0, r1, r2, xj, yf0, yi, xl0, invs, acc);
+                if constexpr (FWD_ROWS == 2) {
+                    if (e & 0x200)
+                        fwd_gauss_r2<2>(r0, r1, r2, sm.g3[s][g], xlf, yf0, yi, xl0, invs, acc);
+                    else if (e & 0x100)
+                        fwd_gauss_r2<1>(r0, r1, r2, 0.f, xlf, yf0, yi, xl0, invs, acc);
+                    else
+                        fwd_gauss_r2<0>(r0, r1, r2, 0.f, xlf, yf0, yi, xl0, invs, acc);
+                } else {
+                    if (e & 0x100)
+                        fwd_gauss<CFG, true>(r0, r1, r2, xj, yf0, yi, xl0, invs, acc);
+                    else
+                        fwd_gauss<CFG, false>(r0, r1, r2, xj, yf0, yi, xl0, invs, acc);
+                }
             }
             // fold the chunk partials into the per-warp totals (second accumulation level)
 #pragma unroll
@@ -335,28 +434,30 @@ __global__ void __launch_bounds__(FWD_THREADS) k_render_fwd(const ImgTable tab,
     const int xl0 = Tx0 + FWD_STRIP * (lane & 3);
     const int yl0 = Ty0 + FWD_ROWS * (lane >> 2);
     float l1 = 0.f;     // fused L1 loss (NEXT-1): sum |I - I_gt| over the stored elements
+    auto store = [&](int y, int x, float R, float G, float B) {
+        if (y >= im.row_end || x >= im.Ws) return;
+        const long long off = im.out_off + ((long long)(y - im.row_begin) * im.Ws + x) * 3;
+        out[off] = R; out[off + 1] = G; out[off + 2] = B;
+        if (LOSS) l1 += fabsf(R - gt[off]) + fabsf(G - gt[off + 1]) + fabsf(B - gt[off + 2]);
+    };
+    if constexpr (FWD_ROWS == 2) {     // acc pairs = (row 0, row 1) of one column
 #pragma unroll
-    for (int r = 0; r < FWD_ROWS; ++r) {
-        const int y = yl0 + r;
-        if (y >= im.row_end) continue;
-        const long long rowoff = im.out_off + ((long long)(y - im.row_begin) * im.Ws) * 3;
-        float* o = out + rowoff;
+        for (int j = 0; j < FWD_STRIP; ++j) {
+            const float2 R = sm.tot[0][3 * j][lane], G = sm.tot[0][3 * j + 1][lane],
+                         B = sm.tot[0][3 * j + 2][lane];
+            store(yl0, xl0 + j, R.x, G.x, B.x);
+            store(yl0 + 1, xl0 + j, R.y, G.y, B.y);
+        }
+    } else {                           // acc pairs = two adjacent columns of one row
 #pragma unroll
-        for (int jp = 0; jp < FWD_STRIP / 2; ++jp) {
-            const int a = (r * (FWD_STRIP / 2) + jp) * 3;
-            const float2 R = sm.tot[0][a][lane], G = sm.tot[0][a + 1][lane],
-                         B = sm.tot[0][a + 2][lane];
-            const int x = xl0 + 2 * jp;
-            if (x < im.Ws) { o[3 * x] = R.x; o[3 * x + 1] = G.x; o[3 * x + 2] = B.x; }
-            if (x + 1 < im.Ws) { o[3 * x + 3] = R.y; o[3 * x + 4] = G.y; o[3 * x + 5] = B.y; }
-            if (LOSS) {
-                const float* t = gt + rowoff;
-                if (x < im.Ws)
-                    l1 += fabsf(R.x - t[3 * x]) + fabsf(G.x - t[3 * x + 1]) +
-                          fabsf(B.x - t[3 * x + 2]);
-                if (x + 1 < im.Ws)
-                    l1 += fabsf(R.y - t[3 * x + 3]) + fabsf(G.y - t[3 * x + 4]) +
-                          fabsf(B.y - t[3 * x + 5]);
+        for (int r = 0; r < FWD_ROWS; ++r) {
+#pragma unroll
+            for (int jp = 0; jp < FWD_STRIP / 2; ++jp) {
+                const int a = (r * (FWD_STRIP / 2) + jp) * 3;
+                const float2 R = sm.tot[0][a][lane], G = sm.tot[0][a + 1][lane],
+                             B = sm.tot[0][a + 2][lane];
+                store(yl0 + r, xl0 + 2 * jp, R.x, G.x, B.x);
+                store(yl0 + r, xl0 + 2 * jp + 1, R.y, G.y, B.y);
             }
         }
     }
@@ -393,7 +494,8 @@ cudaError_t launch_ks3(const ImgTable& tab, const Workspace& ws, float* out, con
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, k_render_fwd<KS, LOSS, CFG>, tab, (const float4*)ws.rec,
-                              (const int*)ws.cell_start, out, gt, loss_acc);
+                              (const int*)ws.cell_start, (const int*)ws.ext, out, gt,
+                              loss_acc);
 }
 
 template <int KS, bool LOSS>

@@ -9,13 +9,15 @@ from ._lib import check
 from .ops import _params, _ptr, _stream_ptr
 
 
-def rects(alpha, mu, sigma, rho, color, H, W, s, ratio=0.1) -> torch.Tensor:
-    """[n, 4] int32 (x0, x1, y0, y1) clipped window rects as the GPU computes them."""
+def rects(alpha, mu, sigma, rho, color, H, W, s, ratio=0.1, support=False) -> torch.Tensor:
+    """[n, 4] int32 (x0, x1, y0, y1) clipped window rects as the GPU computes them
+    (support=True: the support rects the kernels evaluate, reading R21)."""
     (alpha, mu, sigma, rho, color), n = _params(alpha, mu, sigma, rho, color)
     out = torch.empty((n, 4), dtype=torch.int32, device=alpha.device)
-    check(_lib.load().gsr_debug_rects(_ptr(alpha), _ptr(mu), _ptr(sigma), _ptr(rho), _ptr(color),
-                                      n, int(H), int(W), float(s), float(ratio), _ptr(out),
-                                      _stream_ptr(alpha.device)), "gsr_debug_rects")
+    check(_lib.load().gsr_debug_rects_ex(_ptr(alpha), _ptr(mu), _ptr(sigma), _ptr(rho),
+                                         _ptr(color), n, int(H), int(W), float(s), float(ratio),
+                                         _lib.GSR_SUPPORT if support else 0, _ptr(out),
+                                         _stream_ptr(alpha.device)), "gsr_debug_rects_ex")
     return out
 
 

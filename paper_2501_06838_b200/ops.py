@@ -240,8 +240,10 @@ def render_bwd_batched(alpha, mu, sigma, rho, color, lay: Layout, grad_out: torc
     return tuple(grads)
 
 
-def pair_count(alpha, mu, sigma, rho, color, lay: Layout, ratio: float = 0.1) -> int:
-    """P = number of (Gaussian, pixel) pairs inside the windows (synchronises)."""
+def pair_count(alpha, mu, sigma, rho, color, lay: Layout, ratio: float = 0.1,
+               support: bool = False) -> int:
+    """P = number of (Gaussian, pixel) pairs inside the windows (synchronises). support=True:
+    the pairs inside the support rects, i.e. the pairs the kernels evaluate (reading R21)."""
     (alpha, mu, sigma, rho, color), n = _params(alpha, mu, sigma, rho, color)
     dev = alpha.device
     lib = _lib.load()
@@ -251,10 +253,12 @@ def pair_count(alpha, mu, sigma, rho, color, lay: Layout, ratio: float = 0.1) ->
     for g0, g1, o0, arr, m in _chunks(lay):
         nb = _ws_bytes(arr, m, g1 - g0, ratio)
         ws = _workspace(dev, nb)
-        check(lib.gsr_pair_count_batched(_ptr(alpha, g0), _ptr(mu, 2 * g0), _ptr(sigma, 2 * g0),
-                                         _ptr(rho, g0), _ptr(color, 3 * g0), g1 - g0, arr, m,
-                                         float(ratio), tmp.data_ptr(), ws.data_ptr(), ws.numel(),
-                                         st), "gsr_pair_count_batched")
+        check(lib.gsr_pair_count_batched_ex(_ptr(alpha, g0), _ptr(mu, 2 * g0),
+                                            _ptr(sigma, 2 * g0), _ptr(rho, g0),
+                                            _ptr(color, 3 * g0), g1 - g0, arr, m, float(ratio),
+                                            _lib.GSR_SUPPORT if support else 0, tmp.data_ptr(),
+                                            ws.data_ptr(), ws.numel(), st),
+              "gsr_pair_count_batched_ex")
         total += tmp
     return int(total.item())
 

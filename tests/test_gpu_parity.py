@@ -62,13 +62,15 @@ def adversarial_cloud(H, W, s, seed=0):
     return c
 
 
+@pytest.mark.parametrize("support", [False, True])
 @pytest.mark.parametrize("H,W,s,r", [(48, 48, 4.0, 0.1), (20, 33, 2.7, 0.1), (9, 13, 30.0, 0.1),
                                      (16, 16, 1.0, 0.5), (12, 10, 3.3, 1.0)])
-def test_rects_bit_exact(gsr, H, W, s, r):
+def test_rects_bit_exact(gsr, H, W, s, r, support):
+    """Window rects (R2) and support rects (R21) as the GPU computes them == the oracle's."""
     import paper_2501_06838_b200.debug as D
     c = adversarial_cloud(H, W, s)
-    got = D.rects(*to_dev(c), H, W, s, r).cpu().numpy()
-    ref = O.rects(c, H, W, s, r)
+    got = D.rects(*to_dev(c), H, W, s, r, support=support).cpu().numpy()
+    ref = O.rects(c, H, W, s, r, support=support)
     empty_ref = (ref[:, 2] > ref[:, 3]) | (ref[:, 4] > ref[:, 5])
     empty_got = (got[:, 0] > got[:, 1]) | (got[:, 2] > got[:, 3])
     assert np.array_equal(empty_ref, empty_got)
@@ -79,13 +81,13 @@ def test_rects_bit_exact(gsr, H, W, s, r):
 @pytest.mark.parametrize("H,W,s,r", [(48, 48, 4.0, 0.1), (20, 33, 2.7, 0.1), (9, 13, 30.0, 0.1),
                                      (12, 10, 3.3, 1.0)])
 def test_tile_lists_bit_exact(gsr, H, W, s, r):
-    """Per-tile Gaussian lists the render kernels visit == CPU brute force (O(N*tiles)), and
-    their order is (cell, index) ascending -- the stable sort."""
+    """Per-tile Gaussian lists the render kernels visit (support rects, R21) == CPU brute force
+    (O(N*tiles)), and their order is (cell, index) ascending -- the stable sort."""
     import paper_2501_06838_b200.debug as D
     c = adversarial_cloud(H, W, s, seed=3)
     tw, th, cw, ch = gsr.tile_shape()
     counts, ids, cells = [t.cpu().numpy() for t in D.tile_lists(*to_dev(c), H, W, s, r)]
-    rc, rids = O.tile_lists(c, H, W, s, r, tw, th)
+    rc, rids = O.tile_lists(c, H, W, s, r, tw, th, support=True)
     assert np.array_equal(counts.astype(np.int64), rc)
     off = np.concatenate([[0], np.cumsum(counts)])
     for t in range(len(counts)):
@@ -102,6 +104,8 @@ def test_pair_count(gsr):
         c = adversarial_cloud(H, W, s)
         lay = gsr.layout([gsr.Image(H, W, s, 0, c["alpha"].shape[0])])
         assert gsr.pair_count(*to_dev(c), lay) == O.pair_count(c, H, W, s)
+        assert (gsr.pair_count(*to_dev(c), lay, support=True) ==
+                O.pair_count(c, H, W, s, support=True))
 
 
 # --------------------------------------------------------------------------- forward
@@ -123,6 +127,19 @@ def test_fwd_ragged_shapes(gsr, H, W, s, r):
     """Non-multiple-of-tile sizes, s = 1, non-integer s, r = 1 (window = whole image)."""
     c = S.gaussians(H, W, seed=int(100 * s) + H, offset_range=1.0)
     assert_fwd_close(fwd(gsr, c, H, W, s, r), O.render_fwd(c, H, W, s, r))
+
+
+@pytest.mark.parametrize("s,r,sig,dist", [(2.0, 0.6, 1.0, "image"), (3.0, 0.4, 1.0, "image"),
+                                          (4.0, 0.3, 1.0, "image"), (8.0, 0.3, 1.0, "image"),
+                                          (4.0, 0.3, 0.5, "image"), (4.0, 0.3, 2.0, "image"),
+                                          (3.0, 0.4, 1.0, "stress"), (2.5, 0.5, 0.7, "stress")])
+def test_fwd_recurrence_regime(gsr, s, r, sig, dist):
+    """Windows >= 48 HR px (2-row lane blocks) with D = a1/s spanning both sides of the
+    exponential-recurrence threshold (render_fwd.cu, MODE 2: D <= 1), full image vs oracle."""
+    H, W = 24, 24
+    c = S.gaussians(H, W, m=4, seed=int(10 * s) + int(10 * sig), dist=dist)
+    c["sigma"] = (c["sigma"] * np.float32(sig)).astype(np.float32)
+    assert_fwd_close(fwd(gsr, c, H, W, s, r), O.render_fwd(c, H, W, s, r, mode="rect"), dist)
 
 
 def test_fwd_adversarial_and_empty(gsr):

@@ -289,3 +289,67 @@ def test_tile_lists_brute_vs_rect_enumeration(tw, th):
     off = np.concatenate([[0], np.cumsum(counts)])
     for t in range(len(counts)):
         assert list(ids[off[t]:off[t + 1]]) == lists.get(t, []), t
+
+
+# --------------------------------------------------------------------------- R21 support rect
+def test_support_rect_closed_form():
+    """Reading R21: support rect = window rect (R2) cut to the integer box
+    [floor(s(mu - 13.5 sigma)), ceil(s(mu + 13.5 sigma))]. Hand-derived (float32 inputs):
+    mu = (10.3, 7.7), s = 4, H = W = 32.
+      sigma = (0.4, 0.25), r = 0.5: window x: floor(4(10.3 - 16)) + 1 = -22 (clip 0),
+        ceil(4 * 26.3) - 1 = 105; box x: floor(4 * 4.9) = 19, ceil(4 * 15.7) = 63 -> [19, 63];
+        window y: -33 (clip 0) .. ceil(4 * 23.7) - 1 = 94; box y: floor(4 * 4.325) = 17, ceil(4 * 11.075) = 45.
+      sigma = (2, 3), r = 0.1: box wider than the window -> the window rect
+        x: floor(4 * 7.1) + 1 = 29, ceil(4 * 13.5000002) - 1 = 54; y: 18 .. 43."""
+    g = one(mu=(10.3, 7.7), sigma=(0.4, 0.25))
+    g = {k: v.astype(np.float32) for k, v in g.items()}
+    assert list(O.rects(g, 32, 32, 4.0, 0.5, support=True)[0]) == [19, 17, 19, 63, 17, 45]
+    assert list(O.rects(g, 32, 32, 4.0, 0.5)[0]) == [-22, -33, 0, 105, 0, 94]
+    g["sigma"] = np.array([[2.0, 3.0]], np.float32)
+    assert list(O.rects(g, 32, 32, 4.0, 0.1, support=True)[0]) == [29, 18, 29, 54, 18, 43]
+    assert list(O.rects(g, 32, 32, 4.0, 0.1)[0]) == [29, 18, 29, 54, 18, 43]
+
+
+@pytest.mark.parametrize("rho,sig", [(0.0, (0.3, 0.5)), (0.9, (0.4, 0.2)), (-0.99, (0.3, 0.3)),
+                                     (0.5, (0.05, 0.7))])
+def test_support_outside_below_fp32(rho, sig):
+    """R21's premise, checked on the oracle's own fp64 Eq. 2: with the window covering the whole
+    image (r = 1), every pixel outside the support rect receives < 2^-131 * alpha * c * K
+    (K = 1/(2 pi sx sy sqrt(1 - rho^2)), the peak density), below fp32's smallest normal
+    relative to the peak; the peak itself lies inside."""
+    H, W, s = 8, 8, 4.0
+    g = one(mu=(3.3, 4.1), sigma=sig, rho=rho)
+    img = O.render_fwd(g, H, W, s, 1.0, mode="rect")[..., 0]
+    _, _, x0, x1, y0, y1 = O.rects(g, H, W, s, 1.0, support=True)[0]
+    K = 1.0 / (2 * math.pi * sig[0] * sig[1] * math.sqrt(1 - rho * rho))
+    mask = np.ones_like(img, bool)
+    mask[y0:y1 + 1, x0:x1 + 1] = False
+    assert mask.any()
+    assert img[mask].max() < 2.0 ** -131 * K
+    assert img[~mask].max() == img.max() > 0
+
+
+@pytest.mark.parametrize("cfg", [(10, 12, 4.0, 0.3, "image", 0), (9, 7, 2.5, 1.0, "stress", 1),
+                                 (6, 11, 8.0, 0.5, "stress", 2), (12, 12, 1.0, 1.0, "image", 3)])
+def test_support_render_equals_window_render(cfg):
+    """R21: rendering over the support rects differs from the window sum of Alg. 1 only by terms
+    below 2^-131 of each Gaussian's peak (forward and every gradient)."""
+    H, W, s, r, dist, seed = cfg
+    cl = S.gaussians(H, W, m=4, seed=seed, dist=dist, offset_range=1.5)
+    a = O.render_fwd(cl, H, W, s, r, mode="rect")
+    b = O.render_fwd(cl, H, W, s, r, mode="support")
+    sx, sy = cl["sigma"][:, 0].astype(np.float64), cl["sigma"][:, 1].astype(np.float64)
+    rh = cl["rho"].astype(np.float64)
+    peak = np.abs(cl["alpha"]) * np.abs(cl["color"]).max(1) / (
+        2 * np.pi * sx * sy * np.sqrt((1 - rh) * (1 + rh)))
+    Hs, Ws = O.out_dims(H, W, s)
+    bound = 2.0 ** -131 * float(peak.sum())
+    assert np.abs(a - b).max() <= bound
+    assert O.pair_count(cl, H, W, s, r, support=True) <= O.pair_count(cl, H, W, s, r)
+    g = S.grad_out(a.shape, seed=seed)
+    ga = O.render_bwd(cl, H, W, s, r, g, mode="rect")
+    gb = O.render_bwd(cl, H, W, s, r, g, mode="support")
+    for k in ga:
+        # d/dtheta of a dropped term is (polynomial in Q <= 1e3 of it) x the term itself
+        assert np.abs(ga[k] - gb[k]).max() <= 1e6 * bound * Hs * Ws / min(1.0, sx.min(),
+                                                                          sy.min()) ** 2, k

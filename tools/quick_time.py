@@ -19,7 +19,11 @@ def run(name, nimg_override=None, iters=3):
     for (H, W, s), c in zip(imgs, clouds):
         ims.append(gsr.Image(H, W, s, off, c["alpha"].shape[0])); off += c["alpha"].shape[0]
     lay = gsr.layout(ims)
-    P = gsr.pair_count(*dev, lay)
+    Pw = gsr.pair_count(*dev, lay)
+    try:
+        P = gsr.pair_count(*dev, lay, support=True)     # evaluated pairs (reading R21)
+    except Exception:                                   # an older library (A/B runs)
+        P = Pw
     g = torch.rand(lay.out_numel, device="cuda") * 2 - 1
     out = gsr.render_fwd_batched(*dev, lay)
     gr = gsr.render_bwd_batched(*dev, lay, g)
@@ -32,7 +36,7 @@ def run(name, nimg_override=None, iters=3):
         tf.append(e[0].elapsed_time(e[1])); tb.append(e[1].elapsed_time(e[2]))
     tf, tb = min(tf), min(tb)
     peak = 16 * 148 * 1.965e9
-    print(f"{name} imgs={len(imgs)} P={P:.3e} fwd {tf:.3f} ms ({P/tf/1e9:.3f} Tpair/s, {P/tf*1e3/peak:.1%} of SFU) "
+    print(f"{name} imgs={len(imgs)} Pwin={Pw:.3e} Peval={P:.3e} fwd {tf:.3f} ms ({P/tf/1e9:.3f} Tpair/s, {P/tf*1e3/peak:.1%} of SFU) "
           f"bwd {tb:.3f} ms ({P/tb/1e9:.3f} Tpair/s, {P/tb*1e3/(128/12.5*148*1.965e9):.1%} of FP32)", flush=True)
 
 
