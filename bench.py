@@ -268,7 +268,8 @@ def main():
             bounds.append([0, dims[k][0]])
         else:
             rc = gdist.row_pair_counts(host["mu"][offs[k]:offs[k + 1]],
-                                       np.ones(counts[k], bool), H, W, s, RATIO)
+                                       np.ones(counts[k], bool), H, W, s, RATIO,
+                                       sigma=host["sigma"][offs[k]:offs[k + 1]])
             bounds.append(gdist.plan_bands(rc, world))
     if by_image:
         # whole images per rank: contiguous, equal image counts (the images are i.i.d. draws)

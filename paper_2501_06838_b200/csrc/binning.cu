@@ -249,7 +249,8 @@ __global__ void k_records(const float* __restrict__ alpha, const float* __restri
     int k = find_image_by_gauss(tab, i);
     const DevImg& im = tab.img[k];
     float mxf = mu[2 * i], myf = mu[2 * i + 1];
-    Rect r = support_rect(mxf, myf, sigma[2 * i], sigma[2 * i + 1], im);
+    Rect r = window_rect(mxf, myf, im);
+    Rect sr = support_rect(mxf, myf, sigma[2 * i], sigma[2 * i + 1], im);
     double mx = mxf, my = myf;
     double sx = sigma[2 * i], sy = sigma[2 * i + 1], rh = rho[i], al = alpha[i];
     double D = (1.0 - rh) * (1.0 + rh);
@@ -268,9 +269,17 @@ __global__ void k_records(const float* __restrict__ alpha, const float* __restri
     unsigned ys = (unsigned)r.y0 | ((unsigned)r.y1 << 16);
     float4 r2 = make_float4((float)(w * color[3 * i + 1]), (float)(w * color[3 * i + 2]),
                             __uint_as_float(xs), __uint_as_float(ys));
-    rec[3 * p + 0] = r0;
-    rec[3 * p + 1] = r1;
-    rec[3 * p + 2] = r2;
+    // r3: support rect (R21) + the forward's recurrence constants G_t = 2^(-D^2 t^2), t = 1, 2,
+    // with D = a1/s exactly as the forward forms it (fp32 product)
+    const float Df = r1.x * im.invs, d2 = Df * Df;
+    unsigned sxs = (unsigned)sr.x0 | ((unsigned)sr.x1 << 16);
+    unsigned sys = (unsigned)sr.y0 | ((unsigned)sr.y1 << 16);
+    float4 r3 = make_float4(__uint_as_float(sxs), __uint_as_float(sys), exp2f(-d2),
+                            exp2f(-4.f * d2));
+    rec[REC_F4 * p + 0] = r0;
+    rec[REC_F4 * p + 1] = r1;
+    rec[REC_F4 * p + 2] = r2;
+    rec[REC_F4 * p + 3] = r3;
 }
 
 // ---- pair count ---------------------------------------------------------------------------
@@ -344,8 +353,8 @@ __global__ void k_debug_tile_lists(ImgTable tab, const int* __restrict__ ext,
     for (int cy = cy_lo; cy <= cy_hi; ++cy) {
         int row = im.cell_base + cy * im.ncx;
         for (int p = cell_start[row + cx_lo]; p < cell_start[row + cx_hi + 1]; ++p) {
-            float4 r2 = rec[3 * p + 2];
-            unsigned xs = __float_as_uint(r2.z), ys = __float_as_uint(r2.w);
+            float4 r3 = rec[REC_F4 * p + 3];
+            unsigned xs = __float_as_uint(r3.x), ys = __float_as_uint(r3.y);
             int x0 = xs & 0xffff, x1 = xs >> 16, y0 = ys & 0xffff, y1 = ys >> 16;
             if (x1 < Tx0 || x0 > Tx1 || y1 < Ty0 || y0 > Ty1) continue;
             if (ids) {
@@ -372,7 +381,7 @@ size_t binning_bytes(long long n, int total_cells, int total_tiles) {
     b += align256(sizeof(int) * (size_t)(hist + 1));            // hist
     b += align256(sizeof(int) * (size_t)(scan_blocks(scan_src) + 1));  // scan tmp
     b += align256(sizeof(int) * (size_t)(total_cells + 1));     // cell_start
-    b += align256(sizeof(float4) * 3 * (size_t)n);              // records
+    b += align256(sizeof(float4) * REC_F4 * (size_t)n);         // records
     b += align256(sizeof(double) * 8 * (size_t)n);              // moments
     b += align256(sizeof(unsigned long long) * 4);              // counters
     b += align256(sizeof(int) * (size_t)(total_tiles + 1));     // debug tile offsets
@@ -393,7 +402,7 @@ void carve_workspace(void* base, long long n, int total_cells, int total_tiles, 
     ws->hist = (int*)take(sizeof(int) * (size_t)(hist + 1));
     ws->scan_tmp = (int*)take(sizeof(int) * (size_t)(scan_blocks(scan_src) + 1));
     ws->cell_start = (int*)take(sizeof(int) * (size_t)(total_cells + 1));
-    ws->rec = (float4*)take(sizeof(float4) * 3 * (size_t)n);
+    ws->rec = (float4*)take(sizeof(float4) * REC_F4 * (size_t)n);
     ws->moments = (double*)take(sizeof(double) * 8 * (size_t)n);
     ws->counter = (unsigned long long*)take(sizeof(unsigned long long) * 4);
     ws->tile_off = (int*)take(sizeof(int) * (size_t)(total_tiles + 1));

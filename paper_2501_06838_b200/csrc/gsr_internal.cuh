@@ -73,12 +73,17 @@ struct ImgTable {
     DevImg img[MAX_IMAGES];
 };
 
-// Sorted record (48 B = 3 x float4), one per binned Gaussian, in cell order:
+// Sorted record (64 B = REC_F4 x float4), one per binned Gaussian, in cell order:
 //   r0 = {ax, ay, dlx, dly}        anchor (integer HR px, as float) and fp32 residual
 //                                  dl = mu - a/s  (LR px, |dl| <= 0.5/s)
 //   r1 = {a1, b1, c1, cr}          factored exponent: q = -Q/2 log2 e = -(w^2 + v^2),
 //                                  w = a1 dx + b1 dy, v = c1 dy
-//   r2 = {cg, cb, x0|x1<<16, y0|y1<<16}  c' = alpha c K (rgb), clipped rect (int bits)
+//   r2 = {cg, cb, x0|x1<<16, y0|y1<<16}  c' = alpha c K (rgb), clipped WINDOW rect (R2, int
+//                                  bits): the masks (pairs outside it are not in the sum)
+//   r3 = {x0|x1<<16, y0|y1<<16, G1, G2}  clipped SUPPORT rect (R21): tile filtering and loop
+//                                  bounds (pairs outside it are exactly 0 in fp32);
+//                                  G_t = 2^(-D^2 t^2), D = a1/s (forward recurrence)
+constexpr int REC_F4 = 4;
 
 __host__ __device__ inline int find_image_by_tile(const ImgTable& t, int tile) {
     int lo = 0, hi = t.n_imgs - 1;

@@ -29,6 +29,9 @@
 #ifndef GSR_BWD_UNROLL
 #define GSR_BWD_UNROLL 4
 #endif
+#ifndef GSR_BWD_CONTIG
+#define GSR_BWD_CONTIG 1          // 1: each warp scans a contiguous share of every span
+#endif
 #ifndef GSR_BWD_SNAKE
 #define GSR_BWD_SNAKE 1
 #endif
@@ -226,82 +229,129 @@ __global__ void __launch_bounds__(BWD_THREADS) k_render_bwd(
     const int cy_hi = min(im.ncy - 1, (Ty1 - im.row_begin + im.offy) / CELL);
     const float invs = im.invs;
 
+    // Candidate compaction: each warp scans its share of the tile's candidate spans (32 records
+    // at a time, rect test only), appends the candidates whose support rect meets the tile to a
+    // per-warp queue in shared memory, and evaluates full groups of 32 -- so every lane of a
+    // group owns a Gaussian that touches the tile (the spans also hold Gaussians that stop short
+    // of it: the query extent is the largest support in the image).
+    __shared__ int queue[BWD_WARPS][64];
+    const unsigned lt = (1u << lane) - 1u;
+    int qn = 0;                                   // warp-uniform queue length
+    auto group = [&](int p, bool act) {
+        float4 r0 = make_float4(0.f, 0.f, 0.f, 0.f), r1 = r0, r2 = r0, r3 = r0;
+        int x0 = 1, x1 = 0, y0 = 1, y1 = 0;          // window rect (masks)
+        int sx0 = 1, sx1 = 0, sy0 = 1, sy1 = 0;      // support rect (loop bounds)
+        if (act) {
+            r0 = __ldg(rec + (long long)REC_F4 * p);
+            r1 = __ldg(rec + (long long)REC_F4 * p + 1);
+            r2 = __ldg(rec + (long long)REC_F4 * p + 2);
+            r3 = __ldg(rec + (long long)REC_F4 * p + 3);
+            unsigned xs = __float_as_uint(r2.z), ys = __float_as_uint(r2.w);
+            x0 = (int)(xs & 0xffffu); x1 = (int)(xs >> 16);
+            y0 = (int)(ys & 0xffffu); y1 = (int)(ys >> 16);
+            xs = __float_as_uint(r3.x); ys = __float_as_uint(r3.y);
+            sx0 = (int)(xs & 0xffffu); sx1 = (int)(xs >> 16);
+            sy0 = (int)(ys & 0xffffu); sy1 = (int)(ys >> 16);
+        }
+        // warp-uniform loop bounds: union of the active support rects (rows and columns; pairs
+        // outside a lane's support evaluate to exactly 0), and the column range inside every
+        // active lane's window (no per-pixel x mask needed there)
+        const int ya = max(Ty0, (int)__reduce_min_sync(0xffffffffu, act ? sy0 : 0x7fffffff));
+        const int yb = min(Ty1, (int)__reduce_max_sync(0xffffffffu, act ? sy1 : -1));
+        const int xa = max(Tx0, (int)__reduce_min_sync(0xffffffffu, act ? sx0 : 0x7fffffff));
+        const int xb = min(Tx1, (int)__reduce_max_sync(0xffffffffu, act ? sx1 : -1));
+        const int xia = (int)__reduce_max_sync(0xffffffffu, act ? x0 : -1);
+        const int xib = (int)__reduce_min_sync(0xffffffffu, act ? x1 : 0x7fffffff);
+        // column pairs relative to Tx0
+        const int ca = (xa - Tx0) & ~1;
+        const int ce = ((xb - Tx0) | 1) + 1;                  // exclusive, even
+        int ma = ((xia - Tx0) + 1) & ~1;                      // first pair fully >= xia
+        int mb = ((xib - Tx0) + 1) & ~1;                      // pairs [ma, mb) fully <= xib
+        ma = min(max(ma, ca), ce);
+        mb = min(max(mb, ma), ce);
+
+        LaneG L;
+        L.D2 = f2(r1.x * invs);
+        L.cr = f2(r1.w); L.cg = f2(r2.x); L.cb = f2(r2.y);
+        L.x0 = x0; L.x1 = x1;
+        const float kT = (float)Tx0 - r0.x;
+        const float tdl = -r1.x * r0.z;                        // -a1 dl_x
+        macc_t m[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) m[k] = (macc_t)0;
+        for (int y = ya; y <= yb; y += 2) {
+            // rows y and y + 1 (the second one is a phantom when y == yb: u = -inf)
+            const int y1r = y + 1;
+            const bool has1 = y1r <= yb;
+            const float dy0 = fmaf((float)y - r0.y, invs, -r0.w);
+            const float dy1 = fmaf((float)y1r - r0.y, invs, -r0.w);
+            const float v0 = r1.z * dy0, v1 = r1.z * dy1;
+            const float u0 = (y >= y0 && y <= y1) ? -(v0 * v0) : -INFINITY;
+            const float u1 = (has1 && y1r >= y0 && y1r <= y1) ? -(v1 * v1) : -INFINITY;
+            const float2 T0 = f2(fmaf(r1.y, dy0, tdl)), T1 = f2(fmaf(r1.y, dy1, tdl));
+            const float2 U0 = f2(u0), U1 = f2(u1);
+            const int ry0 = y - Ty0, ry1 = has1 ? ry0 + 1 : ry0;
+            const float4* gA0 = &gA[ry0][0];
+            const float2* gB0 = &gB[ry0][0];
+            const float4* gA1 = &gA[ry1][0];
+            const float2* gB1 = &gB[ry1][0];
+            RowAcc A0, A1;
+            A0.FR = A0.FG = A0.FB = A0.W1 = A0.W2 = f2(0.f);
+            A1 = A0;
+            row2_pairs<true>(ca, ma, gA0, gB0, gA1, gB1, kT, L, Tx0, T0, U0, T1, U1, A0, A1);
+            row2_pairs<false>(ma, mb, gA0, gB0, gA1, gB1, kT, L, Tx0, T0, U0, T1, U1, A0, A1);
+            row2_pairs<true>(mb, ce, gA0, gB0, gA1, gB1, kT, L, Tx0, T0, U0, T1, U1, A0, A1);
+            fold_row(A0, v0, r1, r2, m);
+            if (has1) fold_row(A1, v1, r1, r2, m);
+        }
+        if (act) {
+            double* dst = moments + 8LL * perm[p];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) atomicAdd(dst + k, (double)m[k]);
+        }
+    };
+
     for (int cy = cy_lo; cy <= cy_hi; ++cy) {
         const int row = im.cell_base + cy * im.ncx;
-        const int sp0 = cell_start[row + cx_lo], sp1 = cell_start[row + cx_hi + 1];
-        for (int p0 = sp0 + (kpart * BWD_WARPS + warp) * 32; p0 < sp1;
-             p0 += ks * BWD_WARPS * 32) {
+        // this warp's contiguous share of the span (consecutive candidates are spatially close,
+        // which keeps the union of a group's rects tight)
+        const int s0 = cell_start[row + cx_lo], s1 = cell_start[row + cx_hi + 1];
+        const int parts = ks * BWD_WARPS, part = kpart * BWD_WARPS + warp;
+#if GSR_BWD_CONTIG
+        const int sp0 = s0 + (int)(((long long)(s1 - s0) * part) / parts);
+        const int sp1 = s0 + (int)(((long long)(s1 - s0) * (part + 1)) / parts);
+        for (int p0 = sp0; p0 < sp1; p0 += 32) {
+#else
+        const int sp1 = s1;
+        for (int p0 = s0 + part * 32; p0 < sp1; p0 += parts * 32) {
+#endif
             const int p = p0 + lane;
-            bool act = p < sp1;
-            float4 r0 = make_float4(0.f, 0.f, 0.f, 0.f), r1 = r0, r2 = r0;
-            int x0 = 1, x1 = 0, y0 = 1, y1 = 0;
-            if (act) {
-                r0 = __ldg(rec + 3LL * p);
-                r1 = __ldg(rec + 3LL * p + 1);
-                r2 = __ldg(rec + 3LL * p + 2);
-                unsigned xs = __float_as_uint(r2.z), ys = __float_as_uint(r2.w);
-                x0 = (int)(xs & 0xffffu); x1 = (int)(xs >> 16);
-                y0 = (int)(ys & 0xffffu); y1 = (int)(ys >> 16);
-                act = !(x1 < Tx0 || x0 > Tx1 || y1 < Ty0 || y0 > Ty1);
-                if (!act) { x0 = 1; x1 = 0; y0 = 1; y1 = 0; }
+            bool hit = false;
+            if (p < sp1) {
+                const float4 r3 = __ldg(rec + (long long)REC_F4 * p + 3);
+                const unsigned xs = __float_as_uint(r3.x), ys = __float_as_uint(r3.y);
+                const int x0 = (int)(xs & 0xffffu), x1 = (int)(xs >> 16);
+                const int y0 = (int)(ys & 0xffffu), y1 = (int)(ys >> 16);
+                hit = !(x1 < Tx0 || x0 > Tx1 || y1 < Ty0 || y0 > Ty1);
             }
-            if (__ballot_sync(0xffffffffu, act) == 0) continue;
-            // warp-uniform loop bounds: union of the active rects (rows and columns), and the
-            // column range covered by every active lane (no per-pixel x mask needed there)
-            const int ya = max(Ty0, (int)__reduce_min_sync(0xffffffffu, act ? y0 : 0x7fffffff));
-            const int yb = min(Ty1, (int)__reduce_max_sync(0xffffffffu, act ? y1 : -1));
-            const int xa = max(Tx0, (int)__reduce_min_sync(0xffffffffu, act ? x0 : 0x7fffffff));
-            const int xb = min(Tx1, (int)__reduce_max_sync(0xffffffffu, act ? x1 : -1));
-            const int xia = (int)__reduce_max_sync(0xffffffffu, act ? x0 : -1);
-            const int xib = (int)__reduce_min_sync(0xffffffffu, act ? x1 : 0x7fffffff);
-            // column pairs relative to Tx0
-            const int ca = (xa - Tx0) & ~1;
-            const int ce = ((xb - Tx0) | 1) + 1;                  // exclusive, even
-            int ma = ((xia - Tx0) + 1) & ~1;                      // first pair fully >= xia
-            int mb = ((xib - Tx0) + 1) & ~1;                      // pairs [ma, mb) fully <= xib
-            ma = min(max(ma, ca), ce);
-            mb = min(max(mb, ma), ce);
-
-            LaneG L;
-            L.D2 = f2(r1.x * invs);
-            L.cr = f2(r1.w); L.cg = f2(r2.x); L.cb = f2(r2.y);
-            L.x0 = x0; L.x1 = x1;
-            const float kT = (float)Tx0 - r0.x;
-            const float tdl = -r1.x * r0.z;                        // -a1 dl_x
-            macc_t m[8];
-#pragma unroll
-            for (int k = 0; k < 8; ++k) m[k] = (macc_t)0;
-            for (int y = ya; y <= yb; y += 2) {
-                // rows y and y + 1 (the second one is a phantom when y == yb: u = -inf)
-                const int y1r = y + 1;
-                const bool has1 = y1r <= yb;
-                const float dy0 = fmaf((float)y - r0.y, invs, -r0.w);
-                const float dy1 = fmaf((float)y1r - r0.y, invs, -r0.w);
-                const float v0 = r1.z * dy0, v1 = r1.z * dy1;
-                const float u0 = (y >= y0 && y <= y1) ? -(v0 * v0) : -INFINITY;
-                const float u1 = (has1 && y1r >= y0 && y1r <= y1) ? -(v1 * v1) : -INFINITY;
-                const float2 T0 = f2(fmaf(r1.y, dy0, tdl)), T1 = f2(fmaf(r1.y, dy1, tdl));
-                const float2 U0 = f2(u0), U1 = f2(u1);
-                const int ry0 = y - Ty0, ry1 = has1 ? ry0 + 1 : ry0;
-                const float4* gA0 = &gA[ry0][0];
-                const float2* gB0 = &gB[ry0][0];
-                const float4* gA1 = &gA[ry1][0];
-                const float2* gB1 = &gB[ry1][0];
-                RowAcc A0, A1;
-                A0.FR = A0.FG = A0.FB = A0.W1 = A0.W2 = f2(0.f);
-                A1 = A0;
-                row2_pairs<true>(ca, ma, gA0, gB0, gA1, gB1, kT, L, Tx0, T0, U0, T1, U1, A0, A1);
-                row2_pairs<false>(ma, mb, gA0, gB0, gA1, gB1, kT, L, Tx0, T0, U0, T1, U1, A0, A1);
-                row2_pairs<true>(mb, ce, gA0, gB0, gA1, gB1, kT, L, Tx0, T0, U0, T1, U1, A0, A1);
-                fold_row(A0, v0, r1, r2, m);
-                if (has1) fold_row(A1, v1, r1, r2, m);
-            }
-            if (act) {
-                double* dst = moments + 8LL * perm[p];
-#pragma unroll
-                for (int k = 0; k < 8; ++k) atomicAdd(dst + k, (double)m[k]);
+            const unsigned hm = __ballot_sync(0xffffffffu, hit);
+            if (hit) queue[warp][qn + __popc(hm & lt)] = p;
+            qn += __popc(hm);
+            __syncwarp();
+            if (qn >= 32) {
+                const int pg = queue[warp][lane];
+                const int carry = lane < qn - 32 ? queue[warp][32 + lane] : 0;
+                __syncwarp();
+                if (lane < qn - 32) queue[warp][lane] = carry;
+                qn -= 32;
+                __syncwarp();
+                group(pg, true);
             }
         }
+    }
+    if (qn > 0) {
+        const bool act = lane < qn;
+        group(act ? queue[warp][lane] : 0, act);
     }
 }
 

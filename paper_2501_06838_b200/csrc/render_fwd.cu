@@ -10,9 +10,10 @@
 // g = w, w + 4, w + 8, ... of each staged chunk: the warps' loads are identical by construction
 // (a vertical split of the tile would give each warp a different, order-dependent share of every
 // chunk and serialise the ring). The 4 partial images are summed in warp order at the end.
-//   * per Gaussian, warp-uniform: the producer drops it if its rect misses the tile and flags
-//     it "full" if the rect covers all 32 columns and 16 rows (no x mask, no y test);
-//     otherwise the masked path.
+//   * per Gaussian, warp-uniform: the producer drops it if its support rect (R21) misses the
+//     tile and flags it "full" if its window rect covers all 32 columns and 16 rows (no x mask,
+//     no y test: pixels beyond the support evaluate to exactly 0 by themselves); otherwise the
+//     masked path (window edge inside the tile).
 //   * per lane: kx = x - ax (exact small integers, one FADD2 per column pair, shared by the two
 //     rows), per row w = (a1/s) kx + (b1 dy - a1 dl_x) (one FFMA2 per pixel pair), q = -w^2 - v^2
 //     (one FFMA2; the y test folds into -v^2 -> -inf), 2^q on the SFU (ex2.approx.ftz ->
@@ -79,7 +80,7 @@ __device__ __forceinline__ float2 f2(float a) { return make_float2(a, a); }
 template <class CFG>
 struct FwdSmem {
     static constexpr int NACC = CFG::ROWS * (CFG::STRIP / 2) * 3;   // float2 accumulators/thread
-    float4 rec[FWD_STAGES][FWD_CHUNK * 3];
+    float4 rec[FWD_STAGES][FWD_CHUNK * REC_F4];
     float2 tot[FWD_CWARPS][NACC][32];        // per-warp totals (second accumulation level)
     float g3[FWD_STAGES][FWD_CHUNK];         // 2^(-9 D^2) of recurrence-path records
     uint16_t idx[FWD_STAGES][FWD_CHUNK];     // kept records: index | full << 8 | recurrence << 9
@@ -91,7 +92,8 @@ struct FwdSmem {
 };
 
 // Transformed record (written in shared memory by the producer warp, see k_render_fwd):
-//   r0 = {-ax, ay, dl_y, a1/s},  r1 = {-a1 dl_x, b1, c1, c'_r},  r2 = {c'_g, c'_b, x0|x1, y0|y1}
+//   r0 = {-ax, ay, dl_y, a1/s},  r1 = {-a1 dl_x, b1, c1, c'_r},
+//   r2 = {c'_g, c'_b, window x0|x1, y0|y1}  (recurrence path: {c'_g, c'_b, G1, G2})
 template <class CFG, bool FULL>
 __device__ __forceinline__ void fwd_gauss(const float4 r0, const float4 r1, const float4 r2,
                                           const float2 (&xj)[CFG::STRIP / 2], float yf0,
@@ -277,9 +279,10 @@ __global__ void __launch_bounds__(FWD_THREADS) k_render_fwd(const ImgTable tab,
             const int n = prod.next(&start, k == 0 ? krank : KS - 1);
             sm.count[s] = n;
             if (n > 0) {
-                const uint32_t bytes = (uint32_t)n * 48u;
+                const uint32_t bytes = (uint32_t)n * (16u * REC_F4);
                 mbar_arrive_expect_tx(&sm.full_bar[s], bytes);
-                tma_bulk_g2s(&sm.rec[s][0], rec + 3LL * start, bytes, &sm.full_bar[s]);
+                tma_bulk_g2s(&sm.rec[s][0], rec + (long long)REC_F4 * start, bytes,
+                             &sm.full_bar[s]);
             } else {
                 mbar_arrive(&sm.full_bar[s]);      // end marker
             }
@@ -313,24 +316,28 @@ __global__ void __launch_bounds__(FWD_THREADS) k_render_fwd(const ImgTable tab,
                     const int g = g0 + lane;
                     bool keep = false, full = false, rec_ok = false;
                     if (g < n) {
-                        const float4 r2 = sr[3 * g + 2];
+                        // keep: the support rect (R21) meets the tile; "full": the window rect
+                        // (R2) covers every column and every lane row of the tile -- no masks
+                        // (pixels beyond the support evaluate to 0 in fp32 by themselves)
+                        const float4 r2 = sr[REC_F4 * g + 2], r3 = sr[REC_F4 * g + 3];
+                        const unsigned sxs = __float_as_uint(r3.x), sys = __float_as_uint(r3.y);
+                        const int sx0 = (int)(sxs & 0xffffu), sx1 = (int)(sxs >> 16);
+                        const int sy0 = (int)(sys & 0xffffu), sy1 = (int)(sys >> 16);
+                        keep = fy0 <= fy1 && !(sx1 < fx0 || sx0 > fx1 || sy1 < fy0 || sy0 > fy1);
                         const unsigned xs = __float_as_uint(r2.z), ys = __float_as_uint(r2.w);
                         const int x0 = (int)(xs & 0xffffu), x1 = (int)(xs >> 16);
                         const int y0 = (int)(ys & 0xffffu), y1 = (int)(ys >> 16);
-                        keep = fy0 <= fy1 && !(x1 < fx0 || x0 > fx1 || y1 < fy0 || y0 > fy1);
-                        // "full": the rect covers every column and every lane row of the tile
                         full = x0 <= fx0 && x1 >= fx1 && y0 <= fy0 && y1 >= fy0 + FTILE_H - 1;
                         if (keep) {
-                            const float4 r0 = sr[3 * g], r1 = sr[3 * g + 1];
+                            const float4 r0 = sr[REC_F4 * g], r1 = sr[REC_F4 * g + 1];
                             const float D = r1.x * invs;
-                            sr[3 * g] = make_float4(-r0.x, r0.y, r0.w, D);
-                            sr[3 * g + 1] = make_float4(-r1.x * r0.z, r1.y, r1.z, r1.w);
+                            sr[REC_F4 * g] = make_float4(-r0.x, r0.y, r0.w, D);
+                            sr[REC_F4 * g + 1] = make_float4(-r1.x * r0.z, r1.y, r1.z, r1.w);
                             // exponential recurrence (2-row lane blocks): G_t = 2^(-D^2 t^2)
                             rec_ok = CFG::ROWS == 2 && full && D <= FWD_REC_DMAX;
-                            if (rec_ok) {
-                                const float d2 = D * D;
-                                sr[3 * g + 2] = make_float4(r2.x, r2.y, exp2f(-d2), exp2f(-4.f * d2));
-                                sm.g3[sf][g] = exp2f(-9.f * d2);
+                            if (rec_ok) {      // G1, G2 from K1b; G3 = G1^9 = G2^2 G1
+                                sr[REC_F4 * g + 2] = make_float4(r2.x, r2.y, r3.z, r3.w);
+                                sm.g3[sf][g] = r3.w * r3.w * r3.z;
                             }
                         }
                     }
@@ -383,7 +390,8 @@ __global__ void __launch_bounds__(FWD_THREADS) k_render_fwd(const ImgTable tab,
             for (int i = warp; i < nk; i += FWD_CWARPS) {
                 const int e = ix[i];
                 const int g = e & 0xff;
-                const float4 r0 = sr[3 * g], r1 = sr[3 * g + 1], r2 = sr[3 * g + 2];
+                const float4 r0 = sr[REC_F4 * g], r1 = sr[REC_F4 * g + 1],
+                             r2 = sr[REC_F4 * g + 2];
                 if constexpr (FWD_ROWS == 2) {
                     if (e & 0x200)
                         fwd_gauss_r2<2>(r0, r1, r2, sm.g3[s][g], xlf, yf0, yi, xl0, invs, acc);

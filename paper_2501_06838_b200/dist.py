@@ -28,10 +28,14 @@ def out_size(n: int, s: float) -> int:
     return int(math.floor(s * n))
 
 
-def row_pair_counts(mu: np.ndarray, valid: np.ndarray, H: int, W: int, s: float, ratio: float
-                    ) -> np.ndarray:
+SUPPORT_SIGMAS = 13.5      # reading R21: the kernels' evaluation box, +-13.5 sigma
+
+
+def row_pair_counts(mu: np.ndarray, valid: np.ndarray, H: int, W: int, s: float, ratio: float,
+                    sigma: np.ndarray | None = None) -> np.ndarray:
     """Exact pairs per HR row of one image: rowpairs[y] = sum_i [y0_i <= y <= y1_i] (x1_i-x0_i+1),
-    with the integer window rect of reading R2 (fp64, same operation order as the kernels)."""
+    with the integer window rect of reading R2 (fp64, same operation order as the kernels), cut
+    to the support box of reading R21 when sigma is given (the pairs the kernels evaluate)."""
     Hs, Ws = out_size(H, s), out_size(W, s)
     mx = mu[:, 0].astype(np.float64)
     my = mu[:, 1].astype(np.float64)
@@ -42,6 +46,13 @@ def row_pair_counts(mu: np.ndarray, valid: np.ndarray, H: int, W: int, s: float,
         x1 = np.ceil(np.clip(s * (mx + hx), -lim, lim)) - 1
         y0 = np.floor(np.clip(s * (my - hy), -lim, lim)) + 1
         y1 = np.ceil(np.clip(s * (my + hy), -lim, lim)) - 1
+        if sigma is not None:
+            tx = SUPPORT_SIGMAS * sigma[:, 0].astype(np.float64)
+            ty = SUPPORT_SIGMAS * sigma[:, 1].astype(np.float64)
+            x0 = np.maximum(x0, np.floor(np.clip(s * (mx - tx), -lim, lim)))
+            x1 = np.minimum(x1, np.ceil(np.clip(s * (mx + tx), -lim, lim)))
+            y0 = np.maximum(y0, np.floor(np.clip(s * (my - ty), -lim, lim)))
+            y1 = np.minimum(y1, np.ceil(np.clip(s * (my + ty), -lim, lim)))
         x0 = np.maximum(x0, 0); x1 = np.minimum(x1, Ws - 1)
         y0 = np.maximum(y0, 0); y1 = np.minimum(y1, Hs - 1)
         ok = valid & (x0 <= x1) & (y0 <= y1)

@@ -21,6 +21,11 @@ def test_row_pair_counts_match_oracle():
         assert rc.sum() == O.pair_count(c, H, W, s, 0.1)
         for rb, re in [(0, 5), (7, 19), (Hs - 3, Hs)]:
             assert rc[rb:re].sum() == O.pair_count(c, H, W, s, 0.1, rows=(rb, re))
+        # support rects (reading R21): the pairs the kernels evaluate
+        rs = gd.row_pair_counts(c["mu"], np.ones(c["alpha"].shape[0], bool), H, W, s, 0.3,
+                                sigma=c["sigma"])
+        assert rs.sum() == O.pair_count(c, H, W, s, 0.3, support=True)
+        assert rs[7:19].sum() == O.pair_count(c, H, W, s, 0.3, rows=(7, 19), support=True)
 
 
 @pytest.mark.parametrize("G", [1, 2, 3, 4, 8])
