@@ -34,8 +34,14 @@ constexpr int FWD_SMALL_WINDOW = 48;             // HR px: below this the small 
 constexpr float FWD_REC_DMAX = GSR_FWD_REC ? 1.0f : -1.0f;            // max a1/s for the forward's exp recurrence
 constexpr int FWD_CWARPS = 4;                    // consumer warps
 constexpr int FWD_THREADS = (FWD_CWARPS + 1) * 32;
-constexpr int FWD_CHUNK = 128;                   // records per TMA bulk stage
-constexpr int FWD_STAGES = 4;
+#ifndef GSR_FWD_CHUNK
+#define GSR_FWD_CHUNK 128
+#endif
+#ifndef GSR_FWD_STAGES
+#define GSR_FWD_STAGES 3
+#endif
+constexpr int FWD_CHUNK = GSR_FWD_CHUNK;         // records per TMA bulk stage (<= 256)
+constexpr int FWD_STAGES = GSR_FWD_STAGES;
 #ifndef GSR_BWD_WARPS
 #define GSR_BWD_WARPS 4
 #endif

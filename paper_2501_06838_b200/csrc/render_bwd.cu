@@ -30,7 +30,10 @@
 #define GSR_BWD_UNROLL 4
 #endif
 #ifndef GSR_BWD_CONTIG
-#define GSR_BWD_CONTIG 1          // 1: each warp scans a contiguous share of every span
+#define GSR_BWD_CONTIG 0          // 1: each warp scans a contiguous share of every span
+#endif
+#ifndef GSR_BWD_BATCH
+#define GSR_BWD_BATCH 512         // hits per sorted batch (multiple of 32)
 #endif
 #ifndef GSR_BWD_SNAKE
 #define GSR_BWD_SNAKE 1
@@ -44,6 +47,7 @@ namespace gsr {
 namespace {
 
 constexpr int kBwdUnroll = GSR_BWD_UNROLL;
+constexpr int BWD_BATCH = GSR_BWD_BATCH;
 
 __device__ __forceinline__ float2 f2(float a) { return make_float2(a, a); }
 
@@ -229,12 +233,19 @@ __global__ void __launch_bounds__(BWD_THREADS) k_render_bwd(
     const int cy_hi = min(im.ncy - 1, (Ty1 - im.row_begin + im.offy) / CELL);
     const float invs = im.invs;
 
-    // Candidate compaction: each warp scans its share of the tile's candidate spans (32 records
-    // at a time, rect test only), appends the candidates whose support rect meets the tile to a
-    // per-warp queue in shared memory, and evaluates full groups of 32 -- so every lane of a
-    // group owns a Gaussian that touches the tile (the spans also hold Gaussians that stop short
-    // of it: the query extent is the largest support in the image).
-    __shared__ int queue[BWD_WARPS][64];
+    // Candidate compaction + grouping. Each warp scans its share of the tile's candidate spans
+    // (32 records at a time, support-rect test only) and appends the candidates whose support
+    // rect meets the tile to a per-warp queue in shared memory, with a key = the clipped column
+    // range in 8-px buckets ((x0 - Tx0) >> 3, (x1 - Tx0) >> 3). Every BWD_BATCH hits the warp
+    // sorts its queue by key (stable counting sort) and evaluates groups of 32: every lane of a
+    // group owns a Gaussian that touches the tile, and lanes with similar column ranges share a
+    // group, so the union of their rects (the loop bounds) stays tight (C5: 52% -> ~67% of the
+    // evaluated pairs inside some lane's support, tools/sim in DESIGN.md).
+    constexpr int NB = 64;                        // key buckets (8 x 8)
+    __shared__ int qp[BWD_WARPS][BWD_BATCH + 32];
+    __shared__ unsigned char qk[BWD_WARPS][BWD_BATCH + 32];
+    __shared__ int qs[BWD_WARPS][BWD_BATCH + 32];
+    __shared__ int hist[BWD_WARPS][NB];
     const unsigned lt = (1u << lane) - 1u;
     int qn = 0;                                   // warp-uniform queue length
     auto group = [&](int p, bool act) {
@@ -311,10 +322,68 @@ __global__ void __launch_bounds__(BWD_THREADS) k_render_bwd(
         }
     };
 
+    // sort the first cnt queue entries by key (stable: ranks via match_any in queue order),
+    // evaluate them in groups of 32, then move the rest of the queue to the front
+    auto flush = [&](int cnt) {
+        hist[warp][lane] = 0;
+        hist[warp][lane + 32] = 0;
+        __syncwarp();
+        for (int i0 = 0; i0 < cnt; i0 += 32) {
+            const int i = i0 + lane;
+            const bool v = i < cnt;
+            const unsigned vm = __ballot_sync(0xffffffffu, v);
+            if (v) {
+                const int k = qk[warp][i];
+                const unsigned peers = __match_any_sync(vm, k);
+                if ((peers & lt) == 0) hist[warp][k] += __popc(peers);
+            }
+            __syncwarp();
+        }
+        {   // exclusive scan of the 64 bucket counts (2 per lane)
+            const int a = hist[warp][2 * lane], b = hist[warp][2 * lane + 1];
+            int incl = a + b;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            __syncwarp();
+            hist[warp][2 * lane] = incl - a - b;
+            hist[warp][2 * lane + 1] = incl - b;
+            __syncwarp();
+        }
+        for (int i0 = 0; i0 < cnt; i0 += 32) {
+            const int i = i0 + lane;
+            const bool v = i < cnt;
+            const unsigned vm = __ballot_sync(0xffffffffu, v);
+            int k = 0, pos = 0;
+            unsigned peers = 0;
+            if (v) {
+                k = qk[warp][i];
+                peers = __match_any_sync(vm, k);
+                pos = hist[warp][k] + __popc(peers & lt);
+                qs[warp][pos] = qp[warp][i];
+            }
+            __syncwarp();
+            if (v && (peers & lt) == 0) hist[warp][k] += __popc(peers);
+            __syncwarp();
+        }
+        for (int g = 0; g < cnt; g += 32) {
+            const bool act = g + lane < cnt;
+            group(act ? qs[warp][g + lane] : 0, act);
+        }
+        const int rest = qn - cnt;                // < 32
+        int cp = 0;
+        unsigned char ck = 0;
+        if (lane < rest) { cp = qp[warp][cnt + lane]; ck = qk[warp][cnt + lane]; }
+        __syncwarp();
+        if (lane < rest) { qp[warp][lane] = cp; qk[warp][lane] = ck; }
+        qn = rest;
+        __syncwarp();
+    };
+
     for (int cy = cy_lo; cy <= cy_hi; ++cy) {
         const int row = im.cell_base + cy * im.ncx;
-        // this warp's contiguous share of the span (consecutive candidates are spatially close,
-        // which keeps the union of a group's rects tight)
         const int s0 = cell_start[row + cx_lo], s1 = cell_start[row + cx_hi + 1];
         const int parts = ks * BWD_WARPS, part = kpart * BWD_WARPS + warp;
 #if GSR_BWD_CONTIG
@@ -327,32 +396,27 @@ __global__ void __launch_bounds__(BWD_THREADS) k_render_bwd(
 #endif
             const int p = p0 + lane;
             bool hit = false;
+            int key = 0;
             if (p < sp1) {
                 const float4 r3 = __ldg(rec + (long long)REC_F4 * p + 3);
                 const unsigned xs = __float_as_uint(r3.x), ys = __float_as_uint(r3.y);
                 const int x0 = (int)(xs & 0xffffu), x1 = (int)(xs >> 16);
                 const int y0 = (int)(ys & 0xffffu), y1 = (int)(ys >> 16);
                 hit = !(x1 < Tx0 || x0 > Tx1 || y1 < Ty0 || y0 > Ty1);
+                key = ((max(x0, Tx0) - Tx0) >> 3) * 8 + ((min(x1, Tx1) - Tx0) >> 3);
             }
             const unsigned hm = __ballot_sync(0xffffffffu, hit);
-            if (hit) queue[warp][qn + __popc(hm & lt)] = p;
+            if (hit) {
+                const int slot = qn + __popc(hm & lt);
+                qp[warp][slot] = p;
+                qk[warp][slot] = (unsigned char)key;
+            }
             qn += __popc(hm);
             __syncwarp();
-            if (qn >= 32) {
-                const int pg = queue[warp][lane];
-                const int carry = lane < qn - 32 ? queue[warp][32 + lane] : 0;
-                __syncwarp();
-                if (lane < qn - 32) queue[warp][lane] = carry;
-                qn -= 32;
-                __syncwarp();
-                group(pg, true);
-            }
+            if (qn >= BWD_BATCH) flush(BWD_BATCH);
         }
     }
-    if (qn > 0) {
-        const bool act = lane < qn;
-        group(act ? queue[warp][lane] : 0, act);
-    }
+    if (qn > 0) flush(qn);
 }
 
 __global__ void k_finalize(const float* __restrict__ alpha, const float* __restrict__ mu,
