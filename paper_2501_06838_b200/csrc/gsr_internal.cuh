@@ -14,8 +14,14 @@ namespace gsr {
 
 // ---- compile-time geometry -------------------------------------------------------------
 constexpr int CELL = 16;       // cell edge (HR px): binning granularity (sort key)
-constexpr int TILE_W = 64;     // backward render tile (HR px); also the debug tile-list tile
-constexpr int TILE_H = 32;
+#ifndef GSR_BWD_TILE_W
+#define GSR_BWD_TILE_W 64
+#endif
+#ifndef GSR_BWD_TILE_H
+#define GSR_BWD_TILE_H 16
+#endif
+constexpr int TILE_W = GSR_BWD_TILE_W;  // backward render tile (HR px, power of 2 >= 16);
+constexpr int TILE_H = GSR_BWD_TILE_H;  // also the debug tile-list tile (TILE_H even)
 // forward: a CTA renders one tile; each of the 4 consumer warps covers the whole tile (lane l
 // owns a FWD_ROWS x FWD_STRIP block at column group l & 3, row group l >> 2) and takes every 4th
 // Gaussian of each staged chunk, so the warps' work is balanced by construction; one extra warp

@@ -236,7 +236,7 @@ __global__ void __launch_bounds__(BWD_THREADS) k_render_bwd(
     // Candidate compaction + grouping. Each warp scans its share of the tile's candidate spans
     // (32 records at a time, support-rect test only) and appends the candidates whose support
     // rect meets the tile to a per-warp queue in shared memory, with a key = the clipped column
-    // range in 8-px buckets ((x0 - Tx0) >> 3, (x1 - Tx0) >> 3). Every BWD_BATCH hits the warp
+    // range in TILE_W/8-px buckets (8 x 8 keys). Every BWD_BATCH hits the warp
     // sorts its queue by key (stable counting sort) and evaluates groups of 32: every lane of a
     // group owns a Gaussian that touches the tile, and lanes with similar column ranges share a
     // group, so the union of their rects (the loop bounds) stays tight (C5: 52% -> ~67% of the
@@ -403,7 +403,8 @@ __global__ void __launch_bounds__(BWD_THREADS) k_render_bwd(
                 const int x0 = (int)(xs & 0xffffu), x1 = (int)(xs >> 16);
                 const int y0 = (int)(ys & 0xffffu), y1 = (int)(ys >> 16);
                 hit = !(x1 < Tx0 || x0 > Tx1 || y1 < Ty0 || y0 > Ty1);
-                key = ((max(x0, Tx0) - Tx0) >> 3) * 8 + ((min(x1, Tx1) - Tx0) >> 3);
+                key = ((max(x0, Tx0) - Tx0) / (TILE_W / 8)) * 8 +
+                      (min(x1, Tx1) - Tx0) / (TILE_W / 8);
             }
             const unsigned hm = __ballot_sync(0xffffffffu, hit);
             if (hit) {
