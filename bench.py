@@ -226,6 +226,8 @@ def main():
     ap.add_argument("--workload", default="C5", choices=list(S.CONFIGS))
     ap.add_argument("--images", type=int, default=None, help="dev only: first N images")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-groups", type=int, default=8,
+                    help="image groups of the streamed host-memory step (e2e)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--partition", choices=["band", "image"], default="band",
                     help="N>1: row bands of every image (NCCL all-gather + moment all-reduce) or "
@@ -371,6 +373,17 @@ def main():
             for h, d in zip(h_grads, gr):
                 h.copy_(d, non_blocking=True)
 
+        pipeline = "serial (band exchange between forward and backward)"
+        if world == 1 or by_image:
+            # the public host-memory entry point: image groups streamed with H2D / compute /
+            # D2H overlapped on three streams (ops.StreamedFwdBwd)
+            sfb = gsr.StreamedFwdBwd(lay, RATIO, groups=args.e2e_groups, device=dev)
+            pipeline = (f"{len(sfb.groups)} image groups, H2D / compute / D2H overlapped "
+                        "(StreamedFwdBwd)")
+
+            def e2e_step():
+                sfb(hp, hg, h_out, h_grads)
+
         e2e_step()
         torch.cuda.synchronize()
         barrier()
@@ -386,7 +399,7 @@ def main():
         e2e_ms = float(te.item()) / args.steps
         e2e = {"value": full_pix / (e2e_ms * 1e-3) / 1e6, "unit": UNIT,
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-               "ms_per_step": e2e_ms}
+               "ms_per_step": e2e_ms, "pipeline": pipeline}
 
     # ---- roofline of the dominant kernel (per launch, this rank)
     pk = peaks()

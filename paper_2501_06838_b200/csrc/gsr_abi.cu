@@ -184,7 +184,7 @@ gsr_status prepare(const float* alpha, const float* mu, const float* sigma, cons
 
 extern "C" {
 
-const char* gsr_version(void) { return "gsr-b200 0.3 (sm_100a; fwd tile 32x16 | 16x8, bwd tile 64x16, cell 16, support 13.5 sigma)"; }
+const char* gsr_version(void) { return "gsr-b200 0.3 (sm_100a; fwd tile 32x16 | 16x8, bwd tile 64x8, cell 16, support 13.5 sigma)"; }
 
 gsr_status gsr_profile_enable(int32_t on) {
     std::lock_guard<std::mutex> lk(g_prof.mu);

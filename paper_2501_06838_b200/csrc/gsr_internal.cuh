@@ -18,7 +18,7 @@ constexpr int CELL = 16;       // cell edge (HR px): binning granularity (sort k
 #define GSR_BWD_TILE_W 64
 #endif
 #ifndef GSR_BWD_TILE_H
-#define GSR_BWD_TILE_H 16
+#define GSR_BWD_TILE_H 8
 #endif
 constexpr int TILE_W = GSR_BWD_TILE_W;  // backward render tile (HR px, power of 2 >= 16);
 constexpr int TILE_H = GSR_BWD_TILE_H;  // also the debug tile-list tile (TILE_H even)

@@ -366,3 +366,94 @@ def train_step_l1(raw_alpha, offset, ref, raw_sigma, raw_rho, raw_color, lay: La
         _ptr(loss), *[_ptr(grads[k]) for k in RAW], ws.data_ptr(), ws.numel(),
         _stream_ptr(dev)), "gsr_train_step_l1_batched")
     return out, loss, grads
+
+
+# ------------------------------------------------------------------ host-resident batches
+class StreamedFwdBwd:
+    """Forward + backward of a batch whose inputs and outputs live in pinned HOST memory, the
+    way a data pipeline hands it over: the images are processed in `groups` contiguous image
+    groups, and while group k renders on the compute stream, group k+1's parameters and dL/dI
+    are copied host->device on one copy stream and group k-1's image and gradients are copied
+    device->host on another (B200's copy engines run both directions concurrently with the
+    kernels). Each group is one binning + forward + backward (binning reused) + finalize.
+
+        step = StreamedFwdBwd(lay, ratio, groups=8)
+        step(host_params, host_grad_out, host_out, host_grads)   # enqueued on the current stream
+
+    host_params: (alpha, mu, sigma, rho, color) pinned float32 CPU tensors (n Gaussians);
+    host_grad_out / host_out: pinned flat float32 [lay.out_numel]; host_grads: 5 pinned tensors
+    shaped like host_params. The call returns after enqueueing; the current stream waits for all
+    work (synchronize it, or record an event, before reading the host outputs)."""
+
+    def __init__(self, lay: Layout, ratio: float = 0.1, groups: int = 8, device=None):
+        self.lay, self.ratio = lay, float(ratio)
+        self.dev = torch.device(device if device is not None else "cuda")
+        ims = lay.images
+        n = max((im.g_off + im.g_cnt for im in ims), default=0)
+        self.n = n
+        G = max(1, min(groups, len(ims)))
+        self.groups = []
+        for q in range(G):
+            k0, k1 = (q * len(ims)) // G, ((q + 1) * len(ims)) // G
+            if k0 == k1:
+                continue
+            g0 = min(ims[k].g_off for k in range(k0, k1))
+            g1 = max(ims[k].g_off + ims[k].g_cnt for k in range(k0, k1))
+            sub = layout([Image(ims[k].H, ims[k].W, ims[k].s, ims[k].g_off - g0, ims[k].g_cnt,
+                                lay.rows[k][0], lay.rows[k][1]) for k in range(k0, k1)])
+            o0 = lay.out_off[k0]
+            self.groups.append((g0, g1, o0, o0 + sub.out_numel, sub))
+        dev = self.dev
+        widths = (1, 2, 2, 1, 3)
+        self.d_par = [torch.empty((n, w) if w > 1 else (n,), dtype=torch.float32, device=dev)
+                      for w in widths]
+        self.d_grad = [torch.empty_like(t) for t in self.d_par]
+        self.d_g = torch.empty(lay.out_numel, dtype=torch.float32, device=dev)
+        self.d_out = torch.empty(lay.out_numel, dtype=torch.float32, device=dev)
+        self.d_mom = torch.empty((n, 8), dtype=torch.float64, device=dev)
+        nb = 256
+        for g0, g1, o0, o1, sub in self.groups:
+            for c0, c1, _, arr, m in _chunks(sub):
+                nb = max(nb, _ws_bytes(arr, m, c1 - c0, self.ratio))
+        self.ws = torch.empty(nb, dtype=torch.uint8, device=dev)
+        self.s_h2d = torch.cuda.Stream(device=dev)
+        self.s_cmp = torch.cuda.Stream(device=dev)
+        self.s_d2h = torch.cuda.Stream(device=dev)
+
+    def __call__(self, host_params, host_grad_out, host_out, host_grads):
+        cur = torch.cuda.current_stream(self.dev)
+        for s in (self.s_h2d, self.s_cmp, self.s_d2h):
+            s.wait_stream(cur)
+        done_h2d, done_cmp = [], []
+        for g0, g1, o0, o1, sub in self.groups:
+            with torch.cuda.stream(self.s_h2d):
+                for d, h in zip(self.d_par, host_params):
+                    d[g0:g1].copy_(h[g0:g1], non_blocking=True)
+                self.d_g[o0:o1].copy_(host_grad_out[o0:o1], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(self.s_h2d)
+                done_h2d.append(ev)
+        for q, (g0, g1, o0, o1, sub) in enumerate(self.groups):
+            with torch.cuda.stream(self.s_cmp):
+                self.s_cmp.wait_event(done_h2d[q])
+                par = [t[g0:g1] for t in self.d_par]
+                render_fwd_batched(*par, sub, self.ratio, out=self.d_out[o0:o1],
+                                   workspace=self.ws)
+                mom = self.d_mom[g0:g1]
+                mom.zero_()
+                render_bwd_moments_batched(*par, sub, self.d_g[o0:o1], mom, self.ratio,
+                                           workspace=self.ws, reuse_binning=True)
+                check(_lib.load().gsr_finalize_grads(
+                    *[_ptr(t) for t in par], g1 - g0, _ptr(mom),
+                    *[_ptr(t[g0:g1]) for t in self.d_grad], self.s_cmp.cuda_stream),
+                    "gsr_finalize_grads")
+                ev = torch.cuda.Event()
+                ev.record(self.s_cmp)
+                done_cmp.append(ev)
+            with torch.cuda.stream(self.s_d2h):
+                self.s_d2h.wait_event(ev)
+                host_out[o0:o1].copy_(self.d_out[o0:o1], non_blocking=True)
+                for h, d in zip(host_grads, self.d_grad):
+                    h[g0:g1].copy_(d[g0:g1], non_blocking=True)
+        cur.wait_stream(self.s_d2h)
+        cur.wait_stream(self.s_cmp)
