@@ -241,7 +241,7 @@ __global__ void k_records(const float* __restrict__ alpha, const float* __restri
                           const float* __restrict__ sigma, const float* __restrict__ rho,
                           const float* __restrict__ color, long long n, ImgTable tab,
                           const uint32_t* __restrict__ keys, const int* __restrict__ perm,
-                          float4* __restrict__ rec) {
+                          float4* __restrict__ rec, int4* __restrict__ rects) {
     long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= n) return;
     if (keys[p] >= (uint32_t)tab.total_cells) return;
@@ -263,23 +263,29 @@ __global__ void k_records(const float* __restrict__ alpha, const float* __restri
     double axd = rint(im.s * mx), ayd = rint(im.s * my);   // anchor: nearest HR pixel
     double dlx = mx - axd / im.s, dly = my - ayd / im.s;
     double w = al * K;
-    float4 r0 = make_float4((float)axd, (float)ayd, (float)dlx, (float)dly);
-    float4 r1 = make_float4((float)a1, (float)b1, (float)c1, (float)(w * color[3 * i]));
+    // consumer form: r0 = {-ax, ay, dl_y, D}, r1 = {-a1 dl_x, b1, c1, c'_r}
+    // with D = a1/s formed in fp32 (the recurrence constants below use the same D)
+    const float a1f = (float)a1;
+    const float Df = a1f * im.invs, d2 = Df * Df;
+    float4 r0 = make_float4((float)(-axd), (float)ayd, (float)dly, Df);
+    float4 r1 = make_float4((float)(-a1 * dlx), (float)b1, (float)c1, (float)(w * color[3 * i]));
     unsigned xs = (unsigned)r.x0 | ((unsigned)r.x1 << 16);
     unsigned ys = (unsigned)r.y0 | ((unsigned)r.y1 << 16);
     float4 r2 = make_float4((float)(w * color[3 * i + 1]), (float)(w * color[3 * i + 2]),
                             __uint_as_float(xs), __uint_as_float(ys));
-    // r3: support rect (R21) + the forward's recurrence constants G_t = 2^(-D^2 t^2), t = 1, 2,
-    // with D = a1/s exactly as the forward forms it (fp32 product)
-    const float Df = r1.x * im.invs, d2 = Df * Df;
-    unsigned sxs = (unsigned)sr.x0 | ((unsigned)sr.x1 << 16);
-    unsigned sys = (unsigned)sr.y0 | ((unsigned)sr.y1 << 16);
-    float4 r3 = make_float4(__uint_as_float(sxs), __uint_as_float(sys), exp2f(-d2),
-                            exp2f(-4.f * d2));
+    // r3: the forward's exponential-recurrence constants G_t = 2^(-D^2 t^2), t = 1..3, and the
+    // flag "recurrence allowed" (D <= FWD_REC_DMAX, render_fwd.cu MODE 2)
+    const bool rec_ok = Df <= FWD_REC_DMAX;
+    float4 r3 = make_float4(rec_ok ? exp2f(-d2) : 0.f, rec_ok ? exp2f(-4.f * d2) : 0.f,
+                            rec_ok ? exp2f(-9.f * d2) : 0.f, rec_ok ? 1.f : 0.f);
     rec[REC_F4 * p + 0] = r0;
     rec[REC_F4 * p + 1] = r1;
     rec[REC_F4 * p + 2] = r2;
     rec[REC_F4 * p + 3] = r3;
+    // the rect stream the render kernels filter with (16 B per binned Gaussian)
+    unsigned sxs = (unsigned)sr.x0 | ((unsigned)sr.x1 << 16);
+    unsigned sys = (unsigned)sr.y0 | ((unsigned)sr.y1 << 16);
+    rects[p] = make_int4((int)sxs, (int)sys, (int)xs, (int)ys);
 }
 
 // ---- pair count ---------------------------------------------------------------------------
@@ -333,7 +339,7 @@ __global__ void k_debug_rects(const float* __restrict__ alpha, const float* __re
 // keeping the candidates whose rect intersects the tile. One thread per tile (test-only).
 __global__ void k_debug_tile_lists(ImgTable tab, const int* __restrict__ ext,
                                    const int* __restrict__ cell_start,
-                                   const float4* __restrict__ rec, const int* __restrict__ perm,
+                                   const int4* __restrict__ rects, const int* __restrict__ perm,
                                    const uint32_t* __restrict__ keys,
                                    const int* __restrict__ tile_off, int* __restrict__ counts,
                                    int* __restrict__ ids, int* __restrict__ cells) {
@@ -353,8 +359,8 @@ __global__ void k_debug_tile_lists(ImgTable tab, const int* __restrict__ ext,
     for (int cy = cy_lo; cy <= cy_hi; ++cy) {
         int row = im.cell_base + cy * im.ncx;
         for (int p = cell_start[row + cx_lo]; p < cell_start[row + cx_hi + 1]; ++p) {
-            float4 r3 = rec[REC_F4 * p + 3];
-            unsigned xs = __float_as_uint(r3.x), ys = __float_as_uint(r3.y);
+            const int4 rc = rects[p];
+            unsigned xs = (unsigned)rc.x, ys = (unsigned)rc.y;
             int x0 = xs & 0xffff, x1 = xs >> 16, y0 = ys & 0xffff, y1 = ys >> 16;
             if (x1 < Tx0 || x0 > Tx1 || y1 < Ty0 || y0 > Ty1) continue;
             if (ids) {
@@ -382,6 +388,7 @@ size_t binning_bytes(long long n, int total_cells, int total_tiles) {
     b += align256(sizeof(int) * (size_t)(scan_blocks(scan_src) + 1));  // scan tmp
     b += align256(sizeof(int) * (size_t)(total_cells + 1));     // cell_start
     b += align256(sizeof(float4) * REC_F4 * (size_t)n);         // records
+    b += align256(sizeof(int4) * (size_t)n);                    // rect stream
     b += align256(sizeof(double) * 8 * (size_t)n);              // moments
     b += align256(sizeof(unsigned long long) * 4);              // counters
     b += align256(sizeof(int) * (size_t)(total_tiles + 1));     // debug tile offsets
@@ -403,6 +410,7 @@ void carve_workspace(void* base, long long n, int total_cells, int total_tiles, 
     ws->scan_tmp = (int*)take(sizeof(int) * (size_t)(scan_blocks(scan_src) + 1));
     ws->cell_start = (int*)take(sizeof(int) * (size_t)(total_cells + 1));
     ws->rec = (float4*)take(sizeof(float4) * REC_F4 * (size_t)n);
+    ws->rects = (int4*)take(sizeof(int4) * (size_t)n);
     ws->moments = (double*)take(sizeof(double) * 8 * (size_t)n);
     ws->counter = (unsigned long long*)take(sizeof(unsigned long long) * 4);
     ws->tile_off = (int*)take(sizeof(int) * (size_t)(total_tiles + 1));
@@ -448,7 +456,7 @@ cudaError_t bin_gaussians(const float* alpha, const float* mu, const float* sigm
         k_cell_start<<<grid1d(n + 1, 256), 256, 0, st>>>(kin, n, tab.total_cells,
                                                          ws.cell_start);
         k_records<<<grid1d(n, 256), 256, 0, st>>>(alpha, mu, sigma, rho, color, n, tab, kin, vin,
-                                                   ws.rec);
+                                                   ws.rec, ws.rects);
         *perm_out = vin;
         *keys_sorted_out = kin;
     } else {
@@ -499,16 +507,16 @@ cudaError_t launch_debug_tile_lists(const ImgTable& tab, const Workspace& ws, co
     int nt = tab.total_tiles;
     if (nt <= 0) return cudaSuccess;
     if (!ids) {
-        k_debug_tile_lists<<<grid1d(nt, 64), 64, 0, st>>>(tab, ws.ext, ws.cell_start, ws.rec, perm,
+        k_debug_tile_lists<<<grid1d(nt, 64), 64, 0, st>>>(tab, ws.ext, ws.cell_start, ws.rects, perm,
                                                           keys_sorted, nullptr, counts, nullptr,
                                                           nullptr);
     } else {
-        k_debug_tile_lists<<<grid1d(nt, 64), 64, 0, st>>>(tab, ws.ext, ws.cell_start, ws.rec, perm,
+        k_debug_tile_lists<<<grid1d(nt, 64), 64, 0, st>>>(tab, ws.ext, ws.cell_start, ws.rects, perm,
                                                           keys_sorted, nullptr, ws.tile_off,
                                                           nullptr, nullptr);
         cudaError_t e = exclusive_scan_i32(ws.tile_off, ws.tile_off, nt, ws.scan_tmp, st);
         if (e != cudaSuccess) return e;
-        k_debug_tile_lists<<<grid1d(nt, 64), 64, 0, st>>>(tab, ws.ext, ws.cell_start, ws.rec, perm,
+        k_debug_tile_lists<<<grid1d(nt, 64), 64, 0, st>>>(tab, ws.ext, ws.cell_start, ws.rects, perm,
                                                           keys_sorted, ws.tile_off, counts, ids,
                                                           cells);
     }

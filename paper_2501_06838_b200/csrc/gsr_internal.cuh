@@ -85,16 +85,18 @@ struct ImgTable {
     DevImg img[MAX_IMAGES];
 };
 
-// Sorted record (64 B = REC_F4 x float4), one per binned Gaussian, in cell order:
-//   r0 = {ax, ay, dlx, dly}        anchor (integer HR px, as float) and fp32 residual
-//                                  dl = mu - a/s  (LR px, |dl| <= 0.5/s)
-//   r1 = {a1, b1, c1, cr}          factored exponent: q = -Q/2 log2 e = -(w^2 + v^2),
-//                                  w = a1 dx + b1 dy, v = c1 dy
-//   r2 = {cg, cb, x0|x1<<16, y0|y1<<16}  c' = alpha c K (rgb), clipped WINDOW rect (R2, int
-//                                  bits): the masks (pairs outside it are not in the sum)
-//   r3 = {x0|x1<<16, y0|y1<<16, G1, G2}  clipped SUPPORT rect (R21): tile filtering and loop
-//                                  bounds (pairs outside it are exactly 0 in fp32);
-//                                  G_t = 2^(-D^2 t^2), D = a1/s (forward recurrence)
+// Sorted record (64 B = REC_F4 x float4), one per binned Gaussian, in cell order, in the form
+// the render kernels consume (K1b, binning.cu):
+//   r0 = {-ax, ay, dl_y, D}         anchor a = rint(s mu) (integer HR px, as float), fp32
+//                                  residual dl = mu - a/s (LR px), D = a1/s (fp32 product)
+//   r1 = {-a1 dl_x, b1, c1, c'_r}   factored exponent: q = -Q/2 log2 e = -(w^2 + v^2),
+//                                  w = a1 dx + b1 dy, v = c1 dy; c' = alpha c K
+//   r2 = {c'_g, c'_b, x0|x1<<16, y0|y1<<16}  clipped WINDOW rect (R2): the masks
+//   r3 = {G1, G2, G3, rec}         G_t = 2^(-D^2 t^2) and rec = 1 if D <= FWD_REC_DMAX (forward
+//                                  exponential recurrence), else all 0
+// plus the rect stream rects[p] = {support x0|x1<<16, support y0|y1<<16, window x, window y}:
+// the support rect (R21) for tile filtering and loop bounds (pairs outside it are exactly 0
+// in fp32), read by the forward producer and the backward scan without touching the records.
 constexpr int REC_F4 = 4;
 
 __host__ __device__ inline int find_image_by_tile(const ImgTable& t, int tile) {
@@ -228,6 +230,13 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
                  : "memory");
 }
 
+// adds `bytes` to the barrier's expected transaction count without arriving
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar))
                  : "memory");
@@ -295,7 +304,8 @@ struct Workspace {
     int* hist;               // radix histograms [256 * nblocks]
     int* scan_tmp;           // block sums for the scan
     int* cell_start;         // [total_cells + 1]
-    float4* rec;             // [3 * n]
+    float4* rec;             // [REC_F4 * n] records (sorted order)
+    int4* rects;             // [n] {support x, support y, window x, window y} (sorted order)
     double* moments;         // [8 * n] (backward)
     unsigned long long* counter;  // scratch counters
     int* tile_off;           // debug tile lists: [total_tiles + 1]

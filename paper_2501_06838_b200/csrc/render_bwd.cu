@@ -185,7 +185,8 @@ __device__ __forceinline__ void fold_row(const RowAcc& A, float v, const float4 
 }
 
 __global__ void __launch_bounds__(BWD_THREADS) k_render_bwd(
-    const ImgTable tab, const float4* __restrict__ rec, const int* __restrict__ cell_start,
+    const ImgTable tab, const float4* __restrict__ rec, const int4* __restrict__ rects,
+    const int* __restrict__ cell_start,
     const int* __restrict__ ext, const int* __restrict__ perm, const float* __restrict__ grad_out,
     double* __restrict__ moments, int ks, const float* __restrict__ img,
     const float* __restrict__ gt, float inv_numel) {
@@ -249,18 +250,18 @@ __global__ void __launch_bounds__(BWD_THREADS) k_render_bwd(
     const unsigned lt = (1u << lane) - 1u;
     int qn = 0;                                   // warp-uniform queue length
     auto group = [&](int p, bool act) {
-        float4 r0 = make_float4(0.f, 0.f, 0.f, 0.f), r1 = r0, r2 = r0, r3 = r0;
+        float4 r0 = make_float4(0.f, 0.f, 0.f, 0.f), r1 = r0, r2 = r0;
         int x0 = 1, x1 = 0, y0 = 1, y1 = 0;          // window rect (masks)
         int sx0 = 1, sx1 = 0, sy0 = 1, sy1 = 0;      // support rect (loop bounds)
         if (act) {
             r0 = __ldg(rec + (long long)REC_F4 * p);
             r1 = __ldg(rec + (long long)REC_F4 * p + 1);
             r2 = __ldg(rec + (long long)REC_F4 * p + 2);
-            r3 = __ldg(rec + (long long)REC_F4 * p + 3);
-            unsigned xs = __float_as_uint(r2.z), ys = __float_as_uint(r2.w);
+            const int4 rc = __ldg(rects + p);
+            unsigned xs = (unsigned)rc.z, ys = (unsigned)rc.w;
             x0 = (int)(xs & 0xffffu); x1 = (int)(xs >> 16);
             y0 = (int)(ys & 0xffffu); y1 = (int)(ys >> 16);
-            xs = __float_as_uint(r3.x); ys = __float_as_uint(r3.y);
+            xs = (unsigned)rc.x; ys = (unsigned)rc.y;
             sx0 = (int)(xs & 0xffffu); sx1 = (int)(xs >> 16);
             sy0 = (int)(ys & 0xffffu); sy1 = (int)(ys >> 16);
         }
@@ -282,11 +283,11 @@ __global__ void __launch_bounds__(BWD_THREADS) k_render_bwd(
         mb = min(max(mb, ma), ce);
 
         LaneG L;
-        L.D2 = f2(r1.x * invs);
+        L.D2 = f2(r0.w);                                      // D = a1/s
         L.cr = f2(r1.w); L.cg = f2(r2.x); L.cb = f2(r2.y);
         L.x0 = x0; L.x1 = x1;
-        const float kT = (float)Tx0 - r0.x;
-        const float tdl = -r1.x * r0.z;                        // -a1 dl_x
+        const float kT = (float)Tx0 + r0.x;                    // Tx0 - ax
+        const float tdl = r1.x;                                // -a1 dl_x
         macc_t m[8];
 #pragma unroll
         for (int k = 0; k < 8; ++k) m[k] = (macc_t)0;
@@ -294,8 +295,8 @@ __global__ void __launch_bounds__(BWD_THREADS) k_render_bwd(
             // rows y and y + 1 (the second one is a phantom when y == yb: u = -inf)
             const int y1r = y + 1;
             const bool has1 = y1r <= yb;
-            const float dy0 = fmaf((float)y - r0.y, invs, -r0.w);
-            const float dy1 = fmaf((float)y1r - r0.y, invs, -r0.w);
+            const float dy0 = fmaf((float)y - r0.y, invs, -r0.z);
+            const float dy1 = fmaf((float)y1r - r0.y, invs, -r0.z);
             const float v0 = r1.z * dy0, v1 = r1.z * dy1;
             const float u0 = (y >= y0 && y <= y1) ? -(v0 * v0) : -INFINITY;
             const float u1 = (has1 && y1r >= y0 && y1r <= y1) ? -(v1 * v1) : -INFINITY;
@@ -398,8 +399,8 @@ __global__ void __launch_bounds__(BWD_THREADS) k_render_bwd(
             bool hit = false;
             int key = 0;
             if (p < sp1) {
-                const float4 r3 = __ldg(rec + (long long)REC_F4 * p + 3);
-                const unsigned xs = __float_as_uint(r3.x), ys = __float_as_uint(r3.y);
+                const int4 rc = __ldg(rects + p);
+                const unsigned xs = (unsigned)rc.x, ys = (unsigned)rc.y;
                 const int x0 = (int)(xs & 0xffffu), x1 = (int)(xs >> 16);
                 const int y0 = (int)(ys & 0xffffu), y1 = (int)(ys >> 16);
                 hit = !(x1 < Tx0 || x0 > Tx1 || y1 < Ty0 || y0 > Ty1);
@@ -487,7 +488,8 @@ cudaError_t launch_render_bwd_moments(const ImgTable& tab, const Workspace& ws, 
     count_launches(1);
     int h = prof_begin(2, st);
     int ks = split_k_factor(tab.total_tiles);
-    k_render_bwd<<<tab.total_tiles * ks, BWD_THREADS, 0, st>>>(tab, ws.rec, ws.cell_start, ws.ext,
+    k_render_bwd<<<tab.total_tiles * ks, BWD_THREADS, 0, st>>>(tab, ws.rec, ws.rects, ws.cell_start,
+                                                               ws.ext,
                                                                perm, grad_out, moments, ks, img,
                                                                gt, inv_numel);
     prof_end(h, st);

@@ -45,7 +45,7 @@ struct FwdProducer {
             cur = cs[row + cx_lo];
             end = cs[row + cx_hi + 1];
         }
-        int n = min(FWD_CHUNK, end - cur);
+        int n = min(32, end - cur);
         *start = cur;
         cur += n;
         return n;
@@ -80,15 +80,12 @@ __device__ __forceinline__ float2 f2(float a) { return make_float2(a, a); }
 template <class CFG>
 struct FwdSmem {
     static constexpr int NACC = CFG::ROWS * (CFG::STRIP / 2) * 3;   // float2 accumulators/thread
-    float4 rec[FWD_STAGES][FWD_CHUNK * REC_F4];
+    float4 rec[FWD_STAGES][FWD_CHUNK * REC_F4];   // kept records only (gathered by TMA)
     float2 tot[FWD_CWARPS][NACC][32];        // per-warp totals (second accumulation level)
-    float g3[FWD_STAGES][FWD_CHUNK];         // 2^(-9 D^2) of recurrence-path records
-    uint16_t idx[FWD_STAGES][FWD_CHUNK];     // kept records: index | full << 8 | recurrence << 9
-    uint64_t full_bar[FWD_STAGES];           // TMA bytes landed
-    uint64_t ready_bar[FWD_STAGES];          // producer warp filtered + transformed the chunk
+    uint8_t full[FWD_STAGES][FWD_CHUNK];     // 1: the window rect covers the tile (no masks)
+    uint64_t full_bar[FWD_STAGES];           // stage closed by the producer + its bytes landed
     uint64_t empty_bar[FWD_STAGES];          // consumer warps done with the stage
-    int count[FWD_STAGES];                   // records in the chunk (0 = end of the list)
-    int kept[FWD_STAGES];                    // records kept by the filter (-1 = end)
+    int kept[FWD_STAGES];                    // records in the stage (-1 = end of the list)
 };
 
 // Transformed record (written in shared memory by the producer warp, see k_render_fwd):
@@ -161,22 +158,23 @@ __device__ __forceinline__ void fwd_gauss(const float4 r0, const float4 r1, cons
 //           D^2 t^2 <= 9). Error: the exponent of B^t carries t * 2 D |w_a| * 2^-24 relative.
 template <int MODE>
 __device__ __forceinline__ void fwd_gauss_r2(const float4 r0, const float4 r1, const float4 r2,
-                                             float g3, float xlf, float yf0, const int (&yi)[2],
+                                             float g3, float xlf, float2 yrow, const int (&yi)[2],
                                              int xl0, float invs, float2 (&acc)[24]) {
     const float D = r0.w;
     const float2 D2 = f2(D);
     const float kx0 = xlf + r0.x;                           // x - ax of column 0 (exact)
-    const float dy0 = fmaf(yf0 - r0.y, invs, -r0.z);
-    const float dy1 = dy0 + invs;                           // consecutive rows: exact to 1 ulp(1/s)
-    const float v0 = r1.z * dy0, v1 = r1.z * dy1;
-    float2 U = make_float2(-(v0 * v0), -(v1 * v1));
+    // both rows at once: dy = (y - ay)/s - dl_y ((y - ay) exact), v = c1 dy, u = -v^2,
+    // tau = b1 dy - a1 dl_x
+    const float2 dy = __ffma2_rn(__fadd2_rn(yrow, f2(-r0.y)), f2(invs), f2(-r0.z));
+    const float2 v = __fmul2_rn(dy, f2(r1.z));
+    float2 U = __fmul2_rn(make_float2(-v.x, -v.y), v);
     if (MODE == 0) {                                        // lane rows outside [y0, y1]
         const unsigned ys = __float_as_uint(r2.w);
         const int y0 = (int)(ys & 0xffffu), y1 = (int)(ys >> 16);
         U.x = (yi[0] >= y0 && yi[0] <= y1) ? U.x : -INFINITY;
         U.y = (yi[1] >= y0 && yi[1] <= y1) ? U.y : -INFINITY;
     }
-    const float2 T = make_float2(fmaf(r1.y, dy0, r1.x), fmaf(r1.y, dy1, r1.x));  // b1 dy - a1 dl_x
+    const float2 T = __ffma2_rn(f2(r1.y), dy, f2(r1.x));   // b1 dy - a1 dl_x
     const float2 cr = f2(r1.w), cg = f2(r2.x), cb = f2(r2.y);
     auto accum = [&](int j, float2 e) {
         acc[3 * j + 0] = __ffma2_rn(cr, e, acc[3 * j + 0]);
@@ -223,6 +221,7 @@ __device__ __forceinline__ void fwd_gauss_r2(const float4 r0, const float4 r1, c
 template <int KS, bool LOSS, class CFG>
 __global__ void __launch_bounds__(FWD_THREADS) k_render_fwd(const ImgTable tab,
                                                             const float4* __restrict__ rec,
+                                                            const int4* __restrict__ rects,
                                                             const int* __restrict__ cell_start,
                                                             const int* __restrict__ ext,
                                                             float* __restrict__ out,
@@ -245,7 +244,6 @@ __global__ void __launch_bounds__(FWD_THREADS) k_render_fwd(const ImgTable tab,
     if (threadIdx.x == 0) {
         for (int s = 0; s < FWD_STAGES; ++s) {
             mbar_init(&sm.full_bar[s], 1);
-            mbar_init(&sm.ready_bar[s], 32);
             mbar_init(&sm.empty_bar[s], FWD_CWARPS);
         }
         fence_barrier_init();
@@ -260,10 +258,12 @@ __global__ void __launch_bounds__(FWD_THREADS) k_render_fwd(const ImgTable tab,
 
     if (warp == FWD_CWARPS) {
         // ---------------- producer warp --------------------------------------------------------
-        // lane 0 walks the chunk list and issues the TMA bulk copies FWD_STAGES chunks ahead; the
-        // whole warp then filters each landed chunk against the tile (rect intersection, full-x
-        // flag), compacts the kept indices and rewrites the kept records in place into the
-        // consumers' form, so the consumer warps never see a Gaussian that misses the tile.
+        // Walks the tile's candidate spans in batches of 32 and filters them from the 16-B rect
+        // stream (support rect meets the tile? window rect covers it?), FOUR batches of loads in
+        // flight; each lane whose candidate is kept issues a 64-B TMA bulk copy of its record
+        // into the next free slot of the current stage (mbarrier expect_tx per copy), so the
+        // stages hold kept records only. A stage is closed (one arrive on its full barrier) when
+        // it cannot take another batch; the consumers see it once all its bytes have landed.
         FwdProducer prod;
         prod.cs = cell_start;
         prod.row0 = im.cell_base;
@@ -273,95 +273,68 @@ __global__ void __launch_bounds__(FWD_THREADS) k_render_fwd(const ImgTable tab,
         prod.cy = (Ty0 - im.row_begin - query_ext(ext, kimg, 1) + 1 + im.offy) / CELL - 1;
         prod.cy_hi = min(im.ncy - 1, (fy1 - im.row_begin + im.offy) / CELL);
         prod.cur = prod.end = 0;
-        auto issue = [&](int k) -> int {          // lane 0 only
-            const int s = k % FWD_STAGES;
-            int start = 0;
-            const int n = prod.next(&start, k == 0 ? krank : KS - 1);
-            sm.count[s] = n;
-            if (n > 0) {
-                const uint32_t bytes = (uint32_t)n * (16u * REC_F4);
-                mbar_arrive_expect_tx(&sm.full_bar[s], bytes);
-                tma_bulk_g2s(&sm.rec[s][0], rec + (long long)REC_F4 * start, bytes,
-                             &sm.full_bar[s]);
-            } else {
-                mbar_arrive(&sm.full_bar[s]);      // end marker
-            }
-            return n;
-        };
-        int ended = 0;
-        if (lane == 0)
-            for (int k = 0; k < FWD_STAGES && !ended; ++k) ended = issue(k) == 0;
-        ended = __shfl_sync(0xffffffffu, ended, 0);
         const unsigned lt = (1u << lane) - 1u;
-        // Two independent jobs, polled without blocking one on the other: filter chunk kf as soon
-        // as its bytes land, refill the stage of chunk kr once the consumers released it. When
-        // neither is ready the warp sleeps (it shares an SM sub-partition with consumer warps).
-        int kf = 0, kr = 0;
-        bool done = false;
-        while (!done) {
-            bool worked = false;
-            const int sf = kf % FWD_STAGES;
-            if (kf < kr + FWD_STAGES && mbar_test(&sm.full_bar[sf], (uint32_t)((kf / FWD_STAGES) & 1))) {
-                worked = true;
-                const int n = sm.count[sf];
-                if (n == 0) {
-                    if (lane == 0) sm.kept[sf] = -1;
-                    mbar_arrive(&sm.ready_bar[sf]);
-                    done = true;
-                    break;
+        const bool live = fy0 <= fy1;
+        int nb[4], sb[4];                         // batch descriptors (warp-uniform)
+        int4 rb[4];                               // this lane's rect in each batch
+        int first = 1;
+        auto fetch = [&](int j) {
+            nb[j] = live ? prod.next(&sb[j], first ? krank : KS - 1) : 0;
+            first = 0;
+            rb[j] = make_int4(0, 0, 0, 0);
+            if (lane < nb[j]) rb[j] = __ldg(rects + sb[j] + lane);
+        };
+        fetch(0); fetch(1); fetch(2); fetch(3);
+        int k = 0, kept = 0;
+        while (true) {
+            const int s = k % FWD_STAGES;
+            if (nb[0] > 0) {
+                // filter batch 0
+                bool keep = false, full = false;
+                if (lane < nb[0]) {
+                    const unsigned sxs = (unsigned)rb[0].x, sys = (unsigned)rb[0].y;
+                    const int sx0 = (int)(sxs & 0xffffu), sx1 = (int)(sxs >> 16);
+                    const int sy0 = (int)(sys & 0xffffu), sy1 = (int)(sys >> 16);
+                    keep = !(sx1 < fx0 || sx0 > fx1 || sy1 < fy0 || sy0 > fy1);
+                    const unsigned xs = (unsigned)rb[0].z, ys = (unsigned)rb[0].w;
+                    const int x0 = (int)(xs & 0xffffu), x1 = (int)(xs >> 16);
+                    const int y0 = (int)(ys & 0xffffu), y1 = (int)(ys >> 16);
+                    full = x0 <= fx0 && x1 >= fx1 && y0 <= fy0 && y1 >= fy0 + FTILE_H - 1;
                 }
-                int base = 0;
-                float4* sr = &sm.rec[sf][0];
-                for (int g0 = 0; g0 < n; g0 += 32) {
-                    const int g = g0 + lane;
-                    bool keep = false, full = false, rec_ok = false;
-                    if (g < n) {
-                        // keep: the support rect (R21) meets the tile; "full": the window rect
-                        // (R2) covers every column and every lane row of the tile -- no masks
-                        // (pixels beyond the support evaluate to 0 in fp32 by themselves)
-                        const float4 r2 = sr[REC_F4 * g + 2], r3 = sr[REC_F4 * g + 3];
-                        const unsigned sxs = __float_as_uint(r3.x), sys = __float_as_uint(r3.y);
-                        const int sx0 = (int)(sxs & 0xffffu), sx1 = (int)(sxs >> 16);
-                        const int sy0 = (int)(sys & 0xffffu), sy1 = (int)(sys >> 16);
-                        keep = fy0 <= fy1 && !(sx1 < fx0 || sx0 > fx1 || sy1 < fy0 || sy0 > fy1);
-                        const unsigned xs = __float_as_uint(r2.z), ys = __float_as_uint(r2.w);
-                        const int x0 = (int)(xs & 0xffffu), x1 = (int)(xs >> 16);
-                        const int y0 = (int)(ys & 0xffffu), y1 = (int)(ys >> 16);
-                        full = x0 <= fx0 && x1 >= fx1 && y0 <= fy0 && y1 >= fy0 + FTILE_H - 1;
-                        if (keep) {
-                            const float4 r0 = sr[REC_F4 * g], r1 = sr[REC_F4 * g + 1];
-                            const float D = r1.x * invs;
-                            sr[REC_F4 * g] = make_float4(-r0.x, r0.y, r0.w, D);
-                            sr[REC_F4 * g + 1] = make_float4(-r1.x * r0.z, r1.y, r1.z, r1.w);
-                            // exponential recurrence (2-row lane blocks): G_t = 2^(-D^2 t^2)
-                            rec_ok = CFG::ROWS == 2 && full && D <= FWD_REC_DMAX;
-                            if (rec_ok) {      // G1, G2 from K1b; G3 = G1^9 = G2^2 G1
-                                sr[REC_F4 * g + 2] = make_float4(r2.x, r2.y, r3.z, r3.w);
-                                sm.g3[sf][g] = r3.w * r3.w * r3.z;
-                            }
-                        }
-                    }
-                    const unsigned m = __ballot_sync(0xffffffffu, keep);
-                    if (keep)
-                        sm.idx[sf][base + __popc(m & lt)] =
-                            (uint16_t)(g | (full ? 0x100 : 0) | (rec_ok ? 0x200 : 0));
-                    base += __popc(m);
+                const unsigned m = __ballot_sync(0xffffffffu, keep);
+                if (keep) {
+                    const int slot = kept + __popc(m & lt);
+                    sm.full[s][slot] = full ? 1 : 0;
+                    mbar_expect_tx(&sm.full_bar[s], 16u * REC_F4);
+                    tma_bulk_g2s(&sm.rec[s][REC_F4 * slot], rec + (long long)REC_F4 * (sb[0] + lane),
+                                 16u * REC_F4, &sm.full_bar[s]);
                 }
-                if (lane == 0) sm.kept[sf] = base;
-                mbar_arrive(&sm.ready_bar[sf]);    // each lane releases its own smem writes
-                ++kf;
+                kept += __popc(m);
+                // advance the batch ring
+                nb[0] = nb[1]; sb[0] = sb[1]; rb[0] = rb[1];
+                nb[1] = nb[2]; sb[1] = sb[2]; rb[1] = rb[2];
+                nb[2] = nb[3]; sb[2] = sb[3]; rb[2] = rb[3];
+                fetch(3);
             }
-            // refill: chunk kr's stage gets chunk kr + FWD_STAGES once consumers are done with kr
-            if (!ended && kr < kf) {
-                const int sr_ = kr % FWD_STAGES;
-                if (mbar_test(&sm.empty_bar[sr_], (uint32_t)((kr / FWD_STAGES) & 1))) {
-                    worked = true;
-                    if (lane == 0) ended = issue(kr + FWD_STAGES) == 0;
-                    ended = __shfl_sync(0xffffffffu, ended, 0);
-                    ++kr;
-                }
+            const bool end = nb[0] == 0;
+            if (kept > FWD_CHUNK - 32 || (end && kept > 0)) {
+                // close stage s
+                if (lane == 0) sm.kept[s] = kept;
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&sm.full_bar[s]);
+                ++k;
+                kept = 0;
+                if (k >= FWD_STAGES)          // wait until the consumers released the next stage
+                    mbar_wait(&sm.empty_bar[k % FWD_STAGES], (uint32_t)(((k / FWD_STAGES) - 1) & 1));
             }
-            if (!worked) __nanosleep(256);
+            if (end) {
+                const int s2 = k % FWD_STAGES;
+                if (lane == 0) {
+                    sm.kept[s2] = -1;
+                    mbar_arrive(&sm.full_bar[s2]);
+                }
+                break;
+            }
         }
     } else {
         // ---------------- consumer warps ------------------------------------------------------
@@ -372,6 +345,7 @@ __global__ void __launch_bounds__(FWD_THREADS) k_render_fwd(const ImgTable tab,
         for (int jp = 0; jp < FWD_STRIP / 2; ++jp)
             xj[jp] = make_float2((float)(xl0 + 2 * jp), (float)(xl0 + 2 * jp + 1));
         const float xlf = (float)xl0;
+        const float2 yrow = make_float2((float)yl0, (float)(yl0 + 1));
         int yi[FWD_ROWS];
 #pragma unroll
         for (int r = 0; r < FWD_ROWS; ++r) yi[r] = yl0 + r;
@@ -379,34 +353,36 @@ __global__ void __launch_bounds__(FWD_THREADS) k_render_fwd(const ImgTable tab,
 
         for (int k = 0;; ++k) {
             const int s = k % FWD_STAGES;
-            mbar_wait(&sm.ready_bar[s], (uint32_t)((k / FWD_STAGES) & 1));
+            mbar_wait(&sm.full_bar[s], (uint32_t)((k / FWD_STAGES) & 1));
             const int nk = sm.kept[s];
             if (nk < 0) break;
             float2 acc[NACC];
 #pragma unroll
             for (int a = 0; a < NACC; ++a) acc[a] = make_float2(0.f, 0.f);
             const float4* sr = &sm.rec[s][0];
-            const uint16_t* ix = &sm.idx[s][0];
-            for (int i = warp; i < nk; i += FWD_CWARPS) {
-                const int e = ix[i];
-                const int g = e & 0xff;
+            for (int g = warp; g < nk; g += FWD_CWARPS) {
                 const float4 r0 = sr[REC_F4 * g], r1 = sr[REC_F4 * g + 1],
                              r2 = sr[REC_F4 * g + 2];
+                const bool full = sm.full[s][g] != 0;
                 if constexpr (FWD_ROWS == 2) {
-                    if (e & 0x200)
-                        fwd_gauss_r2<2>(r0, r1, r2, sm.g3[s][g], xlf, yf0, yi, xl0, invs, acc);
-                    else if (e & 0x100)
-                        fwd_gauss_r2<1>(r0, r1, r2, 0.f, xlf, yf0, yi, xl0, invs, acc);
-                    else
-                        fwd_gauss_r2<0>(r0, r1, r2, 0.f, xlf, yf0, yi, xl0, invs, acc);
+                    if (full) {
+                        const float4 r3 = sr[REC_F4 * g + 3];
+                        if (r3.w != 0.f)
+                            fwd_gauss_r2<2>(r0, r1, make_float4(r2.x, r2.y, r3.x, r3.y), r3.z, xlf,
+                                            yrow, yi, xl0, invs, acc);
+                        else
+                            fwd_gauss_r2<1>(r0, r1, r2, 0.f, xlf, yrow, yi, xl0, invs, acc);
+                    } else {
+                        fwd_gauss_r2<0>(r0, r1, r2, 0.f, xlf, yrow, yi, xl0, invs, acc);
+                    }
                 } else {
-                    if (e & 0x100)
+                    if (full)
                         fwd_gauss<CFG, true>(r0, r1, r2, xj, yf0, yi, xl0, invs, acc);
                     else
                         fwd_gauss<CFG, false>(r0, r1, r2, xj, yf0, yi, xl0, invs, acc);
                 }
             }
-            // fold the chunk partials into the per-warp totals (second accumulation level)
+            // fold the stage partials into the per-warp totals (second accumulation level)
 #pragma unroll
             for (int a = 0; a < NACC; ++a)
                 sm.tot[warp][a][lane] = __fadd2_rn(sm.tot[warp][a][lane], acc[a]);
@@ -502,7 +478,7 @@ cudaError_t launch_ks3(const ImgTable& tab, const Workspace& ws, float* out, con
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, k_render_fwd<KS, LOSS, CFG>, tab, (const float4*)ws.rec,
-                              (const int*)ws.cell_start, (const int*)ws.ext, out, gt,
+                              (const int4*)ws.rects, (const int*)ws.cell_start, (const int*)ws.ext, out, gt,
                               loss_acc);
 }
 
