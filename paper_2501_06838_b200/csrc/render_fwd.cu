@@ -305,9 +305,17 @@ __global__ void __launch_bounds__(FWD_THREADS) k_render_fwd(const ImgTable tab,
                 if (keep) {
                     const int slot = kept + __popc(m & lt);
                     sm.full[s][slot] = full ? 1 : 0;
-                    mbar_expect_tx(&sm.full_bar[s], 16u * REC_F4);
-                    tma_bulk_g2s(&sm.rec[s][REC_F4 * slot], rec + (long long)REC_F4 * (sb[0] + lane),
-                                 16u * REC_F4, &sm.full_bar[s]);
+                    // one bulk copy per run of consecutive kept candidates (contiguous in the
+                    // source and in the stage): the copies take warp-uniform operands, so every
+                    // copy costs a serialised issue round
+                    if (lane == 0 || !((m >> (lane - 1)) & 1u)) {
+                        const int run = __ffsll(~(unsigned long long)(m >> lane)) - 1;
+                        const uint32_t bytes = (uint32_t)run * (16u * REC_F4);
+                        mbar_expect_tx(&sm.full_bar[s], bytes);
+                        tma_bulk_g2s(&sm.rec[s][REC_F4 * slot],
+                                     rec + (long long)REC_F4 * (sb[0] + lane), bytes,
+                                     &sm.full_bar[s]);
+                    }
                 }
                 kept += __popc(m);
                 // advance the batch ring
