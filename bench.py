@@ -42,10 +42,11 @@ METRIC = "HR Mpix/s & Gaussian-pixel evals/s fwd+bwd at 1/2/4/8 B200; % of roofl
 UNIT = "HR Mpix/s (fwd+bwd)"
 RATIO = 0.1
 SM_COUNT = 148
-# Roofline per pair: forward = 1 ex2 on the SFU (16/clk/SM, measured);
-# backward = 12.5 FP32 lane-ops on the FMA pipe (128 lanes/clk/SM, measured), the minimal
-# instruction sequence of K5 (kx shared by a row pair, w, q, 3 e g, 3 g.c', 4 moments).
-FWD_PAIRS_PER_CLK_SM = 16.0
+# Roofline per evaluated pair, FP32 FMA pipe = 128 lanes/clk/SM
+# (measured): forward on its recurrence path (the C3-C5 path) = 5.25 FP32 lane-ops + 0.5 ex2
+# (SFU 16/clk/SM, measured, is not the binding pipe there); backward = 12.5 FP32 lane-ops, the
+# minimal instruction sequence of K5 (kx shared by a row pair, w, q, 3 e g, 3 g.c', 4 moments).
+FWD_PAIRS_PER_CLK_SM = 128.0 / 5.25   # recurrence path: 5.25 FP32 lane-ops + 0.5 ex2 per pair
 BWD_PAIRS_PER_CLK_SM = 128.0 / 12.5
 
 
@@ -410,7 +411,7 @@ def main():
     per_clk = FWD_PAIRS_PER_CLK_SM if kern == "render_fwd" else BWD_PAIRS_PER_CLK_SM
     peak = per_clk * SM_COUNT * f_clk / 1e9           # Gpair/s
     achieved = P_rank_eval / t_launch / 1e9
-    roof = {"bound": "alu", "pipe": "SFU ex2" if kern == "render_fwd" else "FP32 FMA",
+    roof = {"bound": "alu", "pipe": "FP32 FMA",
             "kernel": kern, "achieved": achieved, "peak": peak, "unit": "Gpair/s",
             "frac": achieved / peak, "traffic": ncu_traffic(args.workload, kern),
             "peak_basis": f"{per_clk:.3f} pairs/clk/SM x {SM_COUNT} SMs x {pk['sm_max_mhz']:.0f} MHz "

@@ -35,8 +35,8 @@ def run(name, nimg_override=None, iters=3):
         gsr.render_bwd_batched(*dev, lay, g); e[2].record(); torch.cuda.synchronize()
         tf.append(e[0].elapsed_time(e[1])); tb.append(e[1].elapsed_time(e[2]))
     tf, tb = min(tf), min(tb)
-    peak = 16 * 148 * 1.965e9
-    print(f"{name} imgs={len(imgs)} Pwin={Pw:.3e} Peval={P:.3e} fwd {tf:.3f} ms ({P/tf/1e9:.3f} Tpair/s, {P/tf*1e3/peak:.1%} of SFU) "
+    peak = 128 / 5.25 * 148 * 1.965e9      # forward, recurrence path (FP32 pipe)
+    print(f"{name} imgs={len(imgs)} Pwin={Pw:.3e} Peval={P:.3e} fwd {tf:.3f} ms ({P/tf/1e9:.3f} Tpair/s, {P/tf*1e3/peak:.1%} of FP32) "
           f"bwd {tb:.3f} ms ({P/tb/1e9:.3f} Tpair/s, {P/tb*1e3/(128/12.5*148*1.965e9):.1%} of FP32)", flush=True)
 
 
