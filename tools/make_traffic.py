@@ -26,7 +26,8 @@ for r in data:
         tot += float(r[ix[m]].replace(",", "")) * mult.get(u, 1)
     res[k] = {"dram_bytes_per_launch": tot, "source": rep,
               "duration_ns_under_ncu": float(r[ix["gpu__time_duration.sum"]].replace(",", ""))
-              * {"nsecond": 1, "usecond": 1e3, "msecond": 1e6, "second": 1e9}.get(
+              * {"nsecond": 1, "ns": 1, "usecond": 1e3, "us": 1e3, "msecond": 1e6, "ms": 1e6,
+                 "second": 1e9, "s": 1e9}.get(
                   units[ix["gpu__time_duration.sum"]], 1)}
 p = Path(__file__).resolve().parents[1] / "profiles" / "ncu_traffic.json"
 d = json.loads(p.read_text()) if p.exists() else {}
