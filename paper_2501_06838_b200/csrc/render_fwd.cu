@@ -286,62 +286,65 @@ __global__ void __launch_bounds__(FWD_THREADS) k_render_fwd(const ImgTable tab,
         };
         fetch(0); fetch(1); fetch(2); fetch(3);
         int k = 0, kept = 0;
-        while (true) {
-            const int s = k % FWD_STAGES;
-            if (nb[0] > 0) {
-                // filter batch 0
-                bool keep = false, full = false;
-                if (lane < nb[0]) {
-                    const unsigned sxs = (unsigned)rb[0].x, sys = (unsigned)rb[0].y;
-                    const int sx0 = (int)(sxs & 0xffffu), sx1 = (int)(sxs >> 16);
-                    const int sy0 = (int)(sys & 0xffffu), sy1 = (int)(sys >> 16);
-                    keep = !(sx1 < fx0 || sx0 > fx1 || sy1 < fy0 || sy0 > fy1);
-                    const unsigned xs = (unsigned)rb[0].z, ys = (unsigned)rb[0].w;
-                    const int x0 = (int)(xs & 0xffffu), x1 = (int)(xs >> 16);
-                    const int y0 = (int)(ys & 0xffffu), y1 = (int)(ys >> 16);
-                    full = x0 <= fx0 && x1 >= fx1 && y0 <= fy0 && y1 >= fy0 + FTILE_H - 1;
-                }
-                const unsigned m = __ballot_sync(0xffffffffu, keep);
-                if (keep) {
-                    const int slot = kept + __popc(m & lt);
-                    sm.full[s][slot] = full ? 1 : 0;
-                    // one bulk copy per run of consecutive kept candidates (contiguous in the
-                    // source and in the stage): the copies take warp-uniform operands, so every
-                    // copy costs a serialised issue round
-                    if (lane == 0 || !((m >> (lane - 1)) & 1u)) {
-                        const int run = __ffsll(~(unsigned long long)(m >> lane)) - 1;
-                        const uint32_t bytes = (uint32_t)run * (16u * REC_F4);
-                        mbar_expect_tx(&sm.full_bar[s], bytes);
-                        tma_bulk_g2s(&sm.rec[s][REC_F4 * slot],
-                                     rec + (long long)REC_F4 * (sb[0] + lane), bytes,
-                                     &sm.full_bar[s]);
+        bool done = false;
+        // the batch ring is walked with static indices (unrolled by 4): batch j is filtered, then
+        // its slot is refilled with the batch four ahead
+        while (!done) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                if (done) break;
+                const int s = k % FWD_STAGES;
+                const bool end = nb[j] == 0;
+                if (!end) {
+                    bool keep = false, full = false;
+                    if (lane < nb[j]) {
+                        const unsigned sxs = (unsigned)rb[j].x, sys = (unsigned)rb[j].y;
+                        const int sx0 = (int)(sxs & 0xffffu), sx1 = (int)(sxs >> 16);
+                        const int sy0 = (int)(sys & 0xffffu), sy1 = (int)(sys >> 16);
+                        keep = !(sx1 < fx0 || sx0 > fx1 || sy1 < fy0 || sy0 > fy1);
+                        const unsigned xs = (unsigned)rb[j].z, ys = (unsigned)rb[j].w;
+                        const int x0 = (int)(xs & 0xffffu), x1 = (int)(xs >> 16);
+                        const int y0 = (int)(ys & 0xffffu), y1 = (int)(ys >> 16);
+                        full = x0 <= fx0 && x1 >= fx1 && y0 <= fy0 && y1 >= fy0 + FTILE_H - 1;
                     }
+                    const unsigned m = __ballot_sync(0xffffffffu, keep);
+                    if (keep) {
+                        const int slot = kept + __popc(m & lt);
+                        sm.full[s][slot] = full ? 1 : 0;
+                        // one bulk copy per run of consecutive kept candidates (contiguous in
+                        // the source and in the stage): the copies take warp-uniform operands,
+                        // so every copy costs a serialised issue round
+                        if (lane == 0 || !((m >> (lane - 1)) & 1u)) {
+                            const int run = __ffsll(~(unsigned long long)(m >> lane)) - 1;
+                            const uint32_t bytes = (uint32_t)run * (16u * REC_F4);
+                            mbar_expect_tx(&sm.full_bar[s], bytes);
+                            tma_bulk_g2s(&sm.rec[s][REC_F4 * slot],
+                                         rec + (long long)REC_F4 * (sb[j] + lane), bytes,
+                                         &sm.full_bar[s]);
+                        }
+                    }
+                    kept += __popc(m);
+                    fetch(j);                     // the batch four ahead
                 }
-                kept += __popc(m);
-                // advance the batch ring
-                nb[0] = nb[1]; sb[0] = sb[1]; rb[0] = rb[1];
-                nb[1] = nb[2]; sb[1] = sb[2]; rb[1] = rb[2];
-                nb[2] = nb[3]; sb[2] = sb[3]; rb[2] = rb[3];
-                fetch(3);
-            }
-            const bool end = nb[0] == 0;
-            if (kept > FWD_CHUNK - 32 || (end && kept > 0)) {
-                // close stage s
-                if (lane == 0) sm.kept[s] = kept;
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&sm.full_bar[s]);
-                ++k;
-                kept = 0;
-                if (k >= FWD_STAGES)          // wait until the consumers released the next stage
-                    mbar_wait(&sm.empty_bar[k % FWD_STAGES], (uint32_t)(((k / FWD_STAGES) - 1) & 1));
-            }
-            if (end) {
-                const int s2 = k % FWD_STAGES;
-                if (lane == 0) {
-                    sm.kept[s2] = -1;
-                    mbar_arrive(&sm.full_bar[s2]);
+                if (kept > FWD_CHUNK - 32 || (end && kept > 0)) {
+                    // close stage s
+                    if (lane == 0) sm.kept[s] = kept;
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&sm.full_bar[s]);
+                    ++k;
+                    kept = 0;
+                    if (k >= FWD_STAGES)      // wait until the consumers released the next stage
+                        mbar_wait(&sm.empty_bar[k % FWD_STAGES],
+                                  (uint32_t)(((k / FWD_STAGES) - 1) & 1));
                 }
-                break;
+                if (end) {
+                    const int s2 = k % FWD_STAGES;
+                    if (lane == 0) {
+                        sm.kept[s2] = -1;
+                        mbar_arrive(&sm.full_bar[s2]);
+                    }
+                    done = true;
+                }
             }
         }
     } else {
