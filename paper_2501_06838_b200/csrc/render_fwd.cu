@@ -31,6 +31,10 @@
 //     reduce their totals through DSMEM in cluster-rank order (deterministic, no atomics).
 #include "gsr_internal.cuh"
 
+#ifndef GSR_FWD_V2
+#define GSR_FWD_V2 1
+#endif
+
 namespace gsr {
 
 namespace {
@@ -218,6 +222,77 @@ __device__ __forceinline__ void fwd_gauss_r2(const float4 r0, const float4 r1, c
     }
 }
 
+// Sum the per-warp partial images in warp order (deterministic) into tot[0], reduce split-K
+// cluster CTAs through DSMEM in rank order, store the tile (and the fused L1 loss).
+template <int KS, bool LOSS, class CFG>
+__device__ __forceinline__ void fwd_epilogue(float2 (*tot)[FwdSmem<CFG>::NACC][32],
+                                             const DevImg& im, int Tx0, int Ty0, int warp,
+                                             int lane, int krank, float* __restrict__ out,
+                                             const float* __restrict__ gt,
+                                             double* __restrict__ loss_acc) {
+    constexpr int FWD_STRIP = CFG::STRIP, FWD_ROWS = CFG::ROWS, NACC = FwdSmem<CFG>::NACC;
+    struct { float2 (*tot)[NACC][32]; } sm = {tot};
+    __syncthreads();
+    if (warp == 0) {
+#pragma unroll 4
+        for (int a = 0; a < NACC; ++a) {
+            float2 v = sm.tot[0][a][lane];
+            for (int q = 1; q < FWD_CWARPS; ++q) v = __fadd2_rn(v, sm.tot[q][a][lane]);
+            sm.tot[0][a][lane] = v;
+        }
+    }
+    if (KS > 1) {
+        cluster_sync_all();                    // every CTA's tile sum is final
+        if (krank == 0 && warp == 0) {
+            for (int a = 0; a < NACC; ++a) {
+                float2 v = make_float2(0.f, 0.f);
+                for (int q = 0; q < KS; ++q) v = __fadd2_rn(v, ld_dsmem_f2(&sm.tot[0][a][lane], q));
+                sm.tot[0][a][lane] = v;        // only this thread reads its own slot afterwards
+            }
+        }
+        cluster_sync_all();                    // keep every CTA's smem alive until read
+        if (krank != 0) return;
+    }
+    if (warp != 0) return;
+
+    const int xl0 = Tx0 + FWD_STRIP * (lane & 3);
+    const int yl0 = Ty0 + FWD_ROWS * (lane >> 2);
+    float l1 = 0.f;     // fused L1 loss (NEXT-1): sum |I - I_gt| over the stored elements
+    auto store = [&](int y, int x, float R, float G, float B) {
+        if (y >= im.row_end || x >= im.Ws) return;
+        const long long off = im.out_off + ((long long)(y - im.row_begin) * im.Ws + x) * 3;
+        out[off] = R; out[off + 1] = G; out[off + 2] = B;
+        if (LOSS) l1 += fabsf(R - gt[off]) + fabsf(G - gt[off + 1]) + fabsf(B - gt[off + 2]);
+    };
+    if constexpr (FWD_ROWS == 2) {     // acc pairs = (row 0, row 1) of one column
+#pragma unroll
+        for (int j = 0; j < FWD_STRIP; ++j) {
+            const float2 R = sm.tot[0][3 * j][lane], G = sm.tot[0][3 * j + 1][lane],
+                         B = sm.tot[0][3 * j + 2][lane];
+            store(yl0, xl0 + j, R.x, G.x, B.x);
+            store(yl0 + 1, xl0 + j, R.y, G.y, B.y);
+        }
+    } else {                           // acc pairs = two adjacent columns of one row
+#pragma unroll
+        for (int r = 0; r < FWD_ROWS; ++r) {
+#pragma unroll
+            for (int jp = 0; jp < FWD_STRIP / 2; ++jp) {
+                const int a = (r * (FWD_STRIP / 2) + jp) * 3;
+                const float2 R = sm.tot[0][a][lane], G = sm.tot[0][a + 1][lane],
+                             B = sm.tot[0][a + 2][lane];
+                store(yl0 + r, xl0 + 2 * jp, R.x, G.x, B.x);
+                store(yl0 + r, xl0 + 2 * jp + 1, R.y, G.y, B.y);
+            }
+        }
+    }
+    if (LOSS) {
+        double d = (double)l1;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+        if (lane == 0) atomicAdd(loss_acc, d);
+    }
+}
+
 template <int KS, bool LOSS, class CFG>
 __global__ void __launch_bounds__(FWD_THREADS) k_render_fwd(const ImgTable tab,
                                                             const float4* __restrict__ rec,
@@ -402,66 +477,216 @@ __global__ void __launch_bounds__(FWD_THREADS) k_render_fwd(const ImgTable tab,
         }
     }
 
-    // sum the 4 warps' partial images in warp order (deterministic) into tot[0]
-    __syncthreads();
-    if (warp == 0) {
-#pragma unroll 4
-        for (int a = 0; a < NACC; ++a) {
-            float2 v = sm.tot[0][a][lane];
-            for (int q = 1; q < FWD_CWARPS; ++q) v = __fadd2_rn(v, sm.tot[q][a][lane]);
-            sm.tot[0][a][lane] = v;
-        }
-    }
-    if (KS > 1) {
-        cluster_sync_all();                    // every CTA's tile sum is final
-        if (krank == 0 && warp == 0) {
-            for (int a = 0; a < NACC; ++a) {
-                float2 v = make_float2(0.f, 0.f);
-                for (int q = 0; q < KS; ++q) v = __fadd2_rn(v, ld_dsmem_f2(&sm.tot[0][a][lane], q));
-                sm.tot[0][a][lane] = v;        // only this thread reads its own slot afterwards
-            }
-        }
-        cluster_sync_all();                    // keep every CTA's smem alive until read
-        if (krank != 0) return;
-    }
-    if (warp != 0) return;
+    fwd_epilogue<KS, LOSS, CFG>(sm.tot, im, Tx0, Ty0, warp, lane, krank, out, gt, loss_acc);
+}
 
+// ------------------------------------------------------------------------------------------
+// K4, warp-autonomous variant (no producer warp): every warp filters its own share of the
+// tile's candidate batches (batch i of the tile goes to warp i mod 4, and to cluster CTA
+// (i / 4) mod KS) from the rect stream, copies its kept records into its own double buffer in
+// shared memory with per-lane cp.async (16-B, L2 -> smem, no uniform-operand serialisation),
+// and evaluates buffer k while the copies of buffer k + 1 are in flight. All warps still cover
+// the whole tile; each sums its own Gaussians, and the warp images are added in warp order.
+#ifndef GSR_FWD_BUF
+#define GSR_FWD_BUF 48
+#endif
+constexpr int FWD_BUF = GSR_FWD_BUF;              // records per warp buffer (> 32)
+constexpr int FWD2_THREADS = FWD_CWARPS * 32;
+
+template <class CFG>
+struct FwdSmem2 {
+    float4 rec[FWD_CWARPS][2][FWD_BUF * REC_F4];
+    uint8_t full[FWD_CWARPS][2][FWD_BUF];
+    float2 tot[FWD_CWARPS][FwdSmem<CFG>::NACC][32];
+};
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+    asm volatile("cp.async.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+template <int KS, bool LOSS, class CFG>
+__global__ void __launch_bounds__(FWD2_THREADS) k_render_fwd2(const ImgTable tab,
+                                                              const float4* __restrict__ rec,
+                                                              const int4* __restrict__ rects,
+                                                              const int* __restrict__ cell_start,
+                                                              const int* __restrict__ ext,
+                                                              float* __restrict__ out,
+                                                              const float* __restrict__ gt,
+                                                              double* __restrict__ loss_acc) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    FwdSmem2<CFG>& sm = *reinterpret_cast<FwdSmem2<CFG>*>(smem_raw);
+    constexpr int FTILE_W = CFG::TW, FTILE_H = CFG::TH, FWD_STRIP = CFG::STRIP,
+                  FWD_ROWS = CFG::ROWS, NACC = FwdSmem<CFG>::NACC;
+
+    const int tile = blockIdx.x / KS;
+    const int krank = KS > 1 ? (int)cluster_rank() : 0;
+    const int kimg = find_image_by_ftile(tab, tile);
+    const DevImg& im = tab.img[kimg];
+    const int t = tile - im.ftile_base;
+    const int Tx0 = (t % im.fntx) * FTILE_W;
+    const int Ty0 = im.row_begin + (t / im.fntx) * FTILE_H;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+    for (int a = 0; a < NACC; ++a) sm.tot[warp][a][lane] = make_float2(0.f, 0.f);
+
+    const int fx0 = Tx0, fx1 = min(Tx0 + FTILE_W - 1, im.Ws - 1);   // tile footprint
+    const int fy0 = Ty0, fy1 = min(Ty0 + FTILE_H - 1, im.row_end - 1);
+    const float invs = im.invs;
+
+    // lane geometry (every warp covers the whole tile)
     const int xl0 = Tx0 + FWD_STRIP * (lane & 3);
     const int yl0 = Ty0 + FWD_ROWS * (lane >> 2);
-    float l1 = 0.f;     // fused L1 loss (NEXT-1): sum |I - I_gt| over the stored elements
-    auto store = [&](int y, int x, float R, float G, float B) {
-        if (y >= im.row_end || x >= im.Ws) return;
-        const long long off = im.out_off + ((long long)(y - im.row_begin) * im.Ws + x) * 3;
-        out[off] = R; out[off + 1] = G; out[off + 2] = B;
-        if (LOSS) l1 += fabsf(R - gt[off]) + fabsf(G - gt[off + 1]) + fabsf(B - gt[off + 2]);
+    float2 xj[FWD_STRIP / 2];
+#pragma unroll
+    for (int jp = 0; jp < FWD_STRIP / 2; ++jp)
+        xj[jp] = make_float2((float)(xl0 + 2 * jp), (float)(xl0 + 2 * jp + 1));
+    const float xlf = (float)xl0;
+    const float2 yrow = make_float2((float)yl0, (float)(yl0 + 1));
+    int yi[FWD_ROWS];
+#pragma unroll
+    for (int r = 0; r < FWD_ROWS; ++r) yi[r] = yl0 + r;
+    const float yf0 = (float)yl0;
+
+    FwdProducer prod;
+    prod.cs = cell_start;
+    prod.row0 = im.cell_base;
+    prod.row_stride = im.ncx;
+    prod.cx_lo = (Tx0 - query_ext(ext, kimg, 0) + 1 + im.offx) / CELL;
+    prod.cx_hi = min(im.ncx - 1, (fx1 + im.offx) / CELL);
+    prod.cy = (Ty0 - im.row_begin - query_ext(ext, kimg, 1) + 1 + im.offy) / CELL - 1;
+    prod.cy_hi = min(im.ncy - 1, (fy1 - im.row_begin + im.offy) / CELL);
+    prod.cur = prod.end = 0;
+    const unsigned lt = (1u << lane) - 1u;
+    const bool live = fy0 <= fy1;
+    int nb[2], sb[2];
+    int4 rb[2];
+    int first = 1;
+    auto fetch = [&](int j) {
+        nb[j] = live ? prod.next(&sb[j], first ? krank * FWD_CWARPS + warp
+                                               : KS * FWD_CWARPS - 1) : 0;
+        first = 0;
+        rb[j] = make_int4(0, 0, 0, 0);
+        if (lane < nb[j]) rb[j] = __ldg(rects + sb[j] + lane);
     };
-    if constexpr (FWD_ROWS == 2) {     // acc pairs = (row 0, row 1) of one column
+
+    auto process = [&](int pbuf, int pcnt) {
+        float2 acc[NACC];
 #pragma unroll
-        for (int j = 0; j < FWD_STRIP; ++j) {
-            const float2 R = sm.tot[0][3 * j][lane], G = sm.tot[0][3 * j + 1][lane],
-                         B = sm.tot[0][3 * j + 2][lane];
-            store(yl0, xl0 + j, R.x, G.x, B.x);
-            store(yl0 + 1, xl0 + j, R.y, G.y, B.y);
-        }
-    } else {                           // acc pairs = two adjacent columns of one row
-#pragma unroll
-        for (int r = 0; r < FWD_ROWS; ++r) {
-#pragma unroll
-            for (int jp = 0; jp < FWD_STRIP / 2; ++jp) {
-                const int a = (r * (FWD_STRIP / 2) + jp) * 3;
-                const float2 R = sm.tot[0][a][lane], G = sm.tot[0][a + 1][lane],
-                             B = sm.tot[0][a + 2][lane];
-                store(yl0 + r, xl0 + 2 * jp, R.x, G.x, B.x);
-                store(yl0 + r, xl0 + 2 * jp + 1, R.y, G.y, B.y);
+        for (int a = 0; a < NACC; ++a) acc[a] = make_float2(0.f, 0.f);
+        const float4* sr = &sm.rec[warp][pbuf][0];
+        for (int g = 0; g < pcnt; ++g) {
+            const float4 r0 = sr[REC_F4 * g], r1 = sr[REC_F4 * g + 1], r2 = sr[REC_F4 * g + 2];
+            const bool full = sm.full[warp][pbuf][g] != 0;
+            if constexpr (FWD_ROWS == 2) {
+                if (full) {
+                    const float4 r3 = sr[REC_F4 * g + 3];
+                    if (r3.w != 0.f)
+                        fwd_gauss_r2<2>(r0, r1, make_float4(r2.x, r2.y, r3.x, r3.y), r3.z, xlf,
+                                        yrow, yi, xl0, invs, acc);
+                    else
+                        fwd_gauss_r2<1>(r0, r1, r2, 0.f, xlf, yrow, yi, xl0, invs, acc);
+                } else {
+                    fwd_gauss_r2<0>(r0, r1, r2, 0.f, xlf, yrow, yi, xl0, invs, acc);
+                }
+            } else {
+                if (full)
+                    fwd_gauss<CFG, true>(r0, r1, r2, xj, yf0, yi, xl0, invs, acc);
+                else
+                    fwd_gauss<CFG, false>(r0, r1, r2, xj, yf0, yi, xl0, invs, acc);
             }
         }
-    }
-    if (LOSS) {
-        double d = (double)l1;
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
-        if (lane == 0) atomicAdd(loss_acc, d);
+        for (int a = 0; a < NACC; ++a)
+            sm.tot[warp][a][lane] = __fadd2_rn(sm.tot[warp][a][lane], acc[a]);
+    };
+
+    fetch(0);
+    fetch(1);
+    int b = 0, cnt = 0, pend = -1;
+    while (true) {
+        const bool end = nb[0] == 0;
+        if (!end) {
+            bool keep = false, full = false;
+            if (lane < nb[0]) {
+                const unsigned sxs = (unsigned)rb[0].x, sys = (unsigned)rb[0].y;
+                const int sx0 = (int)(sxs & 0xffffu), sx1 = (int)(sxs >> 16);
+                const int sy0 = (int)(sys & 0xffffu), sy1 = (int)(sys >> 16);
+                keep = !(sx1 < fx0 || sx0 > fx1 || sy1 < fy0 || sy0 > fy1);
+                const unsigned xs = (unsigned)rb[0].z, ys = (unsigned)rb[0].w;
+                const int x0 = (int)(xs & 0xffffu), x1 = (int)(xs >> 16);
+                const int y0 = (int)(ys & 0xffffu), y1 = (int)(ys >> 16);
+                full = x0 <= fx0 && x1 >= fx1 && y0 <= fy0 && y1 >= fy0 + FTILE_H - 1;
+            }
+            const unsigned m = __ballot_sync(0xffffffffu, keep);
+            if (keep) {
+                const int slot = cnt + __popc(m & lt);
+                sm.full[warp][b][slot] = full ? 1 : 0;
+                const float4* src = rec + (long long)REC_F4 * (sb[0] + lane);
+                float4* dst = &sm.rec[warp][b][REC_F4 * slot];
+#pragma unroll
+                for (int q = 0; q < REC_F4; ++q) cp_async16(dst + q, src + q);
+            }
+            cnt += __popc(m);
+            nb[0] = nb[1]; sb[0] = sb[1]; rb[0] = rb[1];
+            fetch(1);
+        }
+        if (cnt > FWD_BUF - 32 || (end && cnt > 0)) {
+            cp_async_commit();
+            if (pend >= 0) {                  // the other buffer: its copies are older
+                cp_async_wait<1>();
+                __syncwarp();
+                process(b ^ 1, pend);
+                __syncwarp();
+            }
+            pend = cnt;
+            b ^= 1;
+            cnt = 0;
+        }
+        if (end) break;
     }
+    if (pend >= 0) {
+        cp_async_wait<0>();
+        __syncwarp();
+        process(b ^ 1, pend);
+    }
+    fwd_epilogue<KS, LOSS, CFG>(sm.tot, im, Tx0, Ty0, warp, lane, krank, out, gt, loss_acc);
+}
+
+template <int KS, bool LOSS, class CFG>
+cudaError_t launch_ks3_v2(const ImgTable& tab, const Workspace& ws, float* out, const float* gt,
+                          double* loss_acc, cudaStream_t st) {
+    static bool attr_set = false;
+    const size_t smem = sizeof(FwdSmem2<CFG>);
+    if (!attr_set) {
+        cudaError_t e = cudaFuncSetAttribute(k_render_fwd2<KS, LOSS, CFG>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+        if (e != cudaSuccess) return e;
+        attr_set = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)tab.total_ftiles * KS);
+    cfg.blockDim = dim3(FWD2_THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = KS;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, k_render_fwd2<KS, LOSS, CFG>, tab, (const float4*)ws.rec,
+                              (const int4*)ws.rects, (const int*)ws.cell_start,
+                              (const int*)ws.ext, out, gt, loss_acc);
 }
 
 template <int KS, bool LOSS, class CFG>
@@ -496,8 +721,13 @@ cudaError_t launch_ks3(const ImgTable& tab, const Workspace& ws, float* out, con
 template <int KS, bool LOSS>
 cudaError_t launch_ks2(const ImgTable& tab, const Workspace& ws, float* out, const float* gt,
                        double* loss_acc, cudaStream_t st) {
+#if GSR_FWD_V2
+    return tab.fwd_small ? launch_ks3_v2<KS, LOSS, FwdCfgSmall>(tab, ws, out, gt, loss_acc, st)
+                         : launch_ks3_v2<KS, LOSS, FwdCfgLarge>(tab, ws, out, gt, loss_acc, st);
+#else
     return tab.fwd_small ? launch_ks3<KS, LOSS, FwdCfgSmall>(tab, ws, out, gt, loss_acc, st)
                          : launch_ks3<KS, LOSS, FwdCfgLarge>(tab, ws, out, gt, loss_acc, st);
+#endif
 }
 
 template <int KS>
