@@ -274,6 +274,19 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     }
 }
 
+// 16-B asynchronous copy global (L2) -> shared, per thread; completion by commit/wait groups
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+    asm volatile("cp.async.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
 // 1-D TMA bulk copy global -> shared, completion counted on an mbarrier (bytes % 16 == 0).
 __device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, uint32_t bytes,
                                              uint64_t* bar) {

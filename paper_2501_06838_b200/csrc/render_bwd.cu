@@ -32,6 +32,9 @@
 #ifndef GSR_BWD_CONTIG
 #define GSR_BWD_CONTIG 0          // 1: each warp scans a contiguous share of every span
 #endif
+#ifndef GSR_BWD_KQ
+#define GSR_BWD_KQ 16             // grouping key: column buckets per axis (8 or 16)
+#endif
 #ifndef GSR_BWD_BATCH
 #define GSR_BWD_BATCH 512         // hits per sorted batch (multiple of 32)
 #endif
@@ -237,14 +240,16 @@ __global__ void __launch_bounds__(BWD_THREADS) k_render_bwd(
     // Candidate compaction + grouping. Each warp scans its share of the tile's candidate spans
     // (32 records at a time, support-rect test only) and appends the candidates whose support
     // rect meets the tile to a per-warp queue in shared memory, with a key = the clipped column
-    // range in TILE_W/8-px buckets (8 x 8 keys). Every BWD_BATCH hits the warp
+    // range in TILE_W/KQ-px buckets (KQ x KQ keys). Every BWD_BATCH hits the warp
     // sorts its queue by key (stable counting sort) and evaluates groups of 32: every lane of a
     // group owns a Gaussian that touches the tile, and lanes with similar column ranges share a
     // group, so the union of their rects (the loop bounds) stays tight (C5: 52% -> ~67% of the
     // evaluated pairs inside some lane's support, tools/sim in DESIGN.md).
-    constexpr int NB = 64;                        // key buckets (8 x 8)
+    constexpr int KQ = GSR_BWD_KQ;                // column buckets per axis
+    constexpr int NB = KQ * KQ;                   // key buckets (x0 bucket, x1 bucket)
+    constexpr int NBL = NB / 32;                  // buckets per lane in the scan
     __shared__ int qp[BWD_WARPS][BWD_BATCH + 32];
-    __shared__ unsigned char qk[BWD_WARPS][BWD_BATCH + 32];
+    __shared__ unsigned short qk[BWD_WARPS][BWD_BATCH + 32];
     __shared__ int qs[BWD_WARPS][BWD_BATCH + 32];
     __shared__ int hist[BWD_WARPS][NB];
     const unsigned lt = (1u << lane) - 1u;
@@ -326,8 +331,8 @@ __global__ void __launch_bounds__(BWD_THREADS) k_render_bwd(
     // sort the first cnt queue entries by key (stable: ranks via match_any in queue order),
     // evaluate them in groups of 32, then move the rest of the queue to the front
     auto flush = [&](int cnt) {
-        hist[warp][lane] = 0;
-        hist[warp][lane + 32] = 0;
+#pragma unroll
+        for (int q = 0; q < NBL; ++q) hist[warp][NBL * lane + q] = 0;
         __syncwarp();
         for (int i0 = 0; i0 < cnt; i0 += 32) {
             const int i = i0 + lane;
@@ -340,17 +345,21 @@ __global__ void __launch_bounds__(BWD_THREADS) k_render_bwd(
             }
             __syncwarp();
         }
-        {   // exclusive scan of the 64 bucket counts (2 per lane)
-            const int a = hist[warp][2 * lane], b = hist[warp][2 * lane + 1];
-            int incl = a + b;
+        {   // exclusive scan of the NB bucket counts (NBL consecutive buckets per lane)
+            int h[NBL];
+            int sum = 0;
+#pragma unroll
+            for (int q = 0; q < NBL; ++q) { h[q] = hist[warp][NBL * lane + q]; sum += h[q]; }
+            int incl = sum;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
                 const int y = __shfl_up_sync(0xffffffffu, incl, o);
                 if (lane >= o) incl += y;
             }
             __syncwarp();
-            hist[warp][2 * lane] = incl - a - b;
-            hist[warp][2 * lane + 1] = incl - b;
+            int run = incl - sum;
+#pragma unroll
+            for (int q = 0; q < NBL; ++q) { hist[warp][NBL * lane + q] = run; run += h[q]; }
             __syncwarp();
         }
         for (int i0 = 0; i0 < cnt; i0 += 32) {
@@ -375,7 +384,7 @@ __global__ void __launch_bounds__(BWD_THREADS) k_render_bwd(
         }
         const int rest = qn - cnt;                // < 32
         int cp = 0;
-        unsigned char ck = 0;
+        unsigned short ck = 0;
         if (lane < rest) { cp = qp[warp][cnt + lane]; ck = qk[warp][cnt + lane]; }
         __syncwarp();
         if (lane < rest) { qp[warp][lane] = cp; qk[warp][lane] = ck; }
@@ -404,14 +413,14 @@ __global__ void __launch_bounds__(BWD_THREADS) k_render_bwd(
                 const int x0 = (int)(xs & 0xffffu), x1 = (int)(xs >> 16);
                 const int y0 = (int)(ys & 0xffffu), y1 = (int)(ys >> 16);
                 hit = !(x1 < Tx0 || x0 > Tx1 || y1 < Ty0 || y0 > Ty1);
-                key = ((max(x0, Tx0) - Tx0) / (TILE_W / 8)) * 8 +
-                      (min(x1, Tx1) - Tx0) / (TILE_W / 8);
+                key = ((max(x0, Tx0) - Tx0) / (TILE_W / KQ)) * KQ +
+                      (min(x1, Tx1) - Tx0) / (TILE_W / KQ);
             }
             const unsigned hm = __ballot_sync(0xffffffffu, hit);
             if (hit) {
                 const int slot = qn + __popc(hm & lt);
                 qp[warp][slot] = p;
-                qk[warp][slot] = (unsigned char)key;
+                qk[warp][slot] = (unsigned short)key;
             }
             qn += __popc(hm);
             __syncwarp();

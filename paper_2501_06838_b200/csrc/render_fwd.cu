@@ -4,31 +4,30 @@
 //                c'_i * 2^(q_i(x,y)),   q = -(w^2 + v^2),  w = a1 dx + b1 dy,  v = c1 dy,
 //                dx = (x - ax_i)/s - dl_x,  dy = (y - ay_i)/s - dl_y   (= x/s - mu_x, y/s - mu_y)
 //
-// CTA = one FTILE_W x FTILE_H (32 x 16) HR tile, 4 consumer warps + 1 TMA producer warp.
-// Every consumer warp covers the whole tile -- lane l owns the 2 x 8 block at columns
-// Tx0 + 8 (l & 3) .. + 7 and rows Ty0 + 2 (l >> 2) + {0, 1} -- and takes the Gaussians
-// g = w, w + 4, w + 8, ... of each staged chunk: the warps' loads are identical by construction
-// (a vertical split of the tile would give each warp a different, order-dependent share of every
-// chunk and serialise the ring). The 4 partial images are summed in warp order at the end.
-//   * per Gaussian, warp-uniform: the producer drops it if its support rect (R21) misses the
-//     tile and flags it "full" if its window rect covers all 32 columns and 16 rows (no x mask,
-//     no y test: pixels beyond the support evaluate to exactly 0 by themselves); otherwise the
-//     masked path (window edge inside the tile).
-//   * per lane: kx = x - ax (exact small integers, one FADD2 per column pair, shared by the two
-//     rows), per row w = (a1/s) kx + (b1 dy - a1 dl_x) (one FFMA2 per pixel pair), q = -w^2 - v^2
-//     (one FFMA2; the y test folds into -v^2 -> -inf), 2^q on the SFU (ex2.approx.ftz ->
-//     MUFU.EX2), colour += c' 2^q (3 FFMA2). 5.5 FP32 lane-ops + 1 ex2 per pair.
-//   * candidate records (contiguous cell-row spans, binning.cu) stream through a FWD_STAGES-deep
-//     shared-memory ring filled by 1-D TMA bulk copies (cp.async.bulk, mbarrier complete_tx)
-//     issued by the producer warp, which also filters every landed chunk against the tile,
-//     compacts the kept indices and pre-transforms the kept records (full / ready / empty
-//     mbarriers per stage; no CTA-wide barrier in the main loop).
-//   * two-level sums: per-chunk partials in registers, folded into per-thread totals in shared
-//     memory after every chunk (<= 128 Gaussians).
+// CTA = one FTILE_W x FTILE_H (32 x 16) HR tile. Every warp covers the whole tile -- lane l
+// owns the 2 x 8 block at columns Tx0 + 8 (l & 3) .. + 7 and rows Ty0 + 2 (l >> 2) + {0, 1} --
+// for its own share of the tile's Gaussians; the partial images are summed in warp order.
+//   * candidates: the tile's contiguous cell-row spans (binning.cu), walked in batches of 32 and
+//     filtered from the 16-B rect stream: keep if the support rect (R21) meets the tile, "full"
+//     if the window rect covers all 32 columns and 16 rows (no x mask, no y test: pixels beyond
+//     the support evaluate to exactly 0 by themselves); otherwise the masked path.
+//   * default (k_render_fwd2, GSR_FWD_V2=1): warp-autonomous -- each warp filters batches
+//     i = warp (mod 4) and copies its kept 64-B records with per-lane cp.async into its own
+//     double buffer, evaluating one buffer while the other fills.
+//     Alternative (k_render_fwd, GSR_FWD_V2=0): 4 consumer warps + 1 producer warp that filters
+//     and gathers runs of kept records by TMA bulk copies (cp.async.bulk, mbarrier complete_tx)
+//     into a FWD_STAGES-deep ring (full / empty mbarriers per stage).
+//   * per Gaussian, three paths (warp-uniform): exponential recurrence along rows (full, D <= 1:
+//     2 ex2 per 4 pairs), direct (full, D > 1), masked (window edge in the tile). Direct path per
+//     lane: kx = x - ax (exact small integers), w = (a1/s) kx + (b1 dy - a1 dl_x), q = -w^2 - v^2
+//     (the y test folds into -v^2 -> -inf), 2^q on the SFU (ex2.approx.ftz -> MUFU.EX2),
+//     colour += c' 2^q (3 FFMA2, register pairs = the lane's two rows of a column).
+//   * two-level sums: per-buffer partials in registers, folded into per-warp totals in shared
+//     memory.
 //   * two tile configurations (gsr_internal.cuh): 2 x 8 px per lane / 32 x 16 tiles, or for
 //     narrow windows 1 x 4 px per lane / 16 x 8 tiles (fewer masked evaluations).
-//   * split-K for small problems: KS CTAs of a cluster share a tile, take every KS-th chunk, and
-//     reduce their totals through DSMEM in cluster-rank order (deterministic, no atomics).
+//   * split-K for small problems: KS CTAs of a cluster share a tile, take interleaved batches,
+//     and reduce their totals through DSMEM in cluster-rank order (deterministic, no atomics).
 #include "gsr_internal.cuh"
 
 #ifndef GSR_FWD_V2
@@ -487,6 +486,9 @@ __global__ void __launch_bounds__(FWD_THREADS) k_render_fwd(const ImgTable tab,
 // shared memory with per-lane cp.async (16-B, L2 -> smem, no uniform-operand serialisation),
 // and evaluates buffer k while the copies of buffer k + 1 are in flight. All warps still cover
 // the whole tile; each sums its own Gaussians, and the warp images are added in warp order.
+#ifndef GSR_FWD_MINB
+#define GSR_FWD_MINB 4            // CTAs per SM the register allocation must allow
+#endif
 #ifndef GSR_FWD_BUF
 #define GSR_FWD_BUF 48
 #endif
@@ -500,20 +502,9 @@ struct FwdSmem2 {
     float2 tot[FWD_CWARPS][FwdSmem<CFG>::NACC][32];
 };
 
-__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src)
-                 : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() {
-    asm volatile("cp.async.commit_group;" ::: "memory");
-}
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
 
 template <int KS, bool LOSS, class CFG>
-__global__ void __launch_bounds__(FWD2_THREADS) k_render_fwd2(const ImgTable tab,
+__global__ void __launch_bounds__(FWD2_THREADS, GSR_FWD_MINB) k_render_fwd2(const ImgTable tab,
                                                               const float4* __restrict__ rec,
                                                               const int4* __restrict__ rects,
                                                               const int* __restrict__ cell_start,
