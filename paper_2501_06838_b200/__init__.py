@@ -7,9 +7,9 @@ GSASR (arXiv 2501.06838, Eq. 1-4 / Alg. 1), behind the C-ABI in include/gsr.h.
 from ._lib import GsrError, load, out_dims, tile_shape, version
 from .ops import (Image, Layout, finalize_grads, layout, pair_count, render, render_batch,
                   render_bwd, render_bwd_batched, render_bwd_moments_batched, render_fwd,
-                  render_fwd_batched, StreamedFwdBwd)
+                  render_fwd_batched, StreamedFwdBwd, TrainStepGraph, train_step_l1)
 
 __all__ = ["GsrError", "load", "out_dims", "tile_shape", "version", "Image", "Layout",
            "finalize_grads", "layout", "pair_count", "render", "render_batch", "render_bwd",
            "render_bwd_batched", "render_bwd_moments_batched", "render_fwd", "render_fwd_batched",
-           "StreamedFwdBwd"]
+           "StreamedFwdBwd", "TrainStepGraph", "train_step_l1"]
