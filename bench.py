@@ -249,10 +249,18 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # GSR_BENCH_SHARE_GPU=1 (functional check of the sharded path on a 1-GPU box, never a
+    # performance number): every rank on device 0, gloo for the collectives
+    share = os.environ.get("GSR_BENCH_SHARE_GPU") == "1"
+    if share:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     gsr.load()
 
     cfg, imgs = workload(args.workload, args.images)
