@@ -77,8 +77,8 @@ gsr_status build_table(const gsr_image* imgs, int32_t n_imgs, int64_t n_total, d
         if (std::isfinite(w) && w > max_win) max_win = w;
     }
     tab->fwd_small = max_win < (double)FWD_SMALL_WINDOW ? 1 : 0;
-    tab->ftile_w = tab->fwd_small ? FwdCfgSmall::TW : FwdCfgLarge::TW;
-    tab->ftile_h = tab->fwd_small ? FwdCfgSmall::TH : FwdCfgLarge::TH;
+    tab->ftile_w = tab->fwd_small ? FwdCfgSmall::TW : FwdCfgWide::TW;
+    tab->ftile_h = tab->fwd_small ? FwdCfgSmall::TH : FwdCfgWide::TH;
     long long cells = 0, tiles = 0, ftiles = 0, prev_end = 0;
     for (int k = 0; k < n_imgs; ++k) {
         const gsr_image& g = imgs[k];

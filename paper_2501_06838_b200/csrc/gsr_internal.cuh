@@ -31,6 +31,15 @@ constexpr int TILE_H = GSR_BWD_TILE_H;  // also the debug tile-list tile (TILE_H
 //         which wastes far fewer masked evaluations where a window covers only part of a tile.
 struct FwdCfgLarge { static constexpr int ROWS = 2, STRIP = 8, TW = 4 * STRIP, TH = 8 * ROWS; };
 struct FwdCfgSmall { static constexpr int ROWS = 1, STRIP = 4, TW = 4 * STRIP, TH = 8 * ROWS; };
+struct FwdCfgMed { static constexpr int ROWS = 2, STRIP = 4, TW = 4 * STRIP, TH = 8 * ROWS; };
+#ifndef GSR_FWD_MED
+#define GSR_FWD_MED 0             // 1: 16 x 16 tiles (2 x 4 px per lane) instead of 32 x 16
+#endif
+#if GSR_FWD_MED
+using FwdCfgWide = FwdCfgMed;
+#else
+using FwdCfgWide = FwdCfgLarge;
+#endif
 constexpr int FTILE_W = FwdCfgLarge::TW;          // 32
 constexpr int FTILE_H = FwdCfgLarge::TH;          // 16
 constexpr int FWD_SMALL_WINDOW = 48;             // HR px: below this the small tiles are used

@@ -159,10 +159,10 @@ __device__ __forceinline__ void fwd_gauss(const float4 r0, const float4 r1, cons
 //           2^q_a flushes to zero (q_a < -126) has q(kx_a + 3) < -67 (|w_a| > 11.2, D <= 1),
 //           i.e. only values below 2^-67 are lost; products never overflow (q <= 0 and
 //           D^2 t^2 <= 9). Error: the exponent of B^t carries t * 2 D |w_a| * 2^-24 relative.
-template <int MODE>
+template <int MODE, int STRIP>
 __device__ __forceinline__ void fwd_gauss_r2(const float4 r0, const float4 r1, const float4 r2,
                                              float g3, float xlf, float2 yrow, const int (&yi)[2],
-                                             int xl0, float invs, float2 (&acc)[24]) {
+                                             int xl0, float invs, float2 (&acc)[3 * STRIP]) {
     const float D = r0.w;
     const float2 D2 = f2(D);
     const float kx0 = xlf + r0.x;                           // x - ax of column 0 (exact)
@@ -187,7 +187,7 @@ __device__ __forceinline__ void fwd_gauss_r2(const float4 r0, const float4 r1, c
     if (MODE == 2) {
         const float2 G1 = f2(r2.z), G2 = f2(r2.w), G3 = f2(g3), M2D = f2(-2.f * D);
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
+        for (int h = 0; h < STRIP / 4; ++h) {
             const float2 w = __ffma2_rn(D2, f2(kx0 + 4.f * h), T);
             const float2 q = __ffma2_rn(make_float2(-w.x, -w.y), w, U);
             float2 b = __fmul2_rn(w, M2D);
@@ -212,7 +212,7 @@ __device__ __forceinline__ void fwd_gauss_r2(const float4 r0, const float4 r1, c
             x1 = (int)(xs >> 16);
         }
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
+        for (int j = 0; j < STRIP; ++j) {
             const float2 w = __ffma2_rn(D2, f2(kx0 + (float)j), T);
             float2 q = __ffma2_rn(make_float2(-w.x, -w.y), w, U);
             if (MODE == 0 && !(xl0 + j >= x0 && xl0 + j <= x1)) q = f2(-INFINITY);
@@ -453,12 +453,12 @@ __global__ void __launch_bounds__(FWD_THREADS) k_render_fwd(const ImgTable tab,
                     if (full) {
                         const float4 r3 = sr[REC_F4 * g + 3];
                         if (r3.w != 0.f)
-                            fwd_gauss_r2<2>(r0, r1, make_float4(r2.x, r2.y, r3.x, r3.y), r3.z, xlf,
+                            fwd_gauss_r2<2, FWD_STRIP>(r0, r1, make_float4(r2.x, r2.y, r3.x, r3.y), r3.z, xlf,
                                             yrow, yi, xl0, invs, acc);
                         else
-                            fwd_gauss_r2<1>(r0, r1, r2, 0.f, xlf, yrow, yi, xl0, invs, acc);
+                            fwd_gauss_r2<1, FWD_STRIP>(r0, r1, r2, 0.f, xlf, yrow, yi, xl0, invs, acc);
                     } else {
-                        fwd_gauss_r2<0>(r0, r1, r2, 0.f, xlf, yrow, yi, xl0, invs, acc);
+                        fwd_gauss_r2<0, FWD_STRIP>(r0, r1, r2, 0.f, xlf, yrow, yi, xl0, invs, acc);
                     }
                 } else {
                     if (full)
@@ -486,6 +486,9 @@ __global__ void __launch_bounds__(FWD_THREADS) k_render_fwd(const ImgTable tab,
 // shared memory with per-lane cp.async (16-B, L2 -> smem, no uniform-operand serialisation),
 // and evaluates buffer k while the copies of buffer k + 1 are in flight. All warps still cover
 // the whole tile; each sums its own Gaussians, and the warp images are added in warp order.
+#ifndef GSR_FWD_PAIR
+#define GSR_FWD_PAIR 0            // 1: recurrence-path Gaussians two at a time (measured 1% slower)
+#endif
 #ifndef GSR_FWD_MINB
 #define GSR_FWD_MINB 4            // CTAs per SM the register allocation must allow
 #endif
@@ -573,19 +576,19 @@ __global__ void __launch_bounds__(FWD2_THREADS, GSR_FWD_MINB) k_render_fwd2(cons
 #pragma unroll
         for (int a = 0; a < NACC; ++a) acc[a] = make_float2(0.f, 0.f);
         const float4* sr = &sm.rec[warp][pbuf][0];
-        for (int g = 0; g < pcnt; ++g) {
+        auto single = [&](int g) {
             const float4 r0 = sr[REC_F4 * g], r1 = sr[REC_F4 * g + 1], r2 = sr[REC_F4 * g + 2];
             const bool full = sm.full[warp][pbuf][g] != 0;
             if constexpr (FWD_ROWS == 2) {
                 if (full) {
                     const float4 r3 = sr[REC_F4 * g + 3];
                     if (r3.w != 0.f)
-                        fwd_gauss_r2<2>(r0, r1, make_float4(r2.x, r2.y, r3.x, r3.y), r3.z, xlf,
+                        fwd_gauss_r2<2, FWD_STRIP>(r0, r1, make_float4(r2.x, r2.y, r3.x, r3.y), r3.z, xlf,
                                         yrow, yi, xl0, invs, acc);
                     else
-                        fwd_gauss_r2<1>(r0, r1, r2, 0.f, xlf, yrow, yi, xl0, invs, acc);
+                        fwd_gauss_r2<1, FWD_STRIP>(r0, r1, r2, 0.f, xlf, yrow, yi, xl0, invs, acc);
                 } else {
-                    fwd_gauss_r2<0>(r0, r1, r2, 0.f, xlf, yrow, yi, xl0, invs, acc);
+                    fwd_gauss_r2<0, FWD_STRIP>(r0, r1, r2, 0.f, xlf, yrow, yi, xl0, invs, acc);
                 }
             } else {
                 if (full)
@@ -593,6 +596,33 @@ __global__ void __launch_bounds__(FWD2_THREADS, GSR_FWD_MINB) k_render_fwd2(cons
                 else
                     fwd_gauss<CFG, false>(r0, r1, r2, xj, yf0, yi, xl0, invs, acc);
             }
+        };
+        int g = 0;
+        while (g < pcnt) {
+#if GSR_FWD_PAIR
+            if constexpr (FWD_ROWS == 2) {
+                // two recurrence-path Gaussians in one basic block: independent chains the
+                // scheduler interleaves (the kernel is latency-bound at 4 warps per SMSP)
+                if (g + 1 < pcnt) {
+                    const float4 a3 = sr[REC_F4 * g + 3], b3 = sr[REC_F4 * (g + 1) + 3];
+                    if (sm.full[warp][pbuf][g] != 0 && sm.full[warp][pbuf][g + 1] != 0 &&
+                        a3.w != 0.f && b3.w != 0.f) {
+                        const float4 a0 = sr[REC_F4 * g], a1 = sr[REC_F4 * g + 1],
+                                     a2 = sr[REC_F4 * g + 2];
+                        const float4 b0 = sr[REC_F4 * (g + 1)], b1 = sr[REC_F4 * (g + 1) + 1],
+                                     b2 = sr[REC_F4 * (g + 1) + 2];
+                        fwd_gauss_r2<2, FWD_STRIP>(a0, a1, make_float4(a2.x, a2.y, a3.x, a3.y), a3.z, xlf,
+                                        yrow, yi, xl0, invs, acc);
+                        fwd_gauss_r2<2, FWD_STRIP>(b0, b1, make_float4(b2.x, b2.y, b3.x, b3.y), b3.z, xlf,
+                                        yrow, yi, xl0, invs, acc);
+                        g += 2;
+                        continue;
+                    }
+                }
+            }
+#endif
+            single(g);
+            ++g;
         }
 #pragma unroll
         for (int a = 0; a < NACC; ++a)
@@ -714,10 +744,10 @@ cudaError_t launch_ks2(const ImgTable& tab, const Workspace& ws, float* out, con
                        double* loss_acc, cudaStream_t st) {
 #if GSR_FWD_V2
     return tab.fwd_small ? launch_ks3_v2<KS, LOSS, FwdCfgSmall>(tab, ws, out, gt, loss_acc, st)
-                         : launch_ks3_v2<KS, LOSS, FwdCfgLarge>(tab, ws, out, gt, loss_acc, st);
+                         : launch_ks3_v2<KS, LOSS, FwdCfgWide>(tab, ws, out, gt, loss_acc, st);
 #else
     return tab.fwd_small ? launch_ks3<KS, LOSS, FwdCfgSmall>(tab, ws, out, gt, loss_acc, st)
-                         : launch_ks3<KS, LOSS, FwdCfgLarge>(tab, ws, out, gt, loss_acc, st);
+                         : launch_ks3<KS, LOSS, FwdCfgWide>(tab, ws, out, gt, loss_acc, st);
 #endif
 }
 
