@@ -42,6 +42,10 @@
  *       rect is window rect (R2) intersected with the box; its unclipped
  *       origin is max(window origin, box origin). Mode "support" renders over
  *       it; the difference to the window sum is pinned below 1e-30.
+ *   R22 scale vector ("an upsampling scale vector"; NEXT-4): s = (sw, sh),
+ *       sw along x <-> W, sh along y <-> H. Every "s" above applies per axis:
+ *       output floor(sh*H) x floor(sw*W); sample (x/sw, y/sh); window and box
+ *       bounds along x use sw, along y sh. sw = sh is the paper's scalar s.
  *   Summation order: per pixel, ascending Gaussian index (brute and rect modes
  *   therefore give bit-identical results).
  *
@@ -102,16 +106,16 @@ static double oracle_clamp_bound(double v)
     return v;
 }
 
-static int oracle_rect(double mx, double my, int H, int W, double s, double r, int Hs, int Ws,
+static int oracle_rect(double mx, double my, int H, int W, double sw, double sh, double r, int Hs, int Ws,
                        int64_t* x0u, int64_t* y0u, int64_t* x0, int64_t* x1, int64_t* y0,
                        int64_t* y1)
 {
     double hx = r * (double)W;   /* half-extent along x, LR px (R1) */
     double hy = r * (double)H;   /* half-extent along y, LR px (R1) */
-    double lx = s * (mx - hx);
-    double ux = s * (mx + hx);
-    double ly = s * (my - hy);
-    double uy = s * (my + hy);
+    double lx = sw * (mx - hx);
+    double ux = sw * (mx + hx);
+    double ly = sh * (my - hy);
+    double uy = sh * (my + hy);
     if (isnan(lx) || isnan(ux) || isnan(ly) || isnan(uy)) return 0;
     int64_t ax0 = (int64_t)floor(oracle_clamp_bound(lx)) + 1;
     int64_t ax1 = (int64_t)ceil(oracle_clamp_bound(ux)) - 1;
@@ -130,14 +134,14 @@ static int oracle_rect(double mx, double my, int H, int W, double s, double r, i
 /* R21: window rect intersected with the +-13.5 sigma box (see header). */
 #define ORACLE_SUPPORT_SIGMAS 13.5
 static int oracle_support_rect(double mx, double my, double sx, double sy, int H, int W,
-                               double s, double r, int Hs, int Ws, int64_t* x0u, int64_t* y0u,
+                               double sw, double sh, double r, int Hs, int Ws, int64_t* x0u, int64_t* y0u,
                                int64_t* x0, int64_t* x1, int64_t* y0, int64_t* y1)
 {
     int64_t wx0u, wy0u;
-    if (!oracle_rect(mx, my, H, W, s, r, Hs, Ws, &wx0u, &wy0u, x0, x1, y0, y1)) return 0;
+    if (!oracle_rect(mx, my, H, W, sw, sh, r, Hs, Ws, &wx0u, &wy0u, x0, x1, y0, y1)) return 0;
     double tx = ORACLE_SUPPORT_SIGMAS * sx, ty = ORACLE_SUPPORT_SIGMAS * sy;
-    double lx = s * (mx - tx), ux = s * (mx + tx);
-    double ly = s * (my - ty), uy = s * (my + ty);
+    double lx = sw * (mx - tx), ux = sw * (mx + tx);
+    double ly = sh * (my - ty), uy = sh * (my + ty);
     if (isnan(lx) || isnan(ux) || isnan(ly) || isnan(uy)) return 0;
     int64_t bx0 = (int64_t)floor(oracle_clamp_bound(lx));
     int64_t bx1 = (int64_t)ceil(oracle_clamp_bound(ux));
@@ -154,20 +158,20 @@ static int oracle_support_rect(double mx, double my, double sx, double sy, int H
 
 /* rect of Gaussian i in the given mode: 0 = window (R2), 1 = support (R21) */
 static int oracle_rect_mode(int support, const double* mu, const double* sigma, int64_t i, int H,
-                            int W, double s, double r, int Hs, int Ws, int64_t* x0u,
+                            int W, double sw, double sh, double r, int Hs, int Ws, int64_t* x0u,
                             int64_t* y0u, int64_t* x0, int64_t* x1, int64_t* y0, int64_t* y1)
 {
     if (support)
         return oracle_support_rect(mu[2 * i], mu[2 * i + 1], sigma[2 * i], sigma[2 * i + 1], H,
-                                   W, s, r, Hs, Ws, x0u, y0u, x0, x1, y0, y1);
-    return oracle_rect(mu[2 * i], mu[2 * i + 1], H, W, s, r, Hs, Ws, x0u, y0u, x0, x1, y0, y1);
+                                   W, sw, sh, r, Hs, Ws, x0u, y0u, x0, x1, y0, y1);
+    return oracle_rect(mu[2 * i], mu[2 * i + 1], H, W, sw, sh, r, Hs, Ws, x0u, y0u, x0, x1, y0, y1);
 }
 
 /* R4 */
-void gsr_oracle_out_dims(int H, int W, double s, int* Hs, int* Ws)
+void gsr_oracle_out_dims(int H, int W, double sw, double sh, int* Hs, int* Ws)
 {
-    *Hs = (int)floor(s * (double)H);
-    *Ws = (int)floor(s * (double)W);
+    *Hs = (int)floor(sh * (double)H);
+    *Ws = (int)floor(sw * (double)W);
 }
 
 void gsr_oracle_set_threads(int n)
@@ -190,15 +194,15 @@ int gsr_oracle_max_threads(void)
 
 /* Per-Gaussian rects for tests: out[i*6 + {x0u,y0u,x0,x1,y0,y1}], empty -> x0>x1. */
 void gsr_oracle_rects(int64_t n, const double* alpha, const double* mu, const double* sigma,
-                      const double* rho, const double* color, int H, int W, double s, double r,
+                      const double* rho, const double* color, int H, int W, double sw, double sh, double r,
                       int support, int64_t* out)
 {
     int Hs, Ws;
-    gsr_oracle_out_dims(H, W, s, &Hs, &Ws);
+    gsr_oracle_out_dims(H, W, sw, sh, &Hs, &Ws);
     for (int64_t i = 0; i < n; ++i) {
         int64_t x0u = 0, y0u = 0, x0 = 1, x1 = 0, y0 = 1, y1 = 0;
         if (oracle_is_valid(alpha, mu, sigma, rho, color, i))
-            if (!oracle_rect_mode(support, mu, sigma, i, H, W, s, r, Hs, Ws, &x0u, &y0u, &x0, &x1,
+            if (!oracle_rect_mode(support, mu, sigma, i, H, W, sw, sh, r, Hs, Ws, &x0u, &y0u, &x0, &x1,
                                   &y0, &y1)) {
                 x0 = 1; x1 = 0; y0 = 1; y1 = 0;
             }
@@ -211,15 +215,15 @@ void gsr_oracle_rects(int64_t n, const double* alpha, const double* mu, const do
  * to HR rows [row_begin, row_end). */
 int64_t gsr_oracle_pair_count(int64_t n, const double* alpha, const double* mu,
                               const double* sigma, const double* rho, const double* color, int H,
-                              int W, double s, double r, int row_begin, int row_end, int support)
+                              int W, double sw, double sh, double r, int row_begin, int row_end, int support)
 {
     int Hs, Ws;
-    gsr_oracle_out_dims(H, W, s, &Hs, &Ws);
+    gsr_oracle_out_dims(H, W, sw, sh, &Hs, &Ws);
     int64_t total = 0;
     for (int64_t i = 0; i < n; ++i) {
         if (!oracle_is_valid(alpha, mu, sigma, rho, color, i)) continue;
         int64_t x0u, y0u, x0, x1, y0, y1;
-        if (!oracle_rect_mode(support, mu, sigma, i, H, W, s, r, Hs, Ws, &x0u, &y0u, &x0, &x1,
+        if (!oracle_rect_mode(support, mu, sigma, i, H, W, sw, sh, r, Hs, Ws, &x0u, &y0u, &x0, &x1,
                               &y0, &y1))
             continue;
         if (y0 < row_begin) y0 = row_begin;
@@ -239,11 +243,11 @@ int64_t gsr_oracle_pair_count(int64_t n, const double* alpha, const double* mu,
 /* Output rows [row_begin, row_end) only: out[(y-row_begin)*Ws*3 + x*3 + k].  */
 /* ------------------------------------------------------------------------- */
 int gsr_oracle_render_fwd(int64_t n, const double* alpha, const double* mu, const double* sigma,
-                          const double* rho, const double* color, int H, int W, double s,
+                          const double* rho, const double* color, int H, int W, double sw, double sh,
                           double r, int mode, int row_begin, int row_end, double* out)
 {
     int Hs, Ws;
-    gsr_oracle_out_dims(H, W, s, &Hs, &Ws);
+    gsr_oracle_out_dims(H, W, sw, sh, &Hs, &Ws);
     if (row_begin < 0) row_begin = 0;
     if (row_end > Hs) row_end = Hs;
     int rows = row_end - row_begin;
@@ -254,9 +258,9 @@ int gsr_oracle_render_fwd(int64_t n, const double* alpha, const double* mu, cons
     if (mode == 0 || mode == 2) {
 #pragma omp parallel for schedule(dynamic, 1)
         for (int y = row_begin; y < row_end; ++y) {
-            double Y = (double)y / s;                           /* Eq. 4 sample, R3 */
+            double Y = (double)y / sh;                           /* Eq. 4 sample, R3 */
             for (int x = 0; x < Ws; ++x) {
-                double X = (double)x / s;
+                double X = (double)x / sw;
                 double* px = out + ((size_t)(y - row_begin) * Ws + x) * 3;
                 for (int64_t i = 0; i < n; ++i) {               /* ascending i */
                     if (!oracle_is_valid(alpha, mu, sigma, rho, color, i)) continue;
@@ -283,7 +287,7 @@ int gsr_oracle_render_fwd(int64_t n, const double* alpha, const double* mu, cons
             if (!oracle_is_valid(alpha, mu, sigma, rho, color, i)) continue;
             double mx = mu[2 * i], my = mu[2 * i + 1];
             int64_t x0u, y0u, x0, x1, y0, y1;
-            if (!oracle_rect_mode(mode == 3, mu, sigma, i, H, W, s, r, Hs, Ws, &x0u, &y0u, &x0,
+            if (!oracle_rect_mode(mode == 3, mu, sigma, i, H, W, sw, sh, r, Hs, Ws, &x0u, &y0u, &x0,
                                   &x1, &y0, &y1))
                 continue;
             (void)mx; (void)my;
@@ -291,9 +295,9 @@ int gsr_oracle_render_fwd(int64_t n, const double* alpha, const double* mu, cons
             if (y1 > row_end - 1) y1 = row_end - 1;
             for (int64_t y = y0; y <= y1; ++y) {
                 if ((y % nt) != t) continue;
-                double Y = (double)y / s;
+                double Y = (double)y / sh;
                 for (int64_t x = x0; x <= x1; ++x) {
-                    double X = (double)x / s;
+                    double X = (double)x / sw;
                     double f = oracle_density(X - mx, Y - my, sigma[2 * i], sigma[2 * i + 1],
                                               rho[i], NULL);
                     double* px = out + ((size_t)(y - row_begin) * Ws + x) * 3;
@@ -309,13 +313,13 @@ int gsr_oracle_render_fwd(int64_t n, const double* alpha, const double* mu, cons
  * parity at full sizes. out[p*3+k]. */
 int gsr_oracle_render_pixels(int64_t n, const double* alpha, const double* mu,
                              const double* sigma, const double* rho, const double* color, int H,
-                             int W, double s, double r, int64_t npix, const int32_t* px_x,
+                             int W, double sw, double sh, double r, int64_t npix, const int32_t* px_x,
                              const int32_t* px_y, double* out)
 {
     double hx = r * (double)W, hy = r * (double)H;
 #pragma omp parallel for schedule(dynamic, 1)
     for (int64_t p = 0; p < npix; ++p) {
-        double X = (double)px_x[p] / s, Y = (double)px_y[p] / s;
+        double X = (double)px_x[p] / sw, Y = (double)px_y[p] / sh;
         double acc[3] = {0.0, 0.0, 0.0};
         for (int64_t i = 0; i < n; ++i) {
             if (!oracle_is_valid(alpha, mu, sigma, rho, color, i)) continue;
@@ -369,13 +373,13 @@ int gsr_oracle_field(int64_t n, const double* alpha, const double* mu, const dou
 /* (dx = X - mu_x, so d/d mu_x = -d/d dx; d ln K/d rho = rho/D.)              */
 /* ------------------------------------------------------------------------- */
 int gsr_oracle_render_bwd(int64_t n, const double* alpha, const double* mu, const double* sigma,
-                          const double* rho, const double* color, int H, int W, double s,
+                          const double* rho, const double* color, int H, int W, double sw, double sh,
                           double r, int mode, int row_begin, int row_end, const double* grad_out,
                           int64_t nidx, const int64_t* idx, double* d_alpha, double* d_mu,
                           double* d_sigma, double* d_rho, double* d_color, double* absmass)
 {
     int Hs, Ws;
-    gsr_oracle_out_dims(H, W, s, &Hs, &Ws);
+    gsr_oracle_out_dims(H, W, sw, sh, &Hs, &Ws);
     if (row_begin < 0) row_begin = 0;
     if (row_end > Hs) row_end = Hs;
     double hx = r * (double)W, hy = r * (double)H;
@@ -395,7 +399,7 @@ int gsr_oracle_render_bwd(int64_t n, const double* alpha, const double* mu, cons
             int have = 1;
             if (mode == 1 || mode == 3) {
                 int64_t x0u, y0u, x0, x1, y0, y1;
-                have = oracle_rect_mode(mode == 3, mu, sigma, i, H, W, s, r, Hs, Ws, &x0u, &y0u,
+                have = oracle_rect_mode(mode == 3, mu, sigma, i, H, W, sw, sh, r, Hs, Ws, &x0u, &y0u,
                                         &x0, &x1, &y0, &y1);
                 xa = x0; xb = x1;
                 ya = y0 > row_begin ? y0 : row_begin;
@@ -403,9 +407,9 @@ int gsr_oracle_render_bwd(int64_t n, const double* alpha, const double* mu, cons
             }
             if (have) {
                 for (int64_t y = ya; y <= yb; ++y) {
-                    double Y = (double)y / s;
+                    double Y = (double)y / sh;
                     for (int64_t x = xa; x <= xb; ++x) {
-                        double X = (double)x / s;
+                        double X = (double)x / sw;
                         if (mode == 0 && !(fabs(X - mx) < hx && fabs(Y - my) < hy)) continue;
                         const double* g = grad_out + ((size_t)(y - row_begin) * Ws + x) * 3;
                         double dx = X - mx, dy = Y - my, Q;
@@ -469,11 +473,11 @@ int gsr_oracle_render_bwd(int64_t n, const double* alpha, const double* mu, cons
 /* ------------------------------------------------------------------------- */
 int64_t gsr_oracle_tile_lists(int64_t n, const double* alpha, const double* mu,
                               const double* sigma, const double* rho, const double* color, int H,
-                              int W, double s, double r, int tw, int th, int row_begin,
+                              int W, double sw, double sh, double r, int tw, int th, int row_begin,
                               int row_end, int support, int64_t* counts, int64_t* ids)
 {
     int Hs, Ws;
-    gsr_oracle_out_dims(H, W, s, &Hs, &Ws);
+    gsr_oracle_out_dims(H, W, sw, sh, &Hs, &Ws);
     if (row_end > Hs) row_end = Hs;
     int ntx = (Ws + tw - 1) / tw;
     int nty = (row_end - row_begin + th - 1) / th;
@@ -488,7 +492,7 @@ int64_t gsr_oracle_tile_lists(int64_t n, const double* alpha, const double* mu,
             for (int64_t i = 0; i < n; ++i) {
                 if (!oracle_is_valid(alpha, mu, sigma, rho, color, i)) continue;
                 int64_t x0u, y0u, x0, x1, y0, y1;
-                if (!oracle_rect_mode(support, mu, sigma, i, H, W, s, r, Hs, Ws, &x0u, &y0u, &x0,
+                if (!oracle_rect_mode(support, mu, sigma, i, H, W, sw, sh, r, Hs, Ws, &x0u, &y0u, &x0,
                                       &x1, &y0, &y1))
                     continue;
                 if (x1 < tx0 || x0 > tx1 || y1 < ty0 || y0 > ty1) continue;

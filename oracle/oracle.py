@@ -40,11 +40,11 @@ class OracleLib:
     def __init__(self):
         build_oracle()
         lib = ctypes.CDLL(str(_LIB))
-        lib.gsr_oracle_out_dims.argtypes = [_i32, _i32, _dbl, ctypes.POINTER(_i32),
+        lib.gsr_oracle_out_dims.argtypes = [_i32, _i32, _dbl, _dbl, ctypes.POINTER(_i32),
                                             ctypes.POINTER(_i32)]
         lib.gsr_oracle_set_threads.argtypes = [_i32]
         lib.gsr_oracle_max_threads.restype = _i32
-        par = [_i64, _p, _p, _p, _p, _p, _i32, _i32, _dbl, _dbl]
+        par = [_i64, _p, _p, _p, _p, _p, _i32, _i32, _dbl, _dbl, _dbl]
         lib.gsr_oracle_rects.argtypes = par + [_i32, _p]
         lib.gsr_oracle_pair_count.argtypes = par + [_i32, _i32, _i32]
         lib.gsr_oracle_pair_count.restype = _i64
@@ -90,9 +90,18 @@ def max_threads() -> int:
     return int(load().lib.gsr_oracle_max_threads())
 
 
-def out_dims(H: int, W: int, s: float):
+def scales(s):
+    """Scale argument -> (s_w, s_h): a number s is the paper's isotropic scale (s, s); a pair
+    (s_x, s_y) is the NEXT-4 scale vector, s_x along W (x), s_y along H (y), DESIGN R22."""
+    if isinstance(s, (tuple, list, np.ndarray)):
+        sw, sh = (float(v) for v in s)
+        return sw, sh
+    return float(s), float(s)
+
+
+def out_dims(H: int, W: int, s):
     hs, ws = _i32(), _i32()
-    load().lib.gsr_oracle_out_dims(int(H), int(W), float(s), ctypes.byref(hs), ctypes.byref(ws))
+    load().lib.gsr_oracle_out_dims(int(H), int(W), *scales(s), ctypes.byref(hs), ctypes.byref(ws))
     return hs.value, ws.value
 
 
@@ -107,7 +116,7 @@ def render_fwd(cloud, H, W, s, r=0.1, mode="rect", rows=None) -> np.ndarray:
     re = min(re, Hs)
     out = np.zeros((max(re - rb, 0), Ws, 3), np.float64)
     load().lib.gsr_oracle_render_fwd(a.shape[0], _ptr(a), _ptr(mu), _ptr(sg), _ptr(rh), _ptr(c),
-                                     int(H), int(W), float(s), float(r), MODES[mode], int(rb),
+                                     int(H), int(W), *scales(s), float(r), MODES[mode], int(rb),
                                      int(re), _ptr(out))
     return out
 
@@ -118,7 +127,7 @@ def render_pixels(cloud, H, W, s, r, px_x, px_y) -> np.ndarray:
     px_y = np.ascontiguousarray(px_y, np.int32)
     out = np.zeros((px_x.shape[0], 3), np.float64)
     load().lib.gsr_oracle_render_pixels(a.shape[0], _ptr(a), _ptr(mu), _ptr(sg), _ptr(rh),
-                                        _ptr(c), int(H), int(W), float(s), float(r),
+                                        _ptr(c), int(H), int(W), *scales(s), float(r),
                                         px_x.shape[0], _ptr(px_x), _ptr(px_y), _ptr(out))
     return out
 
@@ -152,7 +161,7 @@ def render_bwd(cloud, H, W, s, r, grad_out, mode="rect", rows=None, idx=None,
                color=np.zeros((m, 3)))
     am = np.zeros((m, 9)) if want_absmass else None
     load().lib.gsr_oracle_render_bwd(
-        n, _ptr(a), _ptr(mu), _ptr(sg), _ptr(rh), _ptr(c), int(H), int(W), float(s), float(r),
+        n, _ptr(a), _ptr(mu), _ptr(sg), _ptr(rh), _ptr(c), int(H), int(W), *scales(s), float(r),
         MODES[mode], int(rb), int(re), _ptr(g), m if idx is not None else 0,
         _ptr(idx) if idx is not None else None, _ptr(res["alpha"]), _ptr(res["mu"]),
         _ptr(res["sigma"]), _ptr(res["rho"]), _ptr(res["color"]),
@@ -168,7 +177,7 @@ def rects(cloud, H, W, s, r=0.1, support=False) -> np.ndarray:
     a, mu, sg, rh, c = _params(cloud)
     out = np.zeros((a.shape[0], 6), np.int64)
     load().lib.gsr_oracle_rects(a.shape[0], _ptr(a), _ptr(mu), _ptr(sg), _ptr(rh), _ptr(c),
-                                int(H), int(W), float(s), float(r), int(bool(support)), _ptr(out))
+                                int(H), int(W), *scales(s), float(r), int(bool(support)), _ptr(out))
     return out
 
 
@@ -178,7 +187,7 @@ def pair_count(cloud, H, W, s, r=0.1, rows=None, support=False) -> int:
     Hs, _ = out_dims(H, W, s)
     rb, re = (0, Hs) if rows is None else rows
     return int(load().lib.gsr_oracle_pair_count(a.shape[0], _ptr(a), _ptr(mu), _ptr(sg),
-                                                _ptr(rh), _ptr(c), int(H), int(W), float(s),
+                                                _ptr(rh), _ptr(c), int(H), int(W), *scales(s),
                                                 float(r), int(rb), int(re), int(bool(support))))
 
 
@@ -191,7 +200,7 @@ def tile_lists(cloud, H, W, s, r, tw, th, rows=None, support=False):
     nty = (min(re, Hs) - rb + th - 1) // th
     counts = np.zeros(ntx * nty, np.int64)
     lib = load().lib
-    args = (a.shape[0], _ptr(a), _ptr(mu), _ptr(sg), _ptr(rh), _ptr(c), int(H), int(W), float(s),
+    args = (a.shape[0], _ptr(a), _ptr(mu), _ptr(sg), _ptr(rh), _ptr(c), int(H), int(W), *scales(s),
             float(r), int(tw), int(th), int(rb), int(re), int(bool(support)))
     total = lib.gsr_oracle_tile_lists(*args, _ptr(counts), None)
     ids = np.zeros(max(total, 1), np.int64)

@@ -28,6 +28,8 @@ def loss(cl, H, W, s, r, g):
     (3, 4, 4, 2.0, 0.1, "stress", 3),
     (4, 4, 1, 3.0, 0.5, "stress", 4),
     (2, 3, 4, 3.0, 1.0, "image", 5),
+    (4, 3, 4, (1.7, 2.6), 0.5, "image", 6),     # scale vector (R22)
+    (3, 4, 4, (3.0, 1.25), 0.1, "stress", 7),
 ])
 def test_backward_matches_central_fd(H, W, m, s, r, dist, seed):
     cl = f64(S.gaussians(H, W, m=m, seed=seed, dist=dist))

@@ -236,7 +236,9 @@ def test_invalid_gaussians_contribute_nothing():
 # --------------------------------------------------------------------------- brute vs rect
 @pytest.mark.parametrize("cfg", [(8, 8, 4.0, 0.1, "image", 1), (6, 10, 2.5, 0.1, "stress", 2),
                                  (7, 5, 1.0, 0.5, "image", 3), (5, 5, 3.3, 1.0, "stress", 4),
-                                 (4, 6, 17.0, 0.1, "image", 5)])
+                                 (4, 6, 17.0, 0.1, "image", 5),
+                                 (6, 7, (2.0, 3.5), 0.2, "image", 6),
+                                 (5, 8, (4.25, 1.5), 0.1, "stress", 7)])
 def test_brute_equals_rect_bitwise(cfg):
     """The integer rect (R2) selects exactly the pairs of the literal predicate and the per-pixel
     sum order is ascending i in both modes, so the results are bit-identical."""
@@ -330,7 +332,8 @@ def test_support_outside_below_fp32(rho, sig):
 
 
 @pytest.mark.parametrize("cfg", [(10, 12, 4.0, 0.3, "image", 0), (9, 7, 2.5, 1.0, "stress", 1),
-                                 (6, 11, 8.0, 0.5, "stress", 2), (12, 12, 1.0, 1.0, "image", 3)])
+                                 (6, 11, 8.0, 0.5, "stress", 2), (12, 12, 1.0, 1.0, "image", 3),
+                                 (7, 9, (6.0, 2.5), 0.5, "stress", 4)])
 def test_support_render_equals_window_render(cfg):
     """R21: rendering over the support rects differs from the window sum of Alg. 1 only by terms
     below 2^-131 of each Gaussian's peak (forward and every gradient)."""
@@ -353,3 +356,64 @@ def test_support_render_equals_window_render(cfg):
         # d/dtheta of a dropped term is (polynomial in Q <= 1e3 of it) x the term itself
         assert np.abs(ga[k] - gb[k]).max() <= 1e6 * bound * Hs * Ws / min(1.0, sx.min(),
                                                                           sy.min()) ** 2, k
+
+
+# --------------------------------------------------------------------------- scale vector (R22)
+@pytest.mark.parametrize("sw,sh,H,W", [(2, 3, 6, 7), (3, 2, 5, 4), (1, 4, 4, 6)])
+def test_scale_vector_is_a_subsampling_of_the_isotropic_image(sw, sh, H, W):
+    """R22 ("an upsampling scale vector"): with integer scales (sw, sh), pixel (x, y)
+    samples (x/sw, y/sh) = (x k_x/L, y k_y/L) at the isotropic scale L = sw sh, i.e. pixel
+    (sh x, sw y) of the isotropic image, with the same window test (r W, r H in LR units).
+    The two quotients are correctly rounded from the same real, so in brute mode
+    I_(sw,sh)[y, x] == I_L[sw y, sh x] bit for bit; a swapped axis or scale fails it."""
+    r = 0.3
+    L = float(sw * sh)
+    cl = S.gaussians(H, W, m=4, seed=11, dist="stress", offset_range=1.5)
+    a = O.render_fwd(cl, H, W, (float(sw), float(sh)), r, mode="brute")
+    b = O.render_fwd(cl, H, W, L, r, mode="brute")
+    assert a.shape[:2] == (sh * H, sw * W)
+    assert np.array_equal(b[::sw, ::sh][:sh * H, :sw * W], a)
+    assert a.any()
+
+
+def test_scale_vector_transpose_symmetry():
+    """Swapping the axes of the whole problem (mu, sigma, H <-> W, sw <-> sh; rho is symmetric in
+    Eq. 2) transposes the rendered image and swaps the x/y gradients."""
+    H, W, sw, sh, r = 5, 7, 2.5, 3.25, 0.3
+    cl = {k: np.asarray(v, np.float64) for k, v in S.gaussians(H, W, m=4, seed=12).items()}
+    tr = dict(cl, mu=cl["mu"][:, ::-1].copy(), sigma=cl["sigma"][:, ::-1].copy())
+    a = O.render_fwd(cl, H, W, (sw, sh), r, mode="rect")
+    b = O.render_fwd(tr, W, H, (sh, sw), r, mode="rect")
+    assert a.shape[:2] == (int(math.floor(sh * H)), int(math.floor(sw * W)))
+    np.testing.assert_allclose(b.transpose(1, 0, 2), a, rtol=1e-13, atol=1e-300)
+    g = S.grad_out(a.shape, seed=5)
+    ga = O.render_bwd(cl, H, W, (sw, sh), r, g, mode="rect")
+    gb = O.render_bwd(tr, W, H, (sh, sw), r, g.transpose(1, 0, 2).copy(), mode="rect")
+    for k in ("alpha", "rho", "color"):
+        np.testing.assert_allclose(gb[k], ga[k], rtol=1e-11, atol=1e-14 * np.abs(ga[k]).max())
+    for k in ("mu", "sigma"):
+        np.testing.assert_allclose(gb[k][:, ::-1], ga[k], rtol=1e-11,
+                                   atol=1e-14 * np.abs(ga[k]).max())
+
+
+def test_scale_vector_single_gaussian_closed_form():
+    """Eq. 2 at the R22 sample point: an axis-aligned Gaussian (rho = 0) centred at mu renders
+    alpha c exp(-((x/sw - mu_x)^2/sx^2 + (y/sh - mu_y)^2/sy^2)/2) / (2 pi sx sy) at (x, y)."""
+    sw, sh, mu, sig = 3.0, 1.5, (2.2, 3.1), (0.7, 1.3)
+    a = O.render_fwd(one(mu=mu, sigma=sig, color=(1.0, 0.5, 2.0)), 6, 5, (sw, sh), 1.0,
+                     mode="brute")
+    for (x, y) in [(0, 0), (6, 4), (7, 5), (14, 8)]:
+        X, Y = x / sw, y / sh
+        want = math.exp(-0.5 * ((X - mu[0]) ** 2 / sig[0] ** 2 + (Y - mu[1]) ** 2 / sig[1] ** 2)) \
+            / (2 * math.pi * sig[0] * sig[1])
+        assert a[y, x, 0] == pytest.approx(want, rel=1e-13)
+        assert a[y, x, 2] == pytest.approx(2 * want, rel=1e-13)
+
+
+def test_scale_vector_window_per_axis():
+    """R1/R2/R22: the window is |x/sw - mu_x| < r W and |y/sh - mu_y| < r H: with sw != sh the
+    integer rect spans (about) 2 r W sw columns and 2 r H sh rows."""
+    H, W, sw, sh, r = 10, 20, 2.0, 5.0, 0.1
+    R = O.rects(one(mu=(10.0, 5.0)), H, W, (sw, sh), r)[0]
+    # x: 10 +- 2 (LR) -> (16, 24) exclusive in HR px at sw = 2; y: 5 +- 1 -> (20, 30) at sh = 5
+    assert list(R[2:]) == [17, 23, 21, 29]
