@@ -60,7 +60,14 @@ typedef enum {
 
 #define GSR_MAX_IMAGES 64
 
-/* One image of a (ragged) batch. All images of a call share the parameter arrays: image k owns
+/* Scale vector (reading R22; "receives the predicted 2D Gaussians with an upsampling scale
+ * vector"): an image may carry two scales, `scale` = s_x along x (W) and `scale_y` = s_y along y
+ * (H). Every "s" of the readings above then applies per axis: Hs = floor(s_y H),
+ * Ws = floor(s_x W), sample (x/s_x, y/s_y), window bounds along x with s_x and along y with s_y.
+ * scale_y = 0 means s_y = s_x (the paper's isotropic case). The single-image entry points take
+ * the scalar s only; the batched ones read scale_y from gsr_image.
+ *
+ * One image of a (ragged) batch. All images of a call share the parameter arrays: image k owns
  * Gaussians [g_off, g_off + g_cnt). Its output block starts at float offset out_off of `out`
  * (and of grad_out for the backward) and holds rows [row_begin, row_end) of the HR image:
  * (row_end - row_begin) * Ws * 3 floats, row-major HWC. row_begin = 0, row_end = -1 means the
@@ -68,12 +75,13 @@ typedef enum {
 typedef struct gsr_image {
     int32_t lr_h;      /* H >= 1 */
     int32_t lr_w;      /* W >= 1 */
-    double scale;      /* s >= 1, finite */
+    double scale;      /* s (s_x when scale_y != 0) >= 1, finite */
     int64_t g_off;     /* first Gaussian of this image */
     int64_t g_cnt;     /* number of Gaussians of this image (may be 0) */
     int64_t out_off;   /* float offset of this image's output block */
     int32_t row_begin; /* first HR row of the band, 0 <= row_begin */
     int32_t row_end;   /* one past the last HR row (-1 = Hs); row_begin <= row_end <= Hs */
+    double scale_y;    /* scale along y (H): 0 = `scale` (the paper's scalar s); else >= 1 */
 } gsr_image;
 
 /* Library version string (static storage). */

@@ -31,7 +31,8 @@ GSR_SUPPORT = 0x2
 class GsrImage(ctypes.Structure):
     _fields_ = [("lr_h", ctypes.c_int32), ("lr_w", ctypes.c_int32), ("scale", ctypes.c_double),
                 ("g_off", ctypes.c_int64), ("g_cnt", ctypes.c_int64), ("out_off", ctypes.c_int64),
-                ("row_begin", ctypes.c_int32), ("row_end", ctypes.c_int32)]
+                ("row_begin", ctypes.c_int32), ("row_end", ctypes.c_int32),
+                ("scale_y", ctypes.c_double)]
 
 
 class GsrError(RuntimeError):
@@ -109,18 +110,27 @@ def check(status: int, what: str) -> None:
 
 
 def images_array(imgs):
-    """[(H, W, s, g_off, g_cnt, out_off, row_begin, row_end), ...] -> ctypes array."""
+    """[(H, W, s, g_off, g_cnt, out_off, row_begin, row_end[, s_y]), ...] -> ctypes array
+    (s_y = 0 or absent: isotropic scale s)."""
     arr = (GsrImage * len(imgs))()
     for k, t in enumerate(imgs):
-        H, W, s, go, gc, oo, rb, re = t
-        arr[k] = GsrImage(int(H), int(W), float(s), int(go), int(gc), int(oo), int(rb), int(re))
+        H, W, s, go, gc, oo, rb, re = t[:8]
+        sy = t[8] if len(t) > 8 and t[8] is not None else 0.0
+        arr[k] = GsrImage(int(H), int(W), float(s), int(go), int(gc), int(oo), int(rb), int(re),
+                          float(sy))
     return arr
 
 
-def out_dims(H: int, W: int, s: float):
+def out_dims(H: int, W: int, s: float, s_y: float | None = None):
+    """(Hs, Ws) = (floor(s_y H), floor(s W)) (R4, R22; s_y None or 0: s_y = s)."""
     h, w = _I32(), _I32()
     check(load().gsr_out_dims(int(H), int(W), float(s), ctypes.byref(h), ctypes.byref(w)),
           "gsr_out_dims")
+    if s_y:
+        h2, w2 = _I32(), _I32()
+        check(load().gsr_out_dims(int(H), int(W), float(s_y), ctypes.byref(h2),
+                                  ctypes.byref(w2)), "gsr_out_dims")
+        return h2.value, w.value
     return h.value, w.value
 
 

@@ -260,13 +260,13 @@ __global__ void k_records(const float* __restrict__ alpha, const float* __restri
     double kd = sqrt(HALF_LOG2E / D);
     double a1 = kd / sx, b1 = -rh * kd / sy, c1 = sqrt(HALF_LOG2E) / sy;
     double K = 1.0 / (TWO_PI * sx * sy * sqrt(D));
-    double axd = rint(im.s * mx), ayd = rint(im.s * my);   // anchor: nearest HR pixel
-    double dlx = mx - axd / im.s, dly = my - ayd / im.s;
+    double axd = rint(im.sx * mx), ayd = rint(im.sy * my);   // anchor: nearest HR pixel
+    double dlx = mx - axd / im.sx, dly = my - ayd / im.sy;
     double w = al * K;
     // consumer form: r0 = {-ax, ay, dl_y, D}, r1 = {-a1 dl_x, b1, c1, c'_r}
     // with D = a1/s formed in fp32 (the recurrence constants below use the same D)
     const float a1f = (float)a1;
-    const float Df = a1f * im.invs, d2 = Df * Df;
+    const float Df = a1f * im.invsx, d2 = Df * Df;
     float4 r0 = make_float4((float)(-axd), (float)ayd, (float)dly, Df);
     float4 r1 = make_float4((float)(-a1 * dlx), (float)b1, (float)c1, (float)(w * color[3 * i]));
     unsigned xs = (unsigned)r.x0 | ((unsigned)r.x1 << 16);

@@ -1,5 +1,6 @@
 // gsr_abi.cu -- the C-ABI of include/gsr.h: argument validation, per-image geometry (fp64,
 // host), workspace carving and launch orchestration. No allocation, no stream sync.
+#include <algorithm>
 #include <atomic>
 #include <cmath>
 #include <cstring>
@@ -73,7 +74,8 @@ gsr_status build_table(const gsr_image* imgs, int32_t n_imgs, int64_t n_total, d
     double max_win = 0.0;
     for (int k = 0; k < n_imgs; ++k) {
         const gsr_image& g = imgs[k];
-        double w = 2.0 * ratio * g.scale * (double)(g.lr_h < g.lr_w ? g.lr_h : g.lr_w);
+        const double gsy = g.scale_y > 0.0 ? g.scale_y : g.scale;
+        double w = std::min(2.0 * ratio * g.scale * (double)g.lr_w, 2.0 * ratio * gsy * (double)g.lr_h);
         if (std::isfinite(w) && w > max_win) max_win = w;
     }
     tab->fwd_small = max_win < (double)FWD_SMALL_WINDOW ? 1 : 0;
@@ -84,27 +86,32 @@ gsr_status build_table(const gsr_image* imgs, int32_t n_imgs, int64_t n_total, d
         const gsr_image& g = imgs[k];
         if (g.lr_h < 1 || g.lr_w < 1) return GSR_EINVAL;
         if (!std::isfinite(g.scale) || !(g.scale >= 1.0)) return GSR_EINVAL;
+        if (!std::isfinite(g.scale_y) || g.scale_y < 0.0 || (g.scale_y > 0.0 && g.scale_y < 1.0))
+            return GSR_EINVAL;
+        const double sx = g.scale, sy = g.scale_y > 0.0 ? g.scale_y : g.scale;   // reading R22
         if (g.g_off < prev_end || g.g_cnt < 0 || g.g_off + g.g_cnt > n_total) return GSR_EINVAL;
         if (g.out_off < 0) return GSR_EINVAL;
         prev_end = g.g_off + g.g_cnt;
-        double hsd = std::floor(g.scale * (double)g.lr_h);   // reading R4
-        double wsd = std::floor(g.scale * (double)g.lr_w);
+        double hsd = std::floor(sy * (double)g.lr_h);   // readings R4, R22
+        double wsd = std::floor(sx * (double)g.lr_w);
         if (hsd > MAX_DIM || wsd > MAX_DIM || hsd < 1 || wsd < 1) return GSR_EINVAL;
         DevImg& d = tab->img[k];
-        d.s = g.scale;
+        d.sx = sx;
+        d.sy = sy;
         d.hx = ratio * (double)g.lr_w;    // reading R1: x <-> W
         d.hy = ratio * (double)g.lr_h;
         d.g_off = g.g_off;
         d.g_cnt = g.g_cnt;
         d.out_off = g.out_off;
-        d.invs = (float)(1.0 / g.scale);
+        d.invsx = (float)(1.0 / sx);
+        d.invsy = (float)(1.0 / sy);
         d.H = g.lr_h; d.W = g.lr_w; d.Hs = (int)hsd; d.Ws = (int)wsd;
         int rb = g.row_begin, re = g.row_end < 0 ? d.Hs : g.row_end;
         if (rb < 0 || re > d.Hs || rb > re) return GSR_EINVAL;
         d.row_begin = rb; d.row_end = re;
         // bounds on the unclipped rect extent: width <= 2 s r W + 1 (+ fp64 rounding)
-        d.wmax = (int)std::ceil(2.0 * g.scale * d.hx) + 2;
-        d.hmax = (int)std::ceil(2.0 * g.scale * d.hy) + 2;
+        d.wmax = (int)std::ceil(2.0 * sx * d.hx) + 2;
+        d.hmax = (int)std::ceil(2.0 * sy * d.hy) + 2;
         d.offx = CELL * ceil_div(d.wmax, CELL);
         d.offy = CELL * ceil_div(d.hmax, CELL);
         int nrows = re - rb;
@@ -134,7 +141,7 @@ gsr_status build_table(const gsr_image* imgs, int32_t n_imgs, int64_t n_total, d
 
 gsr_image single(int64_t n, int32_t h, int32_t w, double s) {
     gsr_image g;
-    g.lr_h = h; g.lr_w = w; g.scale = s;
+    g.lr_h = h; g.lr_w = w; g.scale = s; g.scale_y = 0.0;
     g.g_off = 0; g.g_cnt = n; g.out_off = 0; g.row_begin = 0; g.row_end = -1;
     return g;
 }

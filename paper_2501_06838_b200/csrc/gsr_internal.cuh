@@ -71,10 +71,10 @@ constexpr double TWO_PI = 6.28318530717958647693;
 
 // Per-image constants, computed on the host in fp64, passed by value in ImgTable.
 struct DevImg {
-    double s;           // scale
+    double sx, sy;      // scale vector (R22): sx along x <-> W, sy along y <-> H (paper: sx = sy = s)
     double hx, hy;      // window half-extents r*W, r*H (LR px, fp64)
     long long g_off, g_cnt, out_off;
-    float invs;         // fp32(1/s)
+    float invsx, invsy; // fp32(1/sx), fp32(1/sy)
     int H, W, Hs, Ws;
     int row_begin, row_end;   // HR row band
     int offx, offy;           // cell-grid offsets (multiples of CELL, >= max rect extent)
@@ -150,10 +150,10 @@ __device__ __forceinline__ double clamp_bound(double v) {
 __device__ __forceinline__ Rect window_rect(float mux, float muy, const DevImg& im) {
     Rect r;
     double mx = (double)mux, my = (double)muy;
-    double lx = __dmul_rn(im.s, __dsub_rn(mx, im.hx));
-    double ux = __dmul_rn(im.s, __dadd_rn(mx, im.hx));
-    double ly = __dmul_rn(im.s, __dsub_rn(my, im.hy));
-    double uy = __dmul_rn(im.s, __dadd_rn(my, im.hy));
+    double lx = __dmul_rn(im.sx, __dsub_rn(mx, im.hx));
+    double ux = __dmul_rn(im.sx, __dadd_rn(mx, im.hx));
+    double ly = __dmul_rn(im.sy, __dsub_rn(my, im.hy));
+    double uy = __dmul_rn(im.sy, __dadd_rn(my, im.hy));
     long long ax0 = (long long)floor(clamp_bound(lx)) + 1;
     long long ax1 = (long long)ceil(clamp_bound(ux)) - 1;
     long long ay0 = (long long)floor(clamp_bound(ly)) + 1;
@@ -187,10 +187,10 @@ __device__ __forceinline__ Rect support_rect(float mux, float muy, float sxf, fl
     const double mx = (double)mux, my = (double)muy;
     const double tx = __dmul_rn(SUPPORT_SIGMAS, (double)sxf);
     const double ty = __dmul_rn(SUPPORT_SIGMAS, (double)syf);
-    const double lx = __dmul_rn(im.s, __dsub_rn(mx, tx));
-    const double ux = __dmul_rn(im.s, __dadd_rn(mx, tx));
-    const double ly = __dmul_rn(im.s, __dsub_rn(my, ty));
-    const double uy = __dmul_rn(im.s, __dadd_rn(my, ty));
+    const double lx = __dmul_rn(im.sx, __dsub_rn(mx, tx));
+    const double ux = __dmul_rn(im.sx, __dadd_rn(mx, tx));
+    const double ly = __dmul_rn(im.sy, __dsub_rn(my, ty));
+    const double uy = __dmul_rn(im.sy, __dadd_rn(my, ty));
     const int bx0 = (int)floor(clamp_bound(lx)), bx1 = (int)ceil(clamp_bound(ux));
     const int by0 = (int)floor(clamp_bound(ly)), by1 = (int)ceil(clamp_bound(uy));
     r.x0u = max(r.x0u, bx0);

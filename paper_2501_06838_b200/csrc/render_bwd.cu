@@ -235,7 +235,7 @@ __global__ void __launch_bounds__(BWD_THREADS) k_render_bwd(
     const int cx_hi = min(im.ncx - 1, (Tx1 + im.offx) / CELL);
     const int cy_lo = (Ty0 - im.row_begin - query_ext(ext, kimg, 1) + 1 + im.offy) / CELL;
     const int cy_hi = min(im.ncy - 1, (Ty1 - im.row_begin + im.offy) / CELL);
-    const float invs = im.invs;
+    const float invs = im.invsy;     // rows: dy = (y - ay)/sy - dl_y
 
     // Candidate compaction + grouping. Each warp scans its share of the tile's candidate spans
     // (32 records at a time, support-rect test only) and appends the candidates whose support

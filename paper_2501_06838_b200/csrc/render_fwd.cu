@@ -328,7 +328,7 @@ __global__ void __launch_bounds__(FWD_THREADS) k_render_fwd(const ImgTable tab,
 
     const int fx0 = Tx0, fx1 = min(Tx0 + FTILE_W - 1, im.Ws - 1);   // tile footprint
     const int fy0 = Ty0, fy1 = min(Ty0 + FTILE_H - 1, im.row_end - 1);
-    const float invs = im.invs;
+    const float invs = im.invsy;     // rows: dy = (y - ay)/sy - dl_y
 
     if (warp == FWD_CWARPS) {
         // ---------------- producer warp --------------------------------------------------------
@@ -533,7 +533,7 @@ __global__ void __launch_bounds__(FWD2_THREADS, GSR_FWD_MINB) k_render_fwd2(cons
 
     const int fx0 = Tx0, fx1 = min(Tx0 + FTILE_W - 1, im.Ws - 1);   // tile footprint
     const int fy0 = Ty0, fy1 = min(Ty0 + FTILE_H - 1, im.row_end - 1);
-    const float invs = im.invs;
+    const float invs = im.invsy;     // rows: dy = (y - ay)/sy - dl_y
 
     // lane geometry (every warp covers the whole tile)
     const int xl0 = Tx0 + FWD_STRIP * (lane & 3);

@@ -55,7 +55,8 @@ def _ptr(t: torch.Tensor, offset_elems: int = 0) -> int:
 @dataclass
 class Image:
     """One image of a batch: LR size (H, W), scale s, its Gaussians [g_off, g_off+g_cnt) and the
-    HR row band [row_begin, row_end) (row_end = -1: all Hs rows)."""
+    HR row band [row_begin, row_end) (row_end = -1: all Hs rows). s_y (> 0) makes the scale a
+    vector (s_x, s_y) = (s, s_y) (reading R22); None: isotropic s."""
     H: int
     W: int
     s: float
@@ -63,6 +64,7 @@ class Image:
     g_cnt: int
     row_begin: int = 0
     row_end: int = -1
+    s_y: Optional[float] = None
 
 
 @dataclass
@@ -84,7 +86,7 @@ def layout(images: Sequence[Image]) -> Layout:
     dims, rows, offs = [], [], []
     off = 0
     for im in images:
-        Hs, Ws = _lib.out_dims(im.H, im.W, im.s)
+        Hs, Ws = _lib.out_dims(im.H, im.W, im.s, im.s_y)
         rb = im.row_begin
         re = Hs if im.row_end is None or im.row_end < 0 else im.row_end
         dims.append((Hs, Ws))
@@ -107,7 +109,8 @@ def _chunks(lay: Layout):
         for k in sel:
             im = ims[k]
             rb, re = lay.rows[k]
-            recs.append((im.H, im.W, im.s, im.g_off - g0, im.g_cnt, lay.out_off[k] - o0, rb, re))
+            recs.append((im.H, im.W, im.s, im.g_off - g0, im.g_cnt, lay.out_off[k] - o0, rb, re,
+                         im.s_y))
         yield g0, g1, o0, _lib.images_array(recs), len(sel)
 
 
@@ -264,8 +267,17 @@ def pair_count(alpha, mu, sigma, rho, color, lay: Layout, ratio: float = 0.1,
 
 
 # ------------------------------------------------------------------ single image + autograd
+def _scale(s):
+    """A scale argument: a number s (the paper's scalar) or a scale vector (s_x, s_y) (R22)
+    -> (s_x, s_y or None)."""
+    if isinstance(s, (tuple, list)):
+        return float(s[0]), float(s[1])
+    return float(s), None
+
+
 def _single(n, H, W, s):
-    return layout([Image(int(H), int(W), float(s), 0, int(n))])
+    sx, sy = _scale(s)
+    return layout([Image(int(H), int(W), sx, 0, int(n), s_y=sy)])
 
 
 def render_fwd(alpha, mu, sigma, rho, color, H: int, W: int, scale: float,
@@ -305,10 +317,12 @@ class _RenderFn(torch.autograd.Function):
 def render_batch(alpha, mu, sigma, rho, color, images: Sequence[Tuple[int, int, float]],
                  counts: Sequence[int], ratio: float = 0.1):
     """Differentiable ragged batch render. images[k] = (H, W, s) owns counts[k] consecutive
-    Gaussians. Returns (flat output, Layout); Layout.view(flat, k) is image k as [Hs, Ws, 3]."""
+    Gaussians; s is a number or a scale vector (s_x, s_y) (R22). Returns (flat output, Layout);
+    Layout.view(flat, k) is image k as [Hs, Ws, 3]."""
     ims, off = [], 0
     for (H, W, s), c in zip(images, counts):
-        ims.append(Image(int(H), int(W), float(s), off, int(c)))
+        sx, sy = _scale(s)
+        ims.append(Image(int(H), int(W), sx, off, int(c), s_y=sy))
         off += int(c)
     lay = layout(ims)
     return _RenderFn.apply(alpha, mu, sigma, rho, color, lay, float(ratio)), lay
@@ -453,7 +467,8 @@ class StreamedFwdBwd:
             g0 = min(ims[k].g_off for k in range(k0, k1))
             g1 = max(ims[k].g_off + ims[k].g_cnt for k in range(k0, k1))
             sub = layout([Image(ims[k].H, ims[k].W, ims[k].s, ims[k].g_off - g0, ims[k].g_cnt,
-                                lay.rows[k][0], lay.rows[k][1]) for k in range(k0, k1)])
+                                lay.rows[k][0], lay.rows[k][1], ims[k].s_y)
+                          for k in range(k0, k1)])
             o0 = lay.out_off[k0]
             self.groups.append((g0, g1, o0, o0 + sub.out_numel, sub))
         dev = self.dev

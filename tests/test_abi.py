@@ -101,6 +101,17 @@ def test_einval_before_any_launch(lib):
     assert lib.gsr_render_fwd_batched(*ps, 10, imgs, 1, 0.1, dummy, dummy, 1 << 30, None) == 1
     imgs = _lib.images_array([(4, 4, 2.0, 0, 5, 0, 0, 9)])
     assert lib.gsr_render_fwd_batched(*ps, 10, imgs, 1, 0.1, dummy, dummy, 1 << 30, None) == 1
+    # scale vector (R22): scale_y in (0, 1) or non-finite is invalid; the band is checked
+    # against Hs = floor(scale_y H)
+    for sy in (0.5, float("nan"), float("inf"), -2.0):
+        imgs = _lib.images_array([(4, 4, 2.0, 0, 5, 0, 0, -1, sy)])
+        assert lib.gsr_render_fwd_batched(*ps, 10, imgs, 1, 0.1, dummy, dummy, 1 << 30,
+                                          None) == 1, sy
+        assert lib.gsr_workspace_bytes_batched(imgs, 1, 10, 0.1) == 0, sy
+    imgs = _lib.images_array([(4, 4, 2.0, 0, 5, 0, 0, 13, 3.0)])
+    assert lib.gsr_render_fwd_batched(*ps, 10, imgs, 1, 0.1, dummy, dummy, 1 << 30, None) == 1
+    assert lib.gsr_workspace_bytes_batched(_lib.images_array([(4, 4, 2.0, 0, 5, 0, 0, 12, 3.0)]),
+                                           1, 10, 0.1) > 0
     many = _lib.images_array([(4, 4, 2.0, 0, 0, 0, 0, -1)] * 65)
     assert lib.gsr_render_fwd_batched(*ps, 10, many, 65, 0.1, dummy, dummy, 1 << 30, None) == 1
     assert lib.gsr_finalize_grads(*ps, -1, dummy, *ps, None) == 1
