@@ -155,20 +155,46 @@ gsr_status gsr_finalize_grads(const float* alpha, const float* mu, const float* 
  * images and ratio (typically this step's forward), enqueued on the same stream; the binning
  * stage (K1, radix sort, K1b) is skipped. Results are undefined if that precondition is false. */
 #define GSR_REUSE_BINNING 0x1u
-gsr_status gsr_render_bwd_batched_ex(const float* alpha, const float* mu, const float* sigma,
-                                     const float* rho, const float* color, int64_t n_total,
+/* Data formats ("AMP in bfloat16"). Accepted by the _ex entry points
+ * below (the finalize and pair count take GSR_PARAMS_BF16 only); the arithmetic is unchanged
+ * (fp32 evaluation, fp64 rects/finalize), only what is read and written changes:
+ *   GSR_OUT_BF16    the image arrays -- the forward's `out`, the backward's `grad_out` -- hold
+ *                   bfloat16 elements (the forward rounds its fp32 sums to nearest-even on store);
+ *                   gsr_image.out_off and the block sizes count elements.
+ *   GSR_OUT_CHW     the image blocks are planar: element (k, y, x) of image block b at
+ *                   b.out_off + k*rows*Ws + (y - row_begin)*Ws + x, rows = row_end - row_begin
+ *                   (default: HWC, b.out_off + ((y - row_begin)*Ws + x)*3 + k).
+ *   GSR_PARAMS_BF16 the five parameter arrays are bfloat16 (same SoA layouts); they are widened
+ *                   exactly to fp32 where read. Gradients are always written as float32.
+ * The backward's flags must describe the same formats as the forward's when
+ * GSR_REUSE_BINNING is set. The single-image and non-_ex entry points use float32 HWC. */
+#define GSR_OUT_BF16 0x4u
+#define GSR_OUT_CHW 0x8u
+#define GSR_PARAMS_BF16 0x10u
+gsr_status gsr_render_fwd_batched_ex(const void* alpha, const void* mu, const void* sigma,
+                                     const void* rho, const void* color, int64_t n_total,
                                      const gsr_image* imgs, int32_t n_imgs, double ratio,
-                                     const float* grad_out, float* d_alpha, float* d_mu,
+                                     void* out, void* workspace, size_t workspace_bytes,
+                                     uint32_t flags, void* stream);
+gsr_status gsr_render_bwd_batched_ex(const void* alpha, const void* mu, const void* sigma,
+                                     const void* rho, const void* color, int64_t n_total,
+                                     const gsr_image* imgs, int32_t n_imgs, double ratio,
+                                     const void* grad_out, float* d_alpha, float* d_mu,
                                      float* d_sigma, float* d_rho, float* d_color,
                                      void* workspace, size_t workspace_bytes, uint32_t flags,
                                      void* stream);
-gsr_status gsr_render_bwd_moments_batched_ex(const float* alpha, const float* mu,
-                                             const float* sigma, const float* rho,
-                                             const float* color, int64_t n_total,
+gsr_status gsr_render_bwd_moments_batched_ex(const void* alpha, const void* mu,
+                                             const void* sigma, const void* rho,
+                                             const void* color, int64_t n_total,
                                              const gsr_image* imgs, int32_t n_imgs, double ratio,
-                                             const float* grad_out, double* moments,
+                                             const void* grad_out, double* moments,
                                              void* workspace, size_t workspace_bytes,
                                              uint32_t flags, void* stream);
+gsr_status gsr_finalize_grads_ex(const void* alpha, const void* mu, const void* sigma,
+                                 const void* rho, const void* color, int64_t n_total,
+                                 const double* moments, float* d_alpha, float* d_mu,
+                                 float* d_sigma, float* d_rho, float* d_color, uint32_t flags,
+                                 void* stream);
 
 /* ---- training-step adjacency ------------------------------------------
  * One fused training step of the rasterizer for the paper's L1 objective, from the RAW
@@ -207,15 +233,15 @@ gsr_status gsr_train_step_l1_batched(const float* raw_alpha, const float* offset
 /* Number of (Gaussian, pixel) pairs inside the windows, P = sum_i |rect_i| restricted to each
  * image's row band (the paper's work unit). Writes one int64 to *d_pairs (device
  * pointer). Uses the workspace. The _ex form with GSR_SUPPORT counts the pairs inside the
- * support rects instead (the pairs the kernels evaluate; the roofline's work unit). Other flag
- * bits: GSR_EINVAL. */
+ * support rects instead (the pairs the kernels evaluate; the roofline's work unit); it also
+ * accepts GSR_PARAMS_BF16. Other flag bits: GSR_EINVAL. */
 gsr_status gsr_pair_count_batched(const float* alpha, const float* mu, const float* sigma,
                                   const float* rho, const float* color, int64_t n_total,
                                   const gsr_image* imgs, int32_t n_imgs, double ratio,
                                   int64_t* d_pairs, void* workspace, size_t workspace_bytes,
                                   void* stream);
-gsr_status gsr_pair_count_batched_ex(const float* alpha, const float* mu, const float* sigma,
-                                     const float* rho, const float* color, int64_t n_total,
+gsr_status gsr_pair_count_batched_ex(const void* alpha, const void* mu, const void* sigma,
+                                     const void* rho, const void* color, int64_t n_total,
                                      const gsr_image* imgs, int32_t n_imgs, double ratio,
                                      uint32_t flags, int64_t* d_pairs, void* workspace,
                                      size_t workspace_bytes, void* stream);

@@ -23,9 +23,13 @@ EXPORTS = ["gsr_version", "gsr_out_dims", "gsr_workspace_bytes_batched", "gsr_wo
            "gsr_debug_rects", "gsr_debug_tile_lists", "gsr_tile_shape", "gsr_profile_enable",
            "gsr_profile_collect", "gsr_render_bwd_batched_ex", "gsr_render_bwd_moments_batched_ex",
            "gsr_train_workspace_bytes_batched", "gsr_train_step_l1_batched",
-           "gsr_pair_count_batched_ex", "gsr_debug_rects_ex"]
+           "gsr_pair_count_batched_ex", "gsr_debug_rects_ex", "gsr_render_fwd_batched_ex",
+           "gsr_finalize_grads_ex"]
 GSR_REUSE_BINNING = 0x1
 GSR_SUPPORT = 0x2
+GSR_OUT_BF16 = 0x4
+GSR_OUT_CHW = 0x8
+GSR_PARAMS_BF16 = 0x10
 
 
 class GsrImage(ctypes.Structure):
@@ -78,6 +82,10 @@ def load(path: Path | str | None = None):
         "gsr_render_bwd_moments_batched_ex": (par + [_I64, _IMGP, _I32, _D, _P, _P, _P, _SZ,
                                                      ctypes.c_uint32, _P], None),
         "gsr_finalize_grads": (par + [_I64, _P, _P, _P, _P, _P, _P, _P], None),
+        "gsr_finalize_grads_ex": (par + [_I64, _P, _P, _P, _P, _P, _P, ctypes.c_uint32, _P],
+                                  None),
+        "gsr_render_fwd_batched_ex": (par + [_I64, _IMGP, _I32, _D, _P, _P, _SZ, ctypes.c_uint32,
+                                             _P], None),
         "gsr_train_workspace_bytes_batched": ([_IMGP, _I32, _I64, _D], _SZ),
         "gsr_train_step_l1_batched": ([_P] * 6 + [_I64, _IMGP, _I32, _D, ctypes.c_float, _D, _P,
                                                   _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P], None),

@@ -28,9 +28,10 @@ long long rs_blocks(long long n) { return (n + RS_BLOCK - 1) / RS_BLOCK; }
 long long scan_blocks(long long n) { return (n + SCAN_BLOCK - 1) / SCAN_BLOCK; }
 
 // ---- K1: keys ----------------------------------------------------------------------------
-__global__ void k_keys(const float* __restrict__ alpha, const float* __restrict__ mu,
-                       const float* __restrict__ sigma, const float* __restrict__ rho,
-                       const float* __restrict__ color, long long n, ImgTable tab,
+template <class T>
+__global__ void k_keys(const T* __restrict__ alpha, const T* __restrict__ mu,
+                       const T* __restrict__ sigma, const T* __restrict__ rho,
+                       const T* __restrict__ color, long long n, ImgTable tab,
                        uint32_t* __restrict__ keys, int* __restrict__ vals,
                        int* __restrict__ ext) {
     long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -40,10 +41,10 @@ __global__ void k_keys(const float* __restrict__ alpha, const float* __restrict_
         k = find_image_by_gauss(tab, i);
         if (k >= 0) {
             const DevImg& im = tab.img[k];
-            float mx = mu[2 * i], my = mu[2 * i + 1];
-            if (gaussian_valid(alpha[i], mx, my, sigma[2 * i], sigma[2 * i + 1], rho[i],
-                               color[3 * i], color[3 * i + 1], color[3 * i + 2])) {
-                Rect r = support_rect(mx, my, sigma[2 * i], sigma[2 * i + 1], im);
+            float mx = ldf(mu[2 * i]), my = ldf(mu[2 * i + 1]);
+            if (gaussian_valid(ldf(alpha[i]), mx, my, ldf(sigma[2 * i]), ldf(sigma[2 * i + 1]), ldf(rho[i]),
+                               ldf(color[3 * i]), ldf(color[3 * i + 1]), ldf(color[3 * i + 2]))) {
+                Rect r = support_rect(mx, my, ldf(sigma[2 * i]), ldf(sigma[2 * i + 1]), im);
                 if (r.nonempty) {
                     // key: cell of the unclipped support origin (>= the window origin, so
                     // inside the window-sized cell domain)
@@ -237,9 +238,10 @@ __global__ void k_cell_start(const uint32_t* __restrict__ keys, long long n, int
 }
 
 // ---- K1b: records in sorted order ---------------------------------------------------------
-__global__ void k_records(const float* __restrict__ alpha, const float* __restrict__ mu,
-                          const float* __restrict__ sigma, const float* __restrict__ rho,
-                          const float* __restrict__ color, long long n, ImgTable tab,
+template <class T>
+__global__ void k_records(const T* __restrict__ alpha, const T* __restrict__ mu,
+                          const T* __restrict__ sigma, const T* __restrict__ rho,
+                          const T* __restrict__ color, long long n, ImgTable tab,
                           const uint32_t* __restrict__ keys, const int* __restrict__ perm,
                           float4* __restrict__ rec, int4* __restrict__ rects) {
     long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -248,11 +250,11 @@ __global__ void k_records(const float* __restrict__ alpha, const float* __restri
     long long i = perm[p];
     int k = find_image_by_gauss(tab, i);
     const DevImg& im = tab.img[k];
-    float mxf = mu[2 * i], myf = mu[2 * i + 1];
+    float mxf = ldf(mu[2 * i]), myf = ldf(mu[2 * i + 1]);
     Rect r = window_rect(mxf, myf, im);
-    Rect sr = support_rect(mxf, myf, sigma[2 * i], sigma[2 * i + 1], im);
+    Rect sr = support_rect(mxf, myf, ldf(sigma[2 * i]), ldf(sigma[2 * i + 1]), im);
     double mx = mxf, my = myf;
-    double sx = sigma[2 * i], sy = sigma[2 * i + 1], rh = rho[i], al = alpha[i];
+    double sx = ldf(sigma[2 * i]), sy = ldf(sigma[2 * i + 1]), rh = ldf(rho[i]), al = ldf(alpha[i]);
     double D = (1.0 - rh) * (1.0 + rh);
     // exponent in factored form (no cancellation):
     //   q = -Q/2 log2 e = -(w'^2 + v'^2),  w' = a1 dx + b1 dy,  v' = c1 dy
@@ -268,10 +270,10 @@ __global__ void k_records(const float* __restrict__ alpha, const float* __restri
     const float a1f = (float)a1;
     const float Df = a1f * im.invsx, d2 = Df * Df;
     float4 r0 = make_float4((float)(-axd), (float)ayd, (float)dly, Df);
-    float4 r1 = make_float4((float)(-a1 * dlx), (float)b1, (float)c1, (float)(w * color[3 * i]));
+    float4 r1 = make_float4((float)(-a1 * dlx), (float)b1, (float)c1, (float)(w * ldf(color[3 * i])));
     unsigned xs = (unsigned)r.x0 | ((unsigned)r.x1 << 16);
     unsigned ys = (unsigned)r.y0 | ((unsigned)r.y1 << 16);
-    float4 r2 = make_float4((float)(w * color[3 * i + 1]), (float)(w * color[3 * i + 2]),
+    float4 r2 = make_float4((float)(w * ldf(color[3 * i + 1])), (float)(w * ldf(color[3 * i + 2])),
                             __uint_as_float(xs), __uint_as_float(ys));
     // r3: the forward's exponential-recurrence constants G_t = 2^(-D^2 t^2), t = 1..3, and the
     // flag "recurrence allowed" (D <= FWD_REC_DMAX, render_fwd.cu MODE 2)
@@ -289,9 +291,10 @@ __global__ void k_records(const float* __restrict__ alpha, const float* __restri
 }
 
 // ---- pair count ---------------------------------------------------------------------------
-__global__ void k_pair_count(const float* __restrict__ alpha, const float* __restrict__ mu,
-                             const float* __restrict__ sigma, const float* __restrict__ rho,
-                             const float* __restrict__ color, long long n, ImgTable tab,
+template <class T>
+__global__ void k_pair_count(const T* __restrict__ alpha, const T* __restrict__ mu,
+                             const T* __restrict__ sigma, const T* __restrict__ rho,
+                             const T* __restrict__ color, long long n, ImgTable tab,
                              bool support, unsigned long long* __restrict__ out) {
     long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     unsigned long long v = 0;
@@ -299,10 +302,10 @@ __global__ void k_pair_count(const float* __restrict__ alpha, const float* __res
         int k = find_image_by_gauss(tab, i);
         if (k >= 0) {
             const DevImg& im = tab.img[k];
-            float mx = mu[2 * i], my = mu[2 * i + 1];
-            if (gaussian_valid(alpha[i], mx, my, sigma[2 * i], sigma[2 * i + 1], rho[i],
-                               color[3 * i], color[3 * i + 1], color[3 * i + 2])) {
-                Rect r = support ? support_rect(mx, my, sigma[2 * i], sigma[2 * i + 1], im)
+            float mx = ldf(mu[2 * i]), my = ldf(mu[2 * i + 1]);
+            if (gaussian_valid(ldf(alpha[i]), mx, my, ldf(sigma[2 * i]), ldf(sigma[2 * i + 1]), ldf(rho[i]),
+                               ldf(color[3 * i]), ldf(color[3 * i + 1]), ldf(color[3 * i + 2]))) {
+                Rect r = support ? support_rect(mx, my, ldf(sigma[2 * i]), ldf(sigma[2 * i + 1]), im)
                                  : window_rect(mx, my, im);
                 if (r.nonempty)
                     v = (unsigned long long)(r.x1 - r.x0 + 1) * (unsigned long long)(r.y1 - r.y0 + 1);
@@ -324,10 +327,10 @@ __global__ void k_debug_rects(const float* __restrict__ alpha, const float* __re
     int k = find_image_by_gauss(tab, i);
     if (k >= 0) {
         const DevImg& im = tab.img[k];
-        float mx = mu[2 * i], my = mu[2 * i + 1];
-        if (gaussian_valid(alpha[i], mx, my, sigma[2 * i], sigma[2 * i + 1], rho[i],
-                           color[3 * i], color[3 * i + 1], color[3 * i + 2])) {
-            Rect r = support ? support_rect(mx, my, sigma[2 * i], sigma[2 * i + 1], im)
+        float mx = ldf(mu[2 * i]), my = ldf(mu[2 * i + 1]);
+        if (gaussian_valid(ldf(alpha[i]), mx, my, ldf(sigma[2 * i]), ldf(sigma[2 * i + 1]), ldf(rho[i]),
+                           ldf(color[3 * i]), ldf(color[3 * i + 1]), ldf(color[3 * i + 2]))) {
+            Rect r = support ? support_rect(mx, my, ldf(sigma[2 * i]), ldf(sigma[2 * i + 1]), im)
                              : window_rect(mx, my, im);
             if (r.nonempty) o = make_int4(r.x0, r.x1, r.y0, r.y1);
         }
@@ -427,8 +430,9 @@ cudaError_t exclusive_scan_i32(const int* in, int* out, long long n, int* tmp, c
     return cudaGetLastError();
 }
 
-cudaError_t bin_gaussians(const float* alpha, const float* mu, const float* sigma,
-                          const float* rho, const float* color, long long n,
+template <class T>
+cudaError_t bin_gaussians_t(const T* alpha, const T* mu, const T* sigma, const T* rho,
+                            const T* color, long long n,
                           const ImgTable& tab, Workspace& ws, int** perm_out,
                           uint32_t** keys_sorted_out, cudaStream_t st) {
     cudaMemsetAsync(ws.ext, 0, sizeof(int) * 2 * MAX_IMAGES, st);
@@ -478,15 +482,36 @@ void binned_pointers(const ImgTable& tab, long long n, const Workspace& ws, int*
     *keys_sorted = odd ? ws.keys_b : ws.keys_a;
 }
 
-cudaError_t launch_pair_count(const float* alpha, const float* mu, const float* sigma,
-                              const float* rho, const float* color, long long n,
+cudaError_t bin_gaussians(const void* alpha, const void* mu, const void* sigma, const void* rho,
+                          const void* color, long long n, const ImgTable& tab, Workspace& ws,
+                          int** perm_out, uint32_t** keys_sorted_out, cudaStream_t st) {
+    if (tab.params_bf16) {
+        using B = __nv_bfloat16;
+        return bin_gaussians_t((const B*)alpha, (const B*)mu, (const B*)sigma, (const B*)rho,
+                               (const B*)color, n, tab, ws, perm_out, keys_sorted_out, st);
+    }
+    return bin_gaussians_t((const float*)alpha, (const float*)mu, (const float*)sigma,
+                           (const float*)rho, (const float*)color, n, tab, ws, perm_out,
+                           keys_sorted_out, st);
+}
+
+cudaError_t launch_pair_count(const void* alpha, const void* mu, const void* sigma,
+                              const void* rho, const void* color, long long n,
                               const ImgTable& tab, bool support, long long* d_pairs,
                               cudaStream_t st) {
     cudaMemsetAsync(d_pairs, 0, sizeof(long long), st);
     if (n > 0) {
         count_launches(1);
-        k_pair_count<<<grid1d(n, 256), 256, 0, st>>>(alpha, mu, sigma, rho, color, n, tab,
-                                                     support, (unsigned long long*)d_pairs);
+        if (tab.params_bf16) {
+            using B = __nv_bfloat16;
+            k_pair_count<B><<<grid1d(n, 256), 256, 0, st>>>(
+                (const B*)alpha, (const B*)mu, (const B*)sigma, (const B*)rho, (const B*)color, n,
+                tab, support, (unsigned long long*)d_pairs);
+        } else {
+            k_pair_count<float><<<grid1d(n, 256), 256, 0, st>>>(
+                (const float*)alpha, (const float*)mu, (const float*)sigma, (const float*)rho,
+                (const float*)color, n, tab, support, (unsigned long long*)d_pairs);
+        }
     }
     return cudaGetLastError();
 }

@@ -64,12 +64,14 @@ inline int ceil_div(long long a, long long b) { return (int)((a + b - 1) / b); }
 
 // Builds the per-image table; returns GSR_EINVAL on any host-checkable argument error.
 gsr_status build_table(const gsr_image* imgs, int32_t n_imgs, int64_t n_total, double ratio,
-                       ImgTable* tab) {
+                       ImgTable* tab, uint32_t flags = 0u) {
     if (!imgs || n_imgs < 1 || n_imgs > GSR_MAX_IMAGES) return GSR_EINVAL;
     if (n_total < 0 || n_total >= (1LL << 31)) return GSR_EINVAL;
     if (!std::isfinite(ratio) || !(ratio > 0.0) || ratio > 1.0) return GSR_EINVAL;
     std::memset(tab, 0, sizeof(*tab));
     tab->n_imgs = n_imgs;
+    tab->params_bf16 = (flags & GSR_PARAMS_BF16) ? 1 : 0;
+    const int io = ((flags & GSR_OUT_BF16) ? IO_BF16 : 0) | ((flags & GSR_OUT_CHW) ? IO_CHW : 0);
     // forward configuration: small tiles when every window is narrow
     double max_win = 0.0;
     for (int k = 0; k < n_imgs; ++k) {
@@ -109,6 +111,7 @@ gsr_status build_table(const gsr_image* imgs, int32_t n_imgs, int64_t n_total, d
         int rb = g.row_begin, re = g.row_end < 0 ? d.Hs : g.row_end;
         if (rb < 0 || re > d.Hs || rb > re) return GSR_EINVAL;
         d.row_begin = rb; d.row_end = re;
+        d.io = io;
         // bounds on the unclipped rect extent: width <= 2 s r W + 1 (+ fp64 rounding)
         d.wmax = (int)std::ceil(2.0 * sx * d.hx) + 2;
         d.hmax = (int)std::ceil(2.0 * sy * d.hy) + 2;
@@ -146,7 +149,7 @@ gsr_image single(int64_t n, int32_t h, int32_t w, double s) {
     return g;
 }
 
-bool params_ok(const float* a, const float* m, const float* s, const float* r, const float* c,
+bool params_ok(const void* a, const void* m, const void* s, const void* r, const void* c,
                int64_t n) {
     return n == 0 || (a && m && s && r && c);
 }
@@ -167,11 +170,11 @@ struct Prepared {
     uint32_t* keys = nullptr;
 };
 
-gsr_status prepare(const float* alpha, const float* mu, const float* sigma, const float* rho,
-                   const float* color, int64_t n_total, const gsr_image* imgs, int32_t n_imgs,
+gsr_status prepare(const void* alpha, const void* mu, const void* sigma, const void* rho,
+                   const void* color, int64_t n_total, const gsr_image* imgs, int32_t n_imgs,
                    double ratio, void* workspace, size_t workspace_bytes, cudaStream_t st,
-                   Prepared* P, bool bin) {
-    gsr_status s = build_table(imgs, n_imgs, n_total, ratio, &P->tab);
+                   Prepared* P, bool bin, uint32_t flags = 0u) {
+    gsr_status s = build_table(imgs, n_imgs, n_total, ratio, &P->tab, flags);
     if (s != GSR_OK) return s;
     if (!params_ok(alpha, mu, sigma, rho, color, n_total)) return GSR_EINVAL;
     if (!workspace || workspace_bytes < ws_bytes(P->tab, n_total)) return GSR_EWORKSPACE;
@@ -253,17 +256,27 @@ size_t gsr_workspace_bytes(int64_t n, int32_t lr_h, int32_t lr_w, double scale, 
     return gsr_workspace_bytes_batched(&g, 1, n, ratio);
 }
 
+gsr_status gsr_render_fwd_batched_ex(const void* alpha, const void* mu, const void* sigma,
+                                     const void* rho, const void* color, int64_t n_total,
+                                     const gsr_image* imgs, int32_t n_imgs, double ratio,
+                                     void* out, void* workspace, size_t workspace_bytes,
+                                     uint32_t flags, void* stream) {
+    if (!out) return GSR_EINVAL;
+    if (flags & ~(GSR_OUT_BF16 | GSR_OUT_CHW | GSR_PARAMS_BF16)) return GSR_EINVAL;
+    cudaStream_t st = (cudaStream_t)stream;
+    Prepared P;
+    gsr_status s = prepare(alpha, mu, sigma, rho, color, n_total, imgs, n_imgs, ratio, workspace,
+                           workspace_bytes, st, &P, true, flags);
+    if (s != GSR_OK) return s;
+    return finish(launch_render_fwd(P.tab, P.ws, (float*)out, st));
+}
+
 gsr_status gsr_render_fwd_batched(const float* alpha, const float* mu, const float* sigma,
                                   const float* rho, const float* color, int64_t n_total,
                                   const gsr_image* imgs, int32_t n_imgs, double ratio, float* out,
                                   void* workspace, size_t workspace_bytes, void* stream) {
-    if (!out) return GSR_EINVAL;
-    cudaStream_t st = (cudaStream_t)stream;
-    Prepared P;
-    gsr_status s = prepare(alpha, mu, sigma, rho, color, n_total, imgs, n_imgs, ratio, workspace,
-                           workspace_bytes, st, &P, true);
-    if (s != GSR_OK) return s;
-    return finish(launch_render_fwd(P.tab, P.ws, out, st));
+    return gsr_render_fwd_batched_ex(alpha, mu, sigma, rho, color, n_total, imgs, n_imgs, ratio,
+                                     out, workspace, workspace_bytes, 0u, stream);
 }
 
 gsr_status gsr_render_fwd(const float* alpha, const float* mu, const float* sigma,
@@ -275,21 +288,23 @@ gsr_status gsr_render_fwd(const float* alpha, const float* mu, const float* sigm
                                   workspace_bytes, stream);
 }
 
-gsr_status gsr_render_bwd_moments_batched_ex(const float* alpha, const float* mu,
-                                             const float* sigma, const float* rho,
-                                             const float* color, int64_t n_total,
+gsr_status gsr_render_bwd_moments_batched_ex(const void* alpha, const void* mu,
+                                             const void* sigma, const void* rho,
+                                             const void* color, int64_t n_total,
                                              const gsr_image* imgs, int32_t n_imgs, double ratio,
-                                             const float* grad_out, double* moments,
+                                             const void* grad_out, double* moments,
                                              void* workspace, size_t workspace_bytes,
                                              uint32_t flags, void* stream) {
     if (!grad_out || (!moments && n_total > 0)) return GSR_EINVAL;
-    if (flags & ~GSR_REUSE_BINNING) return GSR_EINVAL;
+    if (flags & ~(GSR_REUSE_BINNING | GSR_OUT_BF16 | GSR_OUT_CHW | GSR_PARAMS_BF16))
+        return GSR_EINVAL;
     cudaStream_t st = (cudaStream_t)stream;
     Prepared P;
     gsr_status s = prepare(alpha, mu, sigma, rho, color, n_total, imgs, n_imgs, ratio, workspace,
-                           workspace_bytes, st, &P, !(flags & GSR_REUSE_BINNING));
+                           workspace_bytes, st, &P, !(flags & GSR_REUSE_BINNING), flags);
     if (s != GSR_OK) return s;
-    return finish(launch_render_bwd_moments(P.tab, P.ws, P.perm, grad_out, moments, st));
+    return finish(launch_render_bwd_moments(P.tab, P.ws, P.perm, (const float*)grad_out, moments,
+                                            st));
 }
 
 gsr_status gsr_render_bwd_moments_batched(const float* alpha, const float* mu, const float* sigma,
@@ -306,35 +321,48 @@ gsr_status gsr_finalize_grads(const float* alpha, const float* mu, const float* 
                               const float* rho, const float* color, int64_t n_total,
                               const double* moments, float* d_alpha, float* d_mu, float* d_sigma,
                               float* d_rho, float* d_color, void* stream) {
-    if (n_total < 0) return GSR_EINVAL;
+    return gsr_finalize_grads_ex(alpha, mu, sigma, rho, color, n_total, moments, d_alpha, d_mu,
+                                 d_sigma, d_rho, d_color, 0u, stream);
+}
+
+gsr_status gsr_finalize_grads_ex(const void* alpha, const void* mu, const void* sigma,
+                                 const void* rho, const void* color, int64_t n_total,
+                                 const double* moments, float* d_alpha, float* d_mu,
+                                 float* d_sigma, float* d_rho, float* d_color, uint32_t flags,
+                                 void* stream) {
+    if (n_total < 0 || (flags & ~GSR_PARAMS_BF16)) return GSR_EINVAL;
     if (n_total > 0 && (!params_ok(alpha, mu, sigma, rho, color, n_total) || !moments ||
                         !d_alpha || !d_mu || !d_sigma || !d_rho || !d_color))
         return GSR_EINVAL;
     return finish(launch_finalize(alpha, mu, sigma, rho, color, n_total, moments, d_alpha, d_mu,
-                                  d_sigma, d_rho, d_color, (cudaStream_t)stream));
+                                  d_sigma, d_rho, d_color, (cudaStream_t)stream, nullptr,
+                                  (flags & GSR_PARAMS_BF16) != 0));
 }
 
-gsr_status gsr_render_bwd_batched_ex(const float* alpha, const float* mu, const float* sigma,
-                                     const float* rho, const float* color, int64_t n_total,
+gsr_status gsr_render_bwd_batched_ex(const void* alpha, const void* mu, const void* sigma,
+                                     const void* rho, const void* color, int64_t n_total,
                                      const gsr_image* imgs, int32_t n_imgs, double ratio,
-                                     const float* grad_out, float* d_alpha, float* d_mu,
+                                     const void* grad_out, float* d_alpha, float* d_mu,
                                      float* d_sigma, float* d_rho, float* d_color,
                                      void* workspace, size_t workspace_bytes, uint32_t flags,
                                      void* stream) {
     if (!grad_out) return GSR_EINVAL;
-    if (flags & ~GSR_REUSE_BINNING) return GSR_EINVAL;
+    if (flags & ~(GSR_REUSE_BINNING | GSR_OUT_BF16 | GSR_OUT_CHW | GSR_PARAMS_BF16))
+        return GSR_EINVAL;
     if (n_total > 0 && (!d_alpha || !d_mu || !d_sigma || !d_rho || !d_color)) return GSR_EINVAL;
     cudaStream_t st = (cudaStream_t)stream;
     Prepared P;
     gsr_status s = prepare(alpha, mu, sigma, rho, color, n_total, imgs, n_imgs, ratio, workspace,
-                           workspace_bytes, st, &P, !(flags & GSR_REUSE_BINNING));
+                           workspace_bytes, st, &P, !(flags & GSR_REUSE_BINNING), flags);
     if (s != GSR_OK) return s;
     if (n_total == 0) return GSR_OK;
     cudaMemsetAsync(P.ws.moments, 0, sizeof(double) * 8 * (size_t)n_total, st);
-    cudaError_t e = launch_render_bwd_moments(P.tab, P.ws, P.perm, grad_out, P.ws.moments, st);
+    cudaError_t e = launch_render_bwd_moments(P.tab, P.ws, P.perm, (const float*)grad_out,
+                                              P.ws.moments, st);
     if (e != cudaSuccess) return GSR_ECUDA;
     return finish(launch_finalize(alpha, mu, sigma, rho, color, n_total, P.ws.moments, d_alpha,
-                                  d_mu, d_sigma, d_rho, d_color, st));
+                                  d_mu, d_sigma, d_rho, d_color, st, nullptr,
+                                  P.tab.params_bf16 != 0));
 }
 
 gsr_status gsr_render_bwd_batched(const float* alpha, const float* mu, const float* sigma,
@@ -430,15 +458,15 @@ gsr_status gsr_train_step_l1_batched(const float* raw_alpha, const float* offset
     return finish(cudaSuccess);
 }
 
-gsr_status gsr_pair_count_batched_ex(const float* alpha, const float* mu, const float* sigma,
-                                     const float* rho, const float* color, int64_t n_total,
+gsr_status gsr_pair_count_batched_ex(const void* alpha, const void* mu, const void* sigma,
+                                     const void* rho, const void* color, int64_t n_total,
                                      const gsr_image* imgs, int32_t n_imgs, double ratio,
                                      uint32_t flags, int64_t* d_pairs, void* workspace,
                                      size_t workspace_bytes, void* stream) {
-    if (!d_pairs || (flags & ~GSR_SUPPORT)) return GSR_EINVAL;
+    if (!d_pairs || (flags & ~(GSR_SUPPORT | GSR_PARAMS_BF16))) return GSR_EINVAL;
     Prepared P;
     gsr_status s = prepare(alpha, mu, sigma, rho, color, n_total, imgs, n_imgs, ratio, workspace,
-                           workspace_bytes, (cudaStream_t)stream, &P, false);
+                           workspace_bytes, (cudaStream_t)stream, &P, false, flags);
     if (s != GSR_OK) return s;
     return finish(launch_pair_count(alpha, mu, sigma, rho, color, n_total, P.tab,
                                     (flags & GSR_SUPPORT) != 0, (long long*)d_pairs,

@@ -8,6 +8,7 @@
 //   moments     float64[n][8], original Gaussian order (backward only).
 #pragma once
 #include <cstdint>
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 namespace gsr {
@@ -82,7 +83,11 @@ struct DevImg {
     int ntx, nty, tile_base;  // backward tiles (TILE_W x TILE_H) of this image
     int fntx, fnty, ftile_base;  // forward tiles (ImgTable::ftile_w x ftile_h)
     int wmax, hmax;           // upper bounds on the unclipped rect width/height
+    int io;                   // image I/O format of out / grad_out (IO_BF16 | IO_CHW; 0 = fp32 HWC)
 };
+
+constexpr int IO_BF16 = 1;    // GSR_OUT_BF16: image elements are bfloat16 (RNE on store)
+constexpr int IO_CHW = 2;     // GSR_OUT_CHW: planar blocks, element (k, y, x) at k*rows*Ws + (y-rb)*Ws + x
 
 struct ImgTable {
     int n_imgs;
@@ -91,6 +96,7 @@ struct ImgTable {
     int total_ftiles;         // forward tiles
     int ftile_w, ftile_h;     // forward tile of this call (large or small configuration)
     int fwd_small;            // 1: FwdCfgSmall
+    int params_bf16;          // GSR_PARAMS_BF16: the five parameter arrays are bfloat16
     DevImg img[MAX_IMAGES];
 };
 
@@ -204,6 +210,26 @@ __device__ __forceinline__ Rect support_rect(float mux, float muy, float sxf, fl
     r.nonempty = r.nonempty && r.x0 <= r.x1 && r.y0 <= r.y1 && !isnan(lx) && !isnan(ux) &&
                  !isnan(ly) && !isnan(uy);
     return r;
+}
+
+// parameter element -> float (GSR_PARAMS_BF16: bfloat16 widened exactly)
+__device__ __forceinline__ float ldf(float v) { return v; }
+__device__ __forceinline__ float ldf(__nv_bfloat16 v) { return __bfloat162float(v); }
+
+// ---- image I/O formats (NEXT-4): index and element access of out / grad_out ----------------
+__device__ __forceinline__ long long img_index(const DevImg& im, int y, int x, int k) {
+    const long long r = y - im.row_begin;
+    return (im.io & IO_CHW) ? im.out_off + (long long)k * (im.row_end - im.row_begin) * im.Ws +
+                                  r * im.Ws + x
+                            : im.out_off + (r * im.Ws + x) * 3 + k;
+}
+__device__ __forceinline__ void img_store(void* out, const DevImg& im, long long off, float v) {
+    if (im.io & IO_BF16) ((__nv_bfloat16*)out)[off] = __float2bfloat16_rn(v);
+    else ((float*)out)[off] = v;
+}
+__device__ __forceinline__ float img_load(const void* p, const DevImg& im, long long off) {
+    return (im.io & IO_BF16) ? __bfloat162float(((const __nv_bfloat16*)p)[off])
+                             : ((const float*)p)[off];
 }
 
 __device__ __forceinline__ bool gaussian_valid(float a, float mx, float my, float sx, float sy,
@@ -346,15 +372,16 @@ size_t binning_bytes(long long n, int total_cells, int total_tiles);
 void carve_workspace(void* base, long long n, int total_cells, int total_tiles, Workspace* ws);
 // Runs K1 (keys) + stable radix sort + cell starts + K1b (records). Returns sorted perm in
 // *perm_out (points into ws).
-cudaError_t bin_gaussians(const float* alpha, const float* mu, const float* sigma,
-                          const float* rho, const float* color, long long n,
+// Parameter arrays are float32, or bfloat16 when tab.params_bf16 (GSR_PARAMS_BF16).
+cudaError_t bin_gaussians(const void* alpha, const void* mu, const void* sigma,
+                          const void* rho, const void* color, long long n,
                           const ImgTable& tab, Workspace& ws, int** perm_out,
                           uint32_t** keys_sorted_out, cudaStream_t st);
 // Where a previous bin_gaussians() on the same table left perm / sorted keys in the workspace.
 void binned_pointers(const ImgTable& tab, long long n, const Workspace& ws, int** perm,
                      uint32_t** keys_sorted);
-cudaError_t launch_pair_count(const float* alpha, const float* mu, const float* sigma,
-                              const float* rho, const float* color, long long n,
+cudaError_t launch_pair_count(const void* alpha, const void* mu, const void* sigma,
+                              const void* rho, const void* color, long long n,
                               const ImgTable& tab, bool support, long long* d_pairs,
                               cudaStream_t st);
 cudaError_t launch_debug_rects(const float* alpha, const float* mu, const float* sigma,
@@ -382,11 +409,11 @@ struct RawParams {
     const float* raw_alpha; const float* raw_sigma; const float* raw_rho; const float* raw_color;
     float rho_scale;
 };
-cudaError_t launch_finalize(const float* alpha, const float* mu, const float* sigma,
-                            const float* rho, const float* color, long long n,
+cudaError_t launch_finalize(const void* alpha, const void* mu, const void* sigma,
+                            const void* rho, const void* color, long long n,
                             const double* moments, float* d_alpha, float* d_mu, float* d_sigma,
                             float* d_rho, float* d_color, cudaStream_t st,
-                            const RawParams* raw = nullptr);
+                            const RawParams* raw = nullptr, bool params_bf16 = false);
 // train.cu
 cudaError_t launch_activate(const float* raw_alpha, const float* offset, const float* ref,
                             const float* raw_sigma, const float* raw_rho, const float* raw_color,

@@ -221,9 +221,12 @@ __global__ void __launch_bounds__(BWD_THREADS) k_render_bwd(
                     const float d = img[ro + 3 * x + k] - gt[ro + 3 * x + k];
                     v[k] = d > 0.f ? inv_numel : (d < 0.f ? -inv_numel : 0.f);
                 }
-            } else {
+            } else if (im.io == 0) {
                 const float* g = grad_out + ro;
                 for (int k = 0; k < nv; ++k) v[k] = g[3 * x + k];
+            } else {                           // NEXT-4 image formats (bf16 and/or planar CHW)
+                for (int k = 0; k < nv; ++k)
+                    v[k] = img_load(grad_out, im, img_index(im, y, x + k / 3, k % 3));
             }
         }
         gA[ry][cp] = make_float4(v[0], v[3], v[1], v[4]);
@@ -430,9 +433,10 @@ __global__ void __launch_bounds__(BWD_THREADS) k_render_bwd(
     if (qn > 0) flush(qn);
 }
 
-__global__ void k_finalize(const float* __restrict__ alpha, const float* __restrict__ mu,
-                           const float* __restrict__ sigma, const float* __restrict__ rho,
-                           const float* __restrict__ color, long long n,
+template <class T>
+__global__ void k_finalize(const T* __restrict__ alpha, const T* __restrict__ mu,
+                           const T* __restrict__ sigma, const T* __restrict__ rho,
+                           const T* __restrict__ color, long long n,
                            const double* __restrict__ moments, float* __restrict__ d_alpha,
                            float* __restrict__ d_mu, float* __restrict__ d_sigma,
                            float* __restrict__ d_rho, float* __restrict__ d_color, RawParams raw,
@@ -440,11 +444,11 @@ __global__ void k_finalize(const float* __restrict__ alpha, const float* __restr
     long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     float o[9] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-    if (gaussian_valid(alpha[i], mu[2 * i], mu[2 * i + 1], sigma[2 * i], sigma[2 * i + 1], rho[i],
-                       color[3 * i], color[3 * i + 1], color[3 * i + 2])) {
+    if (gaussian_valid(ldf(alpha[i]), ldf(mu[2 * i]), ldf(mu[2 * i + 1]), ldf(sigma[2 * i]), ldf(sigma[2 * i + 1]), ldf(rho[i]),
+                       ldf(color[3 * i]), ldf(color[3 * i + 1]), ldf(color[3 * i + 2]))) {
         const double* m = moments + 8 * i;
-        double sx = sigma[2 * i], sy = sigma[2 * i + 1], rh = rho[i], al = alpha[i];
-        double c0 = color[3 * i], c1 = color[3 * i + 1], c2 = color[3 * i + 2];
+        double sx = ldf(sigma[2 * i]), sy = ldf(sigma[2 * i + 1]), rh = ldf(rho[i]), al = ldf(alpha[i]);
+        double c0 = ldf(color[3 * i]), c1 = ldf(color[3 * i + 1]), c2 = ldf(color[3 * i + 2]);
         double D = (1.0 - rh) * (1.0 + rh);
         double K = 1.0 / (TWO_PI * sx * sy * sqrt(D));
         double kp = sqrt(HALF_LOG2E / D), kv = sqrt(HALF_LOG2E);
@@ -505,18 +509,27 @@ cudaError_t launch_render_bwd_moments(const ImgTable& tab, const Workspace& ws, 
     return cudaGetLastError();
 }
 
-cudaError_t launch_finalize(const float* alpha, const float* mu, const float* sigma,
-                            const float* rho, const float* color, long long n,
+cudaError_t launch_finalize(const void* alpha, const void* mu, const void* sigma,
+                            const void* rho, const void* color, long long n,
                             const double* moments, float* d_alpha, float* d_mu, float* d_sigma,
-                            float* d_rho, float* d_color, cudaStream_t st, const RawParams* raw) {
+                            float* d_rho, float* d_color, cudaStream_t st, const RawParams* raw,
+                            bool params_bf16) {
     if (n <= 0) return cudaSuccess;
     count_launches(1);
     int h = prof_begin(3, st);
-    k_finalize<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(alpha, mu, sigma, rho, color, n,
-                                                            moments, d_alpha, d_mu, d_sigma,
-                                                            d_rho, d_color,
-                                                            raw ? *raw : RawParams{},
-                                                            raw ? 1 : 0);
+    const unsigned grid = (unsigned)((n + 255) / 256);
+    const RawParams rp = raw ? *raw : RawParams{};
+    if (params_bf16) {
+        using B = __nv_bfloat16;
+        k_finalize<B><<<grid, 256, 0, st>>>((const B*)alpha, (const B*)mu, (const B*)sigma,
+                                            (const B*)rho, (const B*)color, n, moments, d_alpha,
+                                            d_mu, d_sigma, d_rho, d_color, rp, raw ? 1 : 0);
+    } else {
+        k_finalize<float><<<grid, 256, 0, st>>>((const float*)alpha, (const float*)mu,
+                                                (const float*)sigma, (const float*)rho,
+                                                (const float*)color, n, moments, d_alpha, d_mu,
+                                                d_sigma, d_rho, d_color, rp, raw ? 1 : 0);
+    }
     prof_end(h, st);
     return cudaGetLastError();
 }

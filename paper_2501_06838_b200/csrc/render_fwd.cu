@@ -259,6 +259,12 @@ __device__ __forceinline__ void fwd_epilogue(float2 (*tot)[FwdSmem<CFG>::NACC][3
     float l1 = 0.f;     // fused L1 loss (NEXT-1): sum |I - I_gt| over the stored elements
     auto store = [&](int y, int x, float R, float G, float B) {
         if (y >= im.row_end || x >= im.Ws) return;
+        if (!LOSS && im.io != 0) {     // NEXT-4 image formats (bf16 and/or planar CHW)
+            img_store(out, im, img_index(im, y, x, 0), R);
+            img_store(out, im, img_index(im, y, x, 1), G);
+            img_store(out, im, img_index(im, y, x, 2), B);
+            return;
+        }
         const long long off = im.out_off + ((long long)(y - im.row_begin) * im.Ws + x) * 3;
         out[off] = R; out[off + 1] = G; out[off + 2] = B;
         if (LOSS) l1 += fabsf(R - gt[off]) + fabsf(G - gt[off + 1]) + fabsf(B - gt[off + 2]);

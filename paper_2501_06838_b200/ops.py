@@ -23,11 +23,12 @@ def _stream_ptr(device) -> int:
     return torch.cuda.current_stream(device).cuda_stream
 
 
-def _check_param(t: torch.Tensor, name: str, n: Optional[int] = None) -> torch.Tensor:
+def _check_param(t: torch.Tensor, name: str, n: Optional[int] = None,
+                 dtypes=(torch.float32,)) -> torch.Tensor:
     if not isinstance(t, torch.Tensor) or not t.is_cuda:
         raise TypeError(f"{name} must be a CUDA tensor (no CPU fallback)")
-    if t.dtype != torch.float32:
-        raise TypeError(f"{name} must be float32, got {t.dtype}")
+    if t.dtype not in dtypes:
+        raise TypeError(f"{name} must be one of {dtypes}, got {t.dtype}")
     t = t.contiguous()
     w = WIDTH.get(name, None)
     if w is not None:
@@ -38,14 +39,34 @@ def _check_param(t: torch.Tensor, name: str, n: Optional[int] = None) -> torch.T
     return t
 
 
+_FLOATS = (torch.float32, torch.bfloat16)
+
+
 def _params(alpha, mu, sigma, rho, color):
+    """Checked parameter tensors: float32, or all bfloat16 (GSR_PARAMS_BF16, NEXT-4)."""
     n = alpha.shape[0] if isinstance(alpha, torch.Tensor) else None
-    ts = [_check_param(t, k, n) for t, k in zip((alpha, mu, sigma, rho, color), PARAMS)]
+    ts = [_check_param(t, k, n, _FLOATS) for t, k in zip((alpha, mu, sigma, rho, color), PARAMS)]
     dev = ts[0].device
     for t in ts:
         if t.device != dev:
             raise ValueError("all parameters must live on the same device")
+        if t.dtype != ts[0].dtype:
+            raise TypeError("all parameters must have the same dtype")
     return ts, n
+
+
+def _fmt_flags(params, image: Optional[torch.Tensor] = None, out_dtype=None,
+               chw: bool = False) -> int:
+    """GSR_* data-format flags (include/gsr.h, NEXT-4) of a call."""
+    f = _lib.GSR_PARAMS_BF16 if params[0].dtype == torch.bfloat16 else 0
+    dt = out_dtype if out_dtype is not None else (image.dtype if image is not None else None)
+    if dt == torch.bfloat16:
+        f |= _lib.GSR_OUT_BF16
+    elif dt is not None and dt != torch.float32:
+        raise TypeError(f"image dtype must be float32 or bfloat16, got {dt}")
+    if chw:
+        f |= _lib.GSR_OUT_CHW
+    return f
 
 
 def _ptr(t: torch.Tensor, offset_elems: int = 0) -> int:
@@ -75,11 +96,13 @@ class Layout:
     out_off: List[int]                   # float offsets into the flat output
     out_numel: int
 
-    def view(self, flat: torch.Tensor, k: int) -> torch.Tensor:
+    def view(self, flat: torch.Tensor, k: int, chw: bool = False) -> torch.Tensor:
+        """Image k's block of a flat output: [rows, Ws, 3] (HWC) or [3, rows, Ws] (chw)."""
         rb, re = self.rows[k]
         Ws = self.dims[k][1]
         o = self.out_off[k]
-        return flat[o:o + (re - rb) * Ws * 3].view(re - rb, Ws, 3)
+        blk = flat[o:o + (re - rb) * Ws * 3]
+        return blk.view(3, re - rb, Ws) if chw else blk.view(re - rb, Ws, 3)
 
 
 def layout(images: Sequence[Image]) -> Layout:
@@ -163,39 +186,48 @@ def _ws_for(dev, nb, workspace):
 
 def render_fwd_batched(alpha, mu, sigma, rho, color, lay: Layout, ratio: float = 0.1,
                        out: Optional[torch.Tensor] = None,
-                       workspace: Optional[torch.Tensor] = None) -> torch.Tensor:
-    """Forward render of every image of `lay` into one flat float32 buffer (HWC blocks)."""
-    (alpha, mu, sigma, rho, color), n = _params(alpha, mu, sigma, rho, color)
+                       workspace: Optional[torch.Tensor] = None,
+                       out_dtype: Optional[torch.dtype] = None, chw: bool = False) -> torch.Tensor:
+    """Forward render of every image of `lay` into one flat buffer: float32 HWC blocks by
+    default; out_dtype=torch.bfloat16 and/or chw=True select the NEXT-4 formats (GSR_OUT_BF16,
+    GSR_OUT_CHW); bfloat16 parameters are read as such (GSR_PARAMS_BF16)."""
+    params, n = _params(alpha, mu, sigma, rho, color)
+    alpha, mu, sigma, rho, color = params
     dev = alpha.device
     if out is None:
-        out = torch.empty(lay.out_numel, dtype=torch.float32, device=dev)
+        out = torch.empty(lay.out_numel, dtype=out_dtype or torch.float32, device=dev)
+    flags = _fmt_flags(params, out, chw=chw)
     lib = _lib.load()
     st = _stream_ptr(dev)
     for g0, g1, o0, arr, m in _chunks(lay):
         nb = _ws_bytes(arr, m, g1 - g0, ratio)
         ws = _ws_for(dev, nb, workspace)
-        check(lib.gsr_render_fwd_batched(_ptr(alpha, g0), _ptr(mu, 2 * g0), _ptr(sigma, 2 * g0),
-                                         _ptr(rho, g0), _ptr(color, 3 * g0), g1 - g0, arr, m,
-                                         float(ratio), _ptr(out, o0), ws.data_ptr(), ws.numel(),
-                                         st), "gsr_render_fwd_batched")
+        check(lib.gsr_render_fwd_batched_ex(_ptr(alpha, g0), _ptr(mu, 2 * g0),
+                                            _ptr(sigma, 2 * g0), _ptr(rho, g0),
+                                            _ptr(color, 3 * g0), g1 - g0, arr, m, float(ratio),
+                                            _ptr(out, o0), ws.data_ptr(), ws.numel(), flags, st),
+              "gsr_render_fwd_batched_ex")
     return out
 
 
 def render_bwd_moments_batched(alpha, mu, sigma, rho, color, lay: Layout, grad_out: torch.Tensor,
                                moments: torch.Tensor, ratio: float = 0.1,
                                workspace: Optional[torch.Tensor] = None,
-                               reuse_binning: bool = False) -> torch.Tensor:
+                               reuse_binning: bool = False, chw: bool = False) -> torch.Tensor:
     """Accumulate (+=) the backward moments [n, 8] (float64) of every image band of `lay`.
-    reuse_binning: `workspace` holds this layout's binning from the preceding forward."""
-    (alpha, mu, sigma, rho, color), n = _params(alpha, mu, sigma, rho, color)
+    reuse_binning: `workspace` holds this layout's binning from the preceding forward.
+    grad_out float32 or bfloat16, HWC or (chw=True) planar blocks."""
+    params, n = _params(alpha, mu, sigma, rho, color)
+    alpha, mu, sigma, rho, color = params
     dev = alpha.device
-    grad_out = _check_param(grad_out, "grad_out")
+    grad_out = _check_param(grad_out, "grad_out", dtypes=_FLOATS)
     if moments.dtype != torch.float64 or not moments.is_contiguous() or moments.numel() != 8 * n:
         raise ValueError("moments must be a contiguous float64 [n, 8] tensor")
     lib = _lib.load()
     st = _stream_ptr(dev)
     flags = _lib.GSR_REUSE_BINNING if (reuse_binning and workspace is not None and
                                        single_chunk(lay)) else 0
+    flags |= _fmt_flags(params, grad_out, chw=chw)
     for g0, g1, o0, arr, m in _chunks(lay):
         nb = _ws_bytes(arr, m, g1 - g0, ratio)
         ws = _ws_for(dev, nb, workspace)
@@ -208,29 +240,32 @@ def render_bwd_moments_batched(alpha, mu, sigma, rho, color, lay: Layout, grad_o
 
 
 def finalize_grads(alpha, mu, sigma, rho, color, moments: torch.Tensor):
-    """Moments [n, 8] (float64) -> (d_alpha, d_mu, d_sigma, d_rho, d_color)."""
-    (alpha, mu, sigma, rho, color), n = _params(alpha, mu, sigma, rho, color)
-    dev = alpha.device
-    grads = [torch.empty_like(t) for t in (alpha, mu, sigma, rho, color)]
-    check(_lib.load().gsr_finalize_grads(*[_ptr(t) for t in (alpha, mu, sigma, rho, color)], n,
-                                         _ptr(moments), *[_ptr(g) for g in grads],
-                                         _stream_ptr(dev)), "gsr_finalize_grads")
+    """Moments [n, 8] (float64) -> (d_alpha, d_mu, d_sigma, d_rho, d_color) (float32)."""
+    params, n = _params(alpha, mu, sigma, rho, color)
+    dev = params[0].device
+    grads = [torch.empty(t.shape, dtype=torch.float32, device=dev) for t in params]
+    check(_lib.load().gsr_finalize_grads_ex(*[_ptr(t) for t in params], n, _ptr(moments),
+                                            *[_ptr(g) for g in grads], _fmt_flags(params),
+                                            _stream_ptr(dev)), "gsr_finalize_grads_ex")
     return tuple(grads)
 
 
 def render_bwd_batched(alpha, mu, sigma, rho, color, lay: Layout, grad_out: torch.Tensor,
                        ratio: float = 0.1, workspace: Optional[torch.Tensor] = None,
-                       reuse_binning: bool = False):
+                       reuse_binning: bool = False, chw: bool = False):
     """Gradients of sum(grad_out * I) wrt every parameter (float32, input layouts).
-    reuse_binning: `workspace` holds this layout's binning from the preceding forward."""
-    (alpha, mu, sigma, rho, color), n = _params(alpha, mu, sigma, rho, color)
+    reuse_binning: `workspace` holds this layout's binning from the preceding forward.
+    grad_out float32 or bfloat16, HWC or (chw=True) planar blocks."""
+    params, n = _params(alpha, mu, sigma, rho, color)
+    alpha, mu, sigma, rho, color = params
     dev = alpha.device
-    grad_out = _check_param(grad_out, "grad_out")
-    grads = [torch.zeros_like(t) for t in (alpha, mu, sigma, rho, color)]
+    grad_out = _check_param(grad_out, "grad_out", dtypes=_FLOATS)
+    grads = [torch.zeros(t.shape, dtype=torch.float32, device=dev) for t in params]
     lib = _lib.load()
     st = _stream_ptr(dev)
     flags = _lib.GSR_REUSE_BINNING if (reuse_binning and workspace is not None and
                                        single_chunk(lay)) else 0
+    flags |= _fmt_flags(params, grad_out, chw=chw)
     for g0, g1, o0, arr, m in _chunks(lay):
         nb = _ws_bytes(arr, m, g1 - g0, ratio)
         ws = _ws_for(dev, nb, workspace)
@@ -247,7 +282,8 @@ def pair_count(alpha, mu, sigma, rho, color, lay: Layout, ratio: float = 0.1,
                support: bool = False) -> int:
     """P = number of (Gaussian, pixel) pairs inside the windows (synchronises). support=True:
     the pairs inside the support rects, i.e. the pairs the kernels evaluate (reading R21)."""
-    (alpha, mu, sigma, rho, color), n = _params(alpha, mu, sigma, rho, color)
+    params, n = _params(alpha, mu, sigma, rho, color)
+    alpha, mu, sigma, rho, color = params
     dev = alpha.device
     lib = _lib.load()
     st = _stream_ptr(dev)
@@ -259,7 +295,8 @@ def pair_count(alpha, mu, sigma, rho, color, lay: Layout, ratio: float = 0.1,
         check(lib.gsr_pair_count_batched_ex(_ptr(alpha, g0), _ptr(mu, 2 * g0),
                                             _ptr(sigma, 2 * g0), _ptr(rho, g0),
                                             _ptr(color, 3 * g0), g1 - g0, arr, m, float(ratio),
-                                            _lib.GSR_SUPPORT if support else 0, tmp.data_ptr(),
+                                            (_lib.GSR_SUPPORT if support else 0) |
+                                            _fmt_flags(params), tmp.data_ptr(),
                                             ws.data_ptr(), ws.numel(), st),
               "gsr_pair_count_batched_ex")
         total += tmp
@@ -297,21 +334,24 @@ class _RenderFn(torch.autograd.Function):
     (GSR_REUSE_BINNING) -- valid because autograd saves the very same parameter tensors."""
 
     @staticmethod
-    def forward(ctx, alpha, mu, sigma, rho, color, lay, ratio):
-        ctx.lay, ctx.ratio = lay, ratio
+    def forward(ctx, alpha, mu, sigma, rho, color, lay, ratio, out_dtype=None, chw=False):
+        ctx.lay, ctx.ratio, ctx.chw = lay, ratio, chw
         ctx.save_for_backward(alpha, mu, sigma, rho, color)
         ws = workspace_for(alpha, lay, ratio) if single_chunk(lay) else None
         ctx.ws = ws
         return render_fwd_batched(alpha.detach(), mu.detach(), sigma.detach(), rho.detach(),
-                                  color.detach(), lay, ratio, workspace=ws)
+                                  color.detach(), lay, ratio, workspace=ws, out_dtype=out_dtype,
+                                  chw=chw)
 
     @staticmethod
     def backward(ctx, g):
         alpha, mu, sigma, rho, color = ctx.saved_tensors
+        # float32 gradients; autograd casts them to the dtype of bfloat16 inputs
         grads = render_bwd_batched(alpha, mu, sigma, rho, color, ctx.lay, g.contiguous(),
-                                   ctx.ratio, workspace=ctx.ws, reuse_binning=ctx.ws is not None)
+                                   ctx.ratio, workspace=ctx.ws, reuse_binning=ctx.ws is not None,
+                                   chw=ctx.chw)
         ctx.ws = None
-        return (*grads, None, None)
+        return (*grads, None, None, None, None)
 
 
 def render_batch(alpha, mu, sigma, rho, color, images: Sequence[Tuple[int, int, float]],
@@ -329,11 +369,14 @@ def render_batch(alpha, mu, sigma, rho, color, images: Sequence[Tuple[int, int, 
 
 
 def render(alpha, mu, sigma, rho, color, H: int, W: int, scale: float,
-           ratio: float = 0.1) -> torch.Tensor:
-    """I_SR = Eq. 4 / Alg. 1 as a differentiable op: [floor(sH), floor(sW), 3] float32."""
+           ratio: float = 0.1, out_dtype: Optional[torch.dtype] = None,
+           chw: bool = False) -> torch.Tensor:
+    """I_SR = Eq. 4 / Alg. 1 as a differentiable op: [floor(s_y H), floor(s_x W), 3] float32
+    (scale = s or (s_x, s_y)); out_dtype=torch.bfloat16 and chw=True ([3, Hs, Ws]) select the
+    NEXT-4 formats; float32 or bfloat16 parameters."""
     lay = _single(alpha.shape[0], H, W, scale)
-    flat = _RenderFn.apply(alpha, mu, sigma, rho, color, lay, float(ratio))
-    return lay.view(flat, 0)
+    flat = _RenderFn.apply(alpha, mu, sigma, rho, color, lay, float(ratio), out_dtype, chw)
+    return lay.view(flat, 0, chw=chw)
 
 
 # ------------------------------------------------------------------ NEXT-1: fused training step

@@ -112,6 +112,18 @@ def test_einval_before_any_launch(lib):
     assert lib.gsr_render_fwd_batched(*ps, 10, imgs, 1, 0.1, dummy, dummy, 1 << 30, None) == 1
     assert lib.gsr_workspace_bytes_batched(_lib.images_array([(4, 4, 2.0, 0, 5, 0, 0, 12, 3.0)]),
                                            1, 10, 0.1) > 0
+    # data-format flags (NEXT-4): unknown bits and flags an entry point does not take
+    imgs = _lib.images_array([(4, 4, 2.0, 0, 5, 0, 0, -1)])
+    for fl in (_lib.GSR_REUSE_BINNING, _lib.GSR_SUPPORT, 0x40, 0x80000000):
+        assert lib.gsr_render_fwd_batched_ex(*ps, 10, imgs, 1, 0.1, dummy, dummy, 1 << 30, fl,
+                                             None) == 1, fl
+    for fl in (_lib.GSR_SUPPORT, 0x40):
+        assert lib.gsr_render_bwd_batched_ex(*ps, 10, imgs, 1, 0.1, dummy, *ps, dummy, 1 << 30,
+                                             fl, None) == 1, fl
+    for fl in (_lib.GSR_OUT_BF16, _lib.GSR_OUT_CHW, _lib.GSR_REUSE_BINNING):
+        assert lib.gsr_finalize_grads_ex(*ps, 10, dummy, *ps, fl, None) == 1, fl
+    assert lib.gsr_render_fwd_batched_ex(*ps, 10, imgs, 1, 0.1, None, dummy, 1 << 30,
+                                         _lib.GSR_OUT_BF16, None) == 1
     many = _lib.images_array([(4, 4, 2.0, 0, 0, 0, 0, -1)] * 65)
     assert lib.gsr_render_fwd_batched(*ps, 10, many, 65, 0.1, dummy, dummy, 1 << 30, None) == 1
     assert lib.gsr_finalize_grads(*ps, -1, dummy, *ps, None) == 1
