@@ -7,8 +7,9 @@ One step = one pass of the whole hot path over one batch: binning (K1 + radix so
 forward render (K4), backward pair pass (K5) and finalize (K6), for every image of the workload
 (default C5 = BASELINE.json configs[4]: 64 DIV2K-size 255x170 LR images at x8 -> 2040x1360,
 the configuration the metric "... at 1/2/4/8 B200" is quoted on). Under torchrun (N > 1) every
-rank renders a pair-balanced HR row band of every image, then the output bands are all-gathered
-and the backward moments all-reduced over NCCL (paper_2501_06838_b200/dist.py).
+rank renders a pair-balanced HR row band of every image; the output bands are all-gathered over
+NCCL (overlapped with the backward) and the gradients of the seam Gaussians -- support spanning a
+band boundary -- are sum-reduced in one compact buffer (paper_2501_06838_b200/dist.py).
 
 Rank 0 prints ONE JSON line. value = HR Mpix/s of the whole job (fwd+bwd: output pixels of the
 batch per step / step time); gpairs_per_s = (Gaussian, pixel) pairs of the windows resolved per
@@ -291,6 +292,15 @@ def main():
         band_imgs = [gsr.Image(H, W, s, int(offs[k]), counts[k], bounds[k][rank],
                                bounds[k][rank + 1]) for k, (H, W, s) in enumerate(imgs)]
     lay = gsr.layout(band_imgs)
+    # seam set: Gaussians whose support rows span a band boundary -- the only ones
+    # whose gradients are exchanged (dist.reduce_seam); identical on every rank
+    seam_idx = None
+    if world > 1 and not by_image:
+        seam = np.concatenate([
+            gdist.seam_mask(host["mu"][offs[k]:offs[k + 1]], host["sigma"][offs[k]:offs[k + 1]],
+                            np.ones(counts[k], bool), H, W, s, RATIO, bounds[k])
+            for k, (H, W, s) in enumerate(imgs)])
+        seam_idx = torch.from_numpy(np.nonzero(seam)[0].astype(np.int64)).to(dev)
     full_pix = sum(h * w for h, w in dims)
     # P (the paper's work unit): pairs inside the windows; P_eval: pairs inside the support rects,
     # the pairs the kernels evaluate (reading R21; outside them every term is exactly 0 in fp32)
@@ -313,15 +323,17 @@ def main():
     def step():
         # one binning per step: the backward reuses the forward's (GSR_REUSE_BINNING)
         out = gsr.render_fwd_batched(*params, lay, RATIO, workspace=step_ws)
-        gathered = out
-        if world > 1 and not by_image:
-            gathered = gdist.gather_bands(out, gdist.rank_numels(bounds, widths3, world))
+        gathered, work = out, None
+        if world > 1 and not by_image:      # on NCCL's stream, overlapped with the backward
+            gathered, work = gdist.gather_bands(out, gdist.rank_numels(bounds, widths3, world),
+                                                async_op=True)
         moments = torch.zeros((n, 8), dtype=torch.float64, device=dev)
         gsr.render_bwd_moments_batched(*params, lay, g_band, moments, RATIO, workspace=step_ws,
                                        reuse_binning=step_ws is not None)
-        if world > 1 and not by_image:
-            gdist.reduce_moments(moments)
-        grads = gsr.finalize_grads(*params, moments)
+        grads = gsr.finalize_grads(*params, moments)    # linear in the moments: band partials
+        if work is not None:
+            gdist.reduce_seam(grads, seam_idx)          # sum the seam Gaussians' partials
+            work.wait()
         return gathered, grads
 
     def barrier():
@@ -375,9 +387,9 @@ def main():
             mom = torch.zeros((n, 8), dtype=torch.float64, device=dev)
             gsr.render_bwd_moments_batched(*dp, lay, dg, mom, RATIO, workspace=step_ws,
                                            reuse_binning=step_ws is not None)
-            if world > 1 and not by_image:
-                gdist.reduce_moments(mom)
             gr = gsr.finalize_grads(*dp, mom)
+            if world > 1 and not by_image:
+                gdist.reduce_seam(gr, seam_idx)
             h_out.copy_(out, non_blocking=True)
             for h, d in zip(h_grads, gr):
                 h.copy_(d, non_blocking=True)
@@ -467,6 +479,7 @@ def main():
                        "pairs_evaluated_per_pass": P_total_eval,
                        "parallelism": (f"{args.partition} x{world}" if world > 1
                                        else "single GPU"),
+                       "seam_gaussians": int(seam_idx.numel()) if seam_idx is not None else 0,
                        "l2": "working set > 126 MB L2 (params 1.6 GB, image 2.1 GB); no flush"},
             "gpairs_per_s": 2 * P_total / (ms_step * 1e-3) / 1e9,
             "gpairs_evaluated_per_s": 2 * P_total_eval / (ms_step * 1e-3) / 1e9,

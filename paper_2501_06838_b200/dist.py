@@ -9,9 +9,16 @@ per-row pair counts (the work unit), not the row counts.
 Exchange steps (the only collectives):
   forward : all-gather of the output bands (each rank's bands padded to the largest) -> every
             rank holds every band, `assemble_image` views/copies out a full image;
-  backward: every rank accumulates the pair moments [n, 8] (float64) of its bands; Gaussians
-            whose window spans a seam have partial moments on several ranks, so the moments are
-            sum-reduced (all-reduce) before the closed-form finalize (gsr_finalize_grads).
+  backward: every rank accumulates the pair moments [n, 8] (float64) of its bands and
+            finalizes them locally (the closed forms of gsr_finalize_grads are linear in the
+            moments, so a band's gradient is the finalize of its moments). Only SEAM Gaussians --
+            support rect (R21) spanning a band boundary -- have partial gradients on several
+            ranks; they are packed into one compact [n_seam, 9] buffer and sum-reduced
+            (`reduce_seam`). Afterwards rank r holds the final gradient of every Gaussian its
+            band sees (its halo) and 0 for the others; `reduce_seam(full=True)` all-reduces every
+            gradient instead when each rank needs all of them.
+  overlap : the output all-gather is issued asynchronously right after the forward and runs on
+            NCCL's stream while the backward computes (waited for at the end of the step).
 
 The band renderer is injected (`render_band` / `moments_band` / `finalize`), so this host logic
 is tested on CPU with gloo and a CPU stand-in, and runs on B200 with the CUDA path.
@@ -63,6 +70,53 @@ def row_pair_counts(mu: np.ndarray, valid: np.ndarray, H: int, W: int, s: float,
     return np.cumsum(d[:-1])
 
 
+def support_rows(mu: np.ndarray, sigma: np.ndarray, valid: np.ndarray, H: int, W: int, s: float,
+                 ratio: float, s_y: float | None = None):
+    """Clipped HR row range [y0, y1] of every Gaussian's support rect (R2 window cut to the R21
+    box, fp64 in the kernels' operation order); ok = the rect is non-empty."""
+    sy = s if not s_y else s_y
+    Hs, Ws = out_size(H, sy), out_size(W, s)
+    mx = mu[:, 0].astype(np.float64)
+    my = mu[:, 1].astype(np.float64)
+    lim = float(2 ** 30)
+    with np.errstate(invalid="ignore"):
+        x0 = np.floor(np.clip(s * (mx - ratio * W), -lim, lim)) + 1
+        x1 = np.ceil(np.clip(s * (mx + ratio * W), -lim, lim)) - 1
+        y0 = np.floor(np.clip(sy * (my - ratio * H), -lim, lim)) + 1
+        y1 = np.ceil(np.clip(sy * (my + ratio * H), -lim, lim)) - 1
+        tx = SUPPORT_SIGMAS * sigma[:, 0].astype(np.float64)
+        ty = SUPPORT_SIGMAS * sigma[:, 1].astype(np.float64)
+        x0 = np.maximum(x0, np.floor(np.clip(s * (mx - tx), -lim, lim)))
+        x1 = np.minimum(x1, np.ceil(np.clip(s * (mx + tx), -lim, lim)))
+        y0 = np.maximum(y0, np.floor(np.clip(sy * (my - ty), -lim, lim)))
+        y1 = np.minimum(y1, np.ceil(np.clip(sy * (my + ty), -lim, lim)))
+        x0 = np.maximum(x0, 0); x1 = np.minimum(x1, Ws - 1)
+        y0 = np.maximum(y0, 0); y1 = np.minimum(y1, Hs - 1)
+        ok = valid & (x0 <= x1) & (y0 <= y1)
+    return np.where(ok, y0, 0).astype(np.int64), np.where(ok, y1, -1).astype(np.int64), ok
+
+
+def seam_mask(mu: np.ndarray, sigma: np.ndarray, valid: np.ndarray, H: int, W: int, s: float,
+              ratio: float, bounds: Sequence[int], margin: int = 1,
+              s_y: float | None = None) -> np.ndarray:
+    """Gaussians of one image whose support rows meet more than one band of `bounds` (the seam
+    set of SURVEY 8(e)). Conservative: the rows are widened by `margin` -- a Gaussian wrongly
+    marked as a seam only costs buffer space (its partials are complete on one rank, 0 on the
+    others); a seam Gaussian marked interior would lose gradient."""
+    y0, y1, ok = support_rows(mu, sigma, valid, H, W, s, ratio, s_y)
+    b = np.asarray(bounds, np.int64)
+    first = np.searchsorted(b, y0 - margin, side="right") - 1
+    last = np.searchsorted(b, y1 + margin, side="right") - 1
+    return ok & (first < last)
+
+
+def halo_mask(mu: np.ndarray, sigma: np.ndarray, valid: np.ndarray, H: int, W: int, s: float,
+              ratio: float, rows, s_y: float | None = None) -> np.ndarray:
+    """Gaussians of one image whose support rows meet HR rows [rows[0], rows[1]) (exact)."""
+    y0, y1, ok = support_rows(mu, sigma, valid, H, W, s, ratio, s_y)
+    return ok & (y1 >= rows[0]) & (y0 < rows[1])
+
+
 def plan_bands(row_counts: np.ndarray, G: int) -> List[int]:
     """Boundaries b_0 = 0 <= ... <= b_G = Hs splitting the rows into G contiguous bands of
     (nearly) equal pair count; every band gets at least one row when Hs >= G."""
@@ -102,8 +156,9 @@ def rank_numels(bounds: Sequence[Sequence[int]], widths3: Sequence[int], world: 
     return [sum((b[r + 1] - b[r]) * w3 for b, w3 in zip(bounds, widths3)) for r in range(world)]
 
 
-def gather_bands(out, numels: Sequence[int], group=None):
-    """All-gather every rank's flat band buffer, padded to the largest: -> [world, max]."""
+def gather_bands(out, numels: Sequence[int], group=None, async_op: bool = False):
+    """All-gather every rank's flat band buffer, padded to the largest: -> [world, max]
+    (async_op: -> ([world, max], work); the buffer is valid after work.wait())."""
     import torch
     import torch.distributed as dist
     world = len(numels)
@@ -113,10 +168,12 @@ def gather_bands(out, numels: Sequence[int], group=None):
     recv = out.new_empty(world * mx)
     if send.is_cuda and dist.get_backend(group) == "gloo":
         # gloo (the 1-GPU functional check of bench.py) gathers CUDA tensors as a list
-        dist.all_gather(list(recv.view(world, mx).unbind(0)), send.contiguous(), group=group)
+        work = dist.all_gather(list(recv.view(world, mx).unbind(0)), send.contiguous(),
+                               group=group, async_op=async_op)
     else:
-        dist.all_gather_into_tensor(recv, send.contiguous(), group=group)
-    return recv.view(world, mx)
+        work = dist.all_gather_into_tensor(recv, send.contiguous(), group=group,
+                                           async_op=async_op)
+    return (recv.view(world, mx), work) if async_op else recv.view(world, mx)
 
 
 def assemble_image(gathered, bounds: Sequence[Sequence[int]], widths3: Sequence[int], k: int):
@@ -132,27 +189,58 @@ def assemble_image(gathered, bounds: Sequence[Sequence[int]], widths3: Sequence[
 
 
 def reduce_moments(moments, group=None):
-    """Seam reduce: sum the per-rank partial moments [n, 8] (float64) in place."""
+    """Sum the per-rank partial moments [n, 8] (float64) of every Gaussian in place (the
+    uncompacted exchange; `reduce_seam` moves only the seam Gaussians' gradients)."""
     import torch.distributed as dist
     dist.all_reduce(moments, op=dist.ReduceOp.SUM, group=group)
     return moments
 
 
+def reduce_seam(grads, seam_idx, group=None, full: bool = False):
+    """Seam reduce of per-rank partial gradients: `grads` is one [n, k] tensor or a sequence of
+    [n] / [n, k] tensors (the finalize's d_alpha, d_mu, ...); the rows `seam_idx` (int64 tensor on
+    the same device, identical on every rank) are packed into one [n_seam, sum k] buffer,
+    all-reduced, and written back. full=True all-reduces every row instead."""
+    import torch
+    import torch.distributed as dist
+    ts = [grads] if isinstance(grads, torch.Tensor) else list(grads)
+    n = ts[0].shape[0]
+    cols = [t.view(n, -1) for t in ts]
+    if full:
+        for c in cols:
+            dist.all_reduce(c, op=dist.ReduceOp.SUM, group=group)
+        return grads
+    if seam_idx.numel() == 0:
+        return grads
+    buf = torch.cat([c.index_select(0, seam_idx) for c in cols], 1)
+    dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=group)
+    o = 0
+    for c in cols:
+        k = c.shape[1]
+        c.index_copy_(0, seam_idx, buf[:, o:o + k])
+        o += k
+    return grads
+
+
 def sharded_step(rank: int, world: int, bounds: Sequence[Sequence[int]], widths3: Sequence[int],
                  render_band: Callable, moments_band: Callable, finalize: Callable, n: int,
-                 device, group=None, moment_cols: int = 8):
+                 device, group=None, moment_cols: int = 8, seam_idx=None):
     """One fwd+bwd step of a batch under row-band sharding. render_band(rows) -> this rank's flat
     bands (images in order); moments_band(rows, moments) accumulates its band moments;
-    finalize(moments) -> gradients. Returns (gathered bands [world, max] or the local bands,
-    gradients)."""
+    finalize(moments) -> gradients (linear in the moments). seam_idx: the seam Gaussians
+    (`seam_mask`); None = all-reduce every gradient. Returns (gathered bands [world, max] or the
+    local bands, gradients)."""
     import torch
     rows = [(b[rank], b[rank + 1]) for b in bounds]
     out = render_band(rows)
-    gathered = out
-    if world > 1:
-        gathered = gather_bands(out, rank_numels(bounds, widths3, world), group)
+    gathered, work = out, None
+    if world > 1:                      # overlapped with the backward below
+        gathered, work = gather_bands(out, rank_numels(bounds, widths3, world), group,
+                                      async_op=True)
     moments = torch.zeros((n, moment_cols), dtype=torch.float64, device=device)
     moments_band(rows, moments)
+    grads = finalize(moments)
     if world > 1:
-        reduce_moments(moments, group)
-    return gathered, finalize(moments)
+        reduce_seam(grads, seam_idx, group, full=seam_idx is None)
+        work.wait()
+    return gathered, grads

@@ -58,6 +58,28 @@ def _free_port():
     return p
 
 
+def test_support_rows_match_oracle_and_seams():
+    """support_rows reproduces the oracle's support rects (R21) row for row; the seam set is
+    exactly the Gaussians whose rows meet two bands (margin 0) and contains them (margin 1)."""
+    for (H, W, s, sv) in [(20, 25, 3.0, None), (9, 14, 8.0, None), (12, 10, 4.0, 2.5)]:
+        c = S.gaussians(H, W, seed=5, offset_range=1.5)
+        n = c["alpha"].shape[0]
+        valid = np.ones(n, bool)
+        y0, y1, ok = gd.support_rows(c["mu"], c["sigma"], valid, H, W, s, 0.1, s_y=sv)
+        R = O.rects(c, H, W, (s, sv) if sv else s, 0.1, support=True)
+        nonempty = (R[:, 2] <= R[:, 3]) & (R[:, 4] <= R[:, 5])
+        assert np.array_equal(ok, nonempty)
+        assert np.array_equal(y0[ok], R[ok, 4]) and np.array_equal(y1[ok], R[ok, 5])
+        Hs = O.out_dims(H, W, (s, sv) if sv else s)[0]
+        b = [0, Hs // 3, (2 * Hs) // 3 + 1, Hs]
+        exact = gd.seam_mask(c["mu"], c["sigma"], valid, H, W, s, 0.1, b, margin=0, s_y=sv)
+        bands = [gd.halo_mask(c["mu"], c["sigma"], valid, H, W, s, 0.1, (b[g], b[g + 1]), s_y=sv)
+                 for g in range(3)]
+        assert np.array_equal(exact, np.sum(bands, 0) >= 2)
+        wide = gd.seam_mask(c["mu"], c["sigma"], valid, H, W, s, 0.1, b, margin=1, s_y=sv)
+        assert not (exact & ~wide).any() and 0 < exact.sum() < n
+
+
 def _worker(rank, world, port, q):
     import torch
     import torch.distributed as dist
@@ -86,23 +108,42 @@ def _worker(rank, world, port, q):
             for k, ((H, W, s), c, (rb, re)) in enumerate(zip(imgs, clouds, rows)):
                 if re <= rb:
                     continue
-                d = O.render_bwd(c, H, W, s, 0.1, grads_full[k][rb:re], rows=(rb, re))
+                # support mode (R21): the pairs the kernels evaluate, so a Gaussian outside the
+                # band's support halo has exactly zero moments there
+                d = O.render_bwd(c, H, W, s, 0.1, grads_full[k][rb:re], rows=(rb, re),
+                                 mode="support")
                 blk = np.concatenate([d["alpha"][:, None], d["mu"], d["sigma"], d["rho"][:, None],
                                       d["color"]], 1)
                 mom[offs[k]:offs[k + 1]] += torch.from_numpy(blk)
 
-        gathered, grads = gd.sharded_step(rank, world, bounds, widths3, render_band, moments_band,
-                                          lambda m: m, n, "cpu", moment_cols=9)
-        ok = True
-        for k, ((H, W, s), c) in enumerate(zip(imgs, clouds)):
-            full = gd.assemble_image(gathered, bounds, widths3, k).numpy()
-            ref = O.render_fwd(c, H, W, s, 0.1).reshape(dims[k][0], -1)
-            ok &= bool(np.array_equal(full, ref))
-            d = O.render_bwd(c, H, W, s, 0.1, grads_full[k])
-            blk = np.concatenate([d["alpha"][:, None], d["mu"], d["sigma"], d["rho"][:, None],
-                                  d["color"]], 1)
-            ok &= bool(np.allclose(grads[offs[k]:offs[k + 1]].numpy(), blk, rtol=1e-12,
-                                   atol=1e-13))
+        seam = np.concatenate([gd.seam_mask(c["mu"], c["sigma"], np.ones(cn, bool), H, W, s,
+                                            0.1, b)
+                               for (H, W, s), c, cn, b in zip(imgs, clouds, counts, bounds)])
+        halo = np.concatenate([gd.halo_mask(c["mu"], c["sigma"], np.ones(cn, bool), H, W, s, 0.1,
+                                            (b[rank], b[rank + 1]))
+                               for (H, W, s), c, cn, b in zip(imgs, clouds, counts, bounds)])
+        ok = bool(0 < seam.sum() < n)
+        for seam_idx in (torch.from_numpy(np.nonzero(seam)[0]), None):
+            gathered, grads = gd.sharded_step(rank, world, bounds, widths3, render_band,
+                                              moments_band, lambda m: m, n, "cpu", moment_cols=9,
+                                              seam_idx=seam_idx)
+            for k, ((H, W, s), c) in enumerate(zip(imgs, clouds)):
+                full = gd.assemble_image(gathered, bounds, widths3, k).numpy()
+                ref = O.render_fwd(c, H, W, s, 0.1).reshape(dims[k][0], -1)
+                ok &= bool(np.array_equal(full, ref))
+                d = O.render_bwd(c, H, W, s, 0.1, grads_full[k], mode="support")
+                blk = np.concatenate([d["alpha"][:, None], d["mu"], d["sigma"],
+                                      d["rho"][:, None], d["color"]], 1)
+                got = grads[offs[k]:offs[k + 1]].numpy()
+                # seam reduce: final gradients for the rank's halo (and every seam Gaussian),
+                # 0 elsewhere; full: all
+                sel = halo[offs[k]:offs[k + 1]] if seam_idx is not None else slice(None)
+                ok &= bool(np.allclose(got[sel], blk[sel], rtol=1e-12, atol=1e-13))
+                if seam_idx is not None:      # neither in the halo nor reduced: untouched zeros
+                    rest = ~(halo | seam)[offs[k]:offs[k + 1]]
+                    ok &= bool(rest.any() and not got[rest].any())
+                    both = (halo | seam)[offs[k]:offs[k + 1]]
+                    ok &= bool(np.allclose(got[both], blk[both], rtol=1e-12, atol=1e-13))
         q.put((rank, ok))
     finally:
         dist.destroy_process_group()

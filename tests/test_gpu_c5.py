@@ -48,3 +48,50 @@ def test_c5_full_size_sampled():
         sel = torch.from_numpy(offs[k] + idx).cuda()
         got = {kk: grads[kk][sel].cpu().numpy().astype(np.float64) for kk in KEYS}
         assert_bwd_close(got, want, want["absmass"])
+
+
+def test_band_partials_and_seam_set():
+    """The row-band exchange of dist.py on the CUDA path, emulated in one process (this run has
+    one GPU): G = 4 pair-balanced bands of a C5-geometry image; each band's moments are
+    finalized on their own (the finalize is linear in the moments); a Gaussian outside the seam
+    set has a nonzero partial in at most one band, where it equals the oracle's gradient; the
+    band partials summed over the seam set equal the whole-image gradients."""
+    import torch
+    import paper_2501_06838_b200 as gsr
+    from paper_2501_06838_b200 import dist as gd
+    H, W, s, G = 60, 90, 8.0, 4
+    c = S.gaussians(H, W, seed=77)
+    n = c["alpha"].shape[0]
+    dev = [torch.from_numpy(c[k]).cuda() for k in KEYS]
+    valid = np.ones(n, bool)
+    rc = gd.row_pair_counts(c["mu"], valid, H, W, s, 0.1, sigma=c["sigma"])
+    b = gd.plan_bands(rc, G)
+    seam = gd.seam_mask(c["mu"], c["sigma"], valid, H, W, s, 0.1, b)
+    assert 0 < seam.sum() < n
+    Hs, Ws = O.out_dims(H, W, s)
+    g = torch.from_numpy(S.grad_out((Hs, Ws, 3), seed=78)).cuda()
+    parts = []
+    for r in range(G):
+        lay = gsr.layout([gsr.Image(H, W, s, 0, n, b[r], b[r + 1])])
+        mom = torch.zeros((n, 8), dtype=torch.float64, device="cuda")
+        gsr.render_bwd_moments_batched(*dev, lay, g[b[r]:b[r + 1]].reshape(-1).contiguous(),
+                                       mom, 0.1)
+        gr = gsr.finalize_grads(*dev, mom)
+        parts.append(np.concatenate([t.view(n, -1).cpu().numpy() for t in gr], 1)
+                     .astype(np.float64))
+    P = np.stack(parts)                                     # [G, n, 9]
+    nz = (P != 0).any(2).sum(0)                             # bands with a nonzero partial
+    assert (nz[~seam] <= 1).all()
+    full_lay = gsr.layout([gsr.Image(H, W, s, 0, n)])
+    full = np.concatenate([t.view(n, -1).cpu().numpy() for t in
+                           gsr.render_bwd_batched(*dev, full_lay, g.reshape(-1), 0.1)], 1)
+    tot = P.sum(0)
+    scale = np.abs(full).max(0, keepdims=True)
+    assert (np.abs(tot - full) <= 1e-5 * scale).all()
+    rng = np.random.default_rng(3)
+    idx = np.concatenate([rng.choice(np.nonzero(~seam)[0], 12, replace=False),
+                          rng.choice(np.nonzero(seam)[0], 12, replace=False)])
+    want = O.render_bwd(c, H, W, s, 0.1, g.cpu().numpy(), idx=idx, want_absmass=True)
+    got = tot[idx]
+    assert_bwd_close({"alpha": got[:, 0], "mu": got[:, 1:3], "sigma": got[:, 3:5],
+                      "rho": got[:, 5], "color": got[:, 6:9]}, want, want["absmass"])
