@@ -80,6 +80,28 @@ __device__ __forceinline__ float2 ld_dsmem_f2(const float2* local_addr, uint32_t
 
 __device__ __forceinline__ float2 f2(float a) { return make_float2(a, a); }
 
+// Column halves (GSR_FWD_HALVES, large configuration): lane l owns columns 4 (l & 3) + t and
+// 16 + 4 (l & 3) + t (t = 0..3) of its two rows, so anchor h = 0 of every lane lies in the
+// tile's left 16 columns and h = 1 in the right 16. A Gaussian whose support rect misses one
+// half skips that anchor warp-uniformly (flag bits from the filter): at C5 about a third of the
+// lane-pairs outside the supports of partly covered tiles are never evaluated.
+#ifndef GSR_FWD_PACC
+#define GSR_FWD_PACC 1
+#endif
+#ifndef GSR_FWD_HALVES
+#define GSR_FWD_HALVES 1
+#endif
+template <int STRIP>
+__device__ __forceinline__ constexpr bool use_halves() { return GSR_FWD_HALVES && STRIP == 8; }
+template <int STRIP>
+__device__ __forceinline__ constexpr int colx(int j) {   // tile column of the lane's slot j
+    return use_halves<STRIP>() ? (j & 3) + 16 * (j >> 2) : j;
+}
+template <int STRIP>
+__device__ __forceinline__ int lane_x0(int lane) {
+    return use_halves<STRIP>() ? 4 * (lane & 3) : STRIP * (lane & 3);
+}
+
 template <class CFG>
 struct FwdSmem {
     static constexpr int NACC = CFG::ROWS * (CFG::STRIP / 2) * 3;   // float2 accumulators/thread
@@ -159,10 +181,11 @@ __device__ __forceinline__ void fwd_gauss(const float4 r0, const float4 r1, cons
 //           2^q_a flushes to zero (q_a < -126) has q(kx_a + 3) < -67 (|w_a| > 11.2, D <= 1),
 //           i.e. only values below 2^-67 are lost; products never overflow (q <= 0 and
 //           D^2 t^2 <= 9). Error: the exponent of B^t carries t * 2 D |w_a| * 2^-24 relative.
-template <int MODE, int STRIP>
-__device__ __forceinline__ void fwd_gauss_r2(const float4 r0, const float4 r1, const float4 r2,
-                                             float g3, float xlf, float2 yrow, const int (&yi)[2],
-                                             int xl0, float invs, float2 (&acc)[3 * STRIP]) {
+template <int MODE, int STRIP, int HSEL = 3>
+__device__ __forceinline__ void fwd_gauss_r2h(const float4 r0, const float4 r1, const float4 r2,
+                                              float g3, float xlf, float2 yrow, const int (&yi)[2],
+                                              int xl0, float invs, float2 (&acc)[3 * STRIP]) {
+    constexpr int hmask = HSEL;
     const float D = r0.w;
     const float2 D2 = f2(D);
     const float kx0 = xlf + r0.x;                           // x - ax of column 0 (exact)
@@ -188,7 +211,8 @@ __device__ __forceinline__ void fwd_gauss_r2(const float4 r0, const float4 r1, c
         const float2 G1 = f2(r2.z), G2 = f2(r2.w), G3 = f2(g3), M2D = f2(-2.f * D);
 #pragma unroll
         for (int h = 0; h < STRIP / 4; ++h) {
-            const float2 w = __ffma2_rn(D2, f2(kx0 + 4.f * h), T);
+            if (use_halves<STRIP>() && !((hmask >> h) & 1)) continue;   // compile-time skip
+            const float2 w = __ffma2_rn(D2, f2(kx0 + (float)colx<STRIP>(4 * h)), T);
             const float2 q = __ffma2_rn(make_float2(-w.x, -w.y), w, U);
             float2 b = __fmul2_rn(w, M2D);
             b.x = fminf(b.x, 40.f);
@@ -213,12 +237,29 @@ __device__ __forceinline__ void fwd_gauss_r2(const float4 r0, const float4 r1, c
         }
 #pragma unroll
         for (int j = 0; j < STRIP; ++j) {
-            const float2 w = __ffma2_rn(D2, f2(kx0 + (float)j), T);
+            if (use_halves<STRIP>() && !((hmask >> (j >> 2)) & 1)) continue;
+            const int cj = colx<STRIP>(j);
+            const float2 w = __ffma2_rn(D2, f2(kx0 + (float)cj), T);
             float2 q = __ffma2_rn(make_float2(-w.x, -w.y), w, U);
-            if (MODE == 0 && !(xl0 + j >= x0 && xl0 + j <= x1)) q = f2(-INFINITY);
+            if (MODE == 0 && !(xl0 + cj >= x0 && xl0 + cj <= x1)) q = f2(-INFINITY);
             accum(j, make_float2(ex2_approx(q.x), ex2_approx(q.y)));
         }
     }
+}
+
+// hmask (column halves the support meets, GSR_FWD_HALVES): one of three compile-time variants,
+// so the evaluated anchors stay one fully unrolled, interleavable block
+template <int MODE, int STRIP>
+__device__ __forceinline__ void fwd_gauss_r2(const float4 r0, const float4 r1, const float4 r2,
+                                             float g3, float xlf, float2 yrow, const int (&yi)[2],
+                                             int xl0, float invs, float2 (&acc)[3 * STRIP],
+                                             int hmask = 3) {
+    if (use_halves<STRIP>() && hmask == 1)
+        fwd_gauss_r2h<MODE, STRIP, 1>(r0, r1, r2, g3, xlf, yrow, yi, xl0, invs, acc);
+    else if (use_halves<STRIP>() && hmask == 2)
+        fwd_gauss_r2h<MODE, STRIP, 2>(r0, r1, r2, g3, xlf, yrow, yi, xl0, invs, acc);
+    else
+        fwd_gauss_r2h<MODE, STRIP, 3>(r0, r1, r2, g3, xlf, yrow, yi, xl0, invs, acc);
 }
 
 // Sum the per-warp partial images in warp order (deterministic) into tot[0], reduce split-K
@@ -254,7 +295,7 @@ __device__ __forceinline__ void fwd_epilogue(float2 (*tot)[FwdSmem<CFG>::NACC][3
     }
     if (warp != 0) return;
 
-    const int xl0 = Tx0 + FWD_STRIP * (lane & 3);
+    const int xl0 = Tx0 + lane_x0<FWD_STRIP>(lane);
     const int yl0 = Ty0 + FWD_ROWS * (lane >> 2);
     float l1 = 0.f;     // fused L1 loss (NEXT-1): sum |I - I_gt| over the stored elements
     auto store = [&](int y, int x, float R, float G, float B) {
@@ -274,8 +315,8 @@ __device__ __forceinline__ void fwd_epilogue(float2 (*tot)[FwdSmem<CFG>::NACC][3
         for (int j = 0; j < FWD_STRIP; ++j) {
             const float2 R = sm.tot[0][3 * j][lane], G = sm.tot[0][3 * j + 1][lane],
                          B = sm.tot[0][3 * j + 2][lane];
-            store(yl0, xl0 + j, R.x, G.x, B.x);
-            store(yl0 + 1, xl0 + j, R.y, G.y, B.y);
+            store(yl0, xl0 + colx<FWD_STRIP>(j), R.x, G.x, B.x);
+            store(yl0 + 1, xl0 + colx<FWD_STRIP>(j), R.y, G.y, B.y);
         }
     } else {                           // acc pairs = two adjacent columns of one row
 #pragma unroll
@@ -429,7 +470,7 @@ __global__ void __launch_bounds__(FWD_THREADS) k_render_fwd(const ImgTable tab,
         }
     } else {
         // ---------------- consumer warps ------------------------------------------------------
-        const int xl0 = Tx0 + FWD_STRIP * (lane & 3);
+        const int xl0 = Tx0 + lane_x0<FWD_STRIP>(lane);
         const int yl0 = Ty0 + FWD_ROWS * (lane >> 2);
         float2 xj[FWD_STRIP / 2];
 #pragma unroll
@@ -542,7 +583,7 @@ __global__ void __launch_bounds__(FWD2_THREADS, GSR_FWD_MINB) k_render_fwd2(cons
     const float invs = im.invsy;     // rows: dy = (y - ay)/sy - dl_y
 
     // lane geometry (every warp covers the whole tile)
-    const int xl0 = Tx0 + FWD_STRIP * (lane & 3);
+    const int xl0 = Tx0 + lane_x0<FWD_STRIP>(lane);
     const int yl0 = Ty0 + FWD_ROWS * (lane >> 2);
     float2 xj[FWD_STRIP / 2];
 #pragma unroll
@@ -577,24 +618,36 @@ __global__ void __launch_bounds__(FWD2_THREADS, GSR_FWD_MINB) k_render_fwd2(cons
         if (lane < nb[j]) rb[j] = __ldg(rects + sb[j] + lane);
     };
 
+#if GSR_FWD_PACC
+    // experiment: one register accumulator per lane for the whole tile (no per-buffer folds)
+    float2 acc[NACC];
+#pragma unroll
+    for (int a = 0; a < NACC; ++a) acc[a] = make_float2(0.f, 0.f);
+#endif
     auto process = [&](int pbuf, int pcnt) {
+#if !GSR_FWD_PACC
         float2 acc[NACC];
 #pragma unroll
         for (int a = 0; a < NACC; ++a) acc[a] = make_float2(0.f, 0.f);
+#endif
         const float4* sr = &sm.rec[warp][pbuf][0];
         auto single = [&](int g) {
             const float4 r0 = sr[REC_F4 * g], r1 = sr[REC_F4 * g + 1], r2 = sr[REC_F4 * g + 2];
-            const bool full = sm.full[warp][pbuf][g] != 0;
+            const int fl = sm.full[warp][pbuf][g];
+            const bool full = (fl & 1) != 0;
+            const int hm = fl >> 1;
             if constexpr (FWD_ROWS == 2) {
                 if (full) {
                     const float4 r3 = sr[REC_F4 * g + 3];
                     if (r3.w != 0.f)
-                        fwd_gauss_r2<2, FWD_STRIP>(r0, r1, make_float4(r2.x, r2.y, r3.x, r3.y), r3.z, xlf,
-                                        yrow, yi, xl0, invs, acc);
+                        fwd_gauss_r2<2, FWD_STRIP>(r0, r1, make_float4(r2.x, r2.y, r3.x, r3.y),
+                                                   r3.z, xlf, yrow, yi, xl0, invs, acc, hm);
                     else
-                        fwd_gauss_r2<1, FWD_STRIP>(r0, r1, r2, 0.f, xlf, yrow, yi, xl0, invs, acc);
+                        fwd_gauss_r2<1, FWD_STRIP>(r0, r1, r2, 0.f, xlf, yrow, yi, xl0, invs, acc,
+                                                   hm);
                 } else {
-                    fwd_gauss_r2<0, FWD_STRIP>(r0, r1, r2, 0.f, xlf, yrow, yi, xl0, invs, acc);
+                    fwd_gauss_r2<0, FWD_STRIP>(r0, r1, r2, 0.f, xlf, yrow, yi, xl0, invs, acc,
+                                               hm);
                 }
             } else {
                 if (full)
@@ -611,16 +664,17 @@ __global__ void __launch_bounds__(FWD2_THREADS, GSR_FWD_MINB) k_render_fwd2(cons
                 // scheduler interleaves (the kernel is latency-bound at 4 warps per SMSP)
                 if (g + 1 < pcnt) {
                     const float4 a3 = sr[REC_F4 * g + 3], b3 = sr[REC_F4 * (g + 1) + 3];
-                    if (sm.full[warp][pbuf][g] != 0 && sm.full[warp][pbuf][g + 1] != 0 &&
+                    const int fa = sm.full[warp][pbuf][g], fb = sm.full[warp][pbuf][g + 1];
+                    if ((fa & 1) && (fb & 1) &&
                         a3.w != 0.f && b3.w != 0.f) {
                         const float4 a0 = sr[REC_F4 * g], a1 = sr[REC_F4 * g + 1],
                                      a2 = sr[REC_F4 * g + 2];
                         const float4 b0 = sr[REC_F4 * (g + 1)], b1 = sr[REC_F4 * (g + 1) + 1],
                                      b2 = sr[REC_F4 * (g + 1) + 2];
-                        fwd_gauss_r2<2, FWD_STRIP>(a0, a1, make_float4(a2.x, a2.y, a3.x, a3.y), a3.z, xlf,
-                                        yrow, yi, xl0, invs, acc);
-                        fwd_gauss_r2<2, FWD_STRIP>(b0, b1, make_float4(b2.x, b2.y, b3.x, b3.y), b3.z, xlf,
-                                        yrow, yi, xl0, invs, acc);
+                        fwd_gauss_r2<2, FWD_STRIP>(a0, a1, make_float4(a2.x, a2.y, a3.x, a3.y),
+                                                   a3.z, xlf, yrow, yi, xl0, invs, acc, fa >> 1);
+                        fwd_gauss_r2<2, FWD_STRIP>(b0, b1, make_float4(b2.x, b2.y, b3.x, b3.y),
+                                                   b3.z, xlf, yrow, yi, xl0, invs, acc, fb >> 1);
                         g += 2;
                         continue;
                     }
@@ -630,9 +684,11 @@ __global__ void __launch_bounds__(FWD2_THREADS, GSR_FWD_MINB) k_render_fwd2(cons
             single(g);
             ++g;
         }
+#if !GSR_FWD_PACC
 #pragma unroll
         for (int a = 0; a < NACC; ++a)
             sm.tot[warp][a][lane] = __fadd2_rn(sm.tot[warp][a][lane], acc[a]);
+#endif
     };
 
     fetch(0);
@@ -642,6 +698,7 @@ __global__ void __launch_bounds__(FWD2_THREADS, GSR_FWD_MINB) k_render_fwd2(cons
         const bool end = nb[0] == 0;
         if (!end) {
             bool keep = false, full = false;
+            int hb = 3;
             if (lane < nb[0]) {
                 const unsigned sxs = (unsigned)rb[0].x, sys = (unsigned)rb[0].y;
                 const int sx0 = (int)(sxs & 0xffffu), sx1 = (int)(sxs >> 16);
@@ -651,11 +708,14 @@ __global__ void __launch_bounds__(FWD2_THREADS, GSR_FWD_MINB) k_render_fwd2(cons
                 const int x0 = (int)(xs & 0xffffu), x1 = (int)(xs >> 16);
                 const int y0 = (int)(ys & 0xffffu), y1 = (int)(ys >> 16);
                 full = x0 <= fx0 && x1 >= fx1 && y0 <= fy0 && y1 >= fy0 + FTILE_H - 1;
+                // column halves the support meets (bit 0: left 16 columns, bit 1: right 16)
+                hb = use_halves<FWD_STRIP>()
+                         ? (sx0 <= fx0 + 15 ? 1 : 0) | (sx1 >= fx0 + 16 ? 2 : 0) : 3;
             }
             const unsigned m = __ballot_sync(0xffffffffu, keep);
             if (keep) {
                 const int slot = cnt + __popc(m & lt);
-                sm.full[warp][b][slot] = full ? 1 : 0;
+                sm.full[warp][b][slot] = (uint8_t)((full ? 1 : 0) | (hb << 1));
                 const float4* src = rec + (long long)REC_F4 * (sb[0] + lane);
                 float4* dst = &sm.rec[warp][b][REC_F4 * slot];
 #pragma unroll
@@ -684,6 +744,10 @@ __global__ void __launch_bounds__(FWD2_THREADS, GSR_FWD_MINB) k_render_fwd2(cons
         __syncwarp();
         process(b ^ 1, pend);
     }
+#if GSR_FWD_PACC
+#pragma unroll
+    for (int a = 0; a < NACC; ++a) sm.tot[warp][a][lane] = acc[a];
+#endif
     fwd_epilogue<KS, LOSS, CFG>(sm.tot, im, Tx0, Ty0, warp, lane, krank, out, gt, loss_acc);
 }
 
