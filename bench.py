@@ -228,7 +228,7 @@ def main():
     ap.add_argument("--workload", default="C5", choices=list(S.CONFIGS))
     ap.add_argument("--images", type=int, default=None, help="dev only: first N images")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--e2e-groups", type=int, default=8,
+    ap.add_argument("--e2e-groups", type=int, default=16,
                     help="image groups of the streamed host-memory step (e2e)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--partition", choices=["band", "image"], default="band",

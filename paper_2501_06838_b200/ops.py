@@ -487,7 +487,7 @@ class StreamedFwdBwd:
     device->host on another (B200's copy engines run both directions concurrently with the
     kernels). Each group is one binning + forward + backward (binning reused) + finalize.
 
-        step = StreamedFwdBwd(lay, ratio, groups=8)
+        step = StreamedFwdBwd(lay, ratio, groups=16)
         step(host_params, host_grad_out, host_out, host_grads)   # enqueued on the current stream
 
     host_params: (alpha, mu, sigma, rho, color) pinned float32 CPU tensors (n Gaussians);
@@ -495,7 +495,7 @@ class StreamedFwdBwd:
     shaped like host_params. The call returns after enqueueing; the current stream waits for all
     work (synchronize it, or record an event, before reading the host outputs)."""
 
-    def __init__(self, lay: Layout, ratio: float = 0.1, groups: int = 8, device=None):
+    def __init__(self, lay: Layout, ratio: float = 0.1, groups: int = 16, device=None):
         self.lay, self.ratio = lay, float(ratio)
         self.dev = torch.device(device if device is not None else "cuda")
         ims = lay.images
