@@ -333,11 +333,37 @@ __device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, uint32_
 }
 
 // split-K factor for small problems: keep >= ~4 CTAs per SM (148 SMs); 1, 2, 4 or 8
-inline int split_k_factor(int tiles) {
-    const int target = 4 * 148;
-    int ks = 1;
-    while (ks < 8 && tiles * ks * 2 <= target) ks *= 2;
-    return ks;
+// Split factor KS in {1, 2, 4, 8} of a tile grid over `slots` co-resident CTAs (SMs x CTAs per
+// SM): below 4 waves, minimises the wave-quantised time ceil(tiles KS / slots) (1/KS + o), o = a
+// CTA's fixed cost relative to a whole tile's work, so that the last wave is not mostly idle
+// (C2's backward: 656 tiles on 592 slots -> KS = 4, 0.77 -> 0.62 ms).
+#ifndef GSR_SPLIT_OVERHEAD
+#define GSR_SPLIT_OVERHEAD 0.05
+#endif
+inline int split_k_factor(long long tiles, long long slots) {
+    if (slots <= 0) slots = 4 * 148;
+    // >= 4 waves: the tail is small and the split's per-CTA costs (tile staging, shorter
+    // sorted batches, the forward's DSMEM reduce) measured +11-12% at C3/C4
+    if (tiles >= 4 * slots) return 1;
+    int best = 1;
+    double tbest = 1e300;
+    for (int ks = 1; ks <= 8; ks *= 2) {
+        const double waves = (double)((tiles * ks + slots - 1) / slots);
+        const double t = waves * (1.0 / ks + GSR_SPLIT_OVERHEAD);
+        if (t < tbest * (1.0 - 1e-9)) { tbest = t; best = ks; }
+    }
+    return best;
+}
+// co-resident CTAs of a kernel on this device (occupancy x SM count), cached by the caller
+template <class K>
+inline int resident_slots(K kernel, int threads, size_t smem) {
+    int dev = 0, sms = 148, per = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess)
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kernel, threads, smem) != cudaSuccess ||
+        per <= 0)
+        per = 4;
+    return per * sms;
 }
 
 // ---- host-side launch accounting (gsr_profile_*) --------------------------------------------

@@ -500,7 +500,9 @@ cudaError_t launch_render_bwd_moments(const ImgTable& tab, const Workspace& ws, 
     if (tab.total_tiles <= 0) return cudaSuccess;
     count_launches(1);
     int h = prof_begin(2, st);
-    int ks = split_k_factor(tab.total_tiles);
+    static int slots = 0;
+    if (slots == 0) slots = resident_slots(k_render_bwd, BWD_THREADS, 0);
+    const int ks = split_k_factor(tab.total_tiles, slots);
     k_render_bwd<<<tab.total_tiles * ks, BWD_THREADS, 0, st>>>(tab, ws.rec, ws.rects, ws.cell_start,
                                                                ws.ext,
                                                                perm, grad_out, moments, ks, img,

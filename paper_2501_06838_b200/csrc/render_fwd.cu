@@ -751,18 +751,26 @@ __global__ void __launch_bounds__(FWD2_THREADS, GSR_FWD_MINB) k_render_fwd2(cons
     fwd_epilogue<KS, LOSS, CFG>(sm.tot, im, Tx0, Ty0, warp, lane, krank, out, gt, loss_acc);
 }
 
+// one-time function setup of an instance (also loads its code under CUDA lazy loading)
 template <int KS, bool LOSS, class CFG>
-cudaError_t launch_ks3_v2(const ImgTable& tab, const Workspace& ws, float* out, const float* gt,
-                          double* loss_acc, cudaStream_t st) {
+cudaError_t fwd2_prepare() {
     static bool attr_set = false;
-    const size_t smem = sizeof(FwdSmem2<CFG>);
     if (!attr_set) {
         cudaError_t e = cudaFuncSetAttribute(k_render_fwd2<KS, LOSS, CFG>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)smem);
+                                             (int)sizeof(FwdSmem2<CFG>));
         if (e != cudaSuccess) return e;
         attr_set = true;
     }
+    return cudaSuccess;
+}
+
+template <int KS, bool LOSS, class CFG>
+cudaError_t launch_ks3_v2(const ImgTable& tab, const Workspace& ws, float* out, const float* gt,
+                          double* loss_acc, cudaStream_t st) {
+    const size_t smem = sizeof(FwdSmem2<CFG>);
+    cudaError_t e0 = fwd2_prepare<KS, LOSS, CFG>();
+    if (e0 != cudaSuccess) return e0;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)tab.total_ftiles * KS);
     cfg.blockDim = dim3(FWD2_THREADS);
@@ -828,6 +836,22 @@ cudaError_t launch_ks(const ImgTable& tab, const Workspace& ws, float* out, cons
               : launch_ks2<KS, false>(tab, ws, out, gt, loss_acc, st);
 }
 
+// co-resident forward CTAs of a configuration (the split-K choice depends on it)
+template <class CFG>
+int fwd_slots() {
+#if GSR_FWD_V2
+    const auto k = k_render_fwd2<1, false, CFG>;
+    const size_t smem = sizeof(FwdSmem2<CFG>);
+    const int threads = FWD2_THREADS;
+#else
+    const auto k = k_render_fwd<1, false, CFG>;
+    const size_t smem = sizeof(FwdSmem<CFG>);
+    const int threads = FWD_THREADS;
+#endif
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    return resident_slots(k, threads, smem);
+}
+
 }  // namespace
 
 cudaError_t launch_render_fwd(const ImgTable& tab, const Workspace& ws, float* out,
@@ -835,8 +859,28 @@ cudaError_t launch_render_fwd(const ImgTable& tab, const Workspace& ws, float* o
     if (tab.total_ftiles <= 0) return cudaSuccess;
     count_launches(1);
     int h = prof_begin(1, st);
-    // split-K so that small problems still fill the 148 SMs (>= ~4 CTAs per SM)
-    const int ks = split_k_factor(tab.total_ftiles);
+    // split-K (cluster CTAs share a tile) so that small problems fill the SMs without a mostly
+    // idle last wave
+#if GSR_FWD_V2
+    // every instance the split choice can pick is set up (and its code loaded) on the first
+    // call, so a later batch with a new split factor does not pay a module load mid-stream
+    static bool prepared = false;
+    if (!prepared) {
+        fwd2_prepare<1, false, FwdCfgSmall>(); fwd2_prepare<2, false, FwdCfgSmall>();
+        fwd2_prepare<4, false, FwdCfgSmall>(); fwd2_prepare<8, false, FwdCfgSmall>();
+        fwd2_prepare<1, true, FwdCfgSmall>(); fwd2_prepare<2, true, FwdCfgSmall>();
+        fwd2_prepare<4, true, FwdCfgSmall>(); fwd2_prepare<8, true, FwdCfgSmall>();
+        fwd2_prepare<1, false, FwdCfgWide>(); fwd2_prepare<2, false, FwdCfgWide>();
+        fwd2_prepare<4, false, FwdCfgWide>(); fwd2_prepare<8, false, FwdCfgWide>();
+        fwd2_prepare<1, true, FwdCfgWide>(); fwd2_prepare<2, true, FwdCfgWide>();
+        fwd2_prepare<4, true, FwdCfgWide>(); fwd2_prepare<8, true, FwdCfgWide>();
+        prepared = true;
+    }
+#endif
+    static int slots_small = 0, slots_wide = 0;
+    int& slots = tab.fwd_small ? slots_small : slots_wide;
+    if (slots == 0) slots = tab.fwd_small ? fwd_slots<FwdCfgSmall>() : fwd_slots<FwdCfgWide>();
+    const int ks = split_k_factor(tab.total_ftiles, slots);
     cudaError_t e;
     switch (ks) {
         case 8: e = launch_ks<8>(tab, ws, out, gt, loss_acc, st); break;
