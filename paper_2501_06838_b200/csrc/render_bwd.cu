@@ -24,6 +24,8 @@
 // 4 moments); lanes process two rows at once for two independent accumulation chains. Row partials
 // (fp32, <= 16 terms per lane half) are folded into fp64 per-(Gaussian, tile) accumulators, which
 // leave the CTA as 8 fp64 atomics -- the only global atomics of the backward.
+#include <atomic>
+
 #include "gsr_internal.cuh"
 
 #ifndef GSR_BWD_UNROLL
@@ -500,8 +502,12 @@ cudaError_t launch_render_bwd_moments(const ImgTable& tab, const Workspace& ws, 
     if (tab.total_tiles <= 0) return cudaSuccess;
     count_launches(1);
     int h = prof_begin(2, st);
-    static int slots = 0;
-    if (slots == 0) slots = resident_slots(k_render_bwd, BWD_THREADS, 0);
+    static std::atomic<int> slots_cache{0};
+    int slots = slots_cache.load(std::memory_order_relaxed);
+    if (slots == 0) {
+        slots = resident_slots(k_render_bwd, BWD_THREADS, 0);
+        slots_cache.store(slots, std::memory_order_relaxed);
+    }
     const int ks = split_k_factor(tab.total_tiles, slots);
     k_render_bwd<<<tab.total_tiles * ks, BWD_THREADS, 0, st>>>(tab, ws.rec, ws.rects, ws.cell_start,
                                                                ws.ext,

@@ -28,6 +28,9 @@
 //     narrow windows 1 x 4 px per lane / 16 x 8 tiles (fewer masked evaluations).
 //   * split-K for small problems: KS CTAs of a cluster share a tile, take interleaved batches,
 //     and reduce their totals through DSMEM in cluster-rank order (deterministic, no atomics).
+#include <atomic>
+#include <mutex>
+
 #include "gsr_internal.cuh"
 
 #ifndef GSR_FWD_V2
@@ -754,13 +757,13 @@ __global__ void __launch_bounds__(FWD2_THREADS, GSR_FWD_MINB) k_render_fwd2(cons
 // one-time function setup of an instance (also loads its code under CUDA lazy loading)
 template <int KS, bool LOSS, class CFG>
 cudaError_t fwd2_prepare() {
-    static bool attr_set = false;
-    if (!attr_set) {
+    static std::atomic<bool> attr_set{false};    // concurrent first calls just repeat the set
+    if (!attr_set.load(std::memory_order_acquire)) {
         cudaError_t e = cudaFuncSetAttribute(k_render_fwd2<KS, LOSS, CFG>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)sizeof(FwdSmem2<CFG>));
         if (e != cudaSuccess) return e;
-        attr_set = true;
+        attr_set.store(true, std::memory_order_release);
     }
     return cudaSuccess;
 }
@@ -791,14 +794,14 @@ cudaError_t launch_ks3_v2(const ImgTable& tab, const Workspace& ws, float* out, 
 template <int KS, bool LOSS, class CFG>
 cudaError_t launch_ks3(const ImgTable& tab, const Workspace& ws, float* out, const float* gt,
                        double* loss_acc, cudaStream_t st) {
-    static bool attr_set = false;
+    static std::atomic<bool> attr_set{false};
     const size_t smem = sizeof(FwdSmem<CFG>);
-    if (!attr_set) {
+    if (!attr_set.load(std::memory_order_acquire)) {
         cudaError_t e = cudaFuncSetAttribute(k_render_fwd<KS, LOSS, CFG>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)smem);
         if (e != cudaSuccess) return e;
-        attr_set = true;
+        attr_set.store(true, std::memory_order_release);
     }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)tab.total_ftiles * KS);
@@ -864,8 +867,8 @@ cudaError_t launch_render_fwd(const ImgTable& tab, const Workspace& ws, float* o
 #if GSR_FWD_V2
     // every instance the split choice can pick is set up (and its code loaded) on the first
     // call, so a later batch with a new split factor does not pay a module load mid-stream
-    static bool prepared = false;
-    if (!prepared) {
+    static std::once_flag prepared;
+    std::call_once(prepared, [] {
         fwd2_prepare<1, false, FwdCfgSmall>(); fwd2_prepare<2, false, FwdCfgSmall>();
         fwd2_prepare<4, false, FwdCfgSmall>(); fwd2_prepare<8, false, FwdCfgSmall>();
         fwd2_prepare<1, true, FwdCfgSmall>(); fwd2_prepare<2, true, FwdCfgSmall>();
@@ -874,12 +877,15 @@ cudaError_t launch_render_fwd(const ImgTable& tab, const Workspace& ws, float* o
         fwd2_prepare<4, false, FwdCfgWide>(); fwd2_prepare<8, false, FwdCfgWide>();
         fwd2_prepare<1, true, FwdCfgWide>(); fwd2_prepare<2, true, FwdCfgWide>();
         fwd2_prepare<4, true, FwdCfgWide>(); fwd2_prepare<8, true, FwdCfgWide>();
-        prepared = true;
-    }
+    });
 #endif
-    static int slots_small = 0, slots_wide = 0;
-    int& slots = tab.fwd_small ? slots_small : slots_wide;
-    if (slots == 0) slots = tab.fwd_small ? fwd_slots<FwdCfgSmall>() : fwd_slots<FwdCfgWide>();
+    static std::atomic<int> slots_small{0}, slots_wide{0};
+    std::atomic<int>& sl = tab.fwd_small ? slots_small : slots_wide;
+    int slots = sl.load(std::memory_order_relaxed);
+    if (slots == 0) {
+        slots = tab.fwd_small ? fwd_slots<FwdCfgSmall>() : fwd_slots<FwdCfgWide>();
+        sl.store(slots, std::memory_order_relaxed);
+    }
     const int ks = split_k_factor(tab.total_ftiles, slots);
     cudaError_t e;
     switch (ks) {

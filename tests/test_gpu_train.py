@@ -30,12 +30,13 @@ def gt_near(I, seed, delta=2e-3):
     return (I + rng.choice([-delta, delta], size=I.shape)).astype(np.float32)
 
 
-@pytest.mark.parametrize("rho_scale", [1.0, 1 - 1e-4])
-def test_train_step_batch_matches_oracle(rho_scale):
+@pytest.mark.parametrize("rho_scale,scales", [
+    (1.0, [4.0, 2.5, 1.3]), (1 - 1e-4, [4.0, 2.5, 1.3]),
+    (1.0, [(4.0, 2.0), (2.5, 2.5), (1.3, 3.1)])])      # scale vectors (R22)
+def test_train_step_batch_matches_oracle(rho_scale, scales):
     import torch
     import paper_2501_06838_b200 as gsr
     from paper_2501_06838_b200 import ops
-    scales = [4.0, 2.5, 1.3]
     raws, refs, imgs, gts = [], [], [], []
     off = 0
     for k, s in enumerate(scales):
@@ -48,7 +49,8 @@ def test_train_step_batch_matches_oracle(rho_scale):
     raw = {k: np.concatenate([r[k] for r in raws]) for k in RAWK}
     ref = np.concatenate(refs)
     outs, loss, g = T.l1_step(raw, ref, imgs, gts, 0.1, rho_scale)
-    lay = gsr.layout([gsr.Image(H, W, s, go, gc) for (H, W, s, go, gc) in imgs])
+    lay = gsr.layout([gsr.Image(H, W, s[0], go, gc, s_y=s[1]) if isinstance(s, tuple) else
+                      gsr.Image(H, W, s, go, gc) for (H, W, s, go, gc) in imgs])
     dev = {k: torch.from_numpy(v).cuda() for k, v in raw.items()}
     gt_flat = torch.from_numpy(np.concatenate([x.reshape(-1) for x in gts])).cuda()
     out, gl, gg = ops.train_step_l1(dev["raw_alpha"], dev["offset"], torch.from_numpy(ref).cuda(),
