@@ -29,7 +29,7 @@
 #include "gsr_internal.cuh"
 
 #ifndef GSR_BWD_UNROLL
-#define GSR_BWD_UNROLL 4
+#define GSR_BWD_UNROLL 8
 #endif
 #ifndef GSR_BWD_CONTIG
 #define GSR_BWD_CONTIG 0          // 1: each warp scans a contiguous share of every span
