@@ -42,8 +42,7 @@ __global__ void k_keys(const T* __restrict__ alpha, const T* __restrict__ mu,
         if (k >= 0) {
             const DevImg& im = tab.img[k];
             float mx = ldf(mu[2 * i]), my = ldf(mu[2 * i + 1]);
-            if (gaussian_valid(ldf(alpha[i]), mx, my, ldf(sigma[2 * i]), ldf(sigma[2 * i + 1]), ldf(rho[i]),
-                               ldf(color[3 * i]), ldf(color[3 * i + 1]), ldf(color[3 * i + 2]))) {
+            if (valid_at(alpha, mu, sigma, rho, color, i)) {
                 Rect r = support_rect(mx, my, ldf(sigma[2 * i]), ldf(sigma[2 * i + 1]), im);
                 if (r.nonempty) {
                     // key: cell of the unclipped support origin (>= the window origin, so
@@ -254,7 +253,8 @@ __global__ void k_records(const T* __restrict__ alpha, const T* __restrict__ mu,
     Rect r = window_rect(mxf, myf, im);
     Rect sr = support_rect(mxf, myf, ldf(sigma[2 * i]), ldf(sigma[2 * i + 1]), im);
     double mx = mxf, my = myf;
-    double sx = ldf(sigma[2 * i]), sy = ldf(sigma[2 * i + 1]), rh = ldf(rho[i]), al = ldf(alpha[i]);
+    double sx = ldf(sigma[2 * i]), sy = ldf(sigma[2 * i + 1]);
+        double rh = ldf(rho[i]), al = ldf(alpha[i]);
     double D = (1.0 - rh) * (1.0 + rh);
     // exponent in factored form (no cancellation):
     //   q = -Q/2 log2 e = -(w'^2 + v'^2),  w' = a1 dx + b1 dy,  v' = c1 dy
@@ -270,7 +270,8 @@ __global__ void k_records(const T* __restrict__ alpha, const T* __restrict__ mu,
     const float a1f = (float)a1;
     const float Df = a1f * im.invsx, d2 = Df * Df;
     float4 r0 = make_float4((float)(-axd), (float)ayd, (float)dly, Df);
-    float4 r1 = make_float4((float)(-a1 * dlx), (float)b1, (float)c1, (float)(w * ldf(color[3 * i])));
+    float4 r1 = make_float4((float)(-a1 * dlx), (float)b1, (float)c1,
+                            (float)(w * ldf(color[3 * i])));
     unsigned xs = (unsigned)r.x0 | ((unsigned)r.x1 << 16);
     unsigned ys = (unsigned)r.y0 | ((unsigned)r.y1 << 16);
     float4 r2 = make_float4((float)(w * ldf(color[3 * i + 1])), (float)(w * ldf(color[3 * i + 2])),
@@ -303,9 +304,9 @@ __global__ void k_pair_count(const T* __restrict__ alpha, const T* __restrict__ 
         if (k >= 0) {
             const DevImg& im = tab.img[k];
             float mx = ldf(mu[2 * i]), my = ldf(mu[2 * i + 1]);
-            if (gaussian_valid(ldf(alpha[i]), mx, my, ldf(sigma[2 * i]), ldf(sigma[2 * i + 1]), ldf(rho[i]),
-                               ldf(color[3 * i]), ldf(color[3 * i + 1]), ldf(color[3 * i + 2]))) {
-                Rect r = support ? support_rect(mx, my, ldf(sigma[2 * i]), ldf(sigma[2 * i + 1]), im)
+            if (valid_at(alpha, mu, sigma, rho, color, i)) {
+                Rect r = support ? support_rect(mx, my, ldf(sigma[2 * i]), ldf(sigma[2 * i + 1]),
+                                                im)
                                  : window_rect(mx, my, im);
                 if (r.nonempty)
                     v = (unsigned long long)(r.x1 - r.x0 + 1) * (unsigned long long)(r.y1 - r.y0 + 1);
@@ -328,8 +329,7 @@ __global__ void k_debug_rects(const float* __restrict__ alpha, const float* __re
     if (k >= 0) {
         const DevImg& im = tab.img[k];
         float mx = ldf(mu[2 * i]), my = ldf(mu[2 * i + 1]);
-        if (gaussian_valid(ldf(alpha[i]), mx, my, ldf(sigma[2 * i]), ldf(sigma[2 * i + 1]), ldf(rho[i]),
-                           ldf(color[3 * i]), ldf(color[3 * i + 1]), ldf(color[3 * i + 2]))) {
+        if (valid_at(alpha, mu, sigma, rho, color, i)) {
             Rect r = support ? support_rect(mx, my, ldf(sigma[2 * i]), ldf(sigma[2 * i + 1]), im)
                              : window_rect(mx, my, im);
             if (r.nonempty) o = make_int4(r.x0, r.x1, r.y0, r.y1);

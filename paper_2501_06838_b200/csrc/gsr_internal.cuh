@@ -239,6 +239,15 @@ __device__ __forceinline__ bool gaussian_valid(float a, float mx, float my, floa
     return fin && sx > 0.f && sy > 0.f && fabsf(rh) < 1.f;
 }
 
+// validity (R20) of Gaussian i read from the parameter arrays (float32 or bfloat16)
+template <class T>
+__device__ __forceinline__ bool valid_at(const T* alpha, const T* mu, const T* sigma,
+                                         const T* rho, const T* color, long long i) {
+    return gaussian_valid(ldf(alpha[i]), ldf(mu[2 * i]), ldf(mu[2 * i + 1]), ldf(sigma[2 * i]),
+                          ldf(sigma[2 * i + 1]), ldf(rho[i]), ldf(color[3 * i]),
+                          ldf(color[3 * i + 1]), ldf(color[3 * i + 2]));
+}
+
 // ---- PTX helpers ------------------------------------------------------------------------
 __device__ __forceinline__ float ex2_approx(float x) {
     float y;

@@ -446,10 +446,10 @@ __global__ void k_finalize(const T* __restrict__ alpha, const T* __restrict__ mu
     long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     float o[9] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-    if (gaussian_valid(ldf(alpha[i]), ldf(mu[2 * i]), ldf(mu[2 * i + 1]), ldf(sigma[2 * i]), ldf(sigma[2 * i + 1]), ldf(rho[i]),
-                       ldf(color[3 * i]), ldf(color[3 * i + 1]), ldf(color[3 * i + 2]))) {
+    if (valid_at(alpha, mu, sigma, rho, color, i)) {
         const double* m = moments + 8 * i;
-        double sx = ldf(sigma[2 * i]), sy = ldf(sigma[2 * i + 1]), rh = ldf(rho[i]), al = ldf(alpha[i]);
+        double sx = ldf(sigma[2 * i]), sy = ldf(sigma[2 * i + 1]);
+        double rh = ldf(rho[i]), al = ldf(alpha[i]);
         double c0 = ldf(color[3 * i]), c1 = ldf(color[3 * i + 1]), c2 = ldf(color[3 * i + 2]);
         double D = (1.0 - rh) * (1.0 + rh);
         double K = 1.0 / (TWO_PI * sx * sy * sqrt(D));
