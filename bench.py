@@ -190,8 +190,12 @@ def run_reference(args):
     import oracle as O
     H, W, s = imgs[0]
     Hs, Ws = O.out_dims(H, W, s)
-    P_img = O.pair_count(clouds[0], H, W, s, RATIO)
-    P = P_img * len(imgs)                      # images of the workload are i.i.d. draws
+    # P over the whole workload, image by image with the oracle's pair counter (the same seeded
+    # clouds as the GPU arm, so the line's pairs_per_pass equals the GPU line's)
+    P = 0
+    for k, (Hk, Wk, sk) in enumerate(imgs):
+        ck = clouds[0] if k == 0 else S.gaussians(Hk, Wk, seed=1000 + k)
+        P += O.pair_count(ck, Hk, Wk, sk, RATIO)
     pix = sum(O.out_dims(h, w, sc)[0] * O.out_dims(h, w, sc)[1] for h, w, sc in imgs)
     g0 = S.grad_out((Hs, Ws, 3), seed=2000).astype(np.float64)
     times = []
