@@ -32,7 +32,8 @@ def gt_near(I, seed, delta=2e-3):
 
 @pytest.mark.parametrize("rho_scale,scales", [
     (1.0, [4.0, 2.5, 1.3]), (1 - 1e-4, [4.0, 2.5, 1.3]),
-    (1.0, [(4.0, 2.0), (2.5, 2.5), (1.3, 3.1)])])      # scale vectors (R22)
+    (1.0, [(4.0, 2.0), (2.5, 2.5), (1.3, 3.1)]),       # scale vectors (R22)
+    (1.0, [12.5, 7.3])])                                 # HAT-L range s ~ U[1, 16]
 def test_train_step_batch_matches_oracle(rho_scale, scales):
     import torch
     import paper_2501_06838_b200 as gsr
