@@ -364,6 +364,7 @@ int gsr_oracle_field(int64_t n, const double* alpha, const double* mu, const dou
 /* absmass (optional, [n,9]) = sum over pairs of the monomial magnitudes of   */
 /* each term (its fp32 rounding scale, R18), per output:            */
 /*   alpha, mu_x, mu_y, sigma_x, sigma_y, rho, c_r, c_g, c_b                  */
+/* termabs (optional, [n,9]) = sum over pairs of |term| (SURVEY 8(c).18's S). */
 /* mode 0 brute (literal predicate over all pixels), mode 1 rect.             */
 /* Per-pair derivatives (u = dx/sx, v = dy/sy, D = 1-rho^2, w = alpha f g.c): */
 /*   d alpha = f g.c ;  d c_k = alpha f g_k                                   */
@@ -376,7 +377,8 @@ int gsr_oracle_render_bwd(int64_t n, const double* alpha, const double* mu, cons
                           const double* rho, const double* color, int H, int W, double sw, double sh,
                           double r, int mode, int row_begin, int row_end, const double* grad_out,
                           int64_t nidx, const int64_t* idx, double* d_alpha, double* d_mu,
-                          double* d_sigma, double* d_rho, double* d_color, double* absmass)
+                          double* d_sigma, double* d_rho, double* d_color, double* absmass,
+                          double* termabs)
 {
     int Hs, Ws;
     gsr_oracle_out_dims(H, W, sw, sh, &Hs, &Ws);
@@ -390,6 +392,7 @@ int gsr_oracle_render_bwd(int64_t n, const double* alpha, const double* mu, cons
         int64_t i = idx ? idx[t] : t;
         double g9[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
         double a9[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+        double t9[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
         if (oracle_is_valid(alpha, mu, sigma, rho, color, i) && row_begin < row_end) {
             double mx = mu[2 * i], my = mu[2 * i + 1];
             double sx = sigma[2 * i], sy = sigma[2 * i + 1], rh = rho[i], al = alpha[i];
@@ -443,6 +446,7 @@ int gsr_oracle_render_bwd(int64_t n, const double* alpha, const double* mu, cons
                         for (int k = 0; k < 9; ++k) {
                             g9[k] += term[k];
                             a9[k] += mono[k];
+                            t9[k] += fabs(term[k]);
                         }
                     }
                 }
@@ -459,6 +463,8 @@ int gsr_oracle_render_bwd(int64_t n, const double* alpha, const double* mu, cons
         d_color[3 * t + 2] = g9[8];
         if (absmass)
             for (int k = 0; k < 9; ++k) absmass[9 * t + k] = a9[k];
+        if (termabs)
+            for (int k = 0; k < 9; ++k) termabs[9 * t + k] = t9[k];
     }
     return 0;
 }

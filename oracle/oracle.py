@@ -52,7 +52,7 @@ class OracleLib:
         lib.gsr_oracle_render_pixels.argtypes = par + [_i64, _p, _p, _p]
         lib.gsr_oracle_field.argtypes = [_i64, _p, _p, _p, _p, _p, _dbl, _dbl, _i64, _p, _p]
         lib.gsr_oracle_render_bwd.argtypes = par + [_i32, _i32, _i32, _p, _i64, _p, _p, _p, _p,
-                                                    _p, _p, _p]
+                                                    _p, _p, _p, _p]
         lib.gsr_oracle_tile_lists.argtypes = par + [_i32, _i32, _i32, _i32, _i32, _p, _p]
         lib.gsr_oracle_tile_lists.restype = _i64
         self.lib = lib
@@ -145,8 +145,9 @@ def render_bwd(cloud, H, W, s, r, grad_out, mode="rect", rows=None, idx=None,
                want_absmass=False):
     """Gradients (float64) of L = sum(grad_out * I) wrt every parameter.
 
-    Returns dict alpha[n'], mu[n',2], sigma[n',2], rho[n'], color[n',3] (+ absmass[n',9]) for
-    the Gaussians in idx (all if None)."""
+    Returns dict alpha[n'], mu[n',2], sigma[n',2], rho[n'], color[n',3] for the Gaussians in idx
+    (all if None); want_absmass adds absmass[n',9] (sum of the monomial magnitudes of each
+    per-pair term, DESIGN R18) and termabs[n',9] (sum of |term|)."""
     a, mu, sg, rh, c = _params(cloud)
     Hs, Ws = out_dims(H, W, s)
     rb, re = (0, Hs) if rows is None else rows
@@ -160,14 +161,16 @@ def render_bwd(cloud, H, W, s, r, grad_out, mode="rect", rows=None, idx=None,
     res = dict(alpha=np.zeros(m), mu=np.zeros((m, 2)), sigma=np.zeros((m, 2)), rho=np.zeros(m),
                color=np.zeros((m, 3)))
     am = np.zeros((m, 9)) if want_absmass else None
+    ta = np.zeros((m, 9)) if want_absmass else None
     load().lib.gsr_oracle_render_bwd(
         n, _ptr(a), _ptr(mu), _ptr(sg), _ptr(rh), _ptr(c), int(H), int(W), *scales(s), float(r),
         MODES[mode], int(rb), int(re), _ptr(g), m if idx is not None else 0,
         _ptr(idx) if idx is not None else None, _ptr(res["alpha"]), _ptr(res["mu"]),
         _ptr(res["sigma"]), _ptr(res["rho"]), _ptr(res["color"]),
-        _ptr(am) if am is not None else None)
+        _ptr(am) if am is not None else None, _ptr(ta) if ta is not None else None)
     if am is not None:
         res["absmass"] = am
+        res["termabs"] = ta
     return res
 
 

@@ -26,7 +26,7 @@ int gsr_oracle_render_bwd(int64_t n, const double* alpha, const double* mu, cons
                           double sh, double r, int mode, int row_begin, int row_end,
                           const double* grad_out, int64_t nidx, const int64_t* idx,
                           double* d_alpha, double* d_mu, double* d_sigma, double* d_rho,
-                          double* d_color, double* absmass);
+                          double* d_color, double* absmass, double* termabs);
 
 /* CUDA runtime (libcudart), declared here so the test needs no CUDA headers */
 int cudaMalloc(void** p, size_t n);
@@ -123,7 +123,7 @@ static int gpu_part(void) {
     double *oa = malloc(8 * n), *om = malloc(16 * n), *os = malloc(16 * n), *orh = malloc(8 * n),
            *oc = malloc(24 * n);
     gsr_oracle_render_bwd(n, ad, mud, sgd, rhd, cd, H, W, s, s, r, 1, 0, Hs, gd, 0, NULL, oa, om,
-                          os, orh, oc, NULL);
+                          os, orh, oc, NULL, NULL);
     float *fa = malloc(4 * n), *fm = malloc(8 * n), *fs = malloc(8 * n), *fr = malloc(4 * n),
           *fc = malloc(12 * n);
     cudaMemcpy(fa, ga, 4 * n, D2H); cudaMemcpy(fm, gmu, 8 * n, D2H); cudaMemcpy(fs, gsg, 8 * n, D2H);

@@ -254,6 +254,25 @@ def test_brute_equals_rect_bitwise(cfg):
         assert np.array_equal(ga[k], gb[k]), k
 
 
+@pytest.mark.parametrize("cfg", [(8, 9, 4.0, 0.1, "image", 11), (6, 7, 2.7, 1.0, "stress", 12),
+                                 (5, 8, (3.0, 1.75), 0.2, "image", 13),
+                                 (4, 6, 1.0, 1.0, "image", 14)])
+def test_render_pixels_equals_brute_render(cfg):
+    """gsr_oracle_render_pixels (Eq. 4 at an explicit pixel list, literal Alg. 1
+    predicate P:1385) is the checker of the full-size sampled parity tests; it must equal the
+    brute-mode full render bit for bit at every pixel, in any pixel order, including a scale
+    vector (R22) and r = 1 (every window covers the frame)."""
+    H, W, s, r, dist, seed = cfg
+    cl = S.gaussians(H, W, m=4, seed=seed, dist=dist, offset_range=1.5)
+    full = O.render_fwd(cl, H, W, s, r, mode="brute")
+    Hs, Ws = full.shape[:2]
+    ys, xs = np.meshgrid(np.arange(Hs), np.arange(Ws), indexing="ij")
+    perm = np.random.default_rng(seed).permutation(Hs * Ws)
+    got = O.render_pixels(cl, H, W, s, r, xs.reshape(-1)[perm], ys.reshape(-1)[perm])
+    assert np.array_equal(got, full.reshape(-1, 3)[perm])
+    assert np.abs(full).max() > 0
+
+
 def test_pair_count_full_window():
     """r = 1 with every mu inside the frame: every Gaussian's window covers the whole image, so
     P = N * Hs * Ws (S:404-406)."""
