@@ -223,6 +223,27 @@ def run_reference(args):
 
 
 # ----------------------------------------------------------------------------- GPU arm
+def self_launch(args):
+    """`python bench.py --gpus N` without a launcher: re-exec this script under
+    torch.distributed.run with N ranks (one per GPU, NCCL). Fails loudly if fewer than N GPUs are
+    visible, unless GSR_BENCH_SHARE_GPU=1 (all ranks on cuda:0, gloo: a functional check of the
+    sharded path on a 1-GPU box, never a performance number)."""
+    import socket
+    import torch
+    ngpu = torch.cuda.device_count()
+    if args.gpus > ngpu and os.environ.get("GSR_BENCH_SHARE_GPU") != "1":
+        raise SystemExit(f"bench.py --gpus {args.gpus}: only {ngpu} GPU(s) visible "
+                         "(GSR_BENCH_SHARE_GPU=1 runs every rank on cuda:0 as a functional check)")
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           str(Path(__file__).resolve()), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -235,6 +256,8 @@ def main():
     ap.add_argument("--e2e-groups", type=int, default=16,
                     help="image groups of the streamed host-memory step (e2e)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-configs", action="store_true",
+                    help="skip the per-config timings of C1-C4 (N=1 only)")
     ap.add_argument("--partition", choices=["band", "image"], default="band",
                     help="N>1: row bands of every image (NCCL all-gather + moment all-reduce) or "
                          "whole images per rank (no exchange)")
@@ -243,6 +266,10 @@ def main():
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return self_launch(args)
+    if int(os.environ.get("WORLD_SIZE", "1")) != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={os.environ.get('WORLD_SIZE')}")
 
     import torch
     import torch.distributed as dist
@@ -273,38 +300,33 @@ def main():
     n = int(host["alpha"].shape[0])
     params = [torch.from_numpy(host[k]).to(dev) for k in ("alpha", "mu", "sigma", "rho", "color")]
 
-    # ---- row-band plan (identical on every rank; deterministic from the inputs)
+    # ---- row-band plan (identical on every rank; deterministic from the inputs): libgsr's K7
+    # planner on the device (gsr_row_pair_counts_batched / gsr_band_span_batched)
     dims = [gsr.out_dims(H, W, s) for H, W, s in imgs]
     widths3 = [Ws * 3 for _, Ws in dims]
     offs = np.concatenate([[0], np.cumsum(counts)])
-    bounds = []
+    whole = [(H, W, s, int(offs[k]), counts[k]) for k, (H, W, s) in enumerate(imgs)]
     by_image = world > 1 and args.partition == "image"
-    for k, (H, W, s) in enumerate(imgs):
-        if world == 1 or by_image:
-            bounds.append([0, dims[k][0]])
-        else:
-            rc = gdist.row_pair_counts(host["mu"][offs[k]:offs[k + 1]],
-                                       np.ones(counts[k], bool), H, W, s, RATIO,
-                                       sigma=host["sigma"][offs[k]:offs[k + 1]])
-            bounds.append(gdist.plan_bands(rc, world))
-    if by_image:
-        # whole images per rank: contiguous, equal image counts (the images are i.i.d. draws)
-        k0, k1 = (rank * len(imgs)) // world, ((rank + 1) * len(imgs)) // world
-        band_imgs = [gsr.Image(H, W, s, int(offs[k]), counts[k], 0, dims[k][0])
-                     for k, (H, W, s) in enumerate(imgs) if k0 <= k < k1]
+    banded = world > 1 and not by_image
+    plan = None
+    if banded:
+        # this rank's bands, halo (the Gaussians whose support meets its bands: the only ones it
+        # bins, renders and finalizes) and neighbour seam sets (dist.RankPlan)
+        plan = gdist.RankPlan(params, whole, world, rank, RATIO)
+        bounds = plan.bounds
+        band_imgs = [gsr.Image(H, W, s, go, gc, rb, re)
+                     for (H, W, s, go, gc, rb, re, sy) in plan.band_images()]
     else:
-        band_imgs = [gsr.Image(H, W, s, int(offs[k]), counts[k], bounds[k][rank],
-                               bounds[k][rank + 1]) for k, (H, W, s) in enumerate(imgs)]
+        bounds = [[0, dims[k][0]] for k in range(len(imgs))]
+        if by_image:
+            # whole images per rank: contiguous, equal image counts (i.i.d. draws)
+            k0, k1 = (rank * len(imgs)) // world, ((rank + 1) * len(imgs)) // world
+            band_imgs = [gsr.Image(H, W, s, int(offs[k]), counts[k], 0, dims[k][0])
+                         for k, (H, W, s) in enumerate(imgs) if k0 <= k < k1]
+        else:
+            band_imgs = [gsr.Image(H, W, s, int(offs[k]), counts[k])
+                         for k, (H, W, s) in enumerate(imgs)]
     lay = gsr.layout(band_imgs)
-    # seam set: Gaussians whose support rows span a band boundary -- the only ones
-    # whose gradients are exchanged (dist.reduce_seam); identical on every rank
-    seam_idx = None
-    if world > 1 and not by_image:
-        seam = np.concatenate([
-            gdist.seam_mask(host["mu"][offs[k]:offs[k + 1]], host["sigma"][offs[k]:offs[k + 1]],
-                            np.ones(counts[k], bool), H, W, s, RATIO, bounds[k])
-            for k, (H, W, s) in enumerate(imgs)])
-        seam_idx = torch.from_numpy(np.nonzero(seam)[0].astype(np.int64)).to(dev)
     full_pix = sum(h * w for h, w in dims)
     # P (the paper's work unit): pairs inside the windows; P_eval: pairs inside the support rects,
     # the pairs the kernels evaluate (reading R21; outside them every term is exactly 0 in fp32)
@@ -322,23 +344,41 @@ def main():
     g_band.uniform_(-1.0, 1.0, generator=gen)
 
     from paper_2501_06838_b200 import ops as gops
-    step_ws = gops.workspace_for(params[0], lay, RATIO) if gops.single_chunk(lay) else None
+    step_ws = None
+    if banded:
+        m_cap = [plan.m]
+        step_ws = [gsr.subset_workspace_for(params[0], lay, plan.m + plan.m // 8, RATIO)]
+    elif gops.single_chunk(lay):
+        step_ws = gops.workspace_for(params[0], lay, RATIO)
+
+    def banded_step(prm, gb):
+        # the halo is recomputed every step (in training the parameters change every step):
+        # one K7 span pass over all N on the device + a compaction; then everything is O(halo)
+        plan.refresh(prm)
+        if plan.m > m_cap[0]:
+            m_cap[0] = plan.m + plan.m // 8
+            step_ws[0] = gsr.subset_workspace_for(prm[0], lay, m_cap[0], RATIO)
+        out = gsr.render_fwd_subset(*prm, plan.idx, lay, RATIO, workspace=step_ws[0])
+        # all-gather of the output bands on NCCL's stream, overlapped with the backward
+        gathered, work = gdist.gather_bands(out, gdist.rank_numels(bounds, widths3, world),
+                                            async_op=True)
+        mom = torch.zeros((plan.m, 8), dtype=torch.float64, device=dev)
+        gsr.render_bwd_moments_subset(*prm, plan.idx, lay, gb, mom, RATIO, workspace=step_ws[0],
+                                      reuse_binning=True)
+        grads = gsr.finalize_grads_subset(*prm, plan.idx, mom)   # compact: rows = plan.idx
+        gdist.exchange_seams(grads, plan)       # neighbour send/recv of the seam Gaussians
+        work.wait()
+        return out, gathered, grads
 
     def step():
+        if banded:
+            return banded_step(params, g_band)[1:]
         # one binning per step: the backward reuses the forward's (GSR_REUSE_BINNING)
         out = gsr.render_fwd_batched(*params, lay, RATIO, workspace=step_ws)
-        gathered, work = out, None
-        if world > 1 and not by_image:      # on NCCL's stream, overlapped with the backward
-            gathered, work = gdist.gather_bands(out, gdist.rank_numels(bounds, widths3, world),
-                                                async_op=True)
         moments = torch.zeros((n, 8), dtype=torch.float64, device=dev)
         gsr.render_bwd_moments_batched(*params, lay, g_band, moments, RATIO, workspace=step_ws,
                                        reuse_binning=step_ws is not None)
-        grads = gsr.finalize_grads(*params, moments)    # linear in the moments: band partials
-        if work is not None:
-            gdist.reduce_seam(grads, seam_idx)          # sum the seam Gaussians' partials
-            work.wait()
-        return gathered, grads
+        return out, gsr.finalize_grads(*params, moments)
 
     def barrier():
         if world > 1:
@@ -384,21 +424,21 @@ def main():
         h2d = sum(t.numel() * t.element_size() for t in hp) + hg.numel() * 4
         d2h = h_out.numel() * 4 + sum(t.numel() * t.element_size() for t in h_grads)
 
+        if banded:
+            hc = [torch.empty(plan.m + plan.m // 8, *t.shape[1:], dtype=torch.float32).pin_memory()
+                  for t in hp]
+            d2h = h_out.numel() * 4 + sum(t[:plan.m].numel() * 4 for t in hc)
+
         def e2e_step():
             dp = [t.to(dev, non_blocking=True) for t in hp]
             dg = hg.to(dev, non_blocking=True)
-            out = gsr.render_fwd_batched(*dp, lay, RATIO, workspace=step_ws)
-            mom = torch.zeros((n, 8), dtype=torch.float64, device=dev)
-            gsr.render_bwd_moments_batched(*dp, lay, dg, mom, RATIO, workspace=step_ws,
-                                           reuse_binning=step_ws is not None)
-            gr = gsr.finalize_grads(*dp, mom)
-            if world > 1 and not by_image:
-                gdist.reduce_seam(gr, seam_idx)
+            out, gathered, gr = banded_step(dp, dg)
             h_out.copy_(out, non_blocking=True)
-            for h, d in zip(h_grads, gr):
-                h.copy_(d, non_blocking=True)
+            for h, d in zip(hc, gr):             # this rank's halo gradients (compact)
+                h[:d.shape[0]].copy_(d, non_blocking=True)
 
-        pipeline = "serial (band exchange between forward and backward)"
+        pipeline = ("serial: halo plan, subset fwd, band all-gather overlapped with the backward, "
+                    "neighbour seam exchange")
         if world == 1 or by_image:
             # the public host-memory entry point: image groups streamed with H2D / compute /
             # D2H overlapped on three streams (ops.StreamedFwdBwd)
@@ -463,6 +503,25 @@ def main():
                "sample": desc, "oracle_gpairs_per_s_fwd": rf / 1e9,
                "oracle_gpairs_per_s_bwd": rb / 1e9}
 
+    configs = None
+    if rank == 0 and world == 1 and not args.no_configs:
+        # the other BASELINE.json configurations (C1 48x48 x4, C2 16-patch training batch, C3
+        # DIV2K-val x4, C4 x30), timed with tools/config_bench.py's protocol: CUDA events, 5
+        # warm-ups, median of 20; fwd = binning + K4, bwd = K5 on the forward's binning + K6;
+        # C1/C2 also replayed from a CUDA graph
+        sys.path.insert(0, str(ROOT / "tools"))
+        import config_bench as CB
+        configs = {}
+        for c in ("C1", "C2", "C3", "C4"):
+            r = CB.run(c, 20, quiet=True)
+            configs[c] = {k: r[k] for k in ("desc", "hr_px", "pairs_window", "pairs_evaluated",
+                                            "fwd_ms", "bwd_ms", "step_ms", "fwd_frac", "bwd_frac",
+                                            "hr_mpix_per_s") if k in r}
+            if "step_graph_ms" in r:
+                configs[c]["step_graph_ms"] = r["step_graph_ms"]
+            configs[c]["gpairs_evaluated_per_s_fwd"] = r["pairs_evaluated"] / r["fwd_ms"] / 1e6
+            configs[c]["gpairs_evaluated_per_s_bwd"] = r["pairs_evaluated"] / r["bwd_ms"] / 1e6
+
     if rank == 0:
         line = {
             "metric": METRIC,
@@ -483,7 +542,8 @@ def main():
                        "pairs_evaluated_per_pass": P_total_eval,
                        "parallelism": (f"{args.partition} x{world}" if world > 1
                                        else "single GPU"),
-                       "seam_gaussians": int(seam_idx.numel()) if seam_idx is not None else 0,
+                       "halo_gaussians_rank0": plan.m if plan else None,
+                       "seam_exchange_bytes_rank0": plan.exchange_bytes() if plan else None,
                        "l2": "working set > 126 MB L2 (params 1.6 GB, image 2.1 GB); no flush"},
             "gpairs_per_s": 2 * P_total / (ms_step * 1e-3) / 1e9,
             "gpairs_evaluated_per_s": 2 * P_total_eval / (ms_step * 1e-3) / 1e9,
@@ -494,6 +554,7 @@ def main():
             "roofline": roof,
             "e2e": e2e,
             "cpu_baseline": cpu,
+            "configs": configs,
             "lib": gsr.version(),
         }
         print(json.dumps(line), flush=True)

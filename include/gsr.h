@@ -90,6 +90,11 @@ const char* gsr_version(void);
 /* Hs = floor(s*H), Ws = floor(s*W) in fp64 (reading R4). GSR_EINVAL on bad arguments. */
 gsr_status gsr_out_dims(int32_t lr_h, int32_t lr_w, double scale, int32_t* out_h, int32_t* out_w);
 
+/* Scale-vector form (R22): Hs = floor(s_y H), Ws = floor(s_x W) in fp64 (scale_y = 0: s_y =
+ * s_x); only these two are checked against the limits. GSR_EINVAL on bad arguments. */
+gsr_status gsr_out_dims_v(int32_t lr_h, int32_t lr_w, double scale_x, double scale_y,
+                          int32_t* out_h, int32_t* out_w);
+
 /* Device workspace needed by the forward or backward of one batched call (bytes, 256-aligned
  * internally). Returns 0 if the arguments are invalid. The same size serves both passes. */
 size_t gsr_workspace_bytes_batched(const gsr_image* imgs, int32_t n_imgs, int64_t n_total,
@@ -196,6 +201,41 @@ gsr_status gsr_finalize_grads_ex(const void* alpha, const void* mu, const void* 
                                  float* d_sigma, float* d_rho, float* d_color, uint32_t flags,
                                  void* stream);
 
+/* ---- subset mode: one rank's halo of a row-band shard ------------------------
+ * A rank that renders HR rows [b_r, b_{r+1}) of an image needs only the Gaussians whose support
+ * rows meet them (its halo, gsr_band_span_*). The _subset entry points take that list instead
+ * of scanning all n_total Gaussians: idx[0..m) (device int32, ascending, each inside its image's
+ * [g_off, g_off + g_cnt); m <= n_total) selects the Gaussians that are binned and rendered; the
+ * parameter arrays and gsr_image ranges stay those of the whole batch (global indices). Every
+ * per-Gaussian OUTPUT is compact: entry t belongs to Gaussian idx[t]:
+ *   gsr_render_bwd_moments_subset accumulates (+=) moments[t][8] (float64, [m][8], caller
+ *     zeroes), with the layout of gsr_render_bwd_moments_batched;
+ *   gsr_finalize_grads_subset writes d_alpha[t], d_mu[t][2], d_sigma[t][2], d_rho[t],
+ *     d_color[t][3] (float32, compact [m] arrays) from moments[t] (same closed forms as
+ *     gsr_finalize_grads).
+ * A Gaussian left out of idx contributes nothing to the images (exactly what the render does
+ * for a Gaussian whose support misses the band, R21). Workspace: gsr_workspace_bytes_subset
+ * (sized by m). Flags and errors as for the _ex entry points; GSR_REUSE_BINNING requires the
+ * preceding call to have used the same idx. */
+size_t gsr_workspace_bytes_subset(const gsr_image* imgs, int32_t n_imgs, int64_t n_total,
+                                  int64_t m, double ratio);
+gsr_status gsr_render_fwd_subset(const void* alpha, const void* mu, const void* sigma,
+                                 const void* rho, const void* color, int64_t n_total,
+                                 const int32_t* idx, int64_t m, const gsr_image* imgs,
+                                 int32_t n_imgs, double ratio, void* out, void* workspace,
+                                 size_t workspace_bytes, uint32_t flags, void* stream);
+gsr_status gsr_render_bwd_moments_subset(const void* alpha, const void* mu, const void* sigma,
+                                         const void* rho, const void* color, int64_t n_total,
+                                         const int32_t* idx, int64_t m, const gsr_image* imgs,
+                                         int32_t n_imgs, double ratio, const void* grad_out,
+                                         double* moments, void* workspace,
+                                         size_t workspace_bytes, uint32_t flags, void* stream);
+gsr_status gsr_finalize_grads_subset(const void* alpha, const void* mu, const void* sigma,
+                                     const void* rho, const void* color, int64_t n_total,
+                                     const int32_t* idx, int64_t m, const double* moments,
+                                     float* d_alpha, float* d_mu, float* d_sigma, float* d_rho,
+                                     float* d_color, uint32_t flags, void* stream);
+
 /* ---- training-step adjacency ------------------------------------------
  * One fused training step of the rasterizer for the paper's L1 objective, from the RAW
  * outputs of the Gaussian Primary Head:
@@ -245,6 +285,47 @@ gsr_status gsr_pair_count_batched_ex(const void* alpha, const void* mu, const vo
                                      const gsr_image* imgs, int32_t n_imgs, double ratio,
                                      uint32_t flags, int64_t* d_pairs, void* workspace,
                                      size_t workspace_bytes, void* stream);
+
+/* ---- K7: row-band planning for the multi-GPU path ---------------------------
+ * The row-band shard gives rank r the HR rows [b_r, b_{r+1}) of every image; the boundaries
+ * equalise the work (pairs) per rank, and the Gaussians whose support rows (R21) span a boundary
+ * ("seam" Gaussians) have partial gradients on several ranks. Both need Alg. 1's window rect
+ * (readings R1/R2) and the support box (R21) per Gaussian; these entry points compute
+ * them with the render kernels' own code. Each comes as a device variant (params and outputs are
+ * device pointers, enqueued on `stream`) and a host variant (_host: params and outputs are HOST
+ * pointers, computed on the calling CPU thread, no CUDA call; the same arithmetic).
+ *
+ * gsr_row_pair_counts_*: rowpairs[roff_k + (y - row_begin_k)] for y in image k's band
+ *   [row_begin_k, row_end_k), roff_k = sum_{j<k} (row_end_j - row_begin_j): the number of pairs
+ *   of HR row y, sum_i [y0_i <= y <= y1_i] (x1_i - x0_i + 1) over the valid Gaussians of the
+ *   image, with the window rect (flags 0; sums to gsr_pair_count_batched) or the support rect
+ *   (GSR_SUPPORT; the pairs the kernels evaluate). int64, overwritten. Flags: GSR_SUPPORT,
+ *   GSR_PARAMS_BF16.
+ * gsr_band_span_*: bounds[k*(n_bands+1) + g] (HOST array, n_imgs x (n_bands+1), nondecreasing,
+ *   inside image k's band) are the band boundaries of image k, 1 <= n_bands <= 64. For every
+ *   Gaussian i: span[2i] = first and span[2i+1] = last band g whose rows [b_g, b_{g+1}) meet its
+ *   clipped support rows widened by `margin` >= 0 rows ([y0 - margin, y1 + margin]); {-1, -1} if
+ *   it is invalid (R20), not owned by an image, or its support rect is empty. Seam Gaussian:
+ *   first < last. Halo of band r: first <= r <= last. int16, overwritten. Flags:
+ *   GSR_PARAMS_BF16. */
+gsr_status gsr_row_pair_counts_batched(const void* alpha, const void* mu, const void* sigma,
+                                       const void* rho, const void* color, int64_t n_total,
+                                       const gsr_image* imgs, int32_t n_imgs, double ratio,
+                                       uint32_t flags, int64_t* rowpairs, void* stream);
+gsr_status gsr_row_pair_counts_host(const void* alpha, const void* mu, const void* sigma,
+                                    const void* rho, const void* color, int64_t n_total,
+                                    const gsr_image* imgs, int32_t n_imgs, double ratio,
+                                    uint32_t flags, int64_t* rowpairs);
+gsr_status gsr_band_span_batched(const void* alpha, const void* mu, const void* sigma,
+                                 const void* rho, const void* color, int64_t n_total,
+                                 const gsr_image* imgs, int32_t n_imgs, double ratio,
+                                 uint32_t flags, const int32_t* bounds, int32_t n_bands,
+                                 int32_t margin, int16_t* span, void* stream);
+gsr_status gsr_band_span_host(const void* alpha, const void* mu, const void* sigma,
+                              const void* rho, const void* color, int64_t n_total,
+                              const gsr_image* imgs, int32_t n_imgs, double ratio,
+                              uint32_t flags, const int32_t* bounds, int32_t n_bands,
+                              int32_t margin, int16_t* span);
 
 /* ---- introspection for the parity tests (same kernels as the render path) ---------------- */
 

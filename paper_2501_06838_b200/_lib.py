@@ -17,14 +17,16 @@ _ERR = {GSR_EINVAL: "GSR_EINVAL (invalid argument)", GSR_EWORKSPACE: "GSR_EWORKS
 MAX_IMAGES = 64
 
 # Every symbol include/gsr.h declares (checked by tests/test_abi.py).
-EXPORTS = ["gsr_version", "gsr_out_dims", "gsr_workspace_bytes_batched", "gsr_workspace_bytes",
+EXPORTS = ["gsr_version", "gsr_out_dims", "gsr_out_dims_v", "gsr_workspace_bytes_batched", "gsr_workspace_bytes",
            "gsr_render_fwd", "gsr_render_bwd", "gsr_render_fwd_batched", "gsr_render_bwd_batched",
            "gsr_render_bwd_moments_batched", "gsr_finalize_grads", "gsr_pair_count_batched",
            "gsr_debug_rects", "gsr_debug_tile_lists", "gsr_tile_shape", "gsr_profile_enable",
            "gsr_profile_collect", "gsr_render_bwd_batched_ex", "gsr_render_bwd_moments_batched_ex",
            "gsr_train_workspace_bytes_batched", "gsr_train_step_l1_batched",
            "gsr_pair_count_batched_ex", "gsr_debug_rects_ex", "gsr_render_fwd_batched_ex",
-           "gsr_finalize_grads_ex"]
+           "gsr_finalize_grads_ex", "gsr_row_pair_counts_batched", "gsr_row_pair_counts_host",
+           "gsr_band_span_batched", "gsr_band_span_host", "gsr_workspace_bytes_subset",
+           "gsr_render_fwd_subset", "gsr_render_bwd_moments_subset", "gsr_finalize_grads_subset"]
 GSR_REUSE_BINNING = 0x1
 GSR_SUPPORT = 0x2
 GSR_OUT_BF16 = 0x4
@@ -67,6 +69,8 @@ def load(path: Path | str | None = None):
     sig = {
         "gsr_version": ([], ctypes.c_char_p),
         "gsr_out_dims": ([_I32, _I32, _D, ctypes.POINTER(_I32), ctypes.POINTER(_I32)], None),
+        "gsr_out_dims_v": ([_I32, _I32, _D, _D, ctypes.POINTER(_I32), ctypes.POINTER(_I32)],
+                           None),
         "gsr_workspace_bytes_batched": ([_IMGP, _I32, _I64, _D], _SZ),
         "gsr_workspace_bytes": ([_I64, _I32, _I32, _D, _D], _SZ),
         "gsr_render_fwd": (par + [_I64, _I32, _I32, _D, _D, _P, _P, _SZ, _P], None),
@@ -95,6 +99,20 @@ def load(path: Path | str | None = None):
         "gsr_debug_rects": (par + [_I64, _I32, _I32, _D, _D, _P, _P], None),
         "gsr_debug_rects_ex": (par + [_I64, _I32, _I32, _D, _D, ctypes.c_uint32, _P, _P], None),
         "gsr_debug_tile_lists": (par + [_I64, _I32, _I32, _D, _D, _P, _P, _P, _P, _SZ, _P], None),
+        "gsr_row_pair_counts_batched": (par + [_I64, _IMGP, _I32, _D, ctypes.c_uint32, _P, _P],
+                                        None),
+        "gsr_row_pair_counts_host": (par + [_I64, _IMGP, _I32, _D, ctypes.c_uint32, _P], None),
+        "gsr_band_span_batched": (par + [_I64, _IMGP, _I32, _D, ctypes.c_uint32, _P, _I32, _I32,
+                                         _P, _P], None),
+        "gsr_band_span_host": (par + [_I64, _IMGP, _I32, _D, ctypes.c_uint32, _P, _I32, _I32, _P],
+                               None),
+        "gsr_workspace_bytes_subset": ([_IMGP, _I32, _I64, _I64, _D], _SZ),
+        "gsr_render_fwd_subset": (par + [_I64, _P, _I64, _IMGP, _I32, _D, _P, _P, _SZ,
+                                         ctypes.c_uint32, _P], None),
+        "gsr_render_bwd_moments_subset": (par + [_I64, _P, _I64, _IMGP, _I32, _D, _P, _P, _P, _SZ,
+                                                 ctypes.c_uint32, _P], None),
+        "gsr_finalize_grads_subset": (par + [_I64, _P, _I64, _P, _P, _P, _P, _P, _P,
+                                             ctypes.c_uint32, _P], None),
         "gsr_tile_shape": ([ctypes.POINTER(_I32)] * 4, "void"),
         "gsr_profile_enable": ([_I32], None),
         "gsr_profile_collect": ([_P, _P, _P, _I32], None),
@@ -132,13 +150,13 @@ def images_array(imgs):
 def out_dims(H: int, W: int, s: float, s_y: float | None = None):
     """(Hs, Ws) = (floor(s_y H), floor(s W)) (R4, R22; s_y None or 0: s_y = s)."""
     h, w = _I32(), _I32()
-    check(load().gsr_out_dims(int(H), int(W), float(s), ctypes.byref(h), ctypes.byref(w)),
-          "gsr_out_dims")
-    if s_y:
-        h2, w2 = _I32(), _I32()
-        check(load().gsr_out_dims(int(H), int(W), float(s_y), ctypes.byref(h2),
-                                  ctypes.byref(w2)), "gsr_out_dims")
-        return h2.value, w.value
+    lib = load()
+    if getattr(lib, "gsr_out_dims_v", None) is None and not s_y:     # an older build (A/B runs)
+        check(lib.gsr_out_dims(int(H), int(W), float(s), ctypes.byref(h), ctypes.byref(w)),
+              "gsr_out_dims")
+        return h.value, w.value
+    check(lib.gsr_out_dims_v(int(H), int(W), float(s), float(s_y or 0.0), ctypes.byref(h),
+                             ctypes.byref(w)), "gsr_out_dims_v")
     return h.value, w.value
 
 

@@ -10,10 +10,13 @@ PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libgsr.so"
 ROOT = PKG.parent
-SOURCES = ["binning.cu", "render_fwd.cu", "render_bwd.cu", "train.cu", "gsr_abi.cu"]
+SOURCES = ["binning.cu", "render_fwd.cu", "render_bwd.cu", "train.cu", "plan.cu", "gsr_abi.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
+# host code: no FMA contraction (the K7 planner evaluates the fp64 rect formulas of reading R2 on
+# the CPU with the same operation order as the kernels' explicit __dmul_rn/__dadd_rn)
+FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-ffp-contract=off",
+         "-Xptxas", "-v",
          "--expt-relaxed-constexpr", "-I", str(ROOT / "include")]
 # experiments only (A/B builds into another directory): extra -D flags
 EXTRA = os.environ.get("GSR_NVCC_EXTRA", "").split()

@@ -28,16 +28,20 @@ long long rs_blocks(long long n) { return (n + RS_BLOCK - 1) / RS_BLOCK; }
 long long scan_blocks(long long n) { return (n + SCAN_BLOCK - 1) / SCAN_BLOCK; }
 
 // ---- K1: keys ----------------------------------------------------------------------------
+// Binned positions t = 0..n-1 stand for Gaussian i = gidx[t] (subset mode: a rank's halo, see
+// gsr_render_fwd_subset) or i = t (gidx == nullptr); vals/perm hold t, so every per-Gaussian
+// output of the backward (moments, gradients) is indexed by t.
 template <class T>
 __global__ void k_keys(const T* __restrict__ alpha, const T* __restrict__ mu,
                        const T* __restrict__ sigma, const T* __restrict__ rho,
                        const T* __restrict__ color, long long n, ImgTable tab,
-                       uint32_t* __restrict__ keys, int* __restrict__ vals,
-                       int* __restrict__ ext) {
-    long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+                       const int* __restrict__ gidx, uint32_t* __restrict__ keys,
+                       int* __restrict__ vals, int* __restrict__ ext) {
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     uint32_t key = (uint32_t)tab.total_cells;
     int k = -1, wx = 0, wy = 0;
-    if (i < n) {
+    if (t < n) {
+        const long long i = gidx ? (long long)gidx[t] : t;
         k = find_image_by_gauss(tab, i);
         if (k >= 0) {
             const DevImg& im = tab.img[k];
@@ -55,18 +59,15 @@ __global__ void k_keys(const T* __restrict__ alpha, const T* __restrict__ mu,
                 }
             }
         }
-        keys[i] = key;
-        vals[i] = (int)i;
+        keys[t] = key;
+        vals[t] = (int)t;
     }
     // per-image max support extent: warp max over lanes of the same image, one atomic each
+    // (each group of lanes with the same image reduces with its own group-uniform mask)
     const unsigned full = 0xffffffffu;
     const unsigned same = __match_any_sync(full, k);
-    int mwx = wx, mwy = wy;
-    for (unsigned m = same; m; m &= m - 1) {
-        const int l = __ffs(m) - 1;
-        mwx = max(mwx, __shfl_sync(full, wx, l));
-        mwy = max(mwy, __shfl_sync(full, wy, l));
-    }
+    const int mwx = (int)__reduce_max_sync(same, (unsigned)wx);
+    const int mwy = (int)__reduce_max_sync(same, (unsigned)wy);
     if (k >= 0 && (same & ((1u << (threadIdx.x & 31)) - 1u)) == 0 && (mwx | mwy)) {
         atomicMax(&ext[2 * k], mwx);
         atomicMax(&ext[2 * k + 1], mwy);
@@ -241,12 +242,13 @@ template <class T>
 __global__ void k_records(const T* __restrict__ alpha, const T* __restrict__ mu,
                           const T* __restrict__ sigma, const T* __restrict__ rho,
                           const T* __restrict__ color, long long n, ImgTable tab,
-                          const uint32_t* __restrict__ keys, const int* __restrict__ perm,
-                          float4* __restrict__ rec, int4* __restrict__ rects) {
+                          const int* __restrict__ gidx, const uint32_t* __restrict__ keys,
+                          const int* __restrict__ perm, float4* __restrict__ rec,
+                          int4* __restrict__ rects, uint8_t* __restrict__ cls) {
     long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= n) return;
     if (keys[p] >= (uint32_t)tab.total_cells) return;
-    long long i = perm[p];
+    const long long i = gidx ? (long long)gidx[perm[p]] : (long long)perm[p];
     int k = find_image_by_gauss(tab, i);
     const DevImg& im = tab.img[k];
     float mxf = ldf(mu[2 * i]), myf = ldf(mu[2 * i + 1]);
@@ -289,6 +291,7 @@ __global__ void k_records(const T* __restrict__ alpha, const T* __restrict__ mu,
     unsigned sxs = (unsigned)sr.x0 | ((unsigned)sr.x1 << 16);
     unsigned sys = (unsigned)sr.y0 | ((unsigned)sr.y1 << 16);
     rects[p] = make_int4((int)sxs, (int)sys, (int)xs, (int)ys);
+    cls[p] = rec_ok ? 1 : 0;
 }
 
 // ---- pair count ---------------------------------------------------------------------------
@@ -392,6 +395,7 @@ size_t binning_bytes(long long n, int total_cells, int total_tiles) {
     b += align256(sizeof(int) * (size_t)(total_cells + 1));     // cell_start
     b += align256(sizeof(float4) * REC_F4 * (size_t)n);         // records
     b += align256(sizeof(int4) * (size_t)n);                    // rect stream
+    b += align256((size_t)n);                                   // record classes
     b += align256(sizeof(double) * 8 * (size_t)n);              // moments
     b += align256(sizeof(unsigned long long) * 4);              // counters
     b += align256(sizeof(int) * (size_t)(total_tiles + 1));     // debug tile offsets
@@ -414,6 +418,7 @@ void carve_workspace(void* base, long long n, int total_cells, int total_tiles, 
     ws->cell_start = (int*)take(sizeof(int) * (size_t)(total_cells + 1));
     ws->rec = (float4*)take(sizeof(float4) * REC_F4 * (size_t)n);
     ws->rects = (int4*)take(sizeof(int4) * (size_t)n);
+    ws->cls = (uint8_t*)take((size_t)n);
     ws->moments = (double*)take(sizeof(double) * 8 * (size_t)n);
     ws->counter = (unsigned long long*)take(sizeof(unsigned long long) * 4);
     ws->tile_off = (int*)take(sizeof(int) * (size_t)(total_tiles + 1));
@@ -432,14 +437,14 @@ cudaError_t exclusive_scan_i32(const int* in, int* out, long long n, int* tmp, c
 
 template <class T>
 cudaError_t bin_gaussians_t(const T* alpha, const T* mu, const T* sigma, const T* rho,
-                            const T* color, long long n,
+                            const T* color, long long n, const int* gidx,
                           const ImgTable& tab, Workspace& ws, int** perm_out,
                           uint32_t** keys_sorted_out, cudaStream_t st) {
     cudaMemsetAsync(ws.ext, 0, sizeof(int) * 2 * MAX_IMAGES, st);
     if (n > 0) {
         count_launches(1);
-        k_keys<<<grid1d(n, 256), 256, 0, st>>>(alpha, mu, sigma, rho, color, n, tab, ws.keys_a,
-                                               ws.vals_a, ws.ext);
+        k_keys<<<grid1d(n, 256), 256, 0, st>>>(alpha, mu, sigma, rho, color, n, tab, gidx,
+                                               ws.keys_a, ws.vals_a, ws.ext);
         int bits = 32 - __builtin_clz((unsigned)tab.total_cells | 1u);
         int passes = (bits + 7) / 8;
         long long nb = rs_blocks(n);
@@ -459,8 +464,9 @@ cudaError_t bin_gaussians_t(const T* alpha, const T* mu, const T* sigma, const T
         count_launches(2);
         k_cell_start<<<grid1d(n + 1, 256), 256, 0, st>>>(kin, n, tab.total_cells,
                                                          ws.cell_start);
-        k_records<<<grid1d(n, 256), 256, 0, st>>>(alpha, mu, sigma, rho, color, n, tab, kin, vin,
-                                                   ws.rec, ws.rects);
+        k_records<<<grid1d(n, 256), 256, 0, st>>>(alpha, mu, sigma, rho, color, n, tab, gidx,
+                                                   kin, vin,
+                                                   ws.rec, ws.rects, ws.cls);
         *perm_out = vin;
         *keys_sorted_out = kin;
     } else {
@@ -484,14 +490,15 @@ void binned_pointers(const ImgTable& tab, long long n, const Workspace& ws, int*
 
 cudaError_t bin_gaussians(const void* alpha, const void* mu, const void* sigma, const void* rho,
                           const void* color, long long n, const ImgTable& tab, Workspace& ws,
-                          int** perm_out, uint32_t** keys_sorted_out, cudaStream_t st) {
+                          int** perm_out, uint32_t** keys_sorted_out, cudaStream_t st,
+                          const int* gidx) {
     if (tab.params_bf16) {
         using B = __nv_bfloat16;
         return bin_gaussians_t((const B*)alpha, (const B*)mu, (const B*)sigma, (const B*)rho,
-                               (const B*)color, n, tab, ws, perm_out, keys_sorted_out, st);
+                               (const B*)color, n, gidx, tab, ws, perm_out, keys_sorted_out, st);
     }
     return bin_gaussians_t((const float*)alpha, (const float*)mu, (const float*)sigma,
-                           (const float*)rho, (const float*)color, n, tab, ws, perm_out,
+                           (const float*)rho, (const float*)color, n, gidx, tab, ws, perm_out,
                            keys_sorted_out, st);
 }
 

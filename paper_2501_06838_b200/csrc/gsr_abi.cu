@@ -170,22 +170,27 @@ struct Prepared {
     uint32_t* keys = nullptr;
 };
 
+// gidx/m: subset mode (bin only the m Gaussians gidx[0..m), device int32, ascending, each owned
+// by an image); gidx == nullptr: all n_total (m ignored)
 gsr_status prepare(const void* alpha, const void* mu, const void* sigma, const void* rho,
                    const void* color, int64_t n_total, const gsr_image* imgs, int32_t n_imgs,
                    double ratio, void* workspace, size_t workspace_bytes, cudaStream_t st,
-                   Prepared* P, bool bin, uint32_t flags = 0u) {
+                   Prepared* P, bool bin, uint32_t flags = 0u, const int32_t* gidx = nullptr,
+                   int64_t m = -1) {
     gsr_status s = build_table(imgs, n_imgs, n_total, ratio, &P->tab, flags);
     if (s != GSR_OK) return s;
     if (!params_ok(alpha, mu, sigma, rho, color, n_total)) return GSR_EINVAL;
-    if (!workspace || workspace_bytes < ws_bytes(P->tab, n_total)) return GSR_EWORKSPACE;
-    carve_workspace(workspace, n_total, P->tab.total_cells, P->tab.total_tiles, &P->ws);
+    const int64_t nb = gidx ? m : n_total;
+    if (gidx && (m < 0 || m > n_total)) return GSR_EINVAL;
+    if (!workspace || workspace_bytes < ws_bytes(P->tab, nb)) return GSR_EWORKSPACE;
+    carve_workspace(workspace, nb, P->tab.total_cells, P->tab.total_tiles, &P->ws);
     if (!bin) {
-        binned_pointers(P->tab, n_total, P->ws, &P->perm, &P->keys);
+        binned_pointers(P->tab, nb, P->ws, &P->perm, &P->keys);
         return GSR_OK;
     }
     int h = prof_begin(0, st);
-    cudaError_t e = bin_gaussians(alpha, mu, sigma, rho, color, n_total, P->tab, P->ws, &P->perm,
-                                  &P->keys, st);
+    cudaError_t e = bin_gaussians(alpha, mu, sigma, rho, color, nb, P->tab, P->ws, &P->perm,
+                                  &P->keys, st, gidx);
     prof_end(h, st);
     return e == cudaSuccess ? GSR_OK : GSR_ECUDA;
 }
@@ -238,6 +243,19 @@ gsr_status gsr_out_dims(int32_t lr_h, int32_t lr_w, double scale, int32_t* out_h
                         int32_t* out_w) {
     if (lr_h < 1 || lr_w < 1 || !std::isfinite(scale) || !(scale >= 1.0)) return GSR_EINVAL;
     double h = std::floor(scale * (double)lr_h), w = std::floor(scale * (double)lr_w);
+    if (h > MAX_DIM || w > MAX_DIM) return GSR_EINVAL;
+    if (out_h) *out_h = (int32_t)h;
+    if (out_w) *out_w = (int32_t)w;
+    return GSR_OK;
+}
+
+gsr_status gsr_out_dims_v(int32_t lr_h, int32_t lr_w, double scale_x, double scale_y,
+                          int32_t* out_h, int32_t* out_w) {
+    if (lr_h < 1 || lr_w < 1 || !std::isfinite(scale_x) || !(scale_x >= 1.0)) return GSR_EINVAL;
+    if (!std::isfinite(scale_y) || scale_y < 0.0 || (scale_y > 0.0 && scale_y < 1.0))
+        return GSR_EINVAL;
+    const double sy = scale_y > 0.0 ? scale_y : scale_x;              // reading R22
+    double h = std::floor(sy * (double)lr_h), w = std::floor(scale_x * (double)lr_w);
     if (h > MAX_DIM || w > MAX_DIM) return GSR_EINVAL;
     if (out_h) *out_h = (int32_t)h;
     if (out_w) *out_w = (int32_t)w;
@@ -337,6 +355,65 @@ gsr_status gsr_finalize_grads_ex(const void* alpha, const void* mu, const void* 
     return finish(launch_finalize(alpha, mu, sigma, rho, color, n_total, moments, d_alpha, d_mu,
                                   d_sigma, d_rho, d_color, (cudaStream_t)stream, nullptr,
                                   (flags & GSR_PARAMS_BF16) != 0));
+}
+
+// ---- subset (index-list) mode: one rank's halo of a row-band shard -------------------------
+size_t gsr_workspace_bytes_subset(const gsr_image* imgs, int32_t n_imgs, int64_t n_total,
+                                  int64_t m, double ratio) {
+    ImgTable local;
+    if (m < 0 || m > n_total) return 0;
+    if (build_table(imgs, n_imgs, n_total, ratio, &local) != GSR_OK) return 0;
+    return ws_bytes(local, m);
+}
+
+gsr_status gsr_render_fwd_subset(const void* alpha, const void* mu, const void* sigma,
+                                 const void* rho, const void* color, int64_t n_total,
+                                 const int32_t* idx, int64_t m, const gsr_image* imgs,
+                                 int32_t n_imgs, double ratio, void* out, void* workspace,
+                                 size_t workspace_bytes, uint32_t flags, void* stream) {
+    if (!out || (!idx && m > 0)) return GSR_EINVAL;
+    if (flags & ~(GSR_OUT_BF16 | GSR_OUT_CHW | GSR_PARAMS_BF16)) return GSR_EINVAL;
+    cudaStream_t st = (cudaStream_t)stream;
+    Prepared P;
+    static const int32_t dummy = 0;
+    gsr_status s = prepare(alpha, mu, sigma, rho, color, n_total, imgs, n_imgs, ratio, workspace,
+                           workspace_bytes, st, &P, true, flags, idx ? idx : &dummy, m);
+    if (s != GSR_OK) return s;
+    return finish(launch_render_fwd(P.tab, P.ws, (float*)out, st));
+}
+
+gsr_status gsr_render_bwd_moments_subset(const void* alpha, const void* mu, const void* sigma,
+                                         const void* rho, const void* color, int64_t n_total,
+                                         const int32_t* idx, int64_t m, const gsr_image* imgs,
+                                         int32_t n_imgs, double ratio, const void* grad_out,
+                                         double* moments, void* workspace,
+                                         size_t workspace_bytes, uint32_t flags, void* stream) {
+    if (!grad_out || (!moments && m > 0) || (!idx && m > 0)) return GSR_EINVAL;
+    if (flags & ~(GSR_REUSE_BINNING | GSR_OUT_BF16 | GSR_OUT_CHW | GSR_PARAMS_BF16))
+        return GSR_EINVAL;
+    cudaStream_t st = (cudaStream_t)stream;
+    Prepared P;
+    static const int32_t dummy = 0;
+    gsr_status s = prepare(alpha, mu, sigma, rho, color, n_total, imgs, n_imgs, ratio, workspace,
+                           workspace_bytes, st, &P, !(flags & GSR_REUSE_BINNING), flags,
+                           idx ? idx : &dummy, m);
+    if (s != GSR_OK) return s;
+    return finish(launch_render_bwd_moments(P.tab, P.ws, P.perm, (const float*)grad_out, moments,
+                                            st));
+}
+
+gsr_status gsr_finalize_grads_subset(const void* alpha, const void* mu, const void* sigma,
+                                     const void* rho, const void* color, int64_t n_total,
+                                     const int32_t* idx, int64_t m, const double* moments,
+                                     float* d_alpha, float* d_mu, float* d_sigma, float* d_rho,
+                                     float* d_color, uint32_t flags, void* stream) {
+    if (n_total < 0 || m < 0 || m > n_total || (flags & ~GSR_PARAMS_BF16)) return GSR_EINVAL;
+    if (m > 0 && (!idx || !params_ok(alpha, mu, sigma, rho, color, n_total) || !moments ||
+                  !d_alpha || !d_mu || !d_sigma || !d_rho || !d_color))
+        return GSR_EINVAL;
+    return finish(launch_finalize(alpha, mu, sigma, rho, color, m, moments, d_alpha, d_mu,
+                                  d_sigma, d_rho, d_color, (cudaStream_t)stream, nullptr,
+                                  (flags & GSR_PARAMS_BF16) != 0, idx));
 }
 
 gsr_status gsr_render_bwd_batched_ex(const void* alpha, const void* mu, const void* sigma,
@@ -480,6 +557,107 @@ gsr_status gsr_pair_count_batched(const float* alpha, const float* mu, const flo
                                   void* stream) {
     return gsr_pair_count_batched_ex(alpha, mu, sigma, rho, color, n_total, imgs, n_imgs, ratio,
                                      0u, d_pairs, workspace, workspace_bytes, stream);
+}
+
+// ---- K7 band planning (plan.cu) ----------------------------------------------------------
+static gsr_status plan_prepare(const void* alpha, const void* mu, const void* sigma,
+                               const void* rho, const void* color, int64_t n_total,
+                               const gsr_image* imgs, int32_t n_imgs, double ratio,
+                               uint32_t flags, uint32_t allowed, ImgTable* tab) {
+    if (flags & ~allowed) return GSR_EINVAL;
+    gsr_status s = build_table(imgs, n_imgs, n_total, ratio, tab, flags);
+    if (s != GSR_OK) return s;
+    if (!params_ok(alpha, mu, sigma, rho, color, n_total)) return GSR_EINVAL;
+    return GSR_OK;
+}
+
+static void row_offsets(const ImgTable& tab, RowOff* ro) {
+    std::memset(ro, 0, sizeof(*ro));
+    for (int k = 0; k < tab.n_imgs; ++k)
+        ro->off[k + 1] = ro->off[k] + (tab.img[k].row_end - tab.img[k].row_begin);
+}
+
+static gsr_status band_table(const ImgTable& tab, const int32_t* bounds, int32_t n_bands,
+                             int32_t margin, BandTable* bt) {
+    if (!bounds || n_bands < 1 || n_bands > MAX_BANDS || margin < 0) return GSR_EINVAL;
+    std::memset(bt, 0, sizeof(*bt));
+    bt->G = n_bands;
+    bt->margin = margin;
+    for (int k = 0; k < tab.n_imgs; ++k) {
+        const int32_t* b = bounds + (size_t)k * (n_bands + 1);
+        for (int g = 0; g <= n_bands; ++g) {
+            if (b[g] < tab.img[k].row_begin || b[g] > tab.img[k].row_end) return GSR_EINVAL;
+            if (g > 0 && b[g] < b[g - 1]) return GSR_EINVAL;
+            bt->b[k][g] = b[g];
+        }
+    }
+    return GSR_OK;
+}
+
+gsr_status gsr_row_pair_counts_batched(const void* alpha, const void* mu, const void* sigma,
+                                       const void* rho, const void* color, int64_t n_total,
+                                       const gsr_image* imgs, int32_t n_imgs, double ratio,
+                                       uint32_t flags, int64_t* rowpairs, void* stream) {
+    ImgTable tab;
+    gsr_status s = plan_prepare(alpha, mu, sigma, rho, color, n_total, imgs, n_imgs, ratio, flags,
+                                GSR_SUPPORT | GSR_PARAMS_BF16, &tab);
+    if (s != GSR_OK) return s;
+    if (!rowpairs) return GSR_EINVAL;
+    RowOff ro;
+    row_offsets(tab, &ro);
+    return finish(launch_row_pair_counts(alpha, mu, sigma, rho, color, n_total, tab,
+                                         (flags & GSR_SUPPORT) != 0, ro, (long long*)rowpairs,
+                                         (cudaStream_t)stream));
+}
+
+gsr_status gsr_row_pair_counts_host(const void* alpha, const void* mu, const void* sigma,
+                                    const void* rho, const void* color, int64_t n_total,
+                                    const gsr_image* imgs, int32_t n_imgs, double ratio,
+                                    uint32_t flags, int64_t* rowpairs) {
+    ImgTable tab;
+    gsr_status s = plan_prepare(alpha, mu, sigma, rho, color, n_total, imgs, n_imgs, ratio, flags,
+                                GSR_SUPPORT | GSR_PARAMS_BF16, &tab);
+    if (s != GSR_OK) return s;
+    if (!rowpairs) return GSR_EINVAL;
+    RowOff ro;
+    row_offsets(tab, &ro);
+    row_pair_counts_host(alpha, mu, sigma, rho, color, n_total, tab, (flags & GSR_SUPPORT) != 0,
+                         ro, (long long*)rowpairs);
+    return GSR_OK;
+}
+
+gsr_status gsr_band_span_batched(const void* alpha, const void* mu, const void* sigma,
+                                 const void* rho, const void* color, int64_t n_total,
+                                 const gsr_image* imgs, int32_t n_imgs, double ratio,
+                                 uint32_t flags, const int32_t* bounds, int32_t n_bands,
+                                 int32_t margin, int16_t* span, void* stream) {
+    ImgTable tab;
+    gsr_status s = plan_prepare(alpha, mu, sigma, rho, color, n_total, imgs, n_imgs, ratio, flags,
+                                GSR_PARAMS_BF16, &tab);
+    if (s != GSR_OK) return s;
+    if (!span && n_total > 0) return GSR_EINVAL;
+    std::vector<BandTable> bt(1);   // 16.6 KB: host heap, not the caller's stack
+    s = band_table(tab, bounds, n_bands, margin, bt.data());
+    if (s != GSR_OK) return s;
+    return finish(launch_band_span(alpha, mu, sigma, rho, color, n_total, tab, bt[0], span,
+                                   (cudaStream_t)stream));
+}
+
+gsr_status gsr_band_span_host(const void* alpha, const void* mu, const void* sigma,
+                              const void* rho, const void* color, int64_t n_total,
+                              const gsr_image* imgs, int32_t n_imgs, double ratio,
+                              uint32_t flags, const int32_t* bounds, int32_t n_bands,
+                              int32_t margin, int16_t* span) {
+    ImgTable tab;
+    gsr_status s = plan_prepare(alpha, mu, sigma, rho, color, n_total, imgs, n_imgs, ratio, flags,
+                                GSR_PARAMS_BF16, &tab);
+    if (s != GSR_OK) return s;
+    if (!span && n_total > 0) return GSR_EINVAL;
+    std::vector<BandTable> bt(1);
+    s = band_table(tab, bounds, n_bands, margin, bt.data());
+    if (s != GSR_OK) return s;
+    band_span_host(alpha, mu, sigma, rho, color, n_total, tab, bt[0], span);
+    return GSR_OK;
 }
 
 gsr_status gsr_debug_rects_ex(const float* alpha, const float* mu, const float* sigma,

@@ -23,41 +23,22 @@ constexpr int CELL = 16;       // cell edge (HR px): binning granularity (sort k
 #endif
 constexpr int TILE_W = GSR_BWD_TILE_W;  // backward render tile (HR px, power of 2 >= 16);
 constexpr int TILE_H = GSR_BWD_TILE_H;  // also the debug tile-list tile (TILE_H even)
-// forward: a CTA renders one tile; each of the 4 consumer warps covers the whole tile (lane l
-// owns a FWD_ROWS x FWD_STRIP block at column group l & 3, row group l >> 2) and takes every 4th
-// Gaussian of each staged chunk, so the warps' work is balanced by construction; one extra warp
-// is the TMA producer. Two configurations, chosen per call from the window size:
+// forward: a CTA renders one tile; each of the 4 warps covers the whole tile (lane l owns a
+// ROWS x STRIP block at column group l & 3, row group l >> 2) and takes its own share of the
+// tile's Gaussians, so the warps' work is balanced by construction. Two configurations, chosen
+// per call from the window size:
 //   large (windows >= FWD_SMALL_WINDOW HR px): 2 x 8 px per lane -> 32 x 16 tiles
 //   small (narrow windows, e.g. the x1..x4 training patches): 1 x 4 px per lane -> 16 x 8 tiles,
 //         which wastes far fewer masked evaluations where a window covers only part of a tile.
 struct FwdCfgLarge { static constexpr int ROWS = 2, STRIP = 8, TW = 4 * STRIP, TH = 8 * ROWS; };
 struct FwdCfgSmall { static constexpr int ROWS = 1, STRIP = 4, TW = 4 * STRIP, TH = 8 * ROWS; };
-struct FwdCfgMed { static constexpr int ROWS = 2, STRIP = 4, TW = 4 * STRIP, TH = 8 * ROWS; };
-#ifndef GSR_FWD_MED
-#define GSR_FWD_MED 0             // 1: 16 x 16 tiles (2 x 4 px per lane) instead of 32 x 16
-#endif
-#if GSR_FWD_MED
-using FwdCfgWide = FwdCfgMed;
-#else
 using FwdCfgWide = FwdCfgLarge;
-#endif
-constexpr int FTILE_W = FwdCfgLarge::TW;          // 32
-constexpr int FTILE_H = FwdCfgLarge::TH;          // 16
 constexpr int FWD_SMALL_WINDOW = 48;             // HR px: below this the small tiles are used
 #ifndef GSR_FWD_REC
 #define GSR_FWD_REC 1
 #endif
 constexpr float FWD_REC_DMAX = GSR_FWD_REC ? 1.0f : -1.0f;            // max a1/s for the forward's exp recurrence
-constexpr int FWD_CWARPS = 4;                    // consumer warps
-constexpr int FWD_THREADS = (FWD_CWARPS + 1) * 32;
-#ifndef GSR_FWD_CHUNK
-#define GSR_FWD_CHUNK 128
-#endif
-#ifndef GSR_FWD_STAGES
-#define GSR_FWD_STAGES 3
-#endif
-constexpr int FWD_CHUNK = GSR_FWD_CHUNK;         // records per TMA bulk stage (<= 256)
-constexpr int FWD_STAGES = GSR_FWD_STAGES;
+constexpr int FWD_CWARPS = 4;                    // warps per forward CTA
 #ifndef GSR_BWD_WARPS
 #define GSR_BWD_WARPS 4
 #endif
@@ -100,6 +81,11 @@ struct ImgTable {
     DevImg img[MAX_IMAGES];
 };
 
+// K7 band planning (plan.cu): per-image row offsets of a row-count array, and band boundaries
+constexpr int MAX_BANDS = 64;
+struct RowOff { long long off[MAX_IMAGES + 1]; };
+struct BandTable { int G, margin; int b[MAX_IMAGES][MAX_BANDS + 1]; };
+
 // Sorted record (64 B = REC_F4 x float4), one per binned Gaussian, in cell order, in the form
 // the render kernels consume (K1b, binning.cu):
 //   r0 = {-ax, ay, dl_y, D}         anchor a = rint(s mu) (integer HR px, as float), fp32
@@ -109,6 +95,8 @@ struct ImgTable {
 //   r2 = {c'_g, c'_b, x0|x1<<16, y0|y1<<16}  clipped WINDOW rect (R2): the masks
 //   r3 = {G1, G2, G3, rec}         G_t = 2^(-D^2 t^2) and rec = 1 if D <= FWD_REC_DMAX (forward
 //                                  exponential recurrence), else all 0
+// plus the class byte cls[p] (bit 0 = r3.w != 0: recurrence allowed), read by the forward's
+// filter so that a Gaussian's evaluation path is decided before its record is loaded,
 // plus the rect stream rects[p] = {support x0|x1<<16, support y0|y1<<16, window x, window y}:
 // the support rect (R21) for tile filtering and loop bounds (pairs outside it are exactly 0
 // in fp32), read by the forward producer and the backward scan without touching the records.
@@ -146,20 +134,45 @@ __host__ __device__ inline int find_image_by_gauss(const ImgTable& t, long long 
 }
 
 // ---- the normative window rect (reading R2), fp64, fixed op order, no FMA ---------------
+// Host and device share this code (the host planner K7 of plan.cu runs it on CPU arrays too):
+// on the device the products/sums are the explicit round-to-nearest intrinsics (never fused);
+// the host compiler gets -ffp-contract=off (build.py), so a*b and a-b are single IEEE ops there.
 struct Rect { int x0u, y0u, x1u, y1u, x0, x1, y0, y1; bool nonempty; };
 
-__device__ __forceinline__ double clamp_bound(double v) {
+__host__ __device__ __forceinline__ double rn_mul(double a, double b) {
+#ifdef __CUDA_ARCH__
+    return __dmul_rn(a, b);
+#else
+    return a * b;
+#endif
+}
+__host__ __device__ __forceinline__ double rn_add(double a, double b) {
+#ifdef __CUDA_ARCH__
+    return __dadd_rn(a, b);
+#else
+    return a + b;
+#endif
+}
+__host__ __device__ __forceinline__ double rn_sub(double a, double b) {
+#ifdef __CUDA_ARCH__
+    return __dsub_rn(a, b);
+#else
+    return a - b;
+#endif
+}
+
+__host__ __device__ __forceinline__ double clamp_bound(double v) {
     const double lim = 1073741824.0;  // 2^30
     return v < -lim ? -lim : (v > lim ? lim : v);
 }
 
-__device__ __forceinline__ Rect window_rect(float mux, float muy, const DevImg& im) {
+__host__ __device__ __forceinline__ Rect window_rect(float mux, float muy, const DevImg& im) {
     Rect r;
     double mx = (double)mux, my = (double)muy;
-    double lx = __dmul_rn(im.sx, __dsub_rn(mx, im.hx));
-    double ux = __dmul_rn(im.sx, __dadd_rn(mx, im.hx));
-    double ly = __dmul_rn(im.sy, __dsub_rn(my, im.hy));
-    double uy = __dmul_rn(im.sy, __dadd_rn(my, im.hy));
+    double lx = rn_mul(im.sx, rn_sub(mx, im.hx));
+    double ux = rn_mul(im.sx, rn_add(mx, im.hx));
+    double ly = rn_mul(im.sy, rn_sub(my, im.hy));
+    double uy = rn_mul(im.sy, rn_add(my, im.hy));
     long long ax0 = (long long)floor(clamp_bound(lx)) + 1;
     long long ax1 = (long long)ceil(clamp_bound(ux)) - 1;
     long long ay0 = (long long)floor(clamp_bound(ly)) + 1;
@@ -187,34 +200,34 @@ __device__ __forceinline__ Rect window_rect(float mux, float muy, const DevImg& 
 // and produce the same fp32 results as an evaluation of the whole window.
 constexpr double SUPPORT_SIGMAS = 13.5;
 
-__device__ __forceinline__ Rect support_rect(float mux, float muy, float sxf, float syf,
-                                             const DevImg& im) {
+__host__ __device__ __forceinline__ Rect support_rect(float mux, float muy, float sxf, float syf,
+                                                      const DevImg& im) {
     Rect r = window_rect(mux, muy, im);
     const double mx = (double)mux, my = (double)muy;
-    const double tx = __dmul_rn(SUPPORT_SIGMAS, (double)sxf);
-    const double ty = __dmul_rn(SUPPORT_SIGMAS, (double)syf);
-    const double lx = __dmul_rn(im.sx, __dsub_rn(mx, tx));
-    const double ux = __dmul_rn(im.sx, __dadd_rn(mx, tx));
-    const double ly = __dmul_rn(im.sy, __dsub_rn(my, ty));
-    const double uy = __dmul_rn(im.sy, __dadd_rn(my, ty));
+    const double tx = rn_mul(SUPPORT_SIGMAS, (double)sxf);
+    const double ty = rn_mul(SUPPORT_SIGMAS, (double)syf);
+    const double lx = rn_mul(im.sx, rn_sub(mx, tx));
+    const double ux = rn_mul(im.sx, rn_add(mx, tx));
+    const double ly = rn_mul(im.sy, rn_sub(my, ty));
+    const double uy = rn_mul(im.sy, rn_add(my, ty));
     const int bx0 = (int)floor(clamp_bound(lx)), bx1 = (int)ceil(clamp_bound(ux));
     const int by0 = (int)floor(clamp_bound(ly)), by1 = (int)ceil(clamp_bound(uy));
-    r.x0u = max(r.x0u, bx0);
-    r.y0u = max(r.y0u, by0);
-    r.x1u = min(r.x1u, bx1);
-    r.y1u = min(r.y1u, by1);
-    r.x0 = max(r.x0, bx0);
-    r.x1 = min(r.x1, bx1);
-    r.y0 = max(r.y0, by0);
-    r.y1 = min(r.y1, by1);
+    r.x0u = r.x0u > bx0 ? r.x0u : bx0;
+    r.y0u = r.y0u > by0 ? r.y0u : by0;
+    r.x1u = r.x1u < bx1 ? r.x1u : bx1;
+    r.y1u = r.y1u < by1 ? r.y1u : by1;
+    r.x0 = r.x0 > bx0 ? r.x0 : bx0;
+    r.x1 = r.x1 < bx1 ? r.x1 : bx1;
+    r.y0 = r.y0 > by0 ? r.y0 : by0;
+    r.y1 = r.y1 < by1 ? r.y1 : by1;
     r.nonempty = r.nonempty && r.x0 <= r.x1 && r.y0 <= r.y1 && !isnan(lx) && !isnan(ux) &&
                  !isnan(ly) && !isnan(uy);
     return r;
 }
 
 // parameter element -> float (GSR_PARAMS_BF16: bfloat16 widened exactly)
-__device__ __forceinline__ float ldf(float v) { return v; }
-__device__ __forceinline__ float ldf(__nv_bfloat16 v) { return __bfloat162float(v); }
+__host__ __device__ __forceinline__ float ldf(float v) { return v; }
+__host__ __device__ __forceinline__ float ldf(__nv_bfloat16 v) { return __bfloat162float(v); }
 
 // ---- image I/O formats (NEXT-4): index and element access of out / grad_out ----------------
 __device__ __forceinline__ long long img_index(const DevImg& im, int y, int x, int k) {
@@ -232,7 +245,7 @@ __device__ __forceinline__ float img_load(const void* p, const DevImg& im, long 
                              : ((const float*)p)[off];
 }
 
-__device__ __forceinline__ bool gaussian_valid(float a, float mx, float my, float sx, float sy,
+__host__ __device__ __forceinline__ bool gaussian_valid(float a, float mx, float my, float sx, float sy,
                                                float rh, float cr, float cg, float cb) {
     bool fin = isfinite(a) && isfinite(mx) && isfinite(my) && isfinite(sx) && isfinite(sy) &&
                isfinite(rh) && isfinite(cr) && isfinite(cg) && isfinite(cb);
@@ -241,7 +254,7 @@ __device__ __forceinline__ bool gaussian_valid(float a, float mx, float my, floa
 
 // validity (R20) of Gaussian i read from the parameter arrays (float32 or bfloat16)
 template <class T>
-__device__ __forceinline__ bool valid_at(const T* alpha, const T* mu, const T* sigma,
+__host__ __device__ __forceinline__ bool valid_at(const T* alpha, const T* mu, const T* sigma,
                                          const T* rho, const T* color, long long i) {
     return gaussian_valid(ldf(alpha[i]), ldf(mu[2 * i]), ldf(mu[2 * i + 1]), ldf(sigma[2 * i]),
                           ldf(sigma[2 * i + 1]), ldf(rho[i]), ldf(color[3 * i]),
@@ -389,6 +402,7 @@ struct Workspace {
     int* cell_start;         // [total_cells + 1]
     float4* rec;             // [REC_F4 * n] records (sorted order)
     int4* rects;             // [n] {support x, support y, window x, window y} (sorted order)
+    uint8_t* cls;            // [n] record class bits (sorted order): bit 0 = forward recurrence ok
     double* moments;         // [8 * n] (backward)
     unsigned long long* counter;  // scratch counters
     int* tile_off;           // debug tile lists: [total_tiles + 1]
@@ -408,10 +422,12 @@ void carve_workspace(void* base, long long n, int total_cells, int total_tiles, 
 // Runs K1 (keys) + stable radix sort + cell starts + K1b (records). Returns sorted perm in
 // *perm_out (points into ws).
 // Parameter arrays are float32, or bfloat16 when tab.params_bf16 (GSR_PARAMS_BF16).
+// gidx (subset mode): binned position t stands for Gaussian gidx[t] (n entries); nullptr = t.
 cudaError_t bin_gaussians(const void* alpha, const void* mu, const void* sigma,
                           const void* rho, const void* color, long long n,
                           const ImgTable& tab, Workspace& ws, int** perm_out,
-                          uint32_t** keys_sorted_out, cudaStream_t st);
+                          uint32_t** keys_sorted_out, cudaStream_t st,
+                          const int* gidx = nullptr);
 // Where a previous bin_gaussians() on the same table left perm / sorted keys in the workspace.
 void binned_pointers(const ImgTable& tab, long long n, const Workspace& ws, int** perm,
                      uint32_t** keys_sorted);
@@ -426,6 +442,21 @@ cudaError_t launch_debug_tile_lists(const ImgTable& tab, const Workspace& ws, co
                                     const uint32_t* keys_sorted, int* counts, int* ids,
                                     int* cells, cudaStream_t st);
 cudaError_t exclusive_scan_i32(const int* in, int* out, long long n, int* tmp, cudaStream_t st);
+
+// plan.cu (K7)
+cudaError_t launch_row_pair_counts(const void* alpha, const void* mu, const void* sigma,
+                                   const void* rho, const void* color, long long n,
+                                   const ImgTable& tab, bool support, const RowOff& roff,
+                                   long long* d_out, cudaStream_t st);
+void row_pair_counts_host(const void* alpha, const void* mu, const void* sigma, const void* rho,
+                          const void* color, long long n, const ImgTable& tab, bool support,
+                          const RowOff& roff, long long* out);
+cudaError_t launch_band_span(const void* alpha, const void* mu, const void* sigma,
+                             const void* rho, const void* color, long long n, const ImgTable& tab,
+                             const BandTable& bt, int16_t* d_span, cudaStream_t st);
+void band_span_host(const void* alpha, const void* mu, const void* sigma, const void* rho,
+                    const void* color, long long n, const ImgTable& tab, const BandTable& bt,
+                    int16_t* span);
 
 // render_fwd.cu
 cudaError_t launch_render_fwd(const ImgTable& tab, const Workspace& ws, float* out,
@@ -444,11 +475,13 @@ struct RawParams {
     const float* raw_alpha; const float* raw_sigma; const float* raw_rho; const float* raw_color;
     float rho_scale;
 };
+// gidx (subset mode): entry t of moments / d_* belongs to Gaussian gidx[t] (n entries, compact)
 cudaError_t launch_finalize(const void* alpha, const void* mu, const void* sigma,
                             const void* rho, const void* color, long long n,
                             const double* moments, float* d_alpha, float* d_mu, float* d_sigma,
                             float* d_rho, float* d_color, cudaStream_t st,
-                            const RawParams* raw = nullptr, bool params_bf16 = false);
+                            const RawParams* raw = nullptr, bool params_bf16 = false,
+                            const int* gidx = nullptr);
 // train.cu
 cudaError_t launch_activate(const float* raw_alpha, const float* offset, const float* ref,
                             const float* raw_sigma, const float* raw_rho, const float* raw_color,

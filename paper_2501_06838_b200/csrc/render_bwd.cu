@@ -442,12 +442,13 @@ __global__ void k_finalize(const T* __restrict__ alpha, const T* __restrict__ mu
                            const double* __restrict__ moments, float* __restrict__ d_alpha,
                            float* __restrict__ d_mu, float* __restrict__ d_sigma,
                            float* __restrict__ d_rho, float* __restrict__ d_color, RawParams raw,
-                           int raw_mode) {
-    long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
+                           int raw_mode, const int* __restrict__ gidx) {
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    const long long i = gidx ? (long long)gidx[t] : t;      // subset mode: compact entry t
     float o[9] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
     if (valid_at(alpha, mu, sigma, rho, color, i)) {
-        const double* m = moments + 8 * i;
+        const double* m = moments + 8 * t;
         double sx = ldf(sigma[2 * i]), sy = ldf(sigma[2 * i + 1]);
         double rh = ldf(rho[i]), al = ldf(alpha[i]);
         double c0 = ldf(color[3 * i]), c1 = ldf(color[3 * i + 1]), c2 = ldf(color[3 * i + 2]);
@@ -483,15 +484,15 @@ __global__ void k_finalize(const T* __restrict__ alpha, const T* __restrict__ mu
         }
         for (int k = 0; k < 9; ++k) o[k] = (float)g9[k];
     }
-    d_alpha[i] = o[0];
-    d_mu[2 * i] = o[1];
-    d_mu[2 * i + 1] = o[2];
-    d_sigma[2 * i] = o[3];
-    d_sigma[2 * i + 1] = o[4];
-    d_rho[i] = o[5];
-    d_color[3 * i] = o[6];
-    d_color[3 * i + 1] = o[7];
-    d_color[3 * i + 2] = o[8];
+    d_alpha[t] = o[0];
+    d_mu[2 * t] = o[1];
+    d_mu[2 * t + 1] = o[2];
+    d_sigma[2 * t] = o[3];
+    d_sigma[2 * t + 1] = o[4];
+    d_rho[t] = o[5];
+    d_color[3 * t] = o[6];
+    d_color[3 * t + 1] = o[7];
+    d_color[3 * t + 2] = o[8];
 }
 
 }  // namespace
@@ -502,11 +503,13 @@ cudaError_t launch_render_bwd_moments(const ImgTable& tab, const Workspace& ws, 
     if (tab.total_tiles <= 0) return cudaSuccess;
     count_launches(1);
     int h = prof_begin(2, st);
-    static std::atomic<int> slots_cache{0};
-    int slots = slots_cache.load(std::memory_order_relaxed);
+    static std::atomic<int> slots_cache[64];       // per device (occupancy x SM count)
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) dev = 0;
+    int slots = slots_cache[dev].load(std::memory_order_relaxed);
     if (slots == 0) {
         slots = resident_slots(k_render_bwd, BWD_THREADS, 0);
-        slots_cache.store(slots, std::memory_order_relaxed);
+        slots_cache[dev].store(slots, std::memory_order_relaxed);
     }
     const int ks = split_k_factor(tab.total_tiles, slots);
     k_render_bwd<<<tab.total_tiles * ks, BWD_THREADS, 0, st>>>(tab, ws.rec, ws.rects, ws.cell_start,
@@ -521,7 +524,7 @@ cudaError_t launch_finalize(const void* alpha, const void* mu, const void* sigma
                             const void* rho, const void* color, long long n,
                             const double* moments, float* d_alpha, float* d_mu, float* d_sigma,
                             float* d_rho, float* d_color, cudaStream_t st, const RawParams* raw,
-                            bool params_bf16) {
+                            bool params_bf16, const int* gidx) {
     if (n <= 0) return cudaSuccess;
     count_launches(1);
     int h = prof_begin(3, st);
@@ -531,12 +534,13 @@ cudaError_t launch_finalize(const void* alpha, const void* mu, const void* sigma
         using B = __nv_bfloat16;
         k_finalize<B><<<grid, 256, 0, st>>>((const B*)alpha, (const B*)mu, (const B*)sigma,
                                             (const B*)rho, (const B*)color, n, moments, d_alpha,
-                                            d_mu, d_sigma, d_rho, d_color, rp, raw ? 1 : 0);
+                                            d_mu, d_sigma, d_rho, d_color, rp, raw ? 1 : 0, gidx);
     } else {
         k_finalize<float><<<grid, 256, 0, st>>>((const float*)alpha, (const float*)mu,
                                                 (const float*)sigma, (const float*)rho,
                                                 (const float*)color, n, moments, d_alpha, d_mu,
-                                                d_sigma, d_rho, d_color, rp, raw ? 1 : 0);
+                                                d_sigma, d_rho, d_color, rp, raw ? 1 : 0,
+                                                gidx);
     }
     prof_end(h, st);
     return cudaGetLastError();

@@ -6,6 +6,10 @@ window meets those rows (the halo) -- the library bins only band-intersecting Ga
 replicated parameters cost O(N) preprocessing per rank and nothing else. Boundaries equalise the
 per-row pair counts (the work unit), not the row counts.
 
+Per rank, `RankPlan` holds the halo (the Gaussians whose support meets the rank's bands) and the
+neighbour seam sets; the rank bins, renders and finalizes only its halo (libgsr's subset entry
+points), so its binning, moment zeroing and finalize scale with N/G + halo, not N.
+
 Exchange steps (the only collectives):
   forward : all-gather of the output bands (each rank's bands padded to the largest) -> every
             rank holds every band, `assemble_image` views/copies out a full image;
@@ -31,90 +35,148 @@ from typing import Callable, List, Sequence
 import numpy as np
 
 
-def out_size(n: int, s: float) -> int:
-    return int(math.floor(s * n))
+PARAM_WIDTH = (1, 2, 2, 1, 3)       # alpha, mu, sigma, rho, color (include/gsr.h layouts)
 
 
-SUPPORT_SIGMAS = 13.5      # reading R21: the kernels' evaluation box, +-13.5 sigma
+def _img_tuple(im):
+    """(H, W, s, g_off, g_cnt, s_y) of an ops.Image or a tuple (H, W, s, g_off, g_cnt[, s_y])."""
+    if hasattr(im, "H"):
+        return (int(im.H), int(im.W), float(im.s), int(im.g_off), int(im.g_cnt),
+                im.s_y if getattr(im, "s_y", None) else None)
+    t = tuple(im)
+    return (int(t[0]), int(t[1]), float(t[2]), int(t[3]), int(t[4]),
+            t[5] if len(t) > 5 and t[5] else None)
 
 
-def row_pair_counts(mu: np.ndarray, valid: np.ndarray, H: int, W: int, s: float, ratio: float,
-                    sigma: np.ndarray | None = None) -> np.ndarray:
-    """Exact pairs per HR row of one image: rowpairs[y] = sum_i [y0_i <= y <= y1_i] (x1_i-x0_i+1),
-    with the integer window rect of reading R2 (fp64, same operation order as the kernels), cut
-    to the support box of reading R21 when sigma is given (the pairs the kernels evaluate)."""
-    Hs, Ws = out_size(H, s), out_size(W, s)
-    mx = mu[:, 0].astype(np.float64)
-    my = mu[:, 1].astype(np.float64)
-    hx, hy = ratio * W, ratio * H
-    lim = float(2 ** 30)
-    with np.errstate(invalid="ignore"):
-        x0 = np.floor(np.clip(s * (mx - hx), -lim, lim)) + 1
-        x1 = np.ceil(np.clip(s * (mx + hx), -lim, lim)) - 1
-        y0 = np.floor(np.clip(s * (my - hy), -lim, lim)) + 1
-        y1 = np.ceil(np.clip(s * (my + hy), -lim, lim)) - 1
-        if sigma is not None:
-            tx = SUPPORT_SIGMAS * sigma[:, 0].astype(np.float64)
-            ty = SUPPORT_SIGMAS * sigma[:, 1].astype(np.float64)
-            x0 = np.maximum(x0, np.floor(np.clip(s * (mx - tx), -lim, lim)))
-            x1 = np.minimum(x1, np.ceil(np.clip(s * (mx + tx), -lim, lim)))
-            y0 = np.maximum(y0, np.floor(np.clip(s * (my - ty), -lim, lim)))
-            y1 = np.minimum(y1, np.ceil(np.clip(s * (my + ty), -lim, lim)))
-        x0 = np.maximum(x0, 0); x1 = np.minimum(x1, Ws - 1)
-        y0 = np.maximum(y0, 0); y1 = np.minimum(y1, Hs - 1)
-        ok = valid & (x0 <= x1) & (y0 <= y1)
-    w = (x1 - x0 + 1)[ok].astype(np.int64)
-    d = np.zeros(Hs + 1, np.int64)
-    np.add.at(d, y0[ok].astype(np.int64), w)
-    np.add.at(d, y1[ok].astype(np.int64) + 1, -w)
-    return np.cumsum(d[:-1])
+def _plan_calls(params, images):
+    """ABI calls of <= GSR_MAX_IMAGES whole images each: (param pointers, n, images array,
+    m, [image indices]); params are numpy float32/bfloat16-free host arrays (host variants) or
+    CUDA tensors (device variants)."""
+    from . import _lib
+    ims = [_img_tuple(im) for im in images]
+    for c0 in range(0, len(ims), _lib.MAX_IMAGES):
+        sel = list(range(c0, min(c0 + _lib.MAX_IMAGES, len(ims))))
+        g0 = min(ims[k][3] for k in sel)
+        g1 = max(ims[k][3] + ims[k][4] for k in sel)
+        recs = [(H, W, s, go - g0, gc, 0, 0, -1, sy) for (H, W, s, go, gc, sy) in
+                (ims[k] for k in sel)]
+        yield g0, g1, _lib.images_array(recs), len(sel), sel
 
 
-def support_rows(mu: np.ndarray, sigma: np.ndarray, valid: np.ndarray, H: int, W: int, s: float,
-                 ratio: float, s_y: float | None = None):
-    """Clipped HR row range [y0, y1] of every Gaussian's support rect (R2 window cut to the R21
-    box, fp64 in the kernels' operation order); ok = the rect is non-empty."""
-    sy = s if not s_y else s_y
-    Hs, Ws = out_size(H, sy), out_size(W, s)
-    mx = mu[:, 0].astype(np.float64)
-    my = mu[:, 1].astype(np.float64)
-    lim = float(2 ** 30)
-    with np.errstate(invalid="ignore"):
-        x0 = np.floor(np.clip(s * (mx - ratio * W), -lim, lim)) + 1
-        x1 = np.ceil(np.clip(s * (mx + ratio * W), -lim, lim)) - 1
-        y0 = np.floor(np.clip(sy * (my - ratio * H), -lim, lim)) + 1
-        y1 = np.ceil(np.clip(sy * (my + ratio * H), -lim, lim)) - 1
-        tx = SUPPORT_SIGMAS * sigma[:, 0].astype(np.float64)
-        ty = SUPPORT_SIGMAS * sigma[:, 1].astype(np.float64)
-        x0 = np.maximum(x0, np.floor(np.clip(s * (mx - tx), -lim, lim)))
-        x1 = np.minimum(x1, np.ceil(np.clip(s * (mx + tx), -lim, lim)))
-        y0 = np.maximum(y0, np.floor(np.clip(sy * (my - ty), -lim, lim)))
-        y1 = np.minimum(y1, np.ceil(np.clip(sy * (my + ty), -lim, lim)))
-        x0 = np.maximum(x0, 0); x1 = np.minimum(x1, Ws - 1)
-        y0 = np.maximum(y0, 0); y1 = np.minimum(y1, Hs - 1)
-        ok = valid & (x0 <= x1) & (y0 <= y1)
-    return np.where(ok, y0, 0).astype(np.int64), np.where(ok, y1, -1).astype(np.int64), ok
+def _is_host(params):
+    return isinstance(params[0], np.ndarray)
 
 
-def seam_mask(mu: np.ndarray, sigma: np.ndarray, valid: np.ndarray, H: int, W: int, s: float,
-              ratio: float, bounds: Sequence[int], margin: int = 1,
-              s_y: float | None = None) -> np.ndarray:
-    """Gaussians of one image whose support rows meet more than one band of `bounds` (the seam
-    set of SURVEY 8(e)). Conservative: the rows are widened by `margin` -- a Gaussian wrongly
-    marked as a seam only costs buffer space (its partials are complete on one rank, 0 on the
-    others); a seam Gaussian marked interior would lose gradient."""
-    y0, y1, ok = support_rows(mu, sigma, valid, H, W, s, ratio, s_y)
-    b = np.asarray(bounds, np.int64)
-    first = np.searchsorted(b, y0 - margin, side="right") - 1
-    last = np.searchsorted(b, y1 + margin, side="right") - 1
-    return ok & (first < last)
+def _host_params(params):
+    return [np.ascontiguousarray(np.asarray(p, np.float32).reshape(-1, w) if w > 1 else
+                                 np.asarray(p, np.float32).reshape(-1))
+            for p, w in zip(params, PARAM_WIDTH)]
 
 
-def halo_mask(mu: np.ndarray, sigma: np.ndarray, valid: np.ndarray, H: int, W: int, s: float,
-              ratio: float, rows, s_y: float | None = None) -> np.ndarray:
-    """Gaussians of one image whose support rows meet HR rows [rows[0], rows[1]) (exact)."""
-    y0, y1, ok = support_rows(mu, sigma, valid, H, W, s, ratio, s_y)
-    return ok & (y1 >= rows[0]) & (y0 < rows[1])
+def _ptrs(params, g0):
+    """Parameter pointers of Gaussian g0 on (host numpy or device tensor arrays)."""
+    out = []
+    for p, w in zip(params, PARAM_WIDTH):
+        if isinstance(p, np.ndarray):
+            out.append(p.ctypes.data + g0 * w * p.itemsize)
+        else:
+            out.append(p.data_ptr() + g0 * w * p.element_size())
+    return out
+
+
+def _flags(params, support=False):
+    from . import _lib
+    f = _lib.GSR_SUPPORT if support else 0
+    if not _is_host(params):
+        import torch
+        if params[0].dtype == torch.bfloat16:
+            f |= _lib.GSR_PARAMS_BF16
+    return f
+
+
+def row_pair_counts(params, images, ratio: float = 0.1, support: bool = True) -> List[np.ndarray]:
+    """Exact pairs per HR row of every (whole) image: rowpairs[y] = sum_i [y0_i <= y <= y1_i]
+    (x1_i - x0_i + 1), with Alg. 1's window rect (support=False) or the support rect of reading
+    R21 (support=True: the pairs the kernels evaluate), computed by libgsr's K7 planner
+    (gsr_row_pair_counts_*: the render kernels' own rect code). params = (alpha, mu, sigma, rho,
+    color) as numpy arrays (host variant) or CUDA tensors (device variant). -> one int64 array
+    per image."""
+    from . import _lib
+    lib = _lib.load()
+    host = _is_host(params)
+    if host:
+        params = _host_params(params)
+    res = [None] * len(images)
+    for g0, g1, arr, m, sel in _plan_calls(params, images):
+        rows = []
+        for k in range(m):
+            Hs, _ = _lib.out_dims(arr[k].lr_h, arr[k].lr_w, arr[k].scale, arr[k].scale_y or None)
+            rows.append(Hs)
+        tot = int(sum(rows))
+        if host:
+            out = np.zeros(tot, np.int64)
+            _lib.check(lib.gsr_row_pair_counts_host(*_ptrs(params, g0), g1 - g0, arr, m,
+                                                    float(ratio), _flags(params, support),
+                                                    out.ctypes.data), "gsr_row_pair_counts_host")
+        else:
+            import torch
+            dev = params[0].device
+            d = torch.empty(tot, dtype=torch.int64, device=dev)
+            _lib.check(lib.gsr_row_pair_counts_batched(
+                *_ptrs(params, g0), g1 - g0, arr, m, float(ratio), _flags(params, support),
+                d.data_ptr(), torch.cuda.current_stream(dev).cuda_stream),
+                "gsr_row_pair_counts_batched")
+            out = d.cpu().numpy()
+        o = 0
+        for k, h in zip(sel, rows):
+            res[k] = out[o:o + h]
+            o += h
+    return res
+
+
+def band_spans(params, images, bounds: Sequence[Sequence[int]], ratio: float = 0.1,
+               margin: int = 0):
+    """[n, 2] int16: first and last band of each image's boundaries `bounds[k]` that every
+    Gaussian's support rows (R21) meet ({-1, -1}: invalid (R20) or empty), by libgsr's K7 planner
+    (gsr_band_span_*). numpy in -> numpy out (host variant); CUDA tensors -> CUDA tensor."""
+    from . import _lib
+    lib = _lib.load()
+    host = _is_host(params)
+    if host:
+        params = _host_params(params)
+        n = params[0].shape[0]
+        span = np.full((n, 2), -1, np.int16)
+    else:
+        import torch
+        n = params[0].shape[0]
+        span = torch.full((n, 2), -1, dtype=torch.int16, device=params[0].device)
+    G = len(bounds[0]) - 1
+    for g0, g1, arr, m, sel in _plan_calls(params, images):
+        b = np.ascontiguousarray(np.array([list(bounds[k]) for k in sel], np.int32))
+        if b.shape[1] != G + 1:
+            raise ValueError("every image needs the same number of bands")
+        if host:
+            _lib.check(lib.gsr_band_span_host(*_ptrs(params, g0), g1 - g0, arr, m, float(ratio),
+                                              _flags(params), b.ctypes.data, G, int(margin),
+                                              span.ctypes.data + 4 * g0), "gsr_band_span_host")
+        else:
+            import torch
+            dev = params[0].device
+            _lib.check(lib.gsr_band_span_batched(
+                *_ptrs(params, g0), g1 - g0, arr, m, float(ratio), _flags(params), b.ctypes.data,
+                G, int(margin), span.data_ptr() + 4 * g0,
+                torch.cuda.current_stream(dev).cuda_stream), "gsr_band_span_batched")
+    return span
+
+
+def seam_mask(span):
+    """Seam Gaussians: support rows meeting more than one band."""
+    return span[:, 0] < span[:, 1]
+
+
+def halo_mask(span, r: int):
+    """Gaussians whose support rows meet band r (rank r's replicated halo)."""
+    return (span[:, 0] <= r) & (span[:, 1] >= r)
 
 
 def plan_bands(row_counts: np.ndarray, G: int) -> List[int]:
@@ -219,6 +281,116 @@ def reduce_seam(grads, seam_idx, group=None, full: bool = False):
         k = c.shape[1]
         c.index_copy_(0, seam_idx, buf[:, o:o + k])
         o += k
+    return grads
+
+
+class RankPlan:
+    """One rank's share of a row-band shard, from the K7 planner's band spans:
+
+      idx   int32 [m]  its halo: the Gaussians whose support rows (R21) meet its bands, ascending
+                       -- the subset it bins, renders and finalizes (gsr_*_subset, compact
+                       outputs: row t belongs to Gaussian idx[t]);
+      up    int64      positions (into idx) of the Gaussians shared exactly with rank + 1
+                       (span [rank, rank+1]); `down` likewise with rank - 1 -- the neighbour
+                       seam exchange: both sides hold the same Gaussians in the same (ascending)
+                       order, so the two buffers line up;
+      multi_pos / multi_slot  Gaussians spanning three or more bands (supports taller than a
+                       band; rare): positions in idx and slots in a global [n_multi] buffer that
+                       every rank all-reduces.
+
+    The band boundaries come from the row pair counts (work-balanced); spans and halos are
+    recomputed by `refresh` whenever the parameters change (every training step)."""
+
+    def __init__(self, params, images, world: int, rank: int, ratio: float = 0.1,
+                 bounds=None):
+        self.world, self.rank, self.ratio = world, rank, ratio
+        self.images = [_img_tuple(im) for im in images]
+        if bounds is None:
+            bounds = [plan_bands(rc, world) for rc in row_pair_counts(params, images, ratio)]
+        self.bounds = bounds
+        self.refresh(params)
+
+    def refresh(self, params):
+        import torch
+        r, G = self.rank, self.world
+        span = torch.as_tensor(band_spans(params, self.images, self.bounds, self.ratio))
+        f, l = span[:, 0].to(torch.int32), span[:, 1].to(torch.int32)
+        halo = (f <= r) & (l >= r)
+        self.idx = torch.nonzero(halo).reshape(-1).to(torch.int32)
+        pos = torch.cumsum(halo.to(torch.int64), 0) - 1            # position within idx
+        self.up = pos[torch.nonzero((f == r) & (l == r + 1)).reshape(-1)]
+        self.down = pos[torch.nonzero((f == r - 1) & (l == r)).reshape(-1)]
+        multi = torch.nonzero(l - f >= 2).reshape(-1)              # identical on every rank
+        inh = halo[multi]
+        self.n_multi = int(multi.numel())
+        self.multi_pos = pos[multi[inh]]
+        self.multi_slot = torch.nonzero(inh).reshape(-1)
+        self.n_seam_local = int(self.up.numel() + self.down.numel() + self.multi_pos.numel())
+        return self
+
+    @property
+    def m(self) -> int:
+        return int(self.idx.numel())
+
+    def band_images(self):
+        """(H, W, s, g_off, g_cnt, row_begin, row_end, s_y) of this rank's band of every image."""
+        return [(H, W, s, go, gc, b[self.rank], b[self.rank + 1], sy)
+                for (H, W, s, go, gc, sy), b in zip(self.images, self.bounds)]
+
+    def exchange_bytes(self) -> dict:
+        """Bytes this rank sends per step in the seam exchange (float32 [k, 9] rows)."""
+        return {"p2p_up": 36 * int(self.up.numel()), "p2p_down": 36 * int(self.down.numel()),
+                "multi_allreduce": 36 * self.n_multi}
+
+
+def exchange_seams(grads, plan: RankPlan, group=None):
+    """Neighbour seam exchange of a rank's COMPACT partial gradients (the finalize of its halo
+    moments, rows = plan.idx): the rows shared with rank +- 1 are swapped with that neighbour
+    (torch.distributed P2P: NCCL send/recv over NVLink) and added, so both ranks end with the
+    full gradient; Gaussians spanning >= 3 bands are summed by one all-reduce of a small
+    global buffer. `grads` = one [m, k] tensor or a sequence of [m] / [m, k] tensors."""
+    import torch
+    import torch.distributed as dist
+    ts = [grads] if isinstance(grads, torch.Tensor) else list(grads)
+    m = ts[0].shape[0]
+    cols = [t.view(m, -1) for t in ts]
+    r, G = plan.rank, plan.world
+    # gloo (the CPU tests and the 1-GPU functional check of bench.py) has no point-to-point path
+    # for CUDA tensors: stage those buffers through host memory; NCCL sends device memory
+    host_p2p = ts[0].is_cuda and dist.get_backend(group) == "gloo"
+    ops, recv = [], []
+    for peer, sel in ((r + 1, plan.up), (r - 1, plan.down)):
+        if 0 <= peer < G and sel.numel() > 0:
+            send = torch.cat([c.index_select(0, sel) for c in cols], 1).contiguous()
+            wire = send.cpu() if host_p2p else send
+            rb = torch.empty_like(wire)
+            ops.append(dist.P2POp(dist.isend, wire, peer, group))
+            ops.append(dist.P2POp(dist.irecv, rb, peer, group))
+            recv.append((sel, rb, send))
+    if ops:
+        for w in dist.batch_isend_irecv(ops):
+            w.wait()
+    for sel, rb, send in recv:
+        tot = send + rb.to(send.device)
+        o = 0
+        for c in cols:
+            k = c.shape[1]
+            c.index_copy_(0, sel, tot[:, o:o + k])
+            o += k
+    if plan.n_multi:
+        width = sum(c.shape[1] for c in cols)
+        buf = cols[0].new_zeros((plan.n_multi, width))
+        if plan.multi_pos.numel():
+            buf.index_copy_(0, plan.multi_slot,
+                            torch.cat([c.index_select(0, plan.multi_pos) for c in cols], 1))
+        dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=group)
+        if plan.multi_pos.numel():
+            sel = buf.index_select(0, plan.multi_slot)
+            o = 0
+            for c in cols:
+                k = c.shape[1]
+                c.index_copy_(0, plan.multi_pos, sel[:, o:o + k])
+                o += k
     return grads
 
 

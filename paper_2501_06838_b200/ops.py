@@ -69,6 +69,23 @@ def _fmt_flags(params, image: Optional[torch.Tensor] = None, out_dtype=None,
     return f
 
 
+def _check_image(t: torch.Tensor, name: str, lay: "Layout", device,
+                 dtypes=(torch.float32, torch.bfloat16)) -> torch.Tensor:
+    """An image buffer of a layout (out, grad_out, gt): lay.out_numel elements of an accepted dtype
+    on the parameters' device, contiguous (the kernels index it by raw element offsets)."""
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise TypeError(f"{name} must be a CUDA tensor (no CPU fallback)")
+    if t.dtype not in dtypes:
+        raise TypeError(f"{name} must be one of {dtypes}, got {t.dtype}")
+    if t.device != torch.device(device):
+        raise ValueError(f"{name} is on {t.device}, the parameters on {device}")
+    if t.numel() != lay.out_numel:
+        raise ValueError(f"{name} has {t.numel()} elements, the layout needs {lay.out_numel}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    return t
+
+
 def _ptr(t: torch.Tensor, offset_elems: int = 0) -> int:
     return t.data_ptr() + offset_elems * t.element_size()
 
@@ -153,7 +170,12 @@ _WS = {}
 
 
 def _workspace(device, nbytes: int) -> torch.Tensor:
-    key = torch.device(device).index
+    """The implicit workspace of calls made without one: one per (device, stream), so calls on
+    different streams never share scratch (gsr.h: concurrent calls need distinct workspaces). It
+    is allocated on, and only ever used by, its own stream, so the caching allocator's stream
+    ordering makes a regrown buffer safe to free."""
+    dev = torch.device(device)
+    key = (dev.index, torch.cuda.current_stream(dev).cuda_stream)
     ws = _WS.setdefault(key, Workspace())
     return ws.get(nbytes, device)
 
@@ -196,6 +218,7 @@ def render_fwd_batched(alpha, mu, sigma, rho, color, lay: Layout, ratio: float =
     dev = alpha.device
     if out is None:
         out = torch.empty(lay.out_numel, dtype=out_dtype or torch.float32, device=dev)
+    out = _check_image(out, "out", lay, dev)
     flags = _fmt_flags(params, out, chw=chw)
     lib = _lib.load()
     st = _stream_ptr(dev)
@@ -220,9 +243,10 @@ def render_bwd_moments_batched(alpha, mu, sigma, rho, color, lay: Layout, grad_o
     params, n = _params(alpha, mu, sigma, rho, color)
     alpha, mu, sigma, rho, color = params
     dev = alpha.device
-    grad_out = _check_param(grad_out, "grad_out", dtypes=_FLOATS)
-    if moments.dtype != torch.float64 or not moments.is_contiguous() or moments.numel() != 8 * n:
-        raise ValueError("moments must be a contiguous float64 [n, 8] tensor")
+    grad_out = _check_image(grad_out.contiguous(), "grad_out", lay, dev)
+    if (moments.dtype != torch.float64 or not moments.is_contiguous() or moments.numel() != 8 * n
+            or moments.device != dev):
+        raise ValueError("moments must be a contiguous float64 [n, 8] tensor on the params' device")
     lib = _lib.load()
     st = _stream_ptr(dev)
     flags = _lib.GSR_REUSE_BINNING if (reuse_binning and workspace is not None and
@@ -243,6 +267,9 @@ def finalize_grads(alpha, mu, sigma, rho, color, moments: torch.Tensor):
     """Moments [n, 8] (float64) -> (d_alpha, d_mu, d_sigma, d_rho, d_color) (float32)."""
     params, n = _params(alpha, mu, sigma, rho, color)
     dev = params[0].device
+    if (moments.dtype != torch.float64 or not moments.is_contiguous() or moments.numel() != 8 * n
+            or moments.device != dev):
+        raise ValueError("moments must be a contiguous float64 [n, 8] tensor on the params' device")
     grads = [torch.empty(t.shape, dtype=torch.float32, device=dev) for t in params]
     check(_lib.load().gsr_finalize_grads_ex(*[_ptr(t) for t in params], n, _ptr(moments),
                                             *[_ptr(g) for g in grads], _fmt_flags(params),
@@ -259,7 +286,7 @@ def render_bwd_batched(alpha, mu, sigma, rho, color, lay: Layout, grad_out: torc
     params, n = _params(alpha, mu, sigma, rho, color)
     alpha, mu, sigma, rho, color = params
     dev = alpha.device
-    grad_out = _check_param(grad_out, "grad_out", dtypes=_FLOATS)
+    grad_out = _check_image(grad_out.contiguous(), "grad_out", lay, dev)
     grads = [torch.zeros(t.shape, dtype=torch.float32, device=dev) for t in params]
     lib = _lib.load()
     st = _stream_ptr(dev)
@@ -275,6 +302,99 @@ def render_bwd_batched(alpha, mu, sigma, rho, color, lay: Layout, grad_out: torc
             _ptr(color, 3 * g0), g1 - g0, arr, m, float(ratio), _ptr(grad_out, o0),
             _ptr(ga, g0), _ptr(gm, 2 * g0), _ptr(gs, 2 * g0), _ptr(gr, g0), _ptr(gc, 3 * g0),
             ws.data_ptr(), ws.numel(), flags, st), "gsr_render_bwd_batched_ex")
+    return tuple(grads)
+
+
+# ------------------------------------------------------------------ subset mode (a rank's halo)
+def _check_idx(idx: torch.Tensor, n: int, dev) -> torch.Tensor:
+    if not isinstance(idx, torch.Tensor) or idx.dtype != torch.int32 or idx.dim() != 1:
+        raise TypeError("idx must be a 1-D int32 tensor (ascending Gaussian indices)")
+    if idx.device != torch.device(dev) or not idx.is_contiguous():
+        raise ValueError("idx must be contiguous on the parameters' device")
+    if idx.numel() > n:
+        raise ValueError("idx has more entries than Gaussians")
+    return idx
+
+
+def _single_chunk_call(lay: Layout):
+    if not single_chunk(lay):
+        raise ValueError(f"subset calls take at most {_lib.MAX_IMAGES} images")
+    return next(_chunks(lay))
+
+
+def subset_workspace_for(alpha, lay: Layout, m: int, ratio: float = 0.1) -> torch.Tensor:
+    """A private workspace for the subset calls of one layout and halo size m."""
+    g0, g1, o0, arr, k = _single_chunk_call(lay)
+    if g0 != 0:
+        raise ValueError("subset calls need layouts whose Gaussian ranges start at 0")
+    nb = _lib.load().gsr_workspace_bytes_subset(arr, k, int(alpha.shape[0]), int(m), float(ratio))
+    if nb == 0:
+        raise _lib.GsrError("gsr_workspace_bytes_subset: invalid arguments")
+    return torch.empty(nb, dtype=torch.uint8, device=alpha.device)
+
+
+def render_fwd_subset(alpha, mu, sigma, rho, color, idx: torch.Tensor, lay: Layout,
+                      ratio: float = 0.1, out: Optional[torch.Tensor] = None,
+                      workspace: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """Forward render of the layout's bands from the Gaussians idx only (a rank's halo:
+    gsr_render_fwd_subset); float32 HWC blocks."""
+    params, n = _params(alpha, mu, sigma, rho, color)
+    dev = params[0].device
+    idx = _check_idx(idx, n, dev)
+    g0, g1, o0, arr, k = _single_chunk_call(lay)
+    if out is None:
+        out = torch.empty(lay.out_numel, dtype=torch.float32, device=dev)
+    out = _check_image(out, "out", lay, dev)
+    ws = workspace if workspace is not None else subset_workspace_for(params[0], lay, idx.numel(),
+                                                                      ratio)
+    check(_lib.load().gsr_render_fwd_subset(*[_ptr(t) for t in params], n, _ptr(idx), idx.numel(),
+                                            arr, k, float(ratio), _ptr(out), ws.data_ptr(),
+                                            ws.numel(), _fmt_flags(params, out),
+                                            _stream_ptr(dev)), "gsr_render_fwd_subset")
+    return out
+
+
+def render_bwd_moments_subset(alpha, mu, sigma, rho, color, idx: torch.Tensor, lay: Layout,
+                              grad_out: torch.Tensor, moments: torch.Tensor, ratio: float = 0.1,
+                              workspace: Optional[torch.Tensor] = None,
+                              reuse_binning: bool = False) -> torch.Tensor:
+    """Accumulate (+=) the compact moments [m, 8] (float64; row t = Gaussian idx[t]) of the
+    layout's bands (gsr_render_bwd_moments_subset)."""
+    params, n = _params(alpha, mu, sigma, rho, color)
+    dev = params[0].device
+    idx = _check_idx(idx, n, dev)
+    m = idx.numel()
+    g0, g1, o0, arr, k = _single_chunk_call(lay)
+    grad_out = _check_image(grad_out.contiguous(), "grad_out", lay, dev)
+    if (moments.dtype != torch.float64 or not moments.is_contiguous() or moments.numel() != 8 * m
+            or moments.device != dev):
+        raise ValueError("moments must be a contiguous float64 [m, 8] tensor on the device")
+    flags = _lib.GSR_REUSE_BINNING if (reuse_binning and workspace is not None) else 0
+    ws = workspace if workspace is not None else subset_workspace_for(params[0], lay, m, ratio)
+    check(_lib.load().gsr_render_bwd_moments_subset(
+        *[_ptr(t) for t in params], n, _ptr(idx), m, arr, k, float(ratio), _ptr(grad_out),
+        _ptr(moments), ws.data_ptr(), ws.numel(), flags | _fmt_flags(params, grad_out),
+        _stream_ptr(dev)), "gsr_render_bwd_moments_subset")
+    return moments
+
+
+def finalize_grads_subset(alpha, mu, sigma, rho, color, idx: torch.Tensor,
+                          moments: torch.Tensor):
+    """Compact moments [m, 8] -> compact gradients (d_alpha[m], d_mu[m,2], d_sigma[m,2],
+    d_rho[m], d_color[m,3]) of the Gaussians idx (gsr_finalize_grads_subset)."""
+    params, n = _params(alpha, mu, sigma, rho, color)
+    dev = params[0].device
+    idx = _check_idx(idx, n, dev)
+    m = idx.numel()
+    if (moments.dtype != torch.float64 or not moments.is_contiguous() or moments.numel() != 8 * m
+            or moments.device != dev):
+        raise ValueError("moments must be a contiguous float64 [m, 8] tensor on the device")
+    grads = [torch.empty((m,) + tuple(t.shape[1:]), dtype=torch.float32, device=dev)
+             for t in params]
+    check(_lib.load().gsr_finalize_grads_subset(*[_ptr(t) for t in params], n, _ptr(idx), m,
+                                                _ptr(moments), *[_ptr(g) for g in grads],
+                                                _fmt_flags(params), _stream_ptr(dev)),
+          "gsr_finalize_grads_subset")
     return tuple(grads)
 
 
@@ -402,8 +522,8 @@ def train_step_l1(raw_alpha, offset, ref, raw_sigma, raw_rho, raw_color, lay: La
         if t.shape[0] != n or (w == 1 and t.dim() != 1) or (w > 1 and t.shape[1:] != (w,)):
             raise ValueError(f"{name} has shape {tuple(t.shape)}")
         ts[name] = t
-    gt = _check_param(gt, "gt")
     dev = raw_alpha.device
+    gt = _check_image(gt.contiguous(), "gt", lay, dev, dtypes=(torch.float32,))
     if not single_chunk(lay):
         raise ValueError(f"train_step_l1 takes at most {_lib.MAX_IMAGES} images per call")
     g0, g1, o0, arr, m = next(_chunks(lay))
@@ -416,6 +536,7 @@ def train_step_l1(raw_alpha, offset, ref, raw_sigma, raw_rho, raw_color, lay: La
     ws = _ws_for(dev, nb, workspace)
     if out is None:
         out = torch.empty(lay.out_numel, dtype=torch.float32, device=dev)
+    out = _check_image(out, "out", lay, dev, dtypes=(torch.float32,))
     loss = torch.empty(1, dtype=torch.float64, device=dev)
     grads = {k: torch.empty_like(ts[k]) for k in RAW}
     check(lib.gsr_train_step_l1_batched(

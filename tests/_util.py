@@ -38,20 +38,38 @@ def assert_fwd_close(got, want, dist="image", atol=1e-5):
     return float(err.max())
 
 
-def assert_bwd_close(got, want, absmass, rtol=1e-4, mass_floor=1e-1):
-    """Backward gate (R18): |g_gpu - g| <= rtol * max(|g|, mass_floor * S), S = the sum
-    over pairs of the monomial magnitudes of each term (the fp32 rounding scale of the sum): the
-    floor is 1e-5 S; plus an absolute floor of 1e-8 x the largest S of that gradient component."""
+def gate_bounds(want, absmass, rtol=1e-4, dist="image"):
+    """Per-entry bound of the backward gate, |g_gpu - g| <= bound.
+
+    S = the oracle's `absmass`: the sum over pairs of the absolute values of the MONOMIALS of
+    each per-pair derivative (R18). The kernels form the gradients from per-Gaussian
+    moments (K5) through the closed forms of K6, whose rounding scale is exactly this sum of
+    monomials, not the sum of |term| (SURVEY 8(c).18's S_t = oracle `termabs`, <= S): entries
+    whose terms cancel within each pair have |term| << monomials.
+      dist="image" (image-like inputs): 1e-4 max(|g|, 1e-2 S) + 1e-8 max_i S_i -- SURVEY
+        8(c).18's 1e-2 factor; the absolute floor admits only entries whose whole mass lies in the
+        far exp tail (|q| ~ 100, where the fp32 rounding of the exponent alone is ~|q| 2^-24).
+      dist="stress": 1e-4 max(|g|, 1e-1 S) + 1e-8 max_i S_i (R18): sigma down to 0.01 and
+        |rho| -> 1 (D down to 1e-7) put the fp32 rounding above 1e-6 S there.
+    Evidence for both factors, and for why SURVEY's S_t cannot serve as the scale:
+    profiles/r02_bwd_gate.json (tools/bwd_gate_evidence.py)."""
+    w = flat9(want)
+    floor = 1e-2 if dist == "image" else 1e-1
+    atol = 1e-8 * absmass.max(axis=0, keepdims=True)
+    return rtol * np.maximum(np.abs(w), floor * absmass) + atol
+
+
+def assert_bwd_close(got, want, absmass, rtol=1e-4, dist="image"):
+    """Backward gate (gate_bounds): image-like inputs at 1e-2 S, the stress distribution at
+    DESIGN.md R18's 1e-1 S."""
     g = flat9(got)
     w = flat9(want)
-    # absolute floor per gradient component: 1e-8 of the largest term mass of the problem
-    # (entries whose whole mass lies in the exp tail, q < -30, are numerically zero in fp32)
-    atol = 1e-8 * absmass.max(axis=0, keepdims=True)
-    bound = rtol * np.maximum(np.abs(w), mass_floor * absmass) + atol
+    bound = gate_bounds(want, absmass, rtol, dist)
     err = np.abs(g - w)
     bad = err > bound + 1e-30
     rs = err / np.maximum(absmass, 1e-300)
-    print("err/S quantiles p50 %.2e p99 %.2e p99.99 %.2e max %.2e" % (
+    print("[%s gate] err/S quantiles p50 %.2e p99 %.2e p99.99 %.2e max %.2e" % (
+        "image 1e-2 S" if dist == "image" else "stress 1e-1 S (R18)",
         np.quantile(rs, 0.5), np.quantile(rs, 0.99), np.quantile(rs, 0.9999), rs.max()))
     if bad.any():
         ratio = err / (bound + 1e-30)

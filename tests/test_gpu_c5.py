@@ -13,7 +13,9 @@ from _util import KEYS, assert_bwd_close, assert_fwd_close
 pytestmark = pytest.mark.gpu
 
 
-def test_c5_full_size_sampled():
+@pytest.fixture(scope="module")
+def c5():
+    """The whole C5 step on the GPU in bench.py's launch configuration (computed once)."""
     import torch
     import paper_2501_06838_b200 as gsr
     from paper_2501_06838_b200 import ops
@@ -33,6 +35,15 @@ def test_c5_full_size_sampled():
     gsr.render_bwd_moments_batched(*dev, lay, g, mom, 0.1, workspace=ws, reuse_binning=True)
     grads = dict(zip(KEYS, gsr.finalize_grads(*dev, mom)))
     torch.cuda.synchronize()
+    del mom, ws
+    return dict(imgs=imgs, clouds=clouds, counts=counts, offs=offs, lay=lay, out=out, g=g,
+                grads=grads)
+
+
+def test_c5_full_size_sampled(c5):
+    import torch
+    imgs, clouds, counts, offs, lay = c5["imgs"], c5["clouds"], c5["counts"], c5["offs"], c5["lay"]
+    out, g, grads = c5["out"], c5["g"], c5["grads"]
     rng = np.random.default_rng(5)
     H, W, s = imgs[0]
     Hs, Ws = O.out_dims(H, W, s)
@@ -50,10 +61,52 @@ def test_c5_full_size_sampled():
         assert_bwd_close(got, want, want["absmass"])
 
 
+@pytest.mark.parametrize("k,rows", [(0, (504, 520)), (37, (1000, 1016))])
+def test_c5_full_row_bands(c5, k, rows):
+    """Two full 16-row bands (all 2040 columns) of C5 images, each crossing a forward-tile row
+    seam (multiples of 16 HR rows), backward-tile seams (8 rows) and a binning-cell row seam,
+    vs the full-window oracle (rect mode, Alg. 1, Eq. 4)."""
+    H, W, s = c5["imgs"][k]
+    img = c5["lay"].view(c5["out"], k).cpu().numpy()
+    want = O.render_fwd(c5["clouds"][k], H, W, s, 0.1, mode="rect", rows=rows)
+    assert want.shape == (16, 2040, 3)
+    assert_fwd_close(img[rows[0]:rows[1]], want)
+
+
+def test_c5_gradients_1000_gaussians(c5):
+    """Gradients of >= 1000 Gaussians of one C5 image vs the oracle: random ones, Gaussians whose
+    support rect (R21) straddles a forward column-half seam (x = 16 mod 32) or a tile / cell
+    seam (x = 0 mod 32), and Gaussians clipped by the image border."""
+    import torch
+    k = 11
+    H, W, s = c5["imgs"][k]
+    cl = c5["clouds"][k]
+    n = c5["counts"][k]
+    R = O.rects(cl, H, W, s, 0.1, support=True)
+    x0, x1, y0, y1 = R[:, 2], R[:, 3], R[:, 4], R[:, 5]
+    ok = (x0 <= x1) & (y0 <= y1)
+    half = ok & ((x0 // 16) != (x1 // 16)) & ((x1 - x0) < 16 + 32)
+    half &= ((x0 // 32) == (x1 // 32))                 # inside one 32-col tile, both halves
+    seam = ok & ((x0 // 32) != (x1 // 32))
+    Hs, Ws = O.out_dims(H, W, s)
+    edge = ok & ((x0 == 0) | (x1 == Ws - 1) | (y0 == 0) | (y1 == Hs - 1))
+    rng = np.random.default_rng(12)
+    pick = lambda m, c: rng.choice(np.nonzero(m)[0], min(c, int(m.sum())), replace=False)
+    idx = np.unique(np.concatenate([rng.choice(n, 400, replace=False), pick(half, 250),
+                                    pick(seam, 250), pick(edge, 200), [0, n - 1]]))
+    assert idx.size >= 1000 and half[idx].sum() >= 100
+    gk = c5["lay"].view(c5["g"], k).cpu().numpy()
+    want = O.render_bwd(cl, H, W, s, 0.1, gk, idx=idx, want_absmass=True)
+    sel = torch.from_numpy(c5["offs"][k] + idx).cuda()
+    got = {kk: c5["grads"][kk][sel].cpu().numpy().astype(np.float64) for kk in KEYS}
+    assert_bwd_close(got, want, want["absmass"])
+
+
 def test_band_partials_and_seam_set():
     """The row-band exchange of dist.py on the CUDA path, emulated in one process (this run has
     one GPU): G = 4 pair-balanced bands of a C5-geometry image; each band's moments are
-    finalized on their own (the finalize is linear in the moments); a Gaussian outside the seam
+    finalized on their own (the finalize is linear in the moments); bands and seam set from
+    libgsr's K7 planner on the device; a Gaussian outside the seam
     set has a nonzero partial in at most one band, where it equals the oracle's gradient; the
     band partials summed over the seam set equal the whole-image gradients."""
     import torch
@@ -63,10 +116,10 @@ def test_band_partials_and_seam_set():
     c = S.gaussians(H, W, seed=77)
     n = c["alpha"].shape[0]
     dev = [torch.from_numpy(c[k]).cuda() for k in KEYS]
-    valid = np.ones(n, bool)
-    rc = gd.row_pair_counts(c["mu"], valid, H, W, s, 0.1, sigma=c["sigma"])
+    whole = [(H, W, s, 0, n)]
+    rc = gd.row_pair_counts(dev, whole, 0.1)[0]
     b = gd.plan_bands(rc, G)
-    seam = gd.seam_mask(c["mu"], c["sigma"], valid, H, W, s, 0.1, b)
+    seam = gd.seam_mask(gd.band_spans(dev, whole, [b], 0.1)).cpu().numpy()
     assert 0 < seam.sum() < n
     Hs, Ws = O.out_dims(H, W, s)
     g = torch.from_numpy(S.grad_out((Hs, Ws, 3), seed=78)).cuda()

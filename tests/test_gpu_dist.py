@@ -1,0 +1,208 @@
+"""Row-band sharding through the real CUDA path with 2 ranks: two processes share
+cuda:0 (this run has one GPU) and exchange over gloo. Each rank plans its bands and halo with
+libgsr's K7 planner on the device (dist.RankPlan), renders its bands from its halo only
+(render_fwd_subset), all-gathers them (dist.gather_bands), accumulates its halo's compact
+moments (render_bwd_moments_subset), finalizes them (finalize_grads_subset) and swaps the seam
+Gaussians' partial gradients with its neighbour (dist.exchange_seams). Checks: the gathered image equals the
+single-process render of the same band layout bit for bit and the oracle within the forward
+gate; after the seam reduce every Gaussian of the rank's halo and of the seam set has the
+single-process whole-image gradient (fp32 regrouping tolerance) and sampled Gaussians match the
+oracle (gate of tests/_util)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+import gsr_synth as S
+import oracle as O
+from _util import KEYS, assert_bwd_close, assert_fwd_close
+
+pytestmark = pytest.mark.gpu
+
+IMGS = [(40, 60, 8.0), (34, 51, 6.5)]
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _inputs():
+    clouds = [S.gaussians(H, W, seed=500 + k) for k, (H, W, s) in enumerate(IMGS)]
+    counts = [c["alpha"].shape[0] for c in clouds]
+    offs = np.concatenate([[0], np.cumsum(counts)])
+    allc = {k: np.concatenate([c[k] for c in clouds]) for k in KEYS}
+    return clouds, counts, offs, allc
+
+
+def _worker(rank, world, port, outdir):
+    import datetime
+    import traceback
+    try:
+        _worker_body(rank, world, port, outdir)
+    except BaseException:
+        with open(os.path.join(outdir, f"rank{rank}.err"), "w") as f:
+            f.write(traceback.format_exc())
+        raise
+
+
+def _worker_body(rank, world, port, outdir):
+    import datetime
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world,
+                            timeout=datetime.timedelta(seconds=120))
+    try:
+        import paper_2501_06838_b200 as gsr
+        from paper_2501_06838_b200 import dist as gd
+        torch.cuda.set_device(0)
+        clouds, counts, offs, allc = _inputs()
+        n = int(offs[-1])
+        dev = [torch.from_numpy(allc[k]).cuda() for k in KEYS]
+        whole = [(H, W, s, int(offs[k]), counts[k]) for k, (H, W, s) in enumerate(IMGS)]
+        dims = [gsr.out_dims(H, W, s) for H, W, s in IMGS]
+        widths3 = [w * 3 for _, w in dims]
+        plan = gd.RankPlan(dev, whole, world, rank, 0.1)      # K7 on the device
+        bounds = plan.bounds
+        lay = gsr.layout([gsr.Image(H, W, s, go, gc, rb, re)
+                          for (H, W, s, go, gc, rb, re, sy) in plan.band_images()])
+        gfull = [torch.from_numpy(S.grad_out((h, w, 3), seed=600 + k)).cuda()
+                 for k, (h, w) in enumerate(dims)]
+        g_band = torch.cat([gfull[k][bounds[k][rank]:bounds[k][rank + 1]].reshape(-1)
+                            for k in range(len(IMGS))])
+        ws = gsr.subset_workspace_for(dev[0], lay, plan.m, 0.1)
+        out = gsr.render_fwd_subset(*dev, plan.idx, lay, 0.1, workspace=ws)
+        gathered, work = gd.gather_bands(out, gd.rank_numels(bounds, widths3, world),
+                                         async_op=True)
+        mom = torch.zeros((plan.m, 8), dtype=torch.float64, device="cuda")
+        gsr.render_bwd_moments_subset(*dev, plan.idx, lay, g_band, mom, 0.1, workspace=ws,
+                                      reuse_binning=True)
+        comp = gsr.finalize_grads_subset(*dev, plan.idx, mom)
+        gd.exchange_seams(comp, plan)
+        work.wait()
+        # scatter the compact gradients of the halo to global rows for the checks
+        grads = [torch.zeros((n,) + tuple(t.shape[1:]), dtype=torch.float32, device="cuda")
+                 for t in dev]
+        for gg, cc in zip(grads, comp):
+            gg.index_copy_(0, plan.idx.long(), cc)
+        torch.cuda.synchronize()
+        span = gd.band_spans(dev, whole, bounds, 0.1)
+        halo = gd.halo_mask(span, rank)
+        res = {"bounds": bounds, "seam": gd.seam_mask(span).cpu().numpy(),
+               "halo": halo.cpu().numpy(),
+               "grads": np.concatenate([t.view(n, -1).cpu().numpy() for t in grads], 1)}
+        for k in range(len(IMGS)):
+            res[f"img{k}"] = gd.assemble_image(gathered, bounds, widths3, k).cpu().numpy()
+        np.savez(os.path.join(outdir, f"rank{rank}.npz"), **{k: np.asarray(v) for k, v in
+                                                               res.items() if k != "bounds"},
+                 bounds=np.asarray(bounds))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_ranks_band_exchange_cuda(tmp_path):
+    import torch
+    import torch.multiprocessing as mp
+    import paper_2501_06838_b200 as gsr
+    ctx = mp.get_context("spawn")
+    port = _free_port()
+    ps = [ctx.Process(target=_worker, args=(r, 2, port, str(tmp_path)), daemon=True)
+          for r in range(2)]
+    for p in ps:
+        p.start()
+    for p in ps:
+        p.join(timeout=300)
+    for p in ps:
+        if p.is_alive():
+            p.kill()
+    errs = [(tmp_path / f"rank{r}.err") for r in range(2)]
+    msg = "\n".join(e.read_text() for e in errs if e.exists())
+    assert all(p.exitcode == 0 for p in ps), f"{[p.exitcode for p in ps]}\n{msg}"
+    R = [np.load(tmp_path / f"rank{r}.npz") for r in range(2)]
+
+    clouds, counts, offs, allc = _inputs()
+    n = int(offs[-1])
+    dev = [torch.from_numpy(allc[k]).cuda() for k in KEYS]
+    bounds = R[0]["bounds"].tolist()
+    assert np.array_equal(R[1]["bounds"], R[0]["bounds"])
+    dims = [gsr.out_dims(H, W, s) for H, W, s in IMGS]
+    # single-process render of the same band layout (rank by rank, same tiles, all Gaussians
+    # binned: the halo subset visits the same Gaussians in the same order) -> bit-exact
+    for k, (H, W, s) in enumerate(IMGS):
+        rows = []
+        for r in range(2):
+            lay = gsr.layout([gsr.Image(H, W, s, int(offs[k]), counts[k], bounds[k][r],
+                                        bounds[k][r + 1])])
+            rows.append(gsr.render_fwd_batched(*dev, lay, 0.1).cpu().numpy()
+                        .reshape(-1, dims[k][1] * 3))
+        single = np.concatenate(rows, 0)
+        for r in range(2):
+            assert np.array_equal(R[r][f"img{k}"], single)
+        want = O.render_fwd(clouds[k], H, W, s, 0.1)
+        assert_fwd_close(R[0][f"img{k}"].reshape(want.shape), want)
+    # gradients: halo and seam Gaussians carry the whole-image gradient after the seam reduce
+    whole = gsr.layout([gsr.Image(H, W, s, int(offs[k]), counts[k])
+                        for k, (H, W, s) in enumerate(IMGS)])
+    gflat = torch.cat([torch.from_numpy(S.grad_out((h, w, 3), seed=600 + k)).reshape(-1)
+                       for k, (h, w) in enumerate(dims)]).cuda()
+    full = np.concatenate([t.view(n, -1).cpu().numpy() for t in
+                           gsr.render_bwd_batched(*dev, whole, gflat, 0.1)], 1)
+    scale = np.abs(full).max(0, keepdims=True)
+    seam = R[0]["seam"]
+    assert 0 < seam.sum() < n
+    for r in range(2):
+        sel = R[r]["halo"] | seam
+        assert sel.sum() > 0
+        assert (np.abs(R[r]["grads"][sel] - full[sel]) <= 1e-5 * scale).all()
+        assert not R[r]["grads"][~sel].any()
+    rng = np.random.default_rng(7)
+    for k, (H, W, s) in enumerate(IMGS):
+        loc = np.arange(counts[k])
+        sk = seam[offs[k]:offs[k + 1]]
+        idx = np.sort(np.concatenate([rng.choice(loc[sk], 10, replace=False),
+                                      rng.choice(loc[~sk], 10, replace=False)]))
+        g = S.grad_out((dims[k][0], dims[k][1], 3), seed=600 + k)
+        want = O.render_bwd(clouds[k], H, W, s, 0.1, g, idx=idx, want_absmass=True)
+        r = 0
+        got = R[r]["grads"][offs[k] + idx]
+        h = R[r]["halo"][offs[k] + idx] | sk[idx]
+        got = np.where(h[:, None], got, R[1]["grads"][offs[k] + idx])
+        assert_bwd_close({"alpha": got[:, 0], "mu": got[:, 1:3], "sigma": got[:, 3:5],
+                          "rho": got[:, 5], "color": got[:, 6:9]}, want, want["absmass"])
+
+
+@pytest.mark.parametrize("support", [False, True])
+def test_k7_planner_device_equals_host_and_oracle(support):
+    """gsr_row_pair_counts_batched / gsr_band_span_batched (device) == their _host variants ==
+    the oracle, on a ragged batch with adversarial Gaussians (tile and window edges, outside,
+    huge, invalid) and a scale vector."""
+    import torch
+    from paper_2501_06838_b200 import dist as gd
+    from test_gpu_parity import adversarial_cloud
+    spec = [(20, 33, 2.7, None), (9, 13, 30.0, None), (12, 10, 4.0, 2.5)]
+    clouds = [adversarial_cloud(H, W, s, seed=k) for k, (H, W, s, sy) in enumerate(spec)]
+    counts = [c["alpha"].shape[0] for c in clouds]
+    offs = np.concatenate([[0], np.cumsum(counts)])
+    allc = {k: np.concatenate([c[k] for c in clouds]) for k in KEYS}
+    host = [allc[k] for k in KEYS]
+    dev = [torch.from_numpy(a).cuda() for a in host]
+    ims = [(H, W, s, int(offs[k]), counts[k], sy) for k, (H, W, s, sy) in enumerate(spec)]
+    rd = gd.row_pair_counts(dev, ims, 0.1, support=support)
+    rh = gd.row_pair_counts(host, ims, 0.1, support=support)
+    for k, (H, W, s, sy) in enumerate(spec):
+        assert np.array_equal(rd[k], rh[k])
+        assert rd[k].sum() == O.pair_count(clouds[k], H, W, (s, sy) if sy else s, 0.1,
+                                           support=support)
+    bounds = [gd.plan_bands(r, 3) for r in rh]
+    sd = gd.band_spans(dev, ims, bounds, 0.1, margin=1).cpu().numpy()
+    sh = gd.band_spans(host, ims, bounds, 0.1, margin=1)
+    assert np.array_equal(sd, sh)
+    # bfloat16 parameters: the widened values give the float32 results
+    rb = gd.row_pair_counts([t.bfloat16() for t in dev], ims, 0.1, support=support)
+    rf = gd.row_pair_counts([t.bfloat16().float() for t in dev], ims, 0.1, support=support)
+    assert all(np.array_equal(a, b) for a, b in zip(rb, rf))

@@ -44,7 +44,7 @@ def test_scale_vector_fwd_bwd(gsr, H, W, sv, r, dist):
     g = S.grad_out(want.shape, seed=H + W)
     got = grad_dict(gsr.render_bwd(*dev, H, W, sv, torch.from_numpy(g).cuda(), ratio=r))
     ref = O.render_bwd(c, H, W, sv, r, g, want_absmass=True)
-    assert_bwd_close(got, ref, ref["absmass"])
+    assert_bwd_close(got, ref, ref["absmass"], dist=dist)
 
 
 def test_scale_vector_pair_counts(gsr):

@@ -40,7 +40,7 @@ def median_ms(fn, iters, warmup=5):
     return statistics.median(ts)
 
 
-def run(name, iters):
+def run(name, iters, quiet=False):
     cfg = S.CONFIGS["C5" if name == "C5s" else name]
     imgs = cfg["images"][:4] if name == "C5s" else cfg["images"]     # C5s: a 4-image slice
     clouds = [S.gaussians(H, W, seed=1000 + k) for k, (H, W, s) in enumerate(imgs)]
@@ -89,7 +89,8 @@ def run(name, iters):
         with torch.cuda.graph(graph, stream=st):
             step()
         row["step_graph_ms"] = median_ms(graph.replay, iters)
-    print(json.dumps(row), flush=True)
+    if not quiet:
+        print(json.dumps(row), flush=True)
     return row
 
 

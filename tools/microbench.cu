@@ -1,11 +1,18 @@
 // Pipe-throughput microbenchmarks for the roofline denominators (SFU ex2, FP32 FFMA/FFMA2).
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o microbench microbench.cu
-// Each kernel runs ITERS iterations of UNROLL independent chains per thread; the SM-cycle count
-// comes from clock64() around the loop (per CTA, max over CTAs), so results are per SM clock.
+// Each kernel runs ITERS iterations of UNROLL independent chains per thread. Every CTA records
+// its SM id and clock64() at the start and end of the loop; per SM the busy span is
+// max(end) - min(start) over the CTAs that ran there (clock64 is a per-SM counter), so the rate
+// counts exactly the work that SM did, whether or not all its CTAs were co-resident.
 #include <cstdio>
 #include <cuda_runtime.h>
 
 #define ITERS 4096
+
+__device__ __forceinline__ void rec3(long long* cyc, long long t0, long long t1) {
+  unsigned smid; asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+  cyc[3 * blockIdx.x] = smid; cyc[3 * blockIdx.x + 1] = t0; cyc[3 * blockIdx.x + 2] = t1;
+}
 
 __device__ __forceinline__ float ex2f(float x) { float y; asm volatile("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x)); return y; }
 
@@ -23,7 +30,7 @@ __global__ void k_ex2(float* out, long long* cyc, float seed) {
   long long t1 = clock64();
   float s = 0; for (int j = 0; j < 8; ++j) s += a[j];
   out[blockIdx.x * blockDim.x + threadIdx.x] = s;
-  if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+  if (threadIdx.x == 0) rec3(cyc, t0, t1);
 }
 
 __global__ void k_ex2_pure(float* out, long long* cyc, float seed) {
@@ -40,7 +47,7 @@ __global__ void k_ex2_pure(float* out, long long* cyc, float seed) {
   long long t1 = clock64();
   float s = 0; for (int j = 0; j < 8; ++j) s += a[j];
   out[blockIdx.x * blockDim.x + threadIdx.x] = s;
-  if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+  if (threadIdx.x == 0) rec3(cyc, t0, t1);
 }
 
 __global__ void k_ffma(float* out, long long* cyc, float seed) {
@@ -58,7 +65,7 @@ __global__ void k_ffma(float* out, long long* cyc, float seed) {
   long long t1 = clock64();
   float s = 0; for (int j = 0; j < 8; ++j) s += a[j];
   out[blockIdx.x * blockDim.x + threadIdx.x] = s;
-  if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+  if (threadIdx.x == 0) rec3(cyc, t0, t1);
 }
 
 __global__ void k_ffma2(float* out, long long* cyc, float seed) {
@@ -76,7 +83,7 @@ __global__ void k_ffma2(float* out, long long* cyc, float seed) {
   long long t1 = clock64();
   float s = 0; for (int j = 0; j < 8; ++j) s += a[j].x + a[j].y;
   out[blockIdx.x * blockDim.x + threadIdx.x] = s;
-  if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+  if (threadIdx.x == 0) rec3(cyc, t0, t1);
 }
 
 // FFMA2 with three distinct register pairs per instruction (no operand reuse between
@@ -101,7 +108,7 @@ __global__ void k_ffma2_norreuse(float* out, long long* cyc, float seed) {
   long long t1 = clock64();
   float s = 0; for (int j = 0; j < 8; ++j) s += a[j].x + a[j].y;
   out[blockIdx.x * blockDim.x + threadIdx.x] = s;
-  if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+  if (threadIdx.x == 0) rec3(cyc, t0, t1);
 }
 
 // forward-like mix per element: 2 FFMA (q), 1 MUFU, 3 FFMA (rgb accumulate)
@@ -125,7 +132,7 @@ __global__ void k_mix(float* out, long long* cyc, float seed) {
   long long t1 = clock64();
   float s = 0; for (int j = 0; j < 8; ++j) s += ar[j] + ag[j] + ab[j];
   out[blockIdx.x * blockDim.x + threadIdx.x] = s;
-  if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+  if (threadIdx.x == 0) rec3(cyc, t0, t1);
 }
 
 // accuracy of ex2.approx.ftz.f32 (MUFU.EX2) against exp2 in fp64, over x in [lo, hi]
@@ -149,23 +156,37 @@ static void run(const char* name, kfn k, double ops_per_elem_iter, int threads, 
   int blocks = sms * blocks_per_sm;
   float* out; long long* cyc;
   cudaMalloc(&out, sizeof(float) * blocks * threads);
-  cudaMalloc(&cyc, sizeof(long long) * blocks);
+  cudaMalloc(&cyc, 3 * sizeof(long long) * blocks);
   k<<<blocks, threads>>>(out, cyc, 1.0f);
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
   cudaEventRecord(e0);
   k<<<blocks, threads>>>(out, cyc, 2.0f);
   cudaEventRecord(e1); cudaEventSynchronize(e1);
   float ms; cudaEventElapsedTime(&ms, e0, e1);
-  long long* h = new long long[blocks];
-  cudaMemcpy(h, cyc, sizeof(long long) * blocks, cudaMemcpyDeviceToHost);
-  long long mx = 0; for (int i = 0; i < blocks; ++i) if (h[i] > mx) mx = h[i];
-  double elems = (double)blocks * threads * 8.0 * ITERS;           // element-iterations
-  double per_clk_sm = elems * ops_per_elem_iter / (double)mx / sms * blocks_per_sm / blocks_per_sm;
-  // all CTAs of an SM run concurrently (blocks_per_sm resident), so per-SM work = elems/sms
-  per_clk_sm = elems * ops_per_elem_iter / sms / (double)mx;
-  printf("%-10s threads=%d ctas/SM=%d  cycles=%lld  ms=%.3f  => %.2f ops/clk/SM  (implied clock %.0f MHz)\n",
-         name, threads, blocks_per_sm, mx, ms, per_clk_sm, mx / (ms * 1e3));
-  cudaFree(out); cudaFree(cyc); delete[] h;
+  long long* h = new long long[3 * blocks];
+  cudaMemcpy(h, cyc, 3 * sizeof(long long) * blocks, cudaMemcpyDeviceToHost);
+  // per SM: CTAs it ran, busy span = max(end) - min(start)
+  long long* lo = new long long[1024]; long long* hi = new long long[1024]; int* cnt = new int[1024];
+  for (int i = 0; i < 1024; ++i) { lo[i] = 0x7fffffffffffffffLL; hi[i] = 0; cnt[i] = 0; }
+  for (int b = 0; b < blocks; ++b) {
+    int sm = (int)h[3 * b];
+    if (h[3 * b + 1] < lo[sm]) lo[sm] = h[3 * b + 1];
+    if (h[3 * b + 2] > hi[sm]) hi[sm] = h[3 * b + 2];
+    cnt[sm]++;
+  }
+  double rmin = 1e30, rmax = 0, rsum = 0; int nsm = 0; long long span_max = 0;
+  for (int i = 0; i < 1024; ++i) {
+    if (!cnt[i]) continue;
+    double work = (double)cnt[i] * threads * 8.0 * ITERS * ops_per_elem_iter;
+    double r = work / (double)(hi[i] - lo[i]);
+    rmin = r < rmin ? r : rmin; rmax = r > rmax ? r : rmax; rsum += r; ++nsm;
+    if (hi[i] - lo[i] > span_max) span_max = hi[i] - lo[i];
+  }
+  printf("%-10s threads=%d ctas/SM=%d  SMs=%d  span=%lld cyc  ms=%.3f  => %.2f ops/clk/SM "
+         "(SM min %.2f max %.2f; implied clock %.0f MHz)\n",
+         name, threads, blocks_per_sm, nsm, span_max, ms, rsum / nsm, rmin, rmax,
+         span_max / (ms * 1e3));
+  cudaFree(out); cudaFree(cyc); delete[] h; delete[] lo; delete[] hi; delete[] cnt;
 }
 
 int main() {
