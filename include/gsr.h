@@ -326,6 +326,39 @@ gsr_status gsr_band_span_host(const void* alpha, const void* mu, const void* sig
                               const gsr_image* imgs, int32_t n_imgs, double ratio,
                               uint32_t flags, const int32_t* bounds, int32_t n_bands,
                               int32_t margin, int16_t* span);
+/* gsr_rank_halo: rank `rank`'s share of the shard in one fused pass (the band spans above are
+ * computed on the fly, nothing of size n is materialised but a byte per Gaussian of workspace):
+ *   idx[0..m)        ascending indices of its halo (first <= rank <= last): the idx of the
+ *                    gsr_*_subset calls;
+ *   up[0..nu)        positions in idx of the Gaussians whose span is exactly [rank, rank+1] --
+ *                    the seam rows swapped with rank + 1 (ascending Gaussian order, so both
+ *                    neighbours list the same Gaussians in the same order);
+ *   down[0..nd)      likewise [rank-1, rank], swapped with rank - 1;
+ *   multi_pos/multi_slot[0..nm)  Gaussians of the halo spanning >= 3 bands: position in idx and
+ *                    slot in the global list of all nM such Gaussians (every rank all-reduces a
+ *                    [nM] buffer);
+ *   totals[5]        {m, nu, nd, nm, nM} (device int64).
+ * All output arrays are device int32 with capacity n_total; results are written asynchronously
+ * on `stream`. Workspace: gsr_rank_halo_workspace_bytes(n_total). Bounds, n_bands and margin as
+ * for gsr_band_span_*; 0 <= rank < n_bands. Flags: GSR_PARAMS_BF16. */
+size_t gsr_rank_halo_workspace_bytes(int64_t n_total);
+gsr_status gsr_rank_halo(const void* alpha, const void* mu, const void* sigma, const void* rho,
+                         const void* color, int64_t n_total, const gsr_image* imgs,
+                         int32_t n_imgs, double ratio, uint32_t flags, const int32_t* bounds,
+                         int32_t n_bands, int32_t margin, int32_t rank, int32_t* idx,
+                         int32_t* up, int32_t* down, int32_t* multi_pos, int32_t* multi_slot,
+                         int64_t* totals, void* workspace, size_t workspace_bytes,
+                         void* stream);
+
+/* Parameter-domain check (R20): writes result[0] = number of Gaussians outside the
+ * domain (a non-finite field, sigma_x <= 0, sigma_y <= 0 or |rho| >= 1) and result[1] = the
+ * smallest such index (INT64 -1 = 0xffff...ffff when there is none); result is a DEVICE int64[2],
+ * written asynchronously on `stream` (read it after a sync). Such Gaussians are not an error for
+ * the render entry points (they contribute 0 and get zero gradient); this is the debugging aid
+ * that reports them. Flags: GSR_PARAMS_BF16. */
+gsr_status gsr_validate_params(const void* alpha, const void* mu, const void* sigma,
+                               const void* rho, const void* color, int64_t n, uint32_t flags,
+                               int64_t* result, void* stream);
 
 /* ---- introspection for the parity tests (same kernels as the render path) ---------------- */
 

@@ -9,10 +9,11 @@ from .ops import (Image, Layout, finalize_grads, finalize_grads_subset, layout, 
                   render, render_batch, render_bwd, render_bwd_batched,
                   render_bwd_moments_batched, render_bwd_moments_subset, render_fwd,
                   render_fwd_batched, render_fwd_subset, subset_workspace_for, StreamedFwdBwd,
-                  TrainStepGraph, train_step_l1)
+                  TrainStepGraph, train_step_l1, validate_params)
 
 __all__ = ["GsrError", "load", "out_dims", "tile_shape", "version", "Image", "Layout",
            "finalize_grads", "layout", "pair_count", "render", "render_batch", "render_bwd",
            "render_bwd_batched", "render_bwd_moments_batched", "render_fwd", "render_fwd_batched",
            "StreamedFwdBwd", "TrainStepGraph", "train_step_l1", "render_fwd_subset",
-           "render_bwd_moments_subset", "finalize_grads_subset", "subset_workspace_for"]
+           "render_bwd_moments_subset", "finalize_grads_subset", "subset_workspace_for",
+           "validate_params"]

@@ -26,7 +26,8 @@ EXPORTS = ["gsr_version", "gsr_out_dims", "gsr_out_dims_v", "gsr_workspace_bytes
            "gsr_pair_count_batched_ex", "gsr_debug_rects_ex", "gsr_render_fwd_batched_ex",
            "gsr_finalize_grads_ex", "gsr_row_pair_counts_batched", "gsr_row_pair_counts_host",
            "gsr_band_span_batched", "gsr_band_span_host", "gsr_workspace_bytes_subset",
-           "gsr_render_fwd_subset", "gsr_render_bwd_moments_subset", "gsr_finalize_grads_subset"]
+           "gsr_render_fwd_subset", "gsr_render_bwd_moments_subset", "gsr_finalize_grads_subset",
+           "gsr_validate_params", "gsr_rank_halo_workspace_bytes", "gsr_rank_halo"]
 GSR_REUSE_BINNING = 0x1
 GSR_SUPPORT = 0x2
 GSR_OUT_BF16 = 0x4
@@ -113,6 +114,10 @@ def load(path: Path | str | None = None):
                                                  ctypes.c_uint32, _P], None),
         "gsr_finalize_grads_subset": (par + [_I64, _P, _I64, _P, _P, _P, _P, _P, _P,
                                              ctypes.c_uint32, _P], None),
+        "gsr_validate_params": (par + [_I64, ctypes.c_uint32, _P, _P], None),
+        "gsr_rank_halo_workspace_bytes": ([_I64], _SZ),
+        "gsr_rank_halo": (par + [_I64, _IMGP, _I32, _D, ctypes.c_uint32, _P, _I32, _I32, _I32,
+                                 _P, _P, _P, _P, _P, _P, _P, _SZ, _P], None),
         "gsr_tile_shape": ([ctypes.POINTER(_I32)] * 4, "void"),
         "gsr_profile_enable": ([_I32], None),
         "gsr_profile_collect": ([_P, _P, _P, _I32], None),

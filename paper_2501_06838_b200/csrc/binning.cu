@@ -321,6 +321,22 @@ __global__ void k_pair_count(const T* __restrict__ alpha, const T* __restrict__ 
     if ((threadIdx.x & 31) == 0 && v) atomicAdd(out, v);
 }
 
+// R20 parameter-domain check (gsr_validate_params): count of invalid Gaussians and the smallest
+// invalid index (atomicMin), per call
+template <class T>
+__global__ void k_validate(const T* __restrict__ alpha, const T* __restrict__ mu,
+                           const T* __restrict__ sigma, const T* __restrict__ rho,
+                           const T* __restrict__ color, long long n,
+                           unsigned long long* __restrict__ out) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const bool bad = i < n && !valid_at(alpha, mu, sigma, rho, color, i);
+    const unsigned m = __ballot_sync(0xffffffffu, bad);
+    if (m && (threadIdx.x & 31) == 0) {
+        atomicAdd(&out[0], (unsigned long long)__popc(m));
+        atomicMin(&out[1], (unsigned long long)(i + __ffs(m) - 1));
+    }
+}
+
 __global__ void k_debug_rects(const float* __restrict__ alpha, const float* __restrict__ mu,
                               const float* __restrict__ sigma, const float* __restrict__ rho,
                               const float* __restrict__ color, long long n, ImgTable tab,
@@ -519,6 +535,24 @@ cudaError_t launch_pair_count(const void* alpha, const void* mu, const void* sig
                 (const float*)alpha, (const float*)mu, (const float*)sigma, (const float*)rho,
                 (const float*)color, n, tab, support, (unsigned long long*)d_pairs);
         }
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_validate(const void* alpha, const void* mu, const void* sigma,
+                            const void* rho, const void* color, long long n, bool bf16,
+                            unsigned long long* d_out, cudaStream_t st) {
+    if (n <= 0) return cudaSuccess;
+    count_launches(1);
+    if (bf16) {
+        using B = __nv_bfloat16;
+        k_validate<B><<<grid1d(n, 256), 256, 0, st>>>((const B*)alpha, (const B*)mu,
+                                                      (const B*)sigma, (const B*)rho,
+                                                      (const B*)color, n, d_out);
+    } else {
+        k_validate<float><<<grid1d(n, 256), 256, 0, st>>>(
+            (const float*)alpha, (const float*)mu, (const float*)sigma, (const float*)rho,
+            (const float*)color, n, d_out);
     }
     return cudaGetLastError();
 }

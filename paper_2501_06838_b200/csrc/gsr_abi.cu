@@ -559,6 +559,19 @@ gsr_status gsr_pair_count_batched(const float* alpha, const float* mu, const flo
                                      0u, d_pairs, workspace, workspace_bytes, stream);
 }
 
+gsr_status gsr_validate_params(const void* alpha, const void* mu, const void* sigma,
+                               const void* rho, const void* color, int64_t n, uint32_t flags,
+                               int64_t* result, void* stream) {
+    if (n < 0 || !result || (flags & ~GSR_PARAMS_BF16)) return GSR_EINVAL;
+    if (!params_ok(alpha, mu, sigma, rho, color, n)) return GSR_EINVAL;
+    cudaStream_t st = (cudaStream_t)stream;
+    const unsigned long long init[2] = {0ull, ~0ull};
+    cudaMemcpyAsync(result, init, sizeof(init), cudaMemcpyHostToDevice, st);
+    return finish(launch_validate(alpha, mu, sigma, rho, color, n,
+                                  (flags & GSR_PARAMS_BF16) != 0, (unsigned long long*)result,
+                                  st));
+}
+
 // ---- K7 band planning (plan.cu) ----------------------------------------------------------
 static gsr_status plan_prepare(const void* alpha, const void* mu, const void* sigma,
                                const void* rho, const void* color, int64_t n_total,
@@ -641,6 +654,32 @@ gsr_status gsr_band_span_batched(const void* alpha, const void* mu, const void* 
     if (s != GSR_OK) return s;
     return finish(launch_band_span(alpha, mu, sigma, rho, color, n_total, tab, bt[0], span,
                                    (cudaStream_t)stream));
+}
+
+size_t gsr_rank_halo_workspace_bytes(int64_t n_total) {
+    return n_total < 0 ? 0 : rank_halo_bytes(n_total);
+}
+
+gsr_status gsr_rank_halo(const void* alpha, const void* mu, const void* sigma, const void* rho,
+                         const void* color, int64_t n_total, const gsr_image* imgs,
+                         int32_t n_imgs, double ratio, uint32_t flags, const int32_t* bounds,
+                         int32_t n_bands, int32_t margin, int32_t rank, int32_t* idx,
+                         int32_t* up, int32_t* down, int32_t* multi_pos, int32_t* multi_slot,
+                         int64_t* totals, void* workspace, size_t workspace_bytes,
+                         void* stream) {
+    ImgTable tab;
+    gsr_status s = plan_prepare(alpha, mu, sigma, rho, color, n_total, imgs, n_imgs, ratio, flags,
+                                GSR_PARAMS_BF16, &tab);
+    if (s != GSR_OK) return s;
+    if (rank < 0 || rank >= n_bands || !totals) return GSR_EINVAL;
+    if (n_total > 0 && (!idx || !up || !down || !multi_pos || !multi_slot)) return GSR_EINVAL;
+    if (!workspace || workspace_bytes < rank_halo_bytes(n_total)) return GSR_EWORKSPACE;
+    std::vector<BandTable> bt(1);
+    s = band_table(tab, bounds, n_bands, margin, bt.data());
+    if (s != GSR_OK) return s;
+    return finish(launch_rank_halo(alpha, mu, sigma, rho, color, n_total, tab, bt[0], rank,
+                                   workspace, idx, up, down, multi_pos, multi_slot,
+                                   (long long*)totals, (cudaStream_t)stream));
 }
 
 gsr_status gsr_band_span_host(const void* alpha, const void* mu, const void* sigma,

@@ -435,6 +435,9 @@ cudaError_t launch_pair_count(const void* alpha, const void* mu, const void* sig
                               const void* rho, const void* color, long long n,
                               const ImgTable& tab, bool support, long long* d_pairs,
                               cudaStream_t st);
+cudaError_t launch_validate(const void* alpha, const void* mu, const void* sigma,
+                            const void* rho, const void* color, long long n, bool bf16,
+                            unsigned long long* d_out, cudaStream_t st);
 cudaError_t launch_debug_rects(const float* alpha, const float* mu, const float* sigma,
                                const float* rho, const float* color, long long n,
                                const ImgTable& tab, bool support, int* rects, cudaStream_t st);
@@ -457,6 +460,13 @@ cudaError_t launch_band_span(const void* alpha, const void* mu, const void* sigm
 void band_span_host(const void* alpha, const void* mu, const void* sigma, const void* rho,
                     const void* color, long long n, const ImgTable& tab, const BandTable& bt,
                     int16_t* span);
+
+size_t rank_halo_bytes(long long n);
+cudaError_t launch_rank_halo(const void* alpha, const void* mu, const void* sigma,
+                             const void* rho, const void* color, long long n, const ImgTable& tab,
+                             const BandTable& bt, int rank, void* ws, int* idx, int* up,
+                             int* down, int* multi_pos, int* multi_slot, long long* totals,
+                             cudaStream_t st);
 
 // render_fwd.cu
 cudaError_t launch_render_fwd(const ImgTable& tab, const Workspace& ws, float* out,

@@ -15,15 +15,17 @@
 //   d rho = (rho S0 + Spv - rho Spp/D)/D
 // (derivation in DESIGN.md "Backward"; the oracle uses direct per-pair derivatives instead).
 //
-// Layout of K5: one CTA per 32 x 32 HR tile (the forward's tiles) with the tile's dL/dI staged in
-// shared memory as column pairs. Lanes own Gaussians: each warp takes 32 consecutive candidates
-// of a cell-row span, and all 32 lanes walk the same pixels (warp-uniform loop bounds from the
-// union of their rects), reading dL/dI as shared-memory broadcasts. Per-pair work is paired over
-// two pixels with FFMA2. Within a row the vq-dependent moments are factored out
-// (sum_row w vq = vq sum_row w, ...), so a pair costs 12.5 FP32 lane-ops + 1 ex2 (kx shared by a row pair, w, q, 3 e g, 3 g.c',
-// 4 moments); lanes process two rows at once for two independent accumulation chains. Row partials
-// (fp32, <= 16 terms per lane half) are folded into fp64 per-(Gaussian, tile) accumulators, which
-// leave the CTA as 8 fp64 atomics -- the only global atomics of the backward.
+// Layout of K5: one CTA (4 warps) per 64 x 8 HR tile with the tile's dL/dI staged in shared
+// memory as column pairs. Lanes own Gaussians: each warp scans its share of the tile's
+// candidate spans (support rect vs tile; SCAN_U chunks of loads in flight), queues the hits with
+// a key = their clipped column range, sorts each batch of 512 hits by key and evaluates groups of
+// 32: all 32 lanes walk the same pixels (warp-uniform loop bounds from the union of their support
+// rects), reading dL/dI as shared-memory broadcasts. Per-pair work is paired over two pixels with
+// FFMA2. Within a row the vq-dependent moments are factored out (sum_row w vq = vq sum_row w, ...),
+// so a pair costs 12.5 FP32 lane-ops + 1 ex2 (kx shared by a row pair, w, q, 3 e g, 3 g.c',
+// 4 moments); lanes process two rows at once for two independent accumulation chains. Row
+// partials (fp32, <= 32 terms per register half) are folded into fp32 per-(Gaussian, tile)
+// accumulators, which leave the CTA as 8 fp64 atomics -- the only global atomics of the backward.
 #include <atomic>
 
 #include "gsr_internal.cuh"
@@ -31,17 +33,14 @@
 #ifndef GSR_BWD_UNROLL
 #define GSR_BWD_UNROLL 8
 #endif
-#ifndef GSR_BWD_CONTIG
-#define GSR_BWD_CONTIG 0          // 1: each warp scans a contiguous share of every span
+#ifndef GSR_BWD_SCAN_U
+#define GSR_BWD_SCAN_U 4          // candidate chunks whose rect loads are in flight together
 #endif
 #ifndef GSR_BWD_KQ
 #define GSR_BWD_KQ 16             // grouping key: column buckets per axis (8 or 16)
 #endif
 #ifndef GSR_BWD_BATCH
 #define GSR_BWD_BATCH 512         // hits per sorted batch (multiple of 32)
-#endif
-#ifndef GSR_BWD_SNAKE
-#define GSR_BWD_SNAKE 1
 #endif
 #ifndef GSR_BWD_MACC_T
 #define GSR_BWD_MACC_T float      // per-(Gaussian, tile) accumulator type of the row folds
@@ -64,36 +63,6 @@ struct LaneG {        // per-lane Gaussian constants
 struct RowAcc {       // per-row partial sums of a lane (register pairs = two pixels)
     float2 FR, FG, FB, W1, W2;
 };
-
-// One pixel pair (columns c, c+1) of one row: 1 FFMA2 (w) + 1 FFMA2 (q) + 2 ex2 + 3 FFMA2 (e g)
-// + 3 (g . c') + 4 (moments) -- all paired over the two pixels.
-template <bool MASKED>
-__device__ __forceinline__ void pix_pair(const float4 ga, const float2 gb, const float2 kx,
-                                         const float2 T2, const float2 U2, const LaneG& L,
-                                         bool in0, bool in1, RowAcc& A) {
-    const float2 w = __ffma2_rn(L.D2, kx, T2);                       // a1 dx + b1 dy
-    float2 q = __ffma2_rn(make_float2(-w.x, -w.y), w, U2);           // -(w^2) - v^2
-    if (MASKED) {
-        q.x = in0 ? q.x : -INFINITY;
-        q.y = in1 ? q.y : -INFINITY;
-    }
-    const float2 e = make_float2(ex2_approx(q.x), ex2_approx(q.y));
-    const float2 gr = make_float2(ga.x, ga.y), gg = make_float2(ga.z, ga.w);
-    // g . c' first (scalar-broadcast operands), then the accumulations grouped by their shared
-    // operand (e for the three channel sums, g.c' for the two moments) so that consecutive FFMA2s
-    // can hit the operand reuse cache: an FFMA2 that reads three fresh register pairs costs 3
-    // issue cycles instead of 2 (register-file bandwidth; tools/microbench.cu "ffma2_nr").
-    float2 gc = __fmul2_rn(gr, L.cr);
-    gc = __ffma2_rn(gg, L.cg, gc);
-    gc = __ffma2_rn(gb, L.cb, gc);
-    const float2 ed = __fmul2_rn(e, w);                              // e wq
-    const float2 edd = __fmul2_rn(ed, w);                            // e wq^2
-    A.FR = __ffma2_rn(e, gr, A.FR);
-    A.FG = __ffma2_rn(e, gg, A.FG);
-    A.FB = __ffma2_rn(e, gb, A.FB);
-    A.W1 = __ffma2_rn(gc, ed, A.W1);
-    A.W2 = __ffma2_rn(gc, edd, A.W2);
-}
 
 // Both rows of a row pair at one column pair, ordered so that every FFMA2 after the first of a
 // group shares an operand register (same slot) with its predecessor: the operand then comes
@@ -162,13 +131,8 @@ __device__ __forceinline__ void row2_pairs(int c_begin, int c_end, const float4*
             in0 = xa >= L.x0 && xa <= L.x1;
             in1 = xa + 1 >= L.x0 && xa + 1 <= L.x1;
         }
-#if GSR_BWD_SNAKE
         pix_pair2<MASKED>(gA0[cp], gB0[cp], gA1[cp], gB1[cp], kx, T0, U0, T1, U1, L, in0, in1, A0,
                           A1);
-#else
-        pix_pair<MASKED>(gA0[cp], gB0[cp], kx, T0, U0, L, in0, in1, A0);
-        pix_pair<MASKED>(gA1[cp], gB1[cp], kx, T1, U1, L, in0, in1, A1);
-#endif
         kx = __fadd2_rn(kx, two);
     }
 }
@@ -253,9 +217,10 @@ __global__ void __launch_bounds__(BWD_THREADS) k_render_bwd(
     constexpr int KQ = GSR_BWD_KQ;                // column buckets per axis
     constexpr int NB = KQ * KQ;                   // key buckets (x0 bucket, x1 bucket)
     constexpr int NBL = NB / 32;                  // buckets per lane in the scan
-    __shared__ int qp[BWD_WARPS][BWD_BATCH + 32];
-    __shared__ unsigned short qk[BWD_WARPS][BWD_BATCH + 32];
-    __shared__ int qs[BWD_WARPS][BWD_BATCH + 32];
+    constexpr int SCAN_U = GSR_BWD_SCAN_U;
+    __shared__ int qp[BWD_WARPS][BWD_BATCH + 32 * SCAN_U];
+    __shared__ unsigned short qk[BWD_WARPS][BWD_BATCH + 32 * SCAN_U];
+    __shared__ int qs[BWD_WARPS][BWD_BATCH + 32 * SCAN_U];
     __shared__ int hist[BWD_WARPS][NB];
     const unsigned lt = (1u << lane) - 1u;
     int qn = 0;                                   // warp-uniform queue length
@@ -387,47 +352,54 @@ __global__ void __launch_bounds__(BWD_THREADS) k_render_bwd(
             const bool act = g + lane < cnt;
             group(act ? qs[warp][g + lane] : 0, act);
         }
-        const int rest = qn - cnt;                // < 32
-        int cp = 0;
-        unsigned short ck = 0;
-        if (lane < rest) { cp = qp[warp][cnt + lane]; ck = qk[warp][cnt + lane]; }
-        __syncwarp();
-        if (lane < rest) { qp[warp][lane] = cp; qk[warp][lane] = ck; }
+        const int rest = qn - cnt;                // < 32 * SCAN_U, moved to the front
+        for (int r0 = 0; r0 < rest; r0 += 32) {
+            int cp = 0;
+            unsigned short ck = 0;
+            const bool mv = r0 + lane < rest;
+            if (mv) { cp = qp[warp][cnt + r0 + lane]; ck = qk[warp][cnt + r0 + lane]; }
+            __syncwarp();
+            if (mv) { qp[warp][r0 + lane] = cp; qk[warp][r0 + lane] = ck; }
+            __syncwarp();
+        }
         qn = rest;
         __syncwarp();
     };
 
+    // Scan: SCAN_U chunks of 32 candidates (every parts-th chunk of the span, the same order as
+    // one chunk at a time) have their rect loads in flight together, then are queued in order.
     for (int cy = cy_lo; cy <= cy_hi; ++cy) {
         const int row = im.cell_base + cy * im.ncx;
         const int s0 = cell_start[row + cx_lo], s1 = cell_start[row + cx_hi + 1];
         const int parts = ks * BWD_WARPS, part = kpart * BWD_WARPS + warp;
-#if GSR_BWD_CONTIG
-        const int sp0 = s0 + (int)(((long long)(s1 - s0) * part) / parts);
-        const int sp1 = s0 + (int)(((long long)(s1 - s0) * (part + 1)) / parts);
-        for (int p0 = sp0; p0 < sp1; p0 += 32) {
-#else
-        const int sp1 = s1;
-        for (int p0 = s0 + part * 32; p0 < sp1; p0 += parts * 32) {
-#endif
-            const int p = p0 + lane;
-            bool hit = false;
-            int key = 0;
-            if (p < sp1) {
-                const int4 rc = __ldg(rects + p);
-                const unsigned xs = (unsigned)rc.x, ys = (unsigned)rc.y;
-                const int x0 = (int)(xs & 0xffffu), x1 = (int)(xs >> 16);
-                const int y0 = (int)(ys & 0xffffu), y1 = (int)(ys >> 16);
-                hit = !(x1 < Tx0 || x0 > Tx1 || y1 < Ty0 || y0 > Ty1);
-                key = ((max(x0, Tx0) - Tx0) / (TILE_W / KQ)) * KQ +
-                      (min(x1, Tx1) - Tx0) / (TILE_W / KQ);
+        for (int p0 = s0 + part * 32; p0 < s1; p0 += parts * 32 * SCAN_U) {
+            int4 rc[SCAN_U];
+#pragma unroll
+            for (int u = 0; u < SCAN_U; ++u) {
+                const int p = p0 + u * parts * 32 + lane;
+                rc[u] = p < s1 ? __ldg(rects + p) : make_int4(0, 0, 0x7fff7fff, 0);
             }
-            const unsigned hm = __ballot_sync(0xffffffffu, hit);
-            if (hit) {
-                const int slot = qn + __popc(hm & lt);
-                qp[warp][slot] = p;
-                qk[warp][slot] = (unsigned short)key;
+#pragma unroll
+            for (int u = 0; u < SCAN_U; ++u) {
+                const int p = p0 + u * parts * 32 + lane;
+                bool hit = false;
+                int key = 0;
+                if (p < s1) {
+                    const unsigned xs = (unsigned)rc[u].x, ys = (unsigned)rc[u].y;
+                    const int x0 = (int)(xs & 0xffffu), x1 = (int)(xs >> 16);
+                    const int y0 = (int)(ys & 0xffffu), y1 = (int)(ys >> 16);
+                    hit = !(x1 < Tx0 || x0 > Tx1 || y1 < Ty0 || y0 > Ty1);
+                    key = ((max(x0, Tx0) - Tx0) / (TILE_W / KQ)) * KQ +
+                          (min(x1, Tx1) - Tx0) / (TILE_W / KQ);
+                }
+                const unsigned hm = __ballot_sync(0xffffffffu, hit);
+                if (hit) {
+                    const int slot = qn + __popc(hm & lt);
+                    qp[warp][slot] = p;
+                    qk[warp][slot] = (unsigned short)key;
+                }
+                qn += __popc(hm);
             }
-            qn += __popc(hm);
             __syncwarp();
             if (qn >= BWD_BATCH) flush(BWD_BATCH);
         }

@@ -313,6 +313,8 @@ class RankPlan:
     def refresh(self, params):
         import torch
         r, G = self.rank, self.world
+        if not _is_host(params) and len(self.images) <= 64:
+            return self._refresh_device(params)
         span = torch.as_tensor(band_spans(params, self.images, self.bounds, self.ratio))
         f, l = span[:, 0].to(torch.int32), span[:, 1].to(torch.int32)
         halo = (f <= r) & (l >= r)
@@ -326,6 +328,39 @@ class RankPlan:
         self.multi_pos = pos[multi[inh]]
         self.multi_slot = torch.nonzero(inh).reshape(-1)
         self.n_seam_local = int(self.up.numel() + self.down.numel() + self.multi_pos.numel())
+        return self
+
+    def _refresh_device(self, params):
+        """One fused libgsr pass (gsr_rank_halo) instead of materialising the spans: halo
+        compaction and the seam position lists on the device, one sync for the five counts."""
+        import torch
+        from . import _lib
+        lib = _lib.load()
+        dev = params[0].device
+        n = int(params[0].shape[0])
+        if getattr(self, "_buf", None) is None or self._buf[0].numel() < max(n, 1):
+            self._buf = [torch.empty(max(n, 1), dtype=torch.int32, device=dev) for _ in range(5)]
+            self._hws = torch.empty(max(int(lib.gsr_rank_halo_workspace_bytes(n)), 256),
+                                    dtype=torch.uint8, device=dev)
+            self._tot = torch.empty(5, dtype=torch.int64, device=dev)
+        g0, g1, arr, m, sel = next(_plan_calls(params, self.images))
+        if g0 != 0:
+            raise ValueError("RankPlan needs images whose Gaussian ranges start at 0")
+        b = np.ascontiguousarray(np.array(self.bounds, np.int32))
+        _lib.check(lib.gsr_rank_halo(*_ptrs(params, 0), n, arr, m, float(self.ratio),
+                                     _flags(params), b.ctypes.data, self.world, 0, self.rank,
+                                     *[t.data_ptr() for t in self._buf], self._tot.data_ptr(),
+                                     self._hws.data_ptr(), self._hws.numel(),
+                                     torch.cuda.current_stream(dev).cuda_stream),
+                   "gsr_rank_halo")
+        nh, nu, nd, nm, nM = (int(v) for v in self._tot.cpu())
+        self.idx = self._buf[0][:nh]
+        self.up = self._buf[1][:nu].long()
+        self.down = self._buf[2][:nd].long()
+        self.multi_pos = self._buf[3][:nm].long()
+        self.multi_slot = self._buf[4][:nm].long()
+        self.n_multi = nM
+        self.n_seam_local = nu + nd + nm
         return self
 
     @property

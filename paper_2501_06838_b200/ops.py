@@ -305,6 +305,18 @@ def render_bwd_batched(alpha, mu, sigma, rho, color, lay: Layout, grad_out: torc
     return tuple(grads)
 
 
+def validate_params(alpha, mu, sigma, rho, color):
+    """(count, first index or -1) of the Gaussians outside the parameter domain (R20:
+    non-finite field, sigma <= 0 or |rho| >= 1) -- gsr_validate_params; synchronises."""
+    params, n = _params(alpha, mu, sigma, rho, color)
+    dev = params[0].device
+    res = torch.empty(2, dtype=torch.int64, device=dev)
+    check(_lib.load().gsr_validate_params(*[_ptr(t) for t in params], n, _fmt_flags(params),
+                                          _ptr(res), _stream_ptr(dev)), "gsr_validate_params")
+    cnt, first = (int(v) for v in res.cpu())
+    return cnt, (first if cnt else -1)
+
+
 # ------------------------------------------------------------------ subset mode (a rank's halo)
 def _check_idx(idx: torch.Tensor, n: int, dev) -> torch.Tensor:
     if not isinstance(idx, torch.Tensor) or idx.dtype != torch.int32 or idx.dim() != 1:

@@ -131,18 +131,19 @@ def test_two_ranks_band_exchange_cuda(tmp_path):
     bounds = R[0]["bounds"].tolist()
     assert np.array_equal(R[1]["bounds"], R[0]["bounds"])
     dims = [gsr.out_dims(H, W, s) for H, W, s in IMGS]
-    # single-process render of the same band layout (rank by rank, same tiles, all Gaussians
-    # binned: the halo subset visits the same Gaussians in the same order) -> bit-exact
+    # single-process render of each rank's band layout (same images, tiles and split factor;
+    # all Gaussians binned -- the halo subset visits the same Gaussians in the same order)
+    # -> bit-exact
+    widths3 = [w * 3 for _, w in dims]
+    for r in range(2):
+        lay = gsr.layout([gsr.Image(H, W, s, int(offs[k]), counts[k], bounds[k][r],
+                                    bounds[k][r + 1]) for k, (H, W, s) in enumerate(IMGS)])
+        ref = gsr.render_fwd_batched(*dev, lay, 0.1)
+        for k in range(len(IMGS)):
+            got = R[0][f"img{k}"][bounds[k][r]:bounds[k][r + 1]]
+            assert np.array_equal(got, lay.view(ref, k).cpu().numpy().reshape(got.shape))
+            assert np.array_equal(R[1][f"img{k}"], R[0][f"img{k}"])
     for k, (H, W, s) in enumerate(IMGS):
-        rows = []
-        for r in range(2):
-            lay = gsr.layout([gsr.Image(H, W, s, int(offs[k]), counts[k], bounds[k][r],
-                                        bounds[k][r + 1])])
-            rows.append(gsr.render_fwd_batched(*dev, lay, 0.1).cpu().numpy()
-                        .reshape(-1, dims[k][1] * 3))
-        single = np.concatenate(rows, 0)
-        for r in range(2):
-            assert np.array_equal(R[r][f"img{k}"], single)
         want = O.render_fwd(clouds[k], H, W, s, 0.1)
         assert_fwd_close(R[0][f"img{k}"].reshape(want.shape), want)
     # gradients: halo and seam Gaussians carry the whole-image gradient after the seam reduce
@@ -206,3 +207,32 @@ def test_k7_planner_device_equals_host_and_oracle(support):
     rb = gd.row_pair_counts([t.bfloat16() for t in dev], ims, 0.1, support=support)
     rf = gd.row_pair_counts([t.bfloat16().float() for t in dev], ims, 0.1, support=support)
     assert all(np.array_equal(a, b) for a, b in zip(rb, rf))
+
+
+def test_rank_halo_fused_equals_span_path():
+    """gsr_rank_halo (the fused per-rank plan) == the plan built from gsr_band_span_batched with
+    torch set operations, for every rank of G = 3 and 5 on a ragged batch incl. adversarial
+    Gaussians (the multi-band path is exercised at r = 0.5)."""
+    import torch
+    from paper_2501_06838_b200 import dist as gd
+    from test_gpu_parity import adversarial_cloud
+    spec = [(20, 33, 2.7), (12, 18, 6.0), (16, 16, 4.0)]
+    clouds = [adversarial_cloud(H, W, s, seed=k) for k, (H, W, s) in enumerate(spec)]
+    counts = [c["alpha"].shape[0] for c in clouds]
+    offs = np.concatenate([[0], np.cumsum(counts)])
+    dev = [torch.from_numpy(np.concatenate([c[k] for c in clouds])).cuda() for k in KEYS]
+    ims = [(H, W, s, int(offs[k]), counts[k]) for k, (H, W, s) in enumerate(spec)]
+    for ratio in (0.1, 0.5):
+        for G in (3, 5):
+            for r in range(G):
+                a = gd.RankPlan(dev, ims, G, r, ratio)                 # fused device path
+                bnd = a.bounds
+                b = gd.RankPlan.__new__(gd.RankPlan)
+                b.world, b.rank, b.ratio, b.images, b.bounds = G, r, ratio, a.images, bnd
+                gd.RankPlan.refresh(b, [t.cpu().numpy() for t in dev])   # span + torch path
+                assert torch.equal(a.idx.cpu(), b.idx.to(torch.int32))
+                for f in ("up", "down", "multi_pos", "multi_slot"):
+                    assert torch.equal(getattr(a, f).cpu(), getattr(b, f).cpu()), f
+                assert a.n_multi == b.n_multi
+                if ratio == 0.5 and G == 5:
+                    assert a.n_multi > 0

@@ -348,3 +348,15 @@ def test_reuse_binning_matches_rebinning(gsr):
     torch.cuda.synchronize()
     for x, y in zip(a, b):
         assert torch.allclose(x, y, rtol=1e-6, atol=1e-9)
+
+
+def test_validate_params(gsr):
+    """gsr_validate_params reports exactly the Gaussians outside the domain (R20)."""
+    c = adversarial_cloud(20, 33, 2.7)
+    a = np.concatenate([c[k].reshape(len(c["alpha"]), -1) for k in KEYS], 1)
+    bad = ~np.isfinite(a).all(1) | (c["sigma"][:, 0] <= 0) | (c["sigma"][:, 1] <= 0) | \
+        (np.abs(c["rho"]) >= 1)
+    cnt, first = gsr.validate_params(*to_dev(c))
+    assert cnt == int(bad.sum()) > 0 and first == int(np.nonzero(bad)[0][0])
+    ok = S.gaussians(10, 10, seed=1)
+    assert gsr.validate_params(*to_dev(ok)) == (0, -1)
