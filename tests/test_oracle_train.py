@@ -71,3 +71,23 @@ def test_l1_step_gradient_matches_fd(s, r, rho_scale):
             assert abs(an - fd) <= 1e-6 * max(abs(fd), 1e-4) + 1e-10, (name, i, an, fd)
             checked += 1
     assert checked >= 20
+
+
+def test_activate_fp32_is_the_rounded_definition():
+    """Reading R23: activate(fp32=True) = the float32 rounding of the fp64 activations, and mu =
+    the IEEE float32 sum ref + offset (a float32 addition, exactly reproducible)."""
+    rng = np.random.default_rng(5)
+    n = 500
+    ref = (rng.uniform(0, 48, (n, 2))).astype(np.float32)
+    raw = dict(raw_alpha=rng.normal(-3, 1, n), offset=rng.uniform(-0.5, 0.5, (n, 2)),
+               raw_sigma=rng.normal(-0.5, 0.5, (n, 2)), raw_rho=rng.normal(0, 0.5, n),
+               raw_color=rng.normal(0, 1, (n, 3)))
+    raw = {k: v.astype(np.float32) for k, v in raw.items()}
+    a64 = T.activate(raw, ref, 1.0)
+    a32 = T.activate(raw, ref, 1.0, fp32=True)
+    for k in ("alpha", "sigma", "rho", "color"):
+        assert np.array_equal(a32[k], a64[k].astype(np.float32).astype(np.float64)), k
+    mu = np.empty((n, 2), np.float32)
+    np.add(ref, raw["offset"], out=mu)
+    assert np.array_equal(a32["mu"], mu.astype(np.float64))
+    assert np.abs(a32["mu"] - a64["mu"]).max() > 0           # the rounding is real
