@@ -70,3 +70,63 @@ def test_train_step_batch_matches_oracle(rho_scale, scales):
         bound = 1e-4 * np.maximum(np.abs(want), 0.1 * S_) + 1e-8 * S_.max(axis=0, keepdims=True)
         err = np.abs(got - want)
         assert (err <= bound + 1e-30).all(), (name, float((err / (bound + 1e-30)).max()))
+
+
+@pytest.mark.parametrize("B,P,smax,seed", [(16, 48, 4.0, 3),     # EDSR/RDN slice
+                                           (8, 64, 16.0, 4)])    # HAT-L slice
+def test_train_step_real_shapes_and_graph(B, P, smax, seed):
+    """NEXT-2: the fused training step at the paper's per-GPU training batch shapes (m = 16,
+    per-patch s ~ U[1, smax]), launched directly and replayed from a CUDA graph
+    (ops.TrainStepGraph), vs the float64 oracle composition: every image element, the loss,
+    and the raw gradients of 64 sampled Gaussians per patch.
+
+    The oracle activates in fp64 and rounds the render's inputs to float32 as the CUDA path
+    does (reading R23: mu = ref + offset is the fp32 sum -- without it, mu's rounding alone
+    moves narrow Gaussians' terms by ~2e-4 relative); the CUDA sigmoid/tanh are within ~3 ulp
+    of the correctly rounded values, i.e. the render inputs still differ by a few fp32 ulp:
+    forward gate 1e-5 + 2e-6 |I|; raw gradients at R18's 1e-1 S as in
+    test_train_step_batch_matches_oracle."""
+    import torch
+    import paper_2501_06838_b200 as gsr
+    from paper_2501_06838_b200 import ops
+    rng = np.random.default_rng(seed)
+    scales = rng.uniform(1.0, smax, B)
+    raws, refs, imgs, gts, sample = [], [], [], [], []
+    off = 0
+    for k in range(B):
+        raw, ref = raw_cloud(P, P, seed=1000 * seed + k)
+        n = raw["raw_alpha"].shape[0]
+        act = T.activate(raw, ref, 1.0, fp32=True)
+        gts.append(gt_near(O.render_fwd(act, P, P, float(scales[k]), 0.1), seed=k))
+        raws.append(raw); refs.append(ref); imgs.append((P, P, float(scales[k]), off, n))
+        sample.append(np.sort(rng.choice(n, 64, replace=False)))
+        off += n
+    raw = {k: np.concatenate([r[k] for r in raws]) for k in RAWK}
+    ref = np.concatenate(refs)
+    outs, loss, g = T.l1_step(raw, ref, imgs, gts, 0.1, 1.0, sample=sample, fp32=True)
+    rows = np.concatenate([go + sm for (H, W, s, go, gc), sm in zip(imgs, sample)])
+    lay = gsr.layout([gsr.Image(H, W, s, go, gc) for (H, W, s, go, gc) in imgs])
+    dev = {k: torch.from_numpy(v).cuda() for k, v in raw.items()}
+    dref = torch.from_numpy(ref).cuda()
+    gt_flat = torch.from_numpy(np.concatenate([x.reshape(-1) for x in gts])).cuda()
+    args = (dev["raw_alpha"], dev["offset"], dref, dev["raw_sigma"], dev["raw_rho"],
+            dev["raw_color"])
+    direct = ops.train_step_l1(*args, lay, gt_flat, 0.1, 1.0)
+    step = ops.TrainStepGraph(lay, off, ratio=0.1)
+    graph = step(*args, gt_flat)
+    torch.cuda.synchronize()
+    cols = [("raw_alpha", [0]), ("offset", [1, 2]), ("raw_sigma", [3, 4]), ("raw_rho", [5]),
+            ("raw_color", [6, 7, 8])]
+    for out, gl, gg in (direct, graph):
+        for k, o in enumerate(outs):
+            err = np.abs(lay.view(out, k).cpu().numpy().astype(np.float64) - o)
+            assert (err <= 1e-5 + 2e-6 * np.abs(o)).all(), (k, float(err.max()))
+        assert float(gl.item()) == pytest.approx(loss, rel=1e-5)
+        for name, c in cols:
+            got = gg[name].cpu().numpy().astype(np.float64).reshape(off, -1)[rows]
+            want = np.asarray(g[name]).reshape(len(rows), -1)
+            S_ = g["absmass"][:, c]
+            bound = (1e-4 * np.maximum(np.abs(want), 1e-1 * S_) +
+                     1e-8 * S_.max(axis=0, keepdims=True))
+            err = np.abs(got - want)
+            assert (err <= bound + 1e-30).all(), (name, float((err / (bound + 1e-30)).max()))

@@ -1,0 +1,6 @@
+#!/bin/bash
+python __graft_entry__.py > /dev/null
+timeout 900 python -m pytest tests/test_gpu_train.py -q -rf --timeout 600 > gpurun_out/pytest_train.txt 2>&1; tail -4 gpurun_out/pytest_train.txt | cut -c1-300
+for t in racecheck synccheck memcheck; do for c in C1 C2 C5band subset; do
+  timeout 900 compute-sanitizer --tool $t --kernel-name kns=k_ --print-limit 20 python tools/sanitize_run.py $c > gpurun_out/san_${t}_${c}.txt 2>&1; echo "$t $c: $(grep -E 'ERROR SUMMARY|ok' gpurun_out/san_${t}_${c}.txt | tr '\n' ' ')"
+done; done
