@@ -228,7 +228,9 @@ __global__ void __launch_bounds__(BWD_THREADS) k_render_bwd(
         float4 r0 = make_float4(0.f, 0.f, 0.f, 0.f), r1 = r0, r2 = r0;
         int x0 = 1, x1 = 0, y0 = 1, y1 = 0;          // window rect (masks)
         int sx0 = 1, sx1 = 0, sy0 = 1, sy1 = 0;      // support rect (loop bounds)
+        int gdst = 0;                                // the Gaussian's moment row (perm[p])
         if (act) {
+            gdst = __ldg(perm + p);                  // issued early: used after the group loop
             r0 = __ldg(rec + (long long)REC_F4 * p);
             r1 = __ldg(rec + (long long)REC_F4 * p + 1);
             r2 = __ldg(rec + (long long)REC_F4 * p + 2);
@@ -291,11 +293,15 @@ __global__ void __launch_bounds__(BWD_THREADS) k_render_bwd(
             fold_row(A0, v0, r1, r2, m);
             if (has1) fold_row(A1, v1, r1, r2, m);
         }
+#ifndef GSR_BWD_NOATOM
         if (act) {
-            double* dst = moments + 8LL * perm[p];
+            double* dst = moments + 8LL * gdst;
 #pragma unroll
             for (int k = 0; k < 8; ++k) atomicAdd(dst + k, (double)m[k]);
         }
+#else   // diagnostic build only (wrong results): the cost of the atomics
+        if (act && m[0] == 12345.f) moments[8LL * gdst] = m[1] + m[2] + m[3] + m[4] + m[5] + m[6] + m[7];
+#endif
     };
 
     // sort the first cnt queue entries by key (stable: ranks via match_any in queue order),

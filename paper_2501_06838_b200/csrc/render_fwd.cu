@@ -472,7 +472,7 @@ __global__ void __launch_bounds__(FWD2_THREADS, 4) k_render_fwd2(const ImgTable 
                 if constexpr (FWD_ROWS == 2) {
                     // column halves the support meets (left 16 / right 16 columns)
                     const bool hl = sx0 <= fx0 + 15, hr = sx1 >= fx0 + 16;
-                    const int hv = (hl && hr) ? 0 : (hl ? 1 : 2);
+                    const int hv = !use_halves<FWD_STRIP>() || (hl && hr) ? 0 : (hl ? 1 : 2);
                     pth = (full ? ((cb[0] & 1) ? P_REC3 : P_DIR3) : P_MSK3) + hv;
                 } else {
                     pth = full ? 0 : 1;
