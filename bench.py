@@ -491,6 +491,23 @@ def main():
         pko = pc * SM_COUNT * f_clk / 1e9
         roof["other_kernel"] = {"kernel": other, "achieved": P_rank_eval / t_o / 1e9,
                                 "peak": pko, "frac": P_rank_eval / t_o / 1e9 / pko}
+    # the same launches against SURVEY 8(d)'s method-level per-pair costs (independent of this
+    # implementation's instruction counts): forward 1 ex2 + ~8 FP32 per pair -> MUFU-bound 16
+    # pairs/clk/SM; backward 1 ex2 + ~20 FP32 -> 6.4 pairs/clk/SM; and the combined fwd+bwd
+    # roofline fraction (roofline time of both passes / their measured time), both bases
+    t_f = phase_ms.get("render_fwd", 0.0) / max(phase_calls.get("render_fwd", 0), 1) * 1e-3
+    t_b = phase_ms.get("render_bwd", 0.0) / max(phase_calls.get("render_bwd", 0), 1) * 1e-3
+    if t_f > 0 and t_b > 0:
+        sv = {"render_fwd": 16.0, "render_bwd": 6.4}
+        roof["survey_8d_basis"] = {
+            k: {"peak": pc_ * SM_COUNT * f_clk / 1e9,
+                "frac": P_rank_eval / t / 1e9 / (pc_ * SM_COUNT * f_clk / 1e9)}
+            for k, pc_, t in (("render_fwd", sv["render_fwd"], t_f),
+                              ("render_bwd", sv["render_bwd"], t_b))}
+        roof["fwd_bwd_combined_frac"] = (P_rank_eval / (FWD_PAIRS_PER_CLK_SM * SM_COUNT * f_clk) +
+                                         P_rank_eval / (BWD_PAIRS_PER_CLK_SM * SM_COUNT * f_clk)) / (t_f + t_b)
+        roof["fwd_bwd_combined_frac_survey_8d"] = (P_rank_eval / (16.0 * SM_COUNT * f_clk) +
+                                                   P_rank_eval / (6.4 * SM_COUNT * f_clk)) / (t_f + t_b)
     share = {k: v / max(ms_total if world == 1 else ms, 1e-9) for k, v in phase_ms.items()}
 
     cpu = None
