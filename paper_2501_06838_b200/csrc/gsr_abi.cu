@@ -199,7 +199,12 @@ gsr_status prepare(const void* alpha, const void* mu, const void* sigma, const v
 
 extern "C" {
 
-const char* gsr_version(void) { return "gsr-b200 0.3 (sm_100a; fwd tile 32x16 | 16x8, bwd tile 64x8, cell 16, support 13.5 sigma)"; }
+#define GSR_STR2(x) #x
+#define GSR_STR(x) GSR_STR2(x)
+const char* gsr_version(void) {
+    return "gsr-b200 0.4 (sm_100a; fwd 2x8 | 1x" GSR_STR(GSR_FWD_SMALL_STRIP) " px per lane, bwd tile 64x8, "
+           "cell 16, support 13.5 sigma)";
+}
 
 gsr_status gsr_profile_enable(int32_t on) {
     std::lock_guard<std::mutex> lk(g_prof.mu);

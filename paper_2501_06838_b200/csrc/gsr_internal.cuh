@@ -29,9 +29,14 @@ constexpr int TILE_H = GSR_BWD_TILE_H;  // also the debug tile-list tile (TILE_H
 // per call from the window size:
 //   large (windows >= FWD_SMALL_WINDOW HR px): 2 x 8 px per lane -> 32 x 16 tiles
 //   small (narrow windows, e.g. the x1..x4 training patches): 1 x 4 px per lane -> 16 x 8 tiles,
-//         which wastes far fewer masked evaluations where a window covers only part of a tile.
+//         which wastes far fewer masked evaluations where a window covers only part of a tile
+//         (GSR_FWD_SMALL_STRIP=8: 1 x 8 px per lane, 32 x 8 tiles evaluated per 16 x 8 column half;
+//         measured 7% slower at C2)
 struct FwdCfgLarge { static constexpr int ROWS = 2, STRIP = 8, TW = 4 * STRIP, TH = 8 * ROWS; };
-struct FwdCfgSmall { static constexpr int ROWS = 1, STRIP = 4, TW = 4 * STRIP, TH = 8 * ROWS; };
+#ifndef GSR_FWD_SMALL_STRIP
+#define GSR_FWD_SMALL_STRIP 4
+#endif
+struct FwdCfgSmall { static constexpr int ROWS = 1, STRIP = GSR_FWD_SMALL_STRIP, TW = 4 * STRIP, TH = 8 * ROWS; };
 using FwdCfgWide = FwdCfgLarge;
 constexpr int FWD_SMALL_WINDOW = 48;             // HR px: below this the small tiles are used
 #ifndef GSR_FWD_REC

@@ -42,6 +42,9 @@
 #ifndef GSR_BWD_BATCH
 #define GSR_BWD_BATCH 512         // hits per sorted batch (multiple of 32)
 #endif
+#ifndef GSR_BWD_Y
+#define GSR_BWD_Y 1
+#endif
 #ifndef GSR_BWD_MACC_T
 #define GSR_BWD_MACC_T float      // per-(Gaussian, tile) accumulator type of the row folds
 #endif
@@ -69,8 +72,8 @@ struct RowAcc {       // per-row partial sums of a lane (register pairs = two pi
 // from the reuse cache and the instruction reads two fresh register pairs instead of three
 // (register-file bank bandwidth: 2 instead of 3 issue cycles, tools/microbench.cu "ffma2_nr").
 template <bool MASKED>
-__device__ __forceinline__ void pix_pair2(const float4 gaA, const float2 gbA, const float4 gaB,
-                                          const float2 gbB, const float2 kx, const float2 TA,
+__device__ __forceinline__ void pix_pair2(const float4 gaA, const float4 gaB, const float4 gbb,
+                                          const float2 kx, const float2 TA,
                                           const float2 UA, const float2 TB, const float2 UB,
                                           const LaneG& L, bool in0, bool in1, RowAcc& A,
                                           RowAcc& B) {
@@ -86,6 +89,7 @@ __device__ __forceinline__ void pix_pair2(const float4 gaA, const float2 gbA, co
     }
     const float2 grA = make_float2(gaA.x, gaA.y), ggA = make_float2(gaA.z, gaA.w);
     const float2 grB = make_float2(gaB.x, gaB.y), ggB = make_float2(gaB.z, gaB.w);
+    const float2 gbA = make_float2(gbb.x, gbb.y), gbB = make_float2(gbb.z, gbb.w);
     // g . c' of both rows, snake order (c' shared between rows, g between channels)
     float2 gcA = __fmul2_rn(grA, L.cr);
     float2 gcB = __fmul2_rn(grB, L.cr);
@@ -102,21 +106,30 @@ __device__ __forceinline__ void pix_pair2(const float4 gaA, const float2 gbA, co
     B.FB = __ffma2_rn(eB, gbB, B.FB);
     B.FG = __ffma2_rn(eB, ggB, B.FG);
     B.FR = __ffma2_rn(eB, grB, B.FR);
+#if GSR_BWD_Y
+    // y = e (g . c'), W1 += y w' (an FADD2: two register pairs), W2 += (y w') w'
+    const float2 ywA = __fmul2_rn(__fmul2_rn(eA, gcA), wA);
+    const float2 ywB = __fmul2_rn(__fmul2_rn(eB, gcB), wB);
+    A.W1 = __fadd2_rn(A.W1, ywA);
+    A.W2 = __ffma2_rn(ywA, wA, A.W2);
+    B.W1 = __fadd2_rn(B.W1, ywB);
+    B.W2 = __ffma2_rn(ywB, wB, B.W2);
+#else
     const float2 edA = __fmul2_rn(eA, wA), edB = __fmul2_rn(eB, wB);
     const float2 eddA = __fmul2_rn(edA, wA), eddB = __fmul2_rn(edB, wB);
     A.W1 = __ffma2_rn(gcA, edA, A.W1);
     A.W2 = __ffma2_rn(gcA, eddA, A.W2);
     B.W2 = __ffma2_rn(gcB, eddB, B.W2);
     B.W1 = __ffma2_rn(gcB, edB, B.W1);
+#endif
 }
 
 // Columns [c_begin, c_end) (pairs) of two rows at once: the column part (kx, masks, dL/dI
 // addresses) is shared, and the two rows give two independent accumulation chains.
 template <bool MASKED>
 __device__ __forceinline__ void row2_pairs(int c_begin, int c_end, const float4* __restrict__ gA0,
-                                           const float2* __restrict__ gB0,
                                            const float4* __restrict__ gA1,
-                                           const float2* __restrict__ gB1, float kT,
+                                           const float4* __restrict__ gBB, float kT,
                                            const LaneG& L, int Tx0, const float2 T0,
                                            const float2 U0, const float2 T1, const float2 U1,
                                            RowAcc& A0, RowAcc& A1) {
@@ -131,8 +144,7 @@ __device__ __forceinline__ void row2_pairs(int c_begin, int c_end, const float4*
             in0 = xa >= L.x0 && xa <= L.x1;
             in1 = xa + 1 >= L.x0 && xa + 1 <= L.x1;
         }
-        pix_pair2<MASKED>(gA0[cp], gB0[cp], gA1[cp], gB1[cp], kx, T0, U0, T1, U1, L, in0, in1, A0,
-                          A1);
+        pix_pair2<MASKED>(gA0[cp], gA1[cp], gBB[cp], kx, T0, U0, T1, U1, L, in0, in1, A0, A1);
         kx = __fadd2_rn(kx, two);
     }
 }
@@ -160,7 +172,10 @@ __global__ void __launch_bounds__(BWD_THREADS) k_render_bwd(
     double* __restrict__ moments, int ks, const float* __restrict__ img,
     const float* __restrict__ gt, float inv_numel) {
     __shared__ __align__(16) float4 gA[TILE_H][TILE_W / 2];
-    __shared__ __align__(16) float2 gB[TILE_H][TILE_W / 2];
+    // blue channel of two consecutive rows: gBB[r][cp] = {gb(r, 2cp), gb(r, 2cp+1), gb(r+1, 2cp),
+    // gb(r+1, 2cp+1)} (row TILE_H = zeros), so a row pair reads its blue values with one LDS.128
+    __shared__ __align__(16) float4 gBB[TILE_H][TILE_W / 2];
+    __shared__ __align__(16) float2 gB[TILE_H + 1][TILE_W / 2];
 
     const int tile = blockIdx.x / ks;
     const int kpart = blockIdx.x % ks;    // split: this CTA takes every ks-th candidate group
@@ -197,6 +212,13 @@ __global__ void __launch_bounds__(BWD_THREADS) k_render_bwd(
         }
         gA[ry][cp] = make_float4(v[0], v[3], v[1], v[4]);
         gB[ry][cp] = make_float2(v[2], v[5]);
+        if (ry == 0) gB[TILE_H][cp] = make_float2(0.f, 0.f);
+    }
+    __syncthreads();
+    for (int pp = threadIdx.x; pp < TILE_H * (TILE_W / 2); pp += BWD_THREADS) {
+        const int ry = pp / (TILE_W / 2), cp = pp % (TILE_W / 2);
+        const float2 a = gB[ry][cp], b = gB[ry + 1][cp];
+        gBB[ry][cp] = make_float4(a.x, a.y, b.x, b.y);
     }
     __syncthreads();
 
@@ -281,15 +303,14 @@ __global__ void __launch_bounds__(BWD_THREADS) k_render_bwd(
             const float2 U0 = f2(u0), U1 = f2(u1);
             const int ry0 = y - Ty0, ry1 = has1 ? ry0 + 1 : ry0;
             const float4* gA0 = &gA[ry0][0];
-            const float2* gB0 = &gB[ry0][0];
             const float4* gA1 = &gA[ry1][0];
-            const float2* gB1 = &gB[ry1][0];
+            const float4* gBr = &gBB[ry0][0];   // rows ry0, ry0 + 1 (a phantom row 1 has u = -inf)
             RowAcc A0, A1;
             A0.FR = A0.FG = A0.FB = A0.W1 = A0.W2 = f2(0.f);
             A1 = A0;
-            row2_pairs<true>(ca, ma, gA0, gB0, gA1, gB1, kT, L, Tx0, T0, U0, T1, U1, A0, A1);
-            row2_pairs<false>(ma, mb, gA0, gB0, gA1, gB1, kT, L, Tx0, T0, U0, T1, U1, A0, A1);
-            row2_pairs<true>(mb, ce, gA0, gB0, gA1, gB1, kT, L, Tx0, T0, U0, T1, U1, A0, A1);
+            row2_pairs<true>(ca, ma, gA0, gA1, gBr, kT, L, Tx0, T0, U0, T1, U1, A0, A1);
+            row2_pairs<false>(ma, mb, gA0, gA1, gBr, kT, L, Tx0, T0, U0, T1, U1, A0, A1);
+            row2_pairs<true>(mb, ce, gA0, gA1, gBr, kT, L, Tx0, T0, U0, T1, U1, A0, A1);
             fold_row(A0, v0, r1, r2, m);
             if (has1) fold_row(A1, v1, r1, r2, m);
         }

@@ -24,7 +24,8 @@
 //     memory, reduce split-K cluster CTAs through DSMEM in rank order, and store the tile with
 //     coalesced 16-B (float4) stores (scalar at ragged image edges / misaligned rows).
 //   * two tile configurations (gsr_internal.cuh): 2 x 8 px per lane / 32 x 16 tiles, or for
-//     narrow windows 1 x 4 px per lane / 16 x 8 tiles (fewer masked evaluations).
+//     narrow windows 1 x 4 px per lane / 16 x 8 tiles (fewer masked evaluations); a 2 x 8 (or,
+//     as a build option, 1 x 8) block skips the column half of the tile a Gaussian's support misses.
 #include <atomic>
 #include <mutex>
 
@@ -95,7 +96,7 @@ __device__ __forceinline__ float2 f2(float a) { return make_float2(a, a); }
 
 // Staged record (binning.cu K1b): r0 = {-ax, ay, dl_y, a1/s},  r1 = {-a1 dl_x, b1, c1, c'_r},
 //   r2 = {c'_g, c'_b, window x0|x1, y0|y1}  (recurrence path: {c'_g, c'_b, G1, G2})
-template <class CFG, bool FULL>
+template <class CFG, bool FULL, int HSEL = 3>
 __device__ __forceinline__ void fwd_gauss(const float4 r0, const float4 r1, const float4 r2,
                                           const float2 (&xj)[CFG::STRIP / 2], float yf0,
                                           const int (&yi)[CFG::ROWS], int xl0, float invs,
@@ -104,15 +105,19 @@ __device__ __forceinline__ void fwd_gauss(const float4 r0, const float4 r1, cons
     const float2 D2 = f2(r0.w);
     const float2 nax = f2(r0.x);
     // kx = x - ax for the lane's 8 columns: exact small integers (one FADD2 per column pair)
+    // column pair jp lies in column half jp >> 1 (halves: slots 0-3 left, 4-7 right)
+    auto live = [&](int jp) { return !use_halves<FWD_STRIP>() || ((HSEL >> (jp >> 1)) & 1); };
     float2 kx[FWD_STRIP / 2];
 #pragma unroll
-    for (int jp = 0; jp < FWD_STRIP / 2; ++jp) kx[jp] = __fadd2_rn(xj[jp], nax);
+    for (int jp = 0; jp < FWD_STRIP / 2; ++jp)
+        if (live(jp)) kx[jp] = __fadd2_rn(xj[jp], nax);
     bool cin[FWD_STRIP];
     if (!FULL) {
         const unsigned xs = __float_as_uint(r2.z);
         const int x0 = (int)(xs & 0xffffu), x1 = (int)(xs >> 16);
 #pragma unroll
-        for (int j = 0; j < FWD_STRIP; ++j) cin[j] = (xl0 + j >= x0) && (xl0 + j <= x1);
+        for (int j = 0; j < FWD_STRIP; ++j)
+            cin[j] = (xl0 + colx<FWD_STRIP>(j) >= x0) && (xl0 + colx<FWD_STRIP>(j) <= x1);
     }
     const float2 cr = f2(r1.w), cg = f2(r2.x), cb = f2(r2.y);
     float dy = fmaf(yf0 - r0.y, invs, -r0.z);
@@ -130,6 +135,7 @@ __device__ __forceinline__ void fwd_gauss(const float4 r0, const float4 r1, cons
         const float2 T2 = f2(tau), U2 = f2(u);
 #pragma unroll
         for (int jp = 0; jp < FWD_STRIP / 2; ++jp) {
+            if (!live(jp)) continue;                         // compile-time skip
             float2 w = __ffma2_rn(D2, kx[jp], T2);
             float2 q = __ffma2_rn(make_float2(-w.x, -w.y), w, U2);
             if (!FULL) {
@@ -228,7 +234,7 @@ __device__ __forceinline__ void fwd_gauss_r2h(const float4 r0, const float4 r1, 
 
 // Evaluation paths decided by the filter (one byte per staged record). Large configuration:
 // MODE (0 masked, 1 direct, 2 recurrence) x column halves (both, left only, right only);
-// small configuration: 0 = full (no masks), 1 = masked.
+// small configuration: 0..2 full (no masks) x (both, left, right half), 3..5 masked likewise.
 enum : int { P_REC3 = 0, P_REC1, P_REC2, P_DIR3, P_DIR1, P_DIR2, P_MSK3, P_MSK1, P_MSK2 };
 
 constexpr int FWD_BUF = 48;                       // records per warp buffer (> 32)
@@ -312,7 +318,7 @@ __device__ __forceinline__ void fwd_epilogue(FwdSmem2<CFG>& sm, const DevImg& im
             sm.stage[yl + 1][3 * x + k] = v.y;
         } else {                                       // pair = two adjacent columns of one row
             const int jp = (a / 3) % (STRIP / 2), r = (a / 3) / (STRIP / 2);
-            const int x = xl + 2 * jp;
+            const int x = xl + colx<STRIP>(2 * jp);         // + 1: the pair's second column
             sm.stage[yl + r][3 * x + k] = v.x;
             sm.stage[yl + r][3 * (x + 1) + k] = v.y;
         }
@@ -369,7 +375,8 @@ __global__ void __launch_bounds__(FWD2_THREADS, 4) k_render_fwd2(const ImgTable 
     float2 xj[FWD_STRIP / 2];
 #pragma unroll
     for (int jp = 0; jp < FWD_STRIP / 2; ++jp)
-        xj[jp] = make_float2((float)(xl0 + 2 * jp), (float)(xl0 + 2 * jp + 1));
+        xj[jp] = make_float2((float)(xl0 + colx<FWD_STRIP>(2 * jp)),
+                             (float)(xl0 + colx<FWD_STRIP>(2 * jp + 1)));
     const float xlf = (float)xl0;
     const float2 yrow = make_float2((float)yl0, (float)(yl0 + 1));
     int yi[FWD_ROWS];
@@ -443,11 +450,13 @@ __global__ void __launch_bounds__(FWD2_THREADS, 4) k_render_fwd2(const ImgTable 
                     else
                         fwd_gauss_r2h<1, FWD_STRIP, 2>(r0, r1, r2, 0.f, xlf, yrow, yi, xl0, invs, acc);
                 }
-            } else {
-                if (pth == 0)
-                    fwd_gauss<CFG, true>(r0, r1, r2, xj, yf0, yi, xl0, invs, acc);
-                else
-                    fwd_gauss<CFG, false>(r0, r1, r2, xj, yf0, yi, xl0, invs, acc);
+            } else {   // 0..2 full (both / left / right half), 3..5 masked
+                if (pth == 0) fwd_gauss<CFG, true, 3>(r0, r1, r2, xj, yf0, yi, xl0, invs, acc);
+                else if (pth == 1) fwd_gauss<CFG, true, 1>(r0, r1, r2, xj, yf0, yi, xl0, invs, acc);
+                else if (pth == 2) fwd_gauss<CFG, true, 2>(r0, r1, r2, xj, yf0, yi, xl0, invs, acc);
+                else if (pth == 3) fwd_gauss<CFG, false, 3>(r0, r1, r2, xj, yf0, yi, xl0, invs, acc);
+                else if (pth == 4) fwd_gauss<CFG, false, 1>(r0, r1, r2, xj, yf0, yi, xl0, invs, acc);
+                else fwd_gauss<CFG, false, 2>(r0, r1, r2, xj, yf0, yi, xl0, invs, acc);
             }
         }
     };
@@ -469,14 +478,13 @@ __global__ void __launch_bounds__(FWD2_THREADS, 4) k_render_fwd2(const ImgTable 
                 const int x0 = (int)(xs & 0xffffu), x1 = (int)(xs >> 16);
                 const int y0 = (int)(ys & 0xffffu), y1 = (int)(ys >> 16);
                 const bool full = x0 <= fx0 && x1 >= fx1 && y0 <= fy0 && y1 >= fy0 + FTILE_H - 1;
-                if constexpr (FWD_ROWS == 2) {
-                    // column halves the support meets (left 16 / right 16 columns)
-                    const bool hl = sx0 <= fx0 + 15, hr = sx1 >= fx0 + 16;
-                    const int hv = !use_halves<FWD_STRIP>() || (hl && hr) ? 0 : (hl ? 1 : 2);
+                // column halves the support meets (left 16 / right 16 columns)
+                const bool hl = sx0 <= fx0 + 15, hr = sx1 >= fx0 + 16;
+                const int hv = !use_halves<FWD_STRIP>() || (hl && hr) ? 0 : (hl ? 1 : 2);
+                if constexpr (FWD_ROWS == 2)
                     pth = (full ? ((cb[0] & 1) ? P_REC3 : P_DIR3) : P_MSK3) + hv;
-                } else {
-                    pth = full ? 0 : 1;
-                }
+                else
+                    pth = (full ? 0 : 3) + hv;
             }
             const unsigned m = __ballot_sync(0xffffffffu, keep);
             if (keep) {
