@@ -290,7 +290,12 @@ __global__ void __launch_bounds__(BWD_THREADS) k_render_bwd(
         macc_t m[8];
 #pragma unroll
         for (int k = 0; k < 8; ++k) m[k] = (macc_t)0;
+#ifdef GSR_DIAG_BWD_NOEVAL       // timing diagnostic only (wrong results): no pair evaluation
+        const int yb_ = r0.x == 12345.f ? yb : ya - 1;
+        for (int y = ya; y <= yb_; y += 2) {
+#else
         for (int y = ya; y <= yb; y += 2) {
+#endif
             // rows y and y + 1 (the second one is a phantom when y == yb: u = -inf)
             const int y1r = y + 1;
             const bool has1 = y1r <= yb;
@@ -328,6 +333,9 @@ __global__ void __launch_bounds__(BWD_THREADS) k_render_bwd(
     // sort the first cnt queue entries by key (stable: ranks via match_any in queue order),
     // evaluate them in groups of 32, then move the rest of the queue to the front
     auto flush = [&](int cnt) {
+#ifdef GSR_DIAG_BWD_NOFLUSH      // timing diagnostic only (wrong results): scan without evaluation
+        if (qk[warp][0] != 12345) { qn = 0; __syncwarp(); return; }
+#endif
 #pragma unroll
         for (int q = 0; q < NBL; ++q) hist[warp][NBL * lane + q] = 0;
         __syncwarp();

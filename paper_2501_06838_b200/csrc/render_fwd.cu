@@ -31,6 +31,10 @@
 
 #include "gsr_internal.cuh"
 
+#ifndef GSR_FWD_SCAN_D
+#define GSR_FWD_SCAN_D 2          // candidate batches per warp in the scan pipeline (>= 2)
+#endif
+
 namespace gsr {
 
 namespace {
@@ -395,9 +399,11 @@ __global__ void __launch_bounds__(FWD2_THREADS, 4) k_render_fwd2(const ImgTable 
     prod.cur = prod.end = 0;
     const unsigned lt = (1u << lane) - 1u;
     const bool live = fy0 <= fy1;
-    int nb[2], sb[2];
-    int4 rb[2];
-    int cb[2];
+    // candidate batches in flight: batch 0 is filtered while batches 1 .. SD-1 load
+    constexpr int SD = GSR_FWD_SCAN_D;
+    int nb[SD], sb[SD];
+    int4 rb[SD];
+    int cb[SD];
     int first = 1;
     auto fetch = [&](int j) {
         nb[j] = live ? prod.next(&sb[j], first ? krank * FWD_CWARPS + warp
@@ -420,8 +426,15 @@ __global__ void __launch_bounds__(FWD2_THREADS, 4) k_render_fwd2(const ImgTable 
         const float4* sr = &sm.rec[warp][pbuf][0];
         const uint8_t* pp = &sm.path[warp][pbuf][0];
         int pnext = pcnt > 0 ? pp[0] : 0;
+#ifdef GSR_DIAG_FWD_NOEVAL       // timing diagnostic only (wrong results): no evaluation
+        if (pcnt > 0) pcnt = sr[0].x == 12345.f ? 1 : 0;
+#endif
         for (int g = 0; g < pcnt; ++g) {
+#ifdef GSR_DIAG_FWD_NOMASK       // timing diagnostic only (wrong results): masked -> full paths
+            const int pth = FWD_ROWS == 2 ? (pnext >= P_MSK3 ? pnext - 3 : pnext) : (pnext >= 3 ? pnext - 3 : pnext);
+#else
             const int pth = pnext;
+#endif
             if (g + 1 < pcnt) pnext = pp[g + 1];          // next Gaussian's path, one ahead
             const float4* q = sr + REC_F4 * g;
             const float4 r0 = q[0], r1 = q[1], r2 = q[2];
@@ -461,8 +474,8 @@ __global__ void __launch_bounds__(FWD2_THREADS, 4) k_render_fwd2(const ImgTable 
         }
     };
 
-    fetch(0);
-    fetch(1);
+#pragma unroll
+    for (int d = 0; d < SD; ++d) fetch(d);
     int b = 0, cnt = 0, pend = -1;
     while (true) {
         const bool end = nb[0] == 0;
@@ -496,8 +509,11 @@ __global__ void __launch_bounds__(FWD2_THREADS, 4) k_render_fwd2(const ImgTable 
                 for (int q = 0; q < REC_F4; ++q) cp_async16(dst + q, src + q);
             }
             cnt += __popc(m);
-            nb[0] = nb[1]; sb[0] = sb[1]; rb[0] = rb[1]; cb[0] = cb[1];
-            fetch(1);
+#pragma unroll
+            for (int d = 0; d + 1 < SD; ++d) {
+                nb[d] = nb[d + 1]; sb[d] = sb[d + 1]; rb[d] = rb[d + 1]; cb[d] = cb[d + 1];
+            }
+            fetch(SD - 1);
         }
         if (cnt > FWD_BUF - 32 || (end && cnt > 0)) {
             cp_async_commit();
