@@ -518,7 +518,11 @@ cudaError_t launch_render_bwd_moments(const ImgTable& tab, const Workspace& ws, 
         slots = resident_slots(k_render_bwd, BWD_THREADS, 0);
         slots_cache[dev].store(slots, std::memory_order_relaxed);
     }
+#ifdef GSR_FORCE_KS_BWD                 // A/B builds only
+    const int ks = GSR_FORCE_KS_BWD;
+#else
     const int ks = split_k_factor(tab.total_tiles, slots);
+#endif
     k_render_bwd<<<tab.total_tiles * ks, BWD_THREADS, 0, st>>>(tab, ws.rec, ws.rects, ws.cell_start,
                                                                ws.ext,
                                                                perm, grad_out, moments, ks, img,

@@ -240,8 +240,19 @@ __device__ __forceinline__ void fwd_gauss_r2h(const float4 r0, const float4 r1, 
 // MODE (0 masked, 1 direct, 2 recurrence) x column halves (both, left only, right only);
 // small configuration: 0..2 full (no masks) x (both, left, right half), 3..5 masked likewise.
 enum : int { P_REC3 = 0, P_REC1, P_REC2, P_DIR3, P_DIR1, P_DIR2, P_MSK3, P_MSK1, P_MSK2 };
+constexpr int FRONT_PATH = 0;   // P_REC3 (large) / full over both halves (small configuration)
 
 constexpr int FWD_BUF = 48;                       // records per warp buffer (> 32)
+#ifndef GSR_FWD_SPLIT
+#define GSR_FWD_SPLIT 1
+#endif
+#ifndef GSR_FWD_FRONT_UNROLL
+#define GSR_FWD_FRONT_UNROLL 1
+#endif
+constexpr int kFrontUnroll = GSR_FWD_FRONT_UNROLL;
+#ifndef GSR_FWD_HALVES
+#define GSR_FWD_HALVES 1          // skip the column half a Gaussian's support misses
+#endif
 constexpr int FWD2_THREADS = FWD_CWARPS * 32;
 
 template <class CFG>
@@ -422,14 +433,43 @@ __global__ void __launch_bounds__(FWD2_THREADS, 4) k_render_fwd2(const ImgTable 
 #pragma unroll
     for (int a = 0; a < NACC; ++a) acc[a] = make_float2(0.f, 0.f);
 
-    auto process = [&](int pbuf, int pcnt) {
+    // A staged buffer holds the Gaussians of the front path (the most common one: the
+    // recurrence over both column halves, or the unmasked small-tile path) at slots 0, 1, ...
+    // and every other path from slot FWD_BUF - 1 downwards (GSR_FWD_SPLIT): the front run is
+    // evaluated without any per-Gaussian dispatch.
+    auto process_front = [&](int pbuf, int nf) {
+        const float4* q = &sm.rec[warp][pbuf][0];
+#ifdef GSR_DIAG_FWD_NOEVAL
+        if (nf > 0) nf = q[0].x == 12345.f ? 1 : 0;
+#endif
+#pragma unroll kFrontUnroll
+        for (int g = 0; g < nf; ++g, q += REC_F4) {
+            const float4 r0 = q[0], r1 = q[1], r2 = q[2];
+            if constexpr (FWD_ROWS == 2) {
+                const float4 r3 = q[3];
+                const float4 r2g = make_float4(r2.x, r2.y, r3.x, r3.y);
+                fwd_gauss_r2h<2, FWD_STRIP, 3>(r0, r1, r2g, r3.z, xlf, yrow, yi, xl0, invs, acc);
+            } else {
+                fwd_gauss<CFG, true, 3>(r0, r1, r2, xj, yf0, yi, xl0, invs, acc);
+            }
+        }
+    };
+    auto process = [&](int pbuf, int pbeg, int pcnt) {
         const float4* sr = &sm.rec[warp][pbuf][0];
         const uint8_t* pp = &sm.path[warp][pbuf][0];
-        int pnext = pcnt > 0 ? pp[0] : 0;
 #ifdef GSR_DIAG_FWD_NOEVAL       // timing diagnostic only (wrong results): no evaluation
-        if (pcnt > 0) pcnt = sr[0].x == 12345.f ? 1 : 0;
+        if (pcnt > pbeg) pcnt = sr[0].x == 12345.f ? pbeg + 1 : pbeg;
 #endif
-        for (int g = 0; g < pcnt; ++g) {
+        if constexpr (FWD_ROWS == 1 && !use_halves<FWD_STRIP>()) {
+            if (GSR_FWD_SPLIT) {          // the small tiles' other path is the masked one
+                const float4* q = sr + REC_F4 * pbeg;
+                for (int g = pbeg; g < pcnt; ++g, q += REC_F4)
+                    fwd_gauss<CFG, false, 3>(q[0], q[1], q[2], xj, yf0, yi, xl0, invs, acc);
+                return;
+            }
+        }
+        int pnext = pcnt > pbeg ? pp[pbeg] : 0;
+        for (int g = pbeg; g < pcnt; ++g) {
 #ifdef GSR_DIAG_FWD_NOMASK       // timing diagnostic only (wrong results): masked -> full paths
             const int pth = FWD_ROWS == 2 ? (pnext >= P_MSK3 ? pnext - 3 : pnext) : (pnext >= 3 ? pnext - 3 : pnext);
 #else
@@ -476,7 +516,16 @@ __global__ void __launch_bounds__(FWD2_THREADS, 4) k_render_fwd2(const ImgTable 
 
 #pragma unroll
     for (int d = 0; d < SD; ++d) fetch(d);
-    int b = 0, cnt = 0, pend = -1;
+    // cnt / pend: front-path entries of the filling / pending buffer, cntb / pendb: the rest
+    int b = 0, cnt = 0, pend = -1, cntb = 0, pendb = 0;
+    auto run = [&](int buf, int nf, int nbk) {
+        if (GSR_FWD_SPLIT) {
+            process_front(buf, nf);
+            process(buf, FWD_BUF - nbk, FWD_BUF);
+        } else {
+            process(buf, 0, nf);
+        }
+    };
     while (true) {
         const bool end = nb[0] == 0;
         if (!end) {
@@ -493,12 +542,28 @@ __global__ void __launch_bounds__(FWD2_THREADS, 4) k_render_fwd2(const ImgTable 
                 const bool full = x0 <= fx0 && x1 >= fx1 && y0 <= fy0 && y1 >= fy0 + FTILE_H - 1;
                 // column halves the support meets (left 16 / right 16 columns)
                 const bool hl = sx0 <= fx0 + 15, hr = sx1 >= fx0 + 16;
-                const int hv = !use_halves<FWD_STRIP>() || (hl && hr) ? 0 : (hl ? 1 : 2);
+                const int hv = !GSR_FWD_HALVES || !use_halves<FWD_STRIP>() || (hl && hr) ? 0 : (hl ? 1 : 2);
                 if constexpr (FWD_ROWS == 2)
                     pth = (full ? ((cb[0] & 1) ? P_REC3 : P_DIR3) : P_MSK3) + hv;
                 else
                     pth = (full ? 0 : 3) + hv;
             }
+#if GSR_FWD_SPLIT
+            const bool front = keep && pth == FRONT_PATH;
+            const unsigned mf = __ballot_sync(0xffffffffu, front);
+            const unsigned mb = __ballot_sync(0xffffffffu, keep && !front);
+            if (keep) {
+                const int slot = front ? cnt + __popc(mf & lt)
+                                       : FWD_BUF - 1 - (cntb + __popc(mb & lt));
+                sm.path[warp][b][slot] = (uint8_t)pth;
+                const float4* src = rec + (long long)REC_F4 * (sb[0] + lane);
+                float4* dst = &sm.rec[warp][b][REC_F4 * slot];
+#pragma unroll
+                for (int q = 0; q < REC_F4; ++q) cp_async16(dst + q, src + q);
+            }
+            cnt += __popc(mf);
+            cntb += __popc(mb);
+#else
             const unsigned m = __ballot_sync(0xffffffffu, keep);
             if (keep) {
                 const int slot = cnt + __popc(m & lt);
@@ -509,30 +574,35 @@ __global__ void __launch_bounds__(FWD2_THREADS, 4) k_render_fwd2(const ImgTable 
                 for (int q = 0; q < REC_F4; ++q) cp_async16(dst + q, src + q);
             }
             cnt += __popc(m);
+#endif
 #pragma unroll
             for (int d = 0; d + 1 < SD; ++d) {
                 nb[d] = nb[d + 1]; sb[d] = sb[d + 1]; rb[d] = rb[d + 1]; cb[d] = cb[d + 1];
             }
             fetch(SD - 1);
         }
-        if (cnt > FWD_BUF - 32 || (end && cnt > 0)) {
-            cp_async_commit();
-            if (pend >= 0) {                  // the other buffer: its copies are older
-                cp_async_wait<1>();
+        // a full buffer (or the last one) is committed; the OTHER buffer, whose copies are
+        // older, is evaluated meanwhile -- at the end, the last one after all copies landed
+        // (one evaluation call site: the evaluation code is inlined once)
+        const bool fl = cnt + cntb > FWD_BUF - 32 || (end && cnt + cntb > 0);
+        if (fl) cp_async_commit();
+        if (fl || end) {
+            if (pend >= 0) {
+                if (fl) cp_async_wait<1>(); else cp_async_wait<0>();
                 __syncwarp();
-                process(b ^ 1, pend);
+                run(b ^ 1, pend, pendb);
                 __syncwarp();
             }
-            pend = cnt;
-            b ^= 1;
-            cnt = 0;
+            pend = -1;
+            if (fl) {
+                pend = cnt;
+                pendb = cntb;
+                b ^= 1;
+                cnt = 0;
+                cntb = 0;
+            }
         }
-        if (end) break;
-    }
-    if (pend >= 0) {
-        cp_async_wait<0>();
-        __syncwarp();
-        process(b ^ 1, pend);
+        if (end && pend < 0) break;
     }
 #pragma unroll
     for (int a = 0; a < NACC; ++a) sm.tot[warp][a][lane] = acc[a];
@@ -635,7 +705,11 @@ cudaError_t launch_render_fwd(const ImgTable& tab, const Workspace& ws, float* o
         slots = tab.fwd_small ? fwd_slots<FwdCfgSmall>() : fwd_slots<FwdCfgWide>();
         sl.store(slots, std::memory_order_relaxed);
     }
+#ifdef GSR_FORCE_KS_FWD                 // A/B builds only
+    const int ks = GSR_FORCE_KS_FWD;
+#else
     const int ks = split_k_factor(tab.total_ftiles, slots);
+#endif
     cudaError_t e;
     switch (ks) {
         case 8: e = launch_ks<8>(tab, ws, out, gt, loss_acc, st); break;
