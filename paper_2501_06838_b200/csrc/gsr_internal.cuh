@@ -23,7 +23,7 @@ constexpr int CELL = 16;       // cell edge (HR px): binning granularity (sort k
 #endif
 constexpr int TILE_W = GSR_BWD_TILE_W;  // backward render tile (HR px, power of 2 >= 16);
 constexpr int TILE_H = GSR_BWD_TILE_H;  // also the debug tile-list tile (TILE_H even)
-// forward: a CTA renders one tile; each of the 4 warps covers the whole tile (lane l owns a
+// forward: a CTA renders one tile; each of its warps covers the whole tile (lane l owns a
 // ROWS x STRIP block at column group l & 3, row group l >> 2) and takes its own share of the
 // tile's Gaussians, so the warps' work is balanced by construction. Two configurations, chosen
 // per call from the window size:
@@ -32,18 +32,26 @@ constexpr int TILE_H = GSR_BWD_TILE_H;  // also the debug tile-list tile (TILE_H
 //         which wastes far fewer masked evaluations where a window covers only part of a tile
 //         (GSR_FWD_SMALL_STRIP=8: 1 x 8 px per lane, 32 x 8 tiles evaluated per 16 x 8 column half;
 //         measured 7% slower at C2)
-struct FwdCfgLarge { static constexpr int ROWS = 2, STRIP = 8, TW = 4 * STRIP, TH = 8 * ROWS; };
+// warps per forward CTA (each covers the whole tile for its share of the Gaussians): 2 for the
+// large tiles (4 measured +2% at C5), 4 for the small ones (2: +35% at C2)
+#ifndef GSR_FWD_WARPS_LARGE
+#define GSR_FWD_WARPS_LARGE 2
+#endif
+#ifndef GSR_FWD_WARPS_SMALL
+#define GSR_FWD_WARPS_SMALL 4
+#endif
+struct FwdCfgLarge { static constexpr int ROWS = 2, STRIP = 8, TW = 4 * STRIP, TH = 8 * ROWS, WARPS = GSR_FWD_WARPS_LARGE; };
 #ifndef GSR_FWD_SMALL_STRIP
 #define GSR_FWD_SMALL_STRIP 4
 #endif
-struct FwdCfgSmall { static constexpr int ROWS = 1, STRIP = GSR_FWD_SMALL_STRIP, TW = 4 * STRIP, TH = 8 * ROWS; };
+struct FwdCfgSmall { static constexpr int ROWS = 1, STRIP = GSR_FWD_SMALL_STRIP, TW = 4 * STRIP, TH = 8 * ROWS, WARPS = GSR_FWD_WARPS_SMALL; };
 using FwdCfgWide = FwdCfgLarge;
 constexpr int FWD_SMALL_WINDOW = 48;             // HR px: below this the small tiles are used
 #ifndef GSR_FWD_REC
 #define GSR_FWD_REC 1
 #endif
 constexpr float FWD_REC_DMAX = GSR_FWD_REC ? 1.0f : -1.0f;            // max a1/s for the forward's exp recurrence
-constexpr int FWD_CWARPS = 4;                    // warps per forward CTA
+
 #ifndef GSR_BWD_WARPS
 #define GSR_BWD_WARPS 4
 #endif

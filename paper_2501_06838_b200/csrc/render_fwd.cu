@@ -4,22 +4,25 @@
 //                c'_i * 2^(q_i(x,y)),   q = -(w^2 + v^2),  w = a1 dx + b1 dy,  v = c1 dy,
 //                dx = (x - ax_i)/s - dl_x,  dy = (y - ay_i)/s - dl_y   (= x/s - mu_x, y/s - mu_y)
 //
-// CTA = one FTILE_W x FTILE_H (32 x 16) HR tile, 4 warps. Every warp covers the whole tile -- lane
-// l owns the 2 x 8 block at columns Tx0 + 4 (l & 3) + {0..3, 16..19} and rows Ty0 + 2 (l >> 2) +
-// {0, 1} -- for its own share of the tile's Gaussians; the partial images are summed in warp order.
+// CTA = one FTILE_W x FTILE_H (32 x 16) HR tile, W = CFG::WARPS warps (2; 4 for the small tiles).
+// Every warp covers the whole tile -- lane l owns the 2 x 8 block at columns Tx0 + 4 (l & 3) +
+// {0..3, 16..19} and rows Ty0 + 2 (l >> 2) + {0, 1} -- for its own share of the tile's Gaussians;
+// the partial images are summed in warp order.
 //   * candidates: the tile's contiguous cell-row spans (binning.cu), walked in batches of 32
-//     (batch i to warp i mod 4 and, under split-K, to cluster CTA (i / 4) mod KS) and filtered
+//     (batch i to warp i mod W and, under split-K, to cluster CTA (i / W) mod KS) and filtered
 //     from the 16-B rect stream + the record class byte: keep if the support rect (R21) meets
-//     the tile; the filter also decides the Gaussian's evaluation PATH (below), so the consumer
-//     dispatches on one byte read one Gaussian ahead, before the record itself is loaded.
+//     the tile; the filter also decides the Gaussian's evaluation PATH (below).
 //   * staging: each lane whose candidate is kept copies its 64-B record with four 16-B cp.async
-//     into the warp's own double buffer in shared memory; a warp evaluates one buffer while the
-//     copies of the other are in flight.
+//     into the warp's own double buffer in shared memory -- the dominant path (recurrence over
+//     both column halves / the unmasked small tile) from the buffer's front, every other path
+//     from its back with a path byte -- and a warp evaluates one buffer while the copies of the
+//     other are in flight: the front run without any per-Gaussian dispatch (the dispatch's
+//     dependent compare-and-branch chain held ~25% of the stall samples), then the back.
 //   * paths (warp-uniform per Gaussian): exponential recurrence along rows (window rect covers
 //     the tile and D <= 1: 2 ex2 per 4 pairs), direct (covers, D > 1), masked (a window edge
 //     crosses the tile); each in three column-half variants (support meets the left 16, the
 //     right 16 or both columns), compile-time so the evaluated anchors stay one unrolled block.
-//   * sums: one register accumulator per lane-pixel for the whole tile; at the end all 4 warps
+//   * sums: one register accumulator per lane-pixel for the whole tile; at the end all warps
 //     add the warp images (in warp order, deterministic) into an HWC staging tile in shared
 //     memory, reduce split-K cluster CTAs through DSMEM in rank order, and store the tile with
 //     coalesced 16-B (float4) stores (scalar at ragged image edges / misaligned rows).
@@ -253,16 +256,15 @@ constexpr int kFrontUnroll = GSR_FWD_FRONT_UNROLL;
 #ifndef GSR_FWD_HALVES
 #define GSR_FWD_HALVES 1          // skip the column half a Gaussian's support misses
 #endif
-constexpr int FWD2_THREADS = FWD_CWARPS * 32;
 
 template <class CFG>
 struct FwdSmem2 {
     union {
-        float4 rec[FWD_CWARPS][2][FWD_BUF * REC_F4];      // staged records (main loop)
+        float4 rec[CFG::WARPS][2][FWD_BUF * REC_F4];      // staged records (main loop)
         float stage[CFG::TH][CFG::TW * 3];                 // HWC tile (epilogue)
     };
-    uint8_t path[FWD_CWARPS][2][FWD_BUF];
-    float2 tot[FWD_CWARPS][FwdAcc<CFG>::NACC][32];         // per-warp images (epilogue)
+    uint8_t path[CFG::WARPS][2][FWD_BUF];
+    float2 tot[CFG::WARPS][FwdAcc<CFG>::NACC][32];         // per-warp images (epilogue)
 };
 
 // Stores the tile from the HWC staging area (every thread), with the fused L1 loss.
@@ -275,13 +277,13 @@ __device__ __forceinline__ void fwd_store(const float (*stage)[CFG::TW * 3], con
     const int nx = min(TW, im.Ws - Tx0), ny = min(TH, im.row_end - Ty0);
     float l1 = 0.f;
     if (im.io != 0) {                                   // NEXT-4 formats (bf16 / planar CHW)
-        for (int i = threadIdx.x; i < ny * nx * 3; i += FWD2_THREADS) {
+        for (int i = threadIdx.x; i < ny * nx * 3; i += (CFG::WARPS * 32)) {
             const int r = i / (nx * 3), c = i % (nx * 3);
             img_store(out, im, img_index(im, Ty0 + r, Tx0 + c / 3, c % 3), stage[r][c]);
         }
         return;
     }
-    for (int r = threadIdx.x / 32; r < ny; r += FWD_CWARPS) {   // one warp per row, coalesced
+    for (int r = threadIdx.x / 32; r < ny; r += CFG::WARPS) {   // one warp per row, coalesced
         const int lane = threadIdx.x & 31;
         const long long o = im.out_off + ((long long)(r + Ty0 - im.row_begin) * im.Ws + Tx0) * 3;
         const int nf = nx * 3;
@@ -320,11 +322,11 @@ __device__ __forceinline__ void fwd_epilogue(FwdSmem2<CFG>& sm, const DevImg& im
                                              double* __restrict__ loss_acc) {
     constexpr int STRIP = CFG::STRIP, ROWS = CFG::ROWS, NACC = FwdAcc<CFG>::NACC;
     __syncthreads();                                   // every warp's image + no record reads
-    for (int i = threadIdx.x; i < NACC * 32; i += FWD2_THREADS) {
+    for (int i = threadIdx.x; i < NACC * 32; i += (CFG::WARPS * 32)) {
         const int a = i >> 5, l = i & 31;
         float2 v = sm.tot[0][a][l];
 #pragma unroll
-        for (int q = 1; q < FWD_CWARPS; ++q) v = __fadd2_rn(v, sm.tot[q][a][l]);
+        for (int q = 1; q < CFG::WARPS; ++q) v = __fadd2_rn(v, sm.tot[q][a][l]);
         const int xl = lane_x0<STRIP>(l), yl = ROWS * (l >> 2);
         const int k = a % 3;
         if constexpr (ROWS == 2) {                     // pair = (row 0, row 1) of column slot j
@@ -342,7 +344,7 @@ __device__ __forceinline__ void fwd_epilogue(FwdSmem2<CFG>& sm, const DevImg& im
         cluster_sync_all();                            // every CTA's tile is staged
         if (krank == 0) {
             float* st = &sm.stage[0][0];
-            for (int i = threadIdx.x; i < CFG::TH * CFG::TW * 3; i += FWD2_THREADS) {
+            for (int i = threadIdx.x; i < CFG::TH * CFG::TW * 3; i += (CFG::WARPS * 32)) {
                 float v = st[i];
                 for (int q = 1; q < KS; ++q) v += ld_dsmem_f(st + i, q);
                 st[i] = v;
@@ -357,7 +359,7 @@ __device__ __forceinline__ void fwd_epilogue(FwdSmem2<CFG>& sm, const DevImg& im
 }
 
 template <int KS, bool LOSS, class CFG>
-__global__ void __launch_bounds__(FWD2_THREADS, 4) k_render_fwd2(const ImgTable tab,
+__global__ void __launch_bounds__(CFG::WARPS * 32, 16 / CFG::WARPS) k_render_fwd2(const ImgTable tab,
                                                               const float4* __restrict__ rec,
                                                               const int4* __restrict__ rects,
                                                               const uint8_t* __restrict__ cls,
@@ -417,8 +419,8 @@ __global__ void __launch_bounds__(FWD2_THREADS, 4) k_render_fwd2(const ImgTable 
     int cb[SD];
     int first = 1;
     auto fetch = [&](int j) {
-        nb[j] = live ? prod.next(&sb[j], first ? krank * FWD_CWARPS + warp
-                                               : KS * FWD_CWARPS - 1) : 0;
+        nb[j] = live ? prod.next(&sb[j], first ? krank * CFG::WARPS + warp
+                                               : KS * CFG::WARPS - 1) : 0;
         first = 0;
         rb[j] = make_int4(0, 0, 0, 0);
         cb[j] = 0;
@@ -639,7 +641,7 @@ cudaError_t launch_ks3(const ImgTable& tab, const Workspace& ws, float* out, con
     if (e0 != cudaSuccess) return e0;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)tab.total_ftiles * KS);
-    cfg.blockDim = dim3(FWD2_THREADS);
+    cfg.blockDim = dim3((CFG::WARPS * 32));
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
@@ -674,7 +676,7 @@ int fwd_slots() {
     const auto k = k_render_fwd2<1, false, CFG>;
     const size_t smem = sizeof(FwdSmem2<CFG>);
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    return resident_slots(k, FWD2_THREADS, smem);
+    return resident_slots(k, (CFG::WARPS * 32), smem);
 }
 
 }  // namespace
