@@ -59,6 +59,9 @@ void prof_end(int handle, cudaStream_t st) {
 namespace {
 
 constexpr int MAX_DIM = 65535;
+#ifndef GSR_SCHED_DENSE
+#define GSR_SCHED_DENSE 1
+#endif
 
 inline int ceil_div(long long a, long long b) { return (int)((a + b - 1) / b); }
 
@@ -139,6 +142,26 @@ gsr_status build_table(const gsr_image* imgs, int32_t n_imgs, int64_t n_total, d
     tab->total_cells = (int)cells;
     tab->total_tiles = (int)tiles;
     tab->total_ftiles = (int)ftiles;
+    // launch order (GSR_SCHED_DENSE): densest images first -- a tile's cost grows with the
+    // Gaussians per HR pixel (C2: 16 at s = 1, 1 at s = 4), so the heavy tiles start early and
+    // the grid's tail holds light ones; results do not depend on the order
+    for (int k = 0; k < n_imgs; ++k) tab->sched[k] = k;
+#if GSR_SCHED_DENSE
+    auto dens = [&](int k) {
+        const DevImg& d = tab->img[k];
+        return (double)d.g_cnt / std::max(1.0, (double)d.Hs * (double)d.Ws);
+    };
+    std::stable_sort(tab->sched, tab->sched + n_imgs,
+                     [&](int a, int b) { return dens(a) > dens(b); });
+#endif
+    long long st = 0, sft = 0;
+    for (int i = 0; i < n_imgs; ++i) {
+        DevImg& d = tab->img[tab->sched[i]];
+        d.stile_base = (int)st;
+        d.sftile_base = (int)sft;
+        st += (long long)d.ntx * d.nty;
+        sft += (long long)d.fntx * d.fnty;
+    }
     return GSR_OK;
 }
 

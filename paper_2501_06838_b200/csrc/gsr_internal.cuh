@@ -76,6 +76,7 @@ struct DevImg {
     int ncx, ncy, cell_base;  // cells of this image: [cell_base, cell_base + ncx*ncy)
     int ntx, nty, tile_base;  // backward tiles (TILE_W x TILE_H) of this image
     int fntx, fnty, ftile_base;  // forward tiles (ImgTable::ftile_w x ftile_h)
+    int stile_base, sftile_base;  // first backward / forward CTA tile in launch order (schedule)
     int wmax, hmax;           // upper bounds on the unclipped rect width/height
     int io;                   // image I/O format of out / grad_out (IO_BF16 | IO_CHW; 0 = fp32 HWC)
 };
@@ -91,6 +92,9 @@ struct ImgTable {
     int ftile_w, ftile_h;     // forward tile of this call (large or small configuration)
     int fwd_small;            // 1: FwdCfgSmall
     int params_bf16;          // GSR_PARAMS_BF16: the five parameter arrays are bfloat16
+    // launch order of the images' tiles: densest images (most Gaussians per HR pixel, the
+    // heaviest tiles) first, so the tail of the grid holds the light tiles
+    int sched[MAX_IMAGES];
     DevImg img[MAX_IMAGES];
 };
 
@@ -131,6 +135,24 @@ __host__ __device__ inline int find_image_by_ftile(const ImgTable& t, int tile) 
         if (t.img[mid].ftile_base <= tile) lo = mid; else hi = mid - 1;
     }
     return lo;
+}
+
+// image owning the render kernels' CTA tile `tile` (launch order, ImgTable::sched)
+__host__ __device__ inline int find_image_by_stile(const ImgTable& t, int tile) {
+    int lo = 0, hi = t.n_imgs - 1;
+    while (lo < hi) {
+        int mid = (lo + hi + 1) >> 1;
+        if (t.img[t.sched[mid]].stile_base <= tile) lo = mid; else hi = mid - 1;
+    }
+    return t.sched[lo];
+}
+__host__ __device__ inline int find_image_by_sftile(const ImgTable& t, int tile) {
+    int lo = 0, hi = t.n_imgs - 1;
+    while (lo < hi) {
+        int mid = (lo + hi + 1) >> 1;
+        if (t.img[t.sched[mid]].sftile_base <= tile) lo = mid; else hi = mid - 1;
+    }
+    return t.sched[lo];
 }
 
 __host__ __device__ inline int find_image_by_gauss(const ImgTable& t, long long i) {

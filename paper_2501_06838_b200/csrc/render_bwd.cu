@@ -179,9 +179,9 @@ __global__ void __launch_bounds__(BWD_THREADS) k_render_bwd(
 
     const int tile = blockIdx.x / ks;
     const int kpart = blockIdx.x % ks;    // split: this CTA takes every ks-th candidate group
-    const int kimg = find_image_by_tile(tab, tile);
+    const int kimg = find_image_by_stile(tab, tile);
     const DevImg& im = tab.img[kimg];
-    const int t = tile - im.tile_base;
+    const int t = tile - im.stile_base;
     const int Tx0 = (t % im.ntx) * TILE_W;
     const int Ty0 = im.row_begin + (t / im.ntx) * TILE_H;
     const int Tx1 = min(Tx0 + TILE_W - 1, im.Ws - 1);

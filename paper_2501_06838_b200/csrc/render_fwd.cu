@@ -375,9 +375,9 @@ __global__ void __launch_bounds__(CFG::WARPS * 32, 16 / CFG::WARPS) k_render_fwd
 
     const int tile = blockIdx.x / KS;
     const int krank = KS > 1 ? (int)cluster_rank() : 0;
-    const int kimg = find_image_by_ftile(tab, tile);
+    const int kimg = find_image_by_sftile(tab, tile);
     const DevImg& im = tab.img[kimg];
-    const int t = tile - im.ftile_base;
+    const int t = tile - im.sftile_base;
     const int Tx0 = (t % im.fntx) * FTILE_W;
     const int Ty0 = im.row_begin + (t / im.fntx) * FTILE_H;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
