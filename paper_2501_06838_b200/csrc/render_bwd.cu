@@ -54,6 +54,11 @@ namespace gsr {
 namespace {
 
 constexpr int kBwdUnroll = GSR_BWD_UNROLL;
+#ifndef GSR_BWD_UNROLL_MASKED
+#define GSR_BWD_UNROLL_MASKED 4   // the masked column segments (window edges inside the union;
+                                  // C2 -2%, C4/C5 unchanged; 2: +2% at C4/C5)
+#endif
+constexpr int kBwdUnrollMasked = GSR_BWD_UNROLL_MASKED;
 constexpr int BWD_BATCH = GSR_BWD_BATCH;
 
 __device__ __forceinline__ float2 f2(float a) { return make_float2(a, a); }
@@ -135,7 +140,8 @@ __device__ __forceinline__ void row2_pairs(int c_begin, int c_end, const float4*
                                            RowAcc& A0, RowAcc& A1) {
     float2 kx = make_float2(kT + (float)c_begin, kT + (float)(c_begin + 1));
     const float2 two = f2(2.0f);
-#pragma unroll kBwdUnroll
+    constexpr int UNR = MASKED ? kBwdUnrollMasked : kBwdUnroll;
+#pragma unroll UNR
     for (int c = c_begin; c < c_end; c += 2) {
         const int cp = c >> 1;
         bool in0 = true, in1 = true;
