@@ -484,15 +484,17 @@ __global__ void __launch_bounds__(CFG::WARPS * 32, 16 / CFG::WARPS) k_render_fwd
             const float4* q = sr + REC_F4 * g;
             const float4 r0 = q[0], r1 = q[1], r2 = q[2];
             if constexpr (FWD_ROWS == 2) {
-                if (pth <= P_REC2) {
+                // the back's common paths first: the single-half recurrences (P_REC3 is only
+                // here without GSR_FWD_SPLIT)
+                if ((unsigned)(pth - P_REC1) <= (unsigned)(P_REC2 - P_REC1) || pth == P_REC3) {
                     const float4 r3 = q[3];
                     const float4 r2g = make_float4(r2.x, r2.y, r3.x, r3.y);
-                    if (pth == P_REC3)
-                        fwd_gauss_r2h<2, FWD_STRIP, 3>(r0, r1, r2g, r3.z, xlf, yrow, yi, xl0, invs, acc);
-                    else if (pth == P_REC1)
+                    if (pth == P_REC1)
                         fwd_gauss_r2h<2, FWD_STRIP, 1>(r0, r1, r2g, r3.z, xlf, yrow, yi, xl0, invs, acc);
-                    else
+                    else if (pth == P_REC2)
                         fwd_gauss_r2h<2, FWD_STRIP, 2>(r0, r1, r2g, r3.z, xlf, yrow, yi, xl0, invs, acc);
+                    else
+                        fwd_gauss_r2h<2, FWD_STRIP, 3>(r0, r1, r2g, r3.z, xlf, yrow, yi, xl0, invs, acc);
                 } else if (pth >= P_MSK3) {
                     if (pth == P_MSK3)
                         fwd_gauss_r2h<0, FWD_STRIP, 3>(r0, r1, r2, 0.f, xlf, yrow, yi, xl0, invs, acc);
