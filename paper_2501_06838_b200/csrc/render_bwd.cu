@@ -42,9 +42,6 @@
 #ifndef GSR_BWD_BATCH
 #define GSR_BWD_BATCH 512         // hits per sorted batch (multiple of 32)
 #endif
-#ifndef GSR_BWD_Y
-#define GSR_BWD_Y 1
-#endif
 #ifndef GSR_BWD_MACC_T
 #define GSR_BWD_MACC_T float      // per-(Gaussian, tile) accumulator type of the row folds
 #endif
@@ -111,7 +108,6 @@ __device__ __forceinline__ void pix_pair2(const float4 gaA, const float4 gaB, co
     B.FB = __ffma2_rn(eB, gbB, B.FB);
     B.FG = __ffma2_rn(eB, ggB, B.FG);
     B.FR = __ffma2_rn(eB, grB, B.FR);
-#if GSR_BWD_Y
     // y = e (g . c'), W1 += y w' (an FADD2: two register pairs), W2 += (y w') w'
     const float2 ywA = __fmul2_rn(__fmul2_rn(eA, gcA), wA);
     const float2 ywB = __fmul2_rn(__fmul2_rn(eB, gcB), wB);
@@ -119,14 +115,6 @@ __device__ __forceinline__ void pix_pair2(const float4 gaA, const float4 gaB, co
     A.W2 = __ffma2_rn(ywA, wA, A.W2);
     B.W1 = __fadd2_rn(B.W1, ywB);
     B.W2 = __ffma2_rn(ywB, wB, B.W2);
-#else
-    const float2 edA = __fmul2_rn(eA, wA), edB = __fmul2_rn(eB, wB);
-    const float2 eddA = __fmul2_rn(edA, wA), eddB = __fmul2_rn(edB, wB);
-    A.W1 = __ffma2_rn(gcA, edA, A.W1);
-    A.W2 = __ffma2_rn(gcA, eddA, A.W2);
-    B.W2 = __ffma2_rn(gcB, eddB, B.W2);
-    B.W1 = __ffma2_rn(gcB, edB, B.W1);
-#endif
 }
 
 // Columns [c_begin, c_end) (pairs) of two rows at once: the column part (kx, masks, dL/dI
