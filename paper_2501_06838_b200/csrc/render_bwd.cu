@@ -185,7 +185,11 @@ __global__ void __launch_bounds__(BWD_THREADS) k_render_bwd(
     // stage dL/dI of the tile (zeros outside the image / band)
     for (int pp = threadIdx.x; pp < TILE_H * (TILE_W / 2); pp += BWD_THREADS) {
         int ry = pp / (TILE_W / 2), cp = pp % (TILE_W / 2);
+#ifdef GSR_DIAG_BWD_NOSTAGE      // timing diagnostic only (wrong results): no dL/dI loads
+        int y = Ty1 + 1, x = Tx0 + 2 * cp;
+#else
         int y = Ty0 + ry, x = Tx0 + 2 * cp;
+#endif
         float v[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
         if (y <= Ty1) {
             const long long ro = im.out_off + ((long long)(y - im.row_begin) * im.Ws) * 3;
