@@ -152,13 +152,16 @@ def oracle_sample(imgs, clouds, host_grad_img0, budget_s: float, max_threads=Non
     c = clouds[0]
     Hs, Ws = O.out_dims(H, W, s)
     mid = Hs // 2
-    # calibrate on two rows (the first call also warms the OpenMP pool), then size the sample to
-    # ~budget/2 of oracle time per pass
+    # calibrate each pass on a probe (the first forward call also warms the OpenMP pool), then
+    # size both samples to ~budget/2 of oracle time each, so that the two rates are measured on
+    # samples of the same duration whatever the budget (the reference arm and the GPU line's
+    # cpu_baseline then agree)
     O.render_fwd(c, H, W, s, RATIO, mode="rect", rows=(mid, mid + 1))
+    probe = 8
     t0 = time.perf_counter()
-    O.render_fwd(c, H, W, s, RATIO, mode="rect", rows=(mid, mid + 2))
-    t1 = (time.perf_counter() - t0) / 2
-    rows = int(max(1, min(Hs - mid, (budget_s / 2) / max(t1, 1e-3))))
+    O.render_fwd(c, H, W, s, RATIO, mode="rect", rows=(mid, mid + probe))
+    t1 = (time.perf_counter() - t0) / probe
+    rows = int(max(1, min(Hs - mid, (budget_s / 2) / max(t1, 1e-4))))
     t0 = time.perf_counter()
     O.render_fwd(c, H, W, s, RATIO, mode="rect", rows=(mid, mid + rows))
     tf = time.perf_counter() - t0
@@ -166,9 +169,13 @@ def oracle_sample(imgs, clouds, host_grad_img0, budget_s: float, max_threads=Non
     R = O.rects(c, H, W, s, RATIO)
     area = np.maximum(R[:, 3] - R[:, 2] + 1, 0) * np.maximum(R[:, 5] - R[:, 4] + 1, 0)
     rate_f = pf / tf
-    target = int(rate_f * budget_s / 2)
     order = np.argsort(np.abs(c["mu"][:, 1] - H / 2) + np.abs(c["mu"][:, 0] - W / 2))
     cum = np.cumsum(area[order])
+    kp = int(max(1, min(len(order), np.searchsorted(cum, rate_f * 0.05) + 1)))  # ~0.15 s probe
+    t0 = time.perf_counter()
+    O.render_bwd(c, H, W, s, RATIO, host_grad_img0, idx=np.sort(order[:kp]))
+    rate_b0 = float(area[order[:kp]].sum()) / max(time.perf_counter() - t0, 1e-6)
+    target = int(rate_b0 * budget_s / 2)
     k = int(max(1, min(len(order), np.searchsorted(cum, target) + 1)))
     idx = np.sort(order[:k])
     t0 = time.perf_counter()
