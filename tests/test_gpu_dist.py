@@ -10,6 +10,7 @@ single-process whole-image gradient (fp32 regrouping tolerance) and sampled Gaus
 oracle (gate of tests/_util)."""
 import os
 import socket
+from pathlib import Path
 
 import numpy as np
 import pytest
@@ -19,6 +20,8 @@ import oracle as O
 from _util import KEYS, assert_bwd_close, assert_fwd_close
 
 pytestmark = pytest.mark.gpu
+
+ROOT = Path(__file__).resolve().parents[1]
 
 IMGS = [(40, 60, 8.0), (34, 51, 6.5)]
 
@@ -236,3 +239,42 @@ def test_rank_halo_fused_equals_span_path():
                 assert a.n_multi == b.n_multi
                 if ratio == 0.5 and G == 5:
                     assert a.n_multi > 0
+
+
+def _json_line(out: str) -> dict:
+    import json
+    lines = [l for l in out.splitlines() if l.startswith("{")]
+    assert lines, out[-2000:]
+    return json.loads(lines[-1])
+
+
+def test_bench_self_launch_two_ranks():
+    """`bench.py --gpus 2` with no launcher re-executes itself under torch.distributed.run (two
+    ranks sharing cuda:0 over gloo here: GSR_BENCH_SHARE_GPU=1, a functional check of the
+    sharded band path, never a performance number) and rank 0 prints one JSON line."""
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, GSR_BENCH_SHARE_GPU="1")
+    r = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--gpus", "2", "--images", "2",
+                        "--steps", "1", "--warmup", "3", "--no-cpu-baseline", "--no-configs",
+                        "--no-e2e"], capture_output=True, text=True, env=env, timeout=600,
+                       cwd=str(ROOT))
+    assert r.returncode == 0, r.stderr[-3000:]
+    d = _json_line(r.stdout)
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["config"]["halo_gaussians_rank0"] > 0
+
+
+def test_train_dp_launcher_two_ranks():
+    """NEXT-2's data-parallel launcher (tools/train_dp.py): two ranks, each its own 16 patches,
+    the global-mean loss all-reduced (gloo on the shared GPU)."""
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, GSR_BENCH_SHARE_GPU="1")
+    r = subprocess.run([sys.executable, str(ROOT / "tools" / "train_dp.py"), "--gpus", "2",
+                        "--steps", "3"], capture_output=True, text=True, env=env, timeout=600,
+                       cwd=str(ROOT))
+    assert r.returncode == 0, r.stderr[-3000:]
+    d = _json_line(r.stdout)
+    assert d["ranks"] == 2 and d["global_batch"] == 32 and d["global_mean_loss"] > 0
