@@ -42,6 +42,9 @@
 #ifndef GSR_BWD_BATCH
 #define GSR_BWD_BATCH 512         // hits per sorted batch (multiple of 32)
 #endif
+#ifndef GSR_BWD_CTASORT
+#define GSR_BWD_CTASORT 1
+#endif
 #ifndef GSR_BWD_MACC_T
 #define GSR_BWD_MACC_T float      // per-(Gaussian, tile) accumulator type of the row folds
 #endif
@@ -399,6 +402,146 @@ __global__ void __launch_bounds__(BWD_THREADS) k_render_bwd(
         __syncwarp();
     };
 
+#if GSR_BWD_CTASORT
+    // CTA-wide rounds (GSR_BWD_CTASORT): every warp scans its share of the candidate chunks
+    // into its own queue until it holds >= BWD_BATCH hits (or its share is exhausted); then the
+    // CTA sorts the first <= BWD_BATCH hits of every warp's queue together -- key-major, then
+    // warp order, then queue order (stable, deterministic) -- into one list of <= 4 BWD_BATCH
+    // hits, and the warps evaluate its groups of 32 round-robin. The larger sorted batch makes
+    // the groups' column ranges tighter (a replay of one C5 image: 86.6% instead of 81.3% of the
+    // evaluated lane-pairs inside the lane's support) and the groups balance the warps.
+    __shared__ int qs_cta[BWD_WARPS * BWD_BATCH];
+    __shared__ int hist_cta[NB * BWD_WARPS];          // [key][warp]: counts, then offsets
+    __shared__ int sh_qn[BWD_WARPS], sh_done[BWD_WARPS], sh_tot[32];
+    const int parts = ks * BWD_WARPS, part = kpart * BWD_WARPS + warp;
+    int cy = cy_lo - 1, p0 = 0, s1 = 0;
+    bool more = true;
+    auto scan_step = [&]() {                          // one SCAN_U-chunk step of this warp
+        while (p0 >= s1 && cy < cy_hi) {              // next non-empty cell row
+            ++cy;
+            const int row = im.cell_base + cy * im.ncx;
+            const int s0 = cell_start[row + cx_lo];
+            s1 = cell_start[row + cx_hi + 1];
+            p0 = s0 + part * 32;
+        }
+        if (p0 >= s1) { more = false; return; }
+        int4 rc[SCAN_U];
+#pragma unroll
+        for (int u = 0; u < SCAN_U; ++u) {
+            const int p = p0 + u * parts * 32 + lane;
+            rc[u] = p < s1 ? __ldg(rects + p) : make_int4(0, 0, 0x7fff7fff, 0);
+        }
+#pragma unroll
+        for (int u = 0; u < SCAN_U; ++u) {
+            const int p = p0 + u * parts * 32 + lane;
+            bool hit = false;
+            int key = 0;
+            if (p < s1) {
+                const unsigned xs = (unsigned)rc[u].x, ys = (unsigned)rc[u].y;
+                const int x0 = (int)(xs & 0xffffu), x1 = (int)(xs >> 16);
+                const int y0 = (int)(ys & 0xffffu), y1 = (int)(ys >> 16);
+                hit = !(x1 < Tx0 || x0 > Tx1 || y1 < Ty0 || y0 > Ty1);
+                key = ((max(x0, Tx0) - Tx0) / (TILE_W / KQ)) * KQ +
+                      (min(x1, Tx1) - Tx0) / (TILE_W / KQ);
+            }
+            const unsigned hm = __ballot_sync(0xffffffffu, hit);
+            if (hit) {
+                const int slot = qn + __popc(hm & lt);
+                qp[warp][slot] = p;
+                qk[warp][slot] = (unsigned short)key;
+            }
+            qn += __popc(hm);
+        }
+        __syncwarp();
+        p0 += parts * 32 * SCAN_U;
+    };
+    while (true) {
+        while (more && qn < BWD_BATCH) scan_step();
+        if (lane == 0) { sh_qn[warp] = qn; sh_done[warp] = more ? 0 : 1; }
+        __syncthreads();
+        int total = 0, mybase = 0, alldone = 1;
+#pragma unroll
+        for (int w = 0; w < BWD_WARPS; ++w) {
+            const int c = min(sh_qn[w], BWD_BATCH);
+            if (w < warp) mybase += c;
+            total += c;
+            alldone &= sh_done[w];
+        }
+        if (total == 0 && alldone) break;
+        const int cnt = min(qn, BWD_BATCH);
+        // counts per (key, warp)
+        for (int k = lane; k < NB; k += 32) hist_cta[k * BWD_WARPS + warp] = 0;
+        __syncwarp();
+        for (int i0 = 0; i0 < cnt; i0 += 32) {
+            const int i = i0 + lane;
+            const bool v = i < cnt;
+            const unsigned vm = __ballot_sync(0xffffffffu, v);
+            if (v) {
+                const int k = qk[warp][i];
+                const unsigned peers = __match_any_sync(vm, k);
+                if ((peers & lt) == 0) hist_cta[k * BWD_WARPS + warp] += __popc(peers);
+            }
+            __syncwarp();
+        }
+        __syncthreads();
+        {   // exclusive scan of the NB x BWD_WARPS counts (key-major), one block scan
+            constexpr int PER = NB * BWD_WARPS / BWD_THREADS;
+            int* hseg = hist_cta + threadIdx.x * PER;
+            int sum = 0;
+#pragma unroll
+            for (int q = 0; q < PER; ++q) sum += hseg[q];
+            int incl = sum;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            if (lane == 31) sh_tot[warp] = incl;
+            __syncthreads();
+            int wbase = 0;
+#pragma unroll
+            for (int w = 0; w < BWD_WARPS; ++w) wbase += w < warp ? sh_tot[w] : 0;
+            int run = wbase + incl - sum;
+#pragma unroll
+            for (int q = 0; q < PER; ++q) { const int t = hseg[q]; hseg[q] = run; run += t; }
+        }
+        __syncthreads();
+        // stable scatter of this warp's first cnt hits
+        for (int i0 = 0; i0 < cnt; i0 += 32) {
+            const int i = i0 + lane;
+            const bool v = i < cnt;
+            const unsigned vm = __ballot_sync(0xffffffffu, v);
+            int k = 0;
+            unsigned peers = 0;
+            if (v) {
+                k = qk[warp][i];
+                peers = __match_any_sync(vm, k);
+                qs_cta[hist_cta[k * BWD_WARPS + warp] + __popc(peers & lt)] = qp[warp][i];
+            }
+            __syncwarp();
+            if (v && (peers & lt) == 0) hist_cta[k * BWD_WARPS + warp] += __popc(peers);
+            __syncwarp();
+        }
+        __syncthreads();
+        for (int g = warp * 32; g < total; g += BWD_WARPS * 32) {
+            const bool act = g + lane < total;
+            group(act ? qs_cta[g + lane] : 0, act);
+        }
+        const int rest = qn - cnt;                    // < 32 * SCAN_U, moved to the front
+        for (int r0 = 0; r0 < rest; r0 += 32) {
+            int cp = 0;
+            unsigned short ck = 0;
+            const bool mv = r0 + lane < rest;
+            if (mv) { cp = qp[warp][cnt + r0 + lane]; ck = qk[warp][cnt + r0 + lane]; }
+            __syncwarp();
+            if (mv) { qp[warp][r0 + lane] = cp; qk[warp][r0 + lane] = ck; }
+            __syncwarp();
+        }
+        qn = rest;
+        (void)mybase;
+        __syncthreads();
+    }
+#else
     // Scan: SCAN_U chunks of 32 candidates (every parts-th chunk of the span, the same order as
     // one chunk at a time) have their rect loads in flight together, then are queued in order.
     for (int cy = cy_lo; cy <= cy_hi; ++cy) {
@@ -438,6 +581,7 @@ __global__ void __launch_bounds__(BWD_THREADS) k_render_bwd(
         }
     }
     if (qn > 0) flush(qn);
+#endif
 }
 
 template <class T>
