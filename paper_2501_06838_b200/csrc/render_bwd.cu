@@ -411,7 +411,8 @@ __global__ void __launch_bounds__(BWD_THREADS) k_render_bwd(
     // the groups' column ranges tighter (a replay of one C5 image: 86.6% instead of 81.3% of the
     // evaluated lane-pairs inside the lane's support) and the groups balance the warps.
     __shared__ int qs_cta[BWD_WARPS * BWD_BATCH];
-    __shared__ int hist_cta[NB * BWD_WARPS];          // [key][warp]: counts, then offsets
+    // [key][warp]: counts, then offsets (< 4 BWD_BATCH: 16 bits)
+    __shared__ unsigned short hist_cta[NB * BWD_WARPS];
     __shared__ int sh_qn[BWD_WARPS], sh_done[BWD_WARPS], sh_tot[32];
     const int parts = ks * BWD_WARPS, part = kpart * BWD_WARPS + warp;
     int cy = cy_lo - 1, p0 = 0, s1 = 0;
@@ -486,7 +487,7 @@ __global__ void __launch_bounds__(BWD_THREADS) k_render_bwd(
         __syncthreads();
         {   // exclusive scan of the NB x BWD_WARPS counts (key-major), one block scan
             constexpr int PER = NB * BWD_WARPS / BWD_THREADS;
-            int* hseg = hist_cta + threadIdx.x * PER;
+            unsigned short* hseg = hist_cta + threadIdx.x * PER;
             int sum = 0;
 #pragma unroll
             for (int q = 0; q < PER; ++q) sum += hseg[q];
@@ -503,7 +504,11 @@ __global__ void __launch_bounds__(BWD_THREADS) k_render_bwd(
             for (int w = 0; w < BWD_WARPS; ++w) wbase += w < warp ? sh_tot[w] : 0;
             int run = wbase + incl - sum;
 #pragma unroll
-            for (int q = 0; q < PER; ++q) { const int t = hseg[q]; hseg[q] = run; run += t; }
+            for (int q = 0; q < PER; ++q) {
+                const int t = hseg[q];
+                hseg[q] = (unsigned short)run;
+                run += t;
+            }
         }
         __syncthreads();
         // stable scatter of this warp's first cnt hits
