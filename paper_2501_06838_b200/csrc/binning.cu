@@ -62,16 +62,24 @@ __global__ void k_keys(const T* __restrict__ alpha, const T* __restrict__ mu,
         keys[t] = key;
         vals[t] = (int)t;
     }
-    // per-image max support extent: warp max over lanes of the same image, one atomic each
-    // (each group of lanes with the same image reduces with its own group-uniform mask)
+    // per-image max support extent: warp max over lanes of the same image (each group of lanes
+    // with the same image reduces with its own group-uniform mask), then a block max in shared
+    // memory, then one global atomic per (block, image) -- every warp of an image hitting the
+    // same two global words serialised K1 on them (C5: ~86k warps per 4 images)
+    __shared__ int bext[2 * MAX_IMAGES];
+    for (int j = threadIdx.x; j < 2 * MAX_IMAGES; j += blockDim.x) bext[j] = 0;
+    __syncthreads();
     const unsigned full = 0xffffffffu;
     const unsigned same = __match_any_sync(full, k);
     const int mwx = (int)__reduce_max_sync(same, (unsigned)wx);
     const int mwy = (int)__reduce_max_sync(same, (unsigned)wy);
     if (k >= 0 && (same & ((1u << (threadIdx.x & 31)) - 1u)) == 0 && (mwx | mwy)) {
-        atomicMax(&ext[2 * k], mwx);
-        atomicMax(&ext[2 * k + 1], mwy);
+        atomicMax(&bext[2 * k], mwx);
+        atomicMax(&bext[2 * k + 1], mwy);
     }
+    __syncthreads();
+    for (int j = threadIdx.x; j < 2 * MAX_IMAGES; j += blockDim.x)
+        if (bext[j] > 0) atomicMax(&ext[j], bext[j]);
 }
 
 // ---- stable LSD radix sort, 8-bit digits -----------------------------------------------
@@ -247,16 +255,23 @@ __global__ void k_records(const T* __restrict__ alpha, const T* __restrict__ mu,
                           int4* __restrict__ rects, uint8_t* __restrict__ cls) {
     long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= n) return;
-    if (keys[p] >= (uint32_t)tab.total_cells) return;
-    const long long i = gidx ? (long long)gidx[perm[p]] : (long long)perm[p];
+    // the key and the permutation are independent loads; the Gaussian's nine parameters are
+    // then gathered together (one round of memory latency each instead of a chain)
+    const uint32_t key = keys[p];
+    const int pi = perm[p];
+    if (key >= (uint32_t)tab.total_cells) return;
+    const long long i = gidx ? (long long)gidx[pi] : (long long)pi;
+    const float mxf = ldf(mu[2 * i]), myf = ldf(mu[2 * i + 1]);
+    const float sxf = ldf(sigma[2 * i]), syf = ldf(sigma[2 * i + 1]);
+    const float rhf = ldf(rho[i]), alf = ldf(alpha[i]);
+    const float c0f = ldf(color[3 * i]), c1f = ldf(color[3 * i + 1]), c2f = ldf(color[3 * i + 2]);
     int k = find_image_by_gauss(tab, i);
     const DevImg& im = tab.img[k];
-    float mxf = ldf(mu[2 * i]), myf = ldf(mu[2 * i + 1]);
     Rect r = window_rect(mxf, myf, im);
-    Rect sr = support_rect(mxf, myf, ldf(sigma[2 * i]), ldf(sigma[2 * i + 1]), im);
+    Rect sr = support_rect(mxf, myf, sxf, syf, im);
     double mx = mxf, my = myf;
-    double sx = ldf(sigma[2 * i]), sy = ldf(sigma[2 * i + 1]);
-        double rh = ldf(rho[i]), al = ldf(alpha[i]);
+    double sx = sxf, sy = syf;
+    double rh = rhf, al = alf;
     double D = (1.0 - rh) * (1.0 + rh);
     // exponent in factored form (no cancellation):
     //   q = -Q/2 log2 e = -(w'^2 + v'^2),  w' = a1 dx + b1 dy,  v' = c1 dy
@@ -272,12 +287,11 @@ __global__ void k_records(const T* __restrict__ alpha, const T* __restrict__ mu,
     const float a1f = (float)a1;
     const float Df = a1f * im.invsx, d2 = Df * Df;
     float4 r0 = make_float4((float)(-axd), (float)ayd, (float)dly, Df);
-    float4 r1 = make_float4((float)(-a1 * dlx), (float)b1, (float)c1,
-                            (float)(w * ldf(color[3 * i])));
+    float4 r1 = make_float4((float)(-a1 * dlx), (float)b1, (float)c1, (float)(w * c0f));
     unsigned xs = (unsigned)r.x0 | ((unsigned)r.x1 << 16);
     unsigned ys = (unsigned)r.y0 | ((unsigned)r.y1 << 16);
-    float4 r2 = make_float4((float)(w * ldf(color[3 * i + 1])), (float)(w * ldf(color[3 * i + 2])),
-                            __uint_as_float(xs), __uint_as_float(ys));
+    float4 r2 = make_float4((float)(w * c1f), (float)(w * c2f), __uint_as_float(xs),
+                            __uint_as_float(ys));
     // r3: the forward's exponential-recurrence constants G_t = 2^(-D^2 t^2), t = 1..3, and the
     // flag "recurrence allowed" (D <= FWD_REC_DMAX, render_fwd.cu MODE 2)
     const bool rec_ok = Df <= FWD_REC_DMAX;
