@@ -235,14 +235,18 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan_down(const int* __restric
 }
 
 // ---- cell starts from sorted keys --------------------------------------------------------
+// (and the empty reach of every cell, which K1b then raises for the non-empty ones)
 __global__ void k_cell_start(const uint32_t* __restrict__ keys, long long n, int total_cells,
-                             int* __restrict__ cell_start) {
+                             int* __restrict__ cell_start, int2* __restrict__ reach) {
     long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (p > n) return;
     long long prev = p == 0 ? -1 : (long long)keys[p - 1];
     long long cur = p == n ? (long long)total_cells : (long long)keys[p];
     if (cur > total_cells) cur = total_cells;
-    for (long long c = prev + 1; c <= cur; ++c) cell_start[c] = (int)p;
+    for (long long c = prev + 1; c <= cur; ++c) {
+        cell_start[c] = (int)p;
+        if (c < total_cells) reach[c] = make_int2(-1, -1);
+    }
 }
 
 // ---- K1b: records in sorted order ---------------------------------------------------------
@@ -252,14 +256,18 @@ __global__ void k_records(const T* __restrict__ alpha, const T* __restrict__ mu,
                           const T* __restrict__ color, long long n, ImgTable tab,
                           const int* __restrict__ gidx, const uint32_t* __restrict__ keys,
                           const int* __restrict__ perm, float4* __restrict__ rec,
-                          int4* __restrict__ rects, uint8_t* __restrict__ cls) {
+                          int4* __restrict__ rects, uint8_t* __restrict__ cls,
+                          int2* __restrict__ reach) {
     long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (p >= n) return;
     // the key and the permutation are independent loads; the Gaussian's nine parameters are
     // then gathered together (one round of memory latency each instead of a chain)
-    const uint32_t key = keys[p];
+    const uint32_t key = p < n ? keys[p] : 0xffffffffu;
+    const bool valid = key < (uint32_t)tab.total_cells;
+    // cell reach (Workspace::reach): the warp's lanes of one cell (sorted keys: contiguous)
+    // reduce their support rects' right / bottom edges, one atomic pair per cell and warp
+    const unsigned vm = __ballot_sync(0xffffffffu, valid);
+    if (!valid) return;
     const int pi = perm[p];
-    if (key >= (uint32_t)tab.total_cells) return;
     const long long i = gidx ? (long long)gidx[pi] : (long long)pi;
     const float mxf = ldf(mu[2 * i]), myf = ldf(mu[2 * i + 1]);
     const float sxf = ldf(sigma[2 * i]), syf = ldf(sigma[2 * i + 1]);
@@ -306,6 +314,13 @@ __global__ void k_records(const T* __restrict__ alpha, const T* __restrict__ mu,
     unsigned sys = (unsigned)sr.y0 | ((unsigned)sr.y1 << 16);
     rects[p] = make_int4((int)sxs, (int)sys, (int)xs, (int)ys);
     cls[p] = rec_ok ? 1 : 0;
+    const unsigned grp = __match_any_sync(vm, key);
+    const int mx1 = (int)__reduce_max_sync(grp, (unsigned)sr.x1);
+    const int my1 = (int)__reduce_max_sync(grp, (unsigned)sr.y1);
+    if ((threadIdx.x & 31) == __ffs(grp) - 1) {
+        atomicMax(&reach[key].x, mx1);
+        atomicMax(&reach[key].y, my1);
+    }
 }
 
 // ---- pair count ---------------------------------------------------------------------------
@@ -371,10 +386,12 @@ __global__ void k_debug_rects(const float* __restrict__ alpha, const float* __re
     rects[i] = o;
 }
 
-// Materialised per-tile candidate lists, walking the same cell spans as the render kernels and
-// keeping the candidates whose rect intersects the tile. One thread per tile (test-only).
+// Materialised per-tile candidate lists, walking the same cell spans as the render kernels (cell
+// rows trimmed by the cell reach as reach_trim does) and keeping the candidates whose rect
+// intersects the tile. One thread per tile (test-only).
 __global__ void k_debug_tile_lists(ImgTable tab, const int* __restrict__ ext,
                                    const int* __restrict__ cell_start,
+                                   const int2* __restrict__ reach,
                                    const int4* __restrict__ rects, const int* __restrict__ perm,
                                    const uint32_t* __restrict__ keys,
                                    const int* __restrict__ tile_off, int* __restrict__ counts,
@@ -394,7 +411,12 @@ __global__ void k_debug_tile_lists(ImgTable tab, const int* __restrict__ ext,
     int base = ids ? tile_off[tile] : 0;
     for (int cy = cy_lo; cy <= cy_hi; ++cy) {
         int row = im.cell_base + cy * im.ncx;
-        for (int p = cell_start[row + cx_lo]; p < cell_start[row + cx_hi + 1]; ++p) {
+        auto ok = [&](int cx) { return reach[row + cx].x >= Tx0 && reach[row + cx].y >= Ty0; };
+        int lo = cx_lo, hi = cx_hi;
+        while (lo <= cx_hi && !ok(lo)) ++lo;
+        while (hi >= lo && !ok(hi)) --hi;
+        if (lo > hi) continue;
+        for (int p = cell_start[row + lo]; p < cell_start[row + hi + 1]; ++p) {
             const int4 rc = rects[p];
             unsigned xs = (unsigned)rc.x, ys = (unsigned)rc.y;
             int x0 = xs & 0xffff, x1 = xs >> 16, y0 = ys & 0xffff, y1 = ys >> 16;
@@ -423,6 +445,7 @@ size_t binning_bytes(long long n, int total_cells, int total_tiles) {
     b += align256(sizeof(int) * (size_t)(hist + 1));            // hist
     b += align256(sizeof(int) * (size_t)(scan_blocks(scan_src) + 1));  // scan tmp
     b += align256(sizeof(int) * (size_t)(total_cells + 1));     // cell_start
+    b += align256(sizeof(int2) * (size_t)(total_cells + 1));    // cell reach
     b += align256(sizeof(float4) * REC_F4 * (size_t)n);         // records
     b += align256(sizeof(int4) * (size_t)n);                    // rect stream
     b += align256((size_t)n);                                   // record classes
@@ -446,6 +469,7 @@ void carve_workspace(void* base, long long n, int total_cells, int total_tiles, 
     ws->hist = (int*)take(sizeof(int) * (size_t)(hist + 1));
     ws->scan_tmp = (int*)take(sizeof(int) * (size_t)(scan_blocks(scan_src) + 1));
     ws->cell_start = (int*)take(sizeof(int) * (size_t)(total_cells + 1));
+    ws->reach = (int2*)take(sizeof(int2) * (size_t)(total_cells + 1));
     ws->rec = (float4*)take(sizeof(float4) * REC_F4 * (size_t)n);
     ws->rects = (int4*)take(sizeof(int4) * (size_t)n);
     ws->cls = (uint8_t*)take((size_t)n);
@@ -493,15 +517,16 @@ cudaError_t bin_gaussians_t(const T* alpha, const T* mu, const T* sigma, const T
         }
         count_launches(2);
         k_cell_start<<<grid1d(n + 1, 256), 256, 0, st>>>(kin, n, tab.total_cells,
-                                                         ws.cell_start);
+                                                         ws.cell_start, ws.reach);
         k_records<<<grid1d(n, 256), 256, 0, st>>>(alpha, mu, sigma, rho, color, n, tab, gidx,
                                                    kin, vin,
-                                                   ws.rec, ws.rects, ws.cls);
+                                                   ws.rec, ws.rects, ws.cls, ws.reach);
         *perm_out = vin;
         *keys_sorted_out = kin;
     } else {
         // no Gaussians: every cell is empty
         cudaMemsetAsync(ws.cell_start, 0, sizeof(int) * (size_t)(tab.total_cells + 1), st);
+        cudaMemsetAsync(ws.reach, 0xff, sizeof(int2) * (size_t)(tab.total_cells + 1), st);
         *perm_out = ws.vals_a;
         *keys_sorted_out = ws.keys_a;
     }
@@ -587,16 +612,16 @@ cudaError_t launch_debug_tile_lists(const ImgTable& tab, const Workspace& ws, co
     int nt = tab.total_tiles;
     if (nt <= 0) return cudaSuccess;
     if (!ids) {
-        k_debug_tile_lists<<<grid1d(nt, 64), 64, 0, st>>>(tab, ws.ext, ws.cell_start, ws.rects, perm,
+        k_debug_tile_lists<<<grid1d(nt, 64), 64, 0, st>>>(tab, ws.ext, ws.cell_start, ws.reach, ws.rects, perm,
                                                           keys_sorted, nullptr, counts, nullptr,
                                                           nullptr);
     } else {
-        k_debug_tile_lists<<<grid1d(nt, 64), 64, 0, st>>>(tab, ws.ext, ws.cell_start, ws.rects, perm,
+        k_debug_tile_lists<<<grid1d(nt, 64), 64, 0, st>>>(tab, ws.ext, ws.cell_start, ws.reach, ws.rects, perm,
                                                           keys_sorted, nullptr, ws.tile_off,
                                                           nullptr, nullptr);
         cudaError_t e = exclusive_scan_i32(ws.tile_off, ws.tile_off, nt, ws.scan_tmp, st);
         if (e != cudaSuccess) return e;
-        k_debug_tile_lists<<<grid1d(nt, 64), 64, 0, st>>>(tab, ws.ext, ws.cell_start, ws.rects, perm,
+        k_debug_tile_lists<<<grid1d(nt, 64), 64, 0, st>>>(tab, ws.ext, ws.cell_start, ws.reach, ws.rects, perm,
                                                           keys_sorted, ws.tile_off, counts, ids,
                                                           cells);
     }

@@ -443,7 +443,45 @@ struct Workspace {
     int* tile_off;           // debug tile lists: [total_tiles + 1]
     int* ext;                // [2 * MAX_IMAGES]: per image max unclipped support-rect width,
                              // height over the binned Gaussians (tile candidate query, K1)
+    int2* reach;             // [total_cells]: per cell the largest clipped support-rect right
+                             // and bottom edge of its Gaussians ({-1, -1}: empty cell; K1b)
 };
+
+// Trims one cell row [cx_lo, cx_hi] of a tile's candidate query to the cells whose reach
+// (Workspace::reach) meets the tile's first column X0 and row Y0: the cells outside
+// [lo, hi] hold no Gaussian whose support rect reaches the tile, so only candidates the exact
+// rect test would reject are skipped. Warp-collective (every lane, uniform arguments); returns
+// false when no cell of the row can reach the tile.
+__device__ __forceinline__ bool reach_trim(const int2* __restrict__ reach, int row, int cx_lo,
+                                           int cx_hi, int X0, int Y0, int lane, int* lo,
+                                           int* hi) {
+    auto ok = [&](int c) {
+        const int2 r = __ldg(reach + row + c);
+        return r.x >= X0 && r.y >= Y0;
+    };
+    if (cx_hi - cx_lo < 32) {                                 // one load per lane
+        const int c = cx_lo + lane;
+        const unsigned m = __ballot_sync(0xffffffffu, c <= cx_hi && ok(c));
+        if (m == 0u) return false;
+        *lo = cx_lo + __ffs(m) - 1;
+        *hi = cx_lo + 31 - __clz(m);
+        return true;
+    }
+    int l = -1;
+    for (int c0 = cx_lo; c0 <= cx_hi && l < 0; c0 += 32) {
+        const unsigned m = __ballot_sync(0xffffffffu, c0 + lane <= cx_hi && ok(c0 + lane));
+        if (m) l = c0 + __ffs(m) - 1;
+    }
+    if (l < 0) return false;
+    int h = l;
+    for (int c0 = cx_hi; c0 > l; c0 -= 32) {
+        const unsigned m = __ballot_sync(0xffffffffu, c0 - lane > l && ok(c0 - lane));
+        if (m) { h = c0 - (__ffs(m) - 1); break; }
+    }
+    *lo = l;
+    *hi = h;
+    return true;
+}
 
 // Tile candidate query over the cell grid (binning.cu): the Gaussians whose unclipped support
 // origin lies in [T0 - ext + 1, T1]; ext >= 1 keeps the cell range non-empty and in bounds.

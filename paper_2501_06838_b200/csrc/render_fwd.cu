@@ -8,10 +8,11 @@
 // Every warp covers the whole tile -- lane l owns the 2 x 8 block at columns Tx0 + 4 (l & 3) +
 // {0..3, 16..19} and rows Ty0 + 2 (l >> 2) + {0, 1} -- for its own share of the tile's Gaussians;
 // the partial images are summed in warp order.
-//   * candidates: the tile's contiguous cell-row spans (binning.cu), walked in batches of 32
-//     (batch i to warp i mod W and, under split-K, to cluster CTA (i / W) mod KS) and filtered
-//     from the 16-B rect stream + the record class byte: keep if the support rect (R21) meets
-//     the tile; the filter also decides the Gaussian's evaluation PATH (below).
+//   * candidates: the tile's cell-row spans (binning.cu), each trimmed to the cells whose reach
+//     meets the tile, concatenated into one stream (FwdStream) and walked in rounds of 32 W
+//     positions (round i to cluster CTA i mod KS under split-K; warp w takes positions w, w + W,
+//     ...), filtered from the 16-B rect stream + the record class byte: keep if the support
+//     rect (R21) meets the tile; the filter also decides the Gaussian's evaluation PATH (below).
 //   * staging: each lane whose candidate is kept copies its 64-B record with four 16-B cp.async
 //     into the warp's own double buffer in shared memory -- the dominant path (recurrence over
 //     both column halves / the unmasked small tile) from the buffer's front, every other path
@@ -34,6 +35,9 @@
 
 #include "gsr_internal.cuh"
 
+#ifndef GSR_CELL_REACH
+#define GSR_CELL_REACH 1          // trim the tiles' cell rows by the cell reach (A/B)
+#endif
 #ifndef GSR_FWD_SCAN_D
 #define GSR_FWD_SCAN_D 2          // candidate batches per warp in the scan pipeline (>= 2)
 #endif
@@ -59,26 +63,84 @@ __device__ __forceinline__ float ld_dsmem_f(const float* local_addr, uint32_t ra
     return v;
 }
 
-// candidate spans of a tile: cell rows cy..cy_hi, columns cx_lo..cx_hi, in batches of <= 32
-struct FwdProducer {
-    int cy, cy_hi, row_stride, row0, cx_lo, cx_hi, cur, end;
+// Candidate stream of a tile: the cell-row spans of up to 32 rows at a time
+// (a chunk), each trimmed by the cell reach, concatenated into one sequence of positions. Warp 0
+// builds the chunk table (row starts + exclusive prefix of the row lengths) in shared memory
+// for the CTA. The positions are taken in rounds of 32 W per CTA (split-K: round i to cluster
+// CTA i mod KS), and inside a round warp w takes positions w, w + W, w + 2 W, ...: the kept
+// candidates cluster along the sequence (the cells nearest the tile), and the interleave gives
+// every warp an even share of each cluster (whole batches per warp left one warp waiting at the
+// epilogue for up to 20% of the samples at C4), with a fixed, deterministic assignment.
+struct FwdChunk {
+    int pre[33];             // exclusive prefix of the rows' lengths; pre[32] = total
+    int st[32];              // first record of each row
+    int cy_next;             // first cell row after the chunk
+};
+struct FwdStream {
+    int cy_hi, row0, row_stride, cx_lo, cx_hi, X0, Y0;
     const int* cs;
-    __device__ int raw_next(int* start) {
-        while (cur >= end) {
-            if (++cy > cy_hi) return 0;
-            int row = row0 + cy * row_stride;
-            cur = cs[row + cx_lo];
-            end = cs[row + cx_hi + 1];
+    const int2* reach;
+    // warp 0: the chunk from cell row cy on with at least one candidate (or none left: total 0)
+    __device__ __noinline__ void build(FwdChunk& ch, int cy, int lane) const {
+        while (true) {
+            const int nrows = cy <= cy_hi ? min(32, cy_hi - cy + 1) : 0;
+            int mylo = 0, myhi = -1;
+            if (!GSR_CELL_REACH) {
+                mylo = cx_lo;
+                myhi = cx_hi;
+            } else if (cx_hi - cx_lo < 32) {
+                for (int i0 = 0; i0 < nrows; i0 += 4) {      // 4 rows' reach loads in flight
+                    bool okv[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int c = cx_lo + lane;
+                        okv[u] = false;
+                        if (i0 + u < nrows && c <= cx_hi) {
+                            const int2 r = __ldg(reach + row0 + (cy + i0 + u) * row_stride + c);
+                            okv[u] = r.x >= X0 && r.y >= Y0;
+                        }
+                    }
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const unsigned m = __ballot_sync(0xffffffffu, okv[u]);
+                        if (lane == i0 + u && m) {
+                            mylo = cx_lo + __ffs(m) - 1;
+                            myhi = cx_lo + 31 - __clz(m);
+                        }
+                    }
+                }
+            } else {
+                for (int i = 0; i < nrows; ++i) {
+                    int lo, hi;
+                    const bool any = reach_trim(reach, row0 + (cy + i) * row_stride, cx_lo,
+                                                cx_hi, X0, Y0, lane, &lo, &hi);
+                    if (any && lane == i) { mylo = lo; myhi = hi; }
+                }
+            }
+            int s0 = 0, len = 0;
+            if (lane < nrows && myhi >= mylo) {
+                const int row = row0 + (cy + lane) * row_stride;
+                s0 = cs[row + mylo];
+                len = cs[row + myhi + 1] - s0;
+            }
+            int inc = len;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int t = __shfl_up_sync(0xffffffffu, inc, o);
+                if (lane >= o) inc += t;
+            }
+            cy += nrows;
+            const int total = __shfl_sync(0xffffffffu, inc, 31);
+            if (total > 0 || nrows == 0) {
+                ch.st[lane] = s0;
+                ch.pre[lane + 1] = inc;
+                if (lane == 0) {
+                    ch.pre[0] = 0;
+                    ch.cy_next = cy;
+                }
+                return;
+            }
         }
-        int n = min(32, end - cur);
-        *start = cur;
-        cur += n;
-        return n;
-    }
-    __device__ int next(int* start, int skip) {   // drop `skip` batches, then take one
-        for (int k = 0; k < skip; ++k)
-            if (raw_next(start) == 0) return 0;
-        return raw_next(start);
     }
 };
 
@@ -256,9 +318,6 @@ constexpr int kFrontUnroll = GSR_FWD_FRONT_UNROLL;
 #ifndef GSR_FWD_CUTMASK
 #define GSR_FWD_CUTMASK 1         // mask only the window edges that cut the support box
 #endif
-#ifndef GSR_FWD_SNAKE
-#define GSR_FWD_SNAKE 1           // snake order of the candidate batches over the warps
-#endif
 #ifndef GSR_FWD_HALVES
 #define GSR_FWD_HALVES 1          // skip the column half a Gaussian's support misses
 #endif
@@ -270,7 +329,10 @@ struct FwdSmem2 {
         float stage[CFG::TH][CFG::TW * 3];                 // HWC tile (epilogue)
     };
     uint8_t path[CFG::WARPS][2][FWD_BUF];
-    float2 tot[CFG::WARPS][FwdAcc<CFG>::NACC][32];         // per-warp images (epilogue)
+    struct PerWarp {
+        float2 tot[FwdAcc<CFG>::NACC][32];                 // the warp's image (epilogue)
+    } wp[CFG::WARPS];
+    FwdChunk chunk;                                        // candidate stream table
 };
 
 // Stores the tile from the HWC staging area (every thread), with the fused L1 loss.
@@ -330,9 +392,9 @@ __device__ __forceinline__ void fwd_epilogue(FwdSmem2<CFG>& sm, const DevImg& im
     __syncthreads();                                   // every warp's image + no record reads
     for (int i = threadIdx.x; i < NACC * 32; i += (CFG::WARPS * 32)) {
         const int a = i >> 5, l = i & 31;
-        float2 v = sm.tot[0][a][l];
+        float2 v = sm.wp[0].tot[a][l];
 #pragma unroll
-        for (int q = 1; q < CFG::WARPS; ++q) v = __fadd2_rn(v, sm.tot[q][a][l]);
+        for (int q = 1; q < CFG::WARPS; ++q) v = __fadd2_rn(v, sm.wp[q].tot[a][l]);
         const int xl = lane_x0<STRIP>(l), yl = ROWS * (l >> 2);
         const int k = a % 3;
         if constexpr (ROWS == 2) {                     // pair = (row 0, row 1) of column slot j
@@ -371,6 +433,7 @@ __global__ void __launch_bounds__(CFG::WARPS * 32, 16 / CFG::WARPS) k_render_fwd
                                                               const uint8_t* __restrict__ cls,
                                                               const int* __restrict__ cell_start,
                                                               const int* __restrict__ ext,
+                                                              const int2* __restrict__ reach,
                                                               float* __restrict__ out,
                                                               const float* __restrict__ gt,
                                                               double* __restrict__ loss_acc) {
@@ -407,43 +470,61 @@ __global__ void __launch_bounds__(CFG::WARPS * 32, 16 / CFG::WARPS) k_render_fwd
     for (int r = 0; r < FWD_ROWS; ++r) yi[r] = yl0 + r;
     const float yf0 = (float)yl0;
 
-    FwdProducer prod;
-    prod.cs = cell_start;
-    prod.row0 = im.cell_base;
-    prod.row_stride = im.ncx;
-    prod.cx_lo = (Tx0 - query_ext(ext, kimg, 0) + 1 + im.offx) / CELL;
-    prod.cx_hi = min(im.ncx - 1, (fx1 + im.offx) / CELL);
-    prod.cy = (Ty0 - im.row_begin - query_ext(ext, kimg, 1) + 1 + im.offy) / CELL - 1;
-    prod.cy_hi = min(im.ncy - 1, (fy1 - im.row_begin + im.offy) / CELL);
-    prod.cur = prod.end = 0;
-    const unsigned lt = (1u << lane) - 1u;
     const bool live = fy0 <= fy1;
+    FwdStream vs;
+    vs.cs = cell_start;
+    vs.reach = reach;
+    vs.row0 = im.cell_base;
+    vs.row_stride = im.ncx;
+    vs.cx_lo = (Tx0 - query_ext(ext, kimg, 0) + 1 + im.offx) / CELL;
+    vs.cx_hi = min(im.ncx - 1, (fx1 + im.offx) / CELL);
+    vs.cy_hi = min(im.ncy - 1, (fy1 - im.row_begin + im.offy) / CELL);
+    vs.X0 = fx0;
+    vs.Y0 = fy0;
+    const int cy_first = (Ty0 - im.row_begin - query_ext(ext, kimg, 1) + 1 + im.offy) / CELL;
+    if (warp == 0) vs.build(sm.chunk, live ? cy_first : vs.cy_hi + 1, lane);
+    __syncthreads();
+    int ctotal = sm.chunk.pre[32], r0 = 0, round = 0;
+    const unsigned lt = (1u << lane) - 1u;
     // candidate batches in flight: batch 0 is filtered while batches 1 .. SD-1 load
     constexpr int SD = GSR_FWD_SCAN_D;
-    int nb[SD], sb[SD];
+    int nb[SD], sb[SD];                 // candidates in the batch, the lane's candidate position
     int4 rb[SD];
     int cb[SD];
-    int first = 1;
-    // batch order over the P = KS * W parts: rounds of P batches; part p takes position p of
-    // every round, or (large tiles, GSR_FWD_SNAKE) position p in even rounds and P - 1 - p in
-    // odd ones, so that a trend of the kept counts along the candidate order spreads evenly
-    // over the warps (C5 -1.2%; the small tiles: C2 +5%, kept round-robin)
-    constexpr int NPARTS = KS * CFG::WARPS;
-    constexpr bool SNAKE = GSR_FWD_SNAKE && FWD_ROWS == 2;
-    const int mypart = krank * CFG::WARPS + warp;
-    int round = 0;
+    // positions: rounds of 32 W per CTA (round i to cluster CTA i mod KS), warp w takes
+    // positions w, w + W, ... of its CTA's rounds (FwdStream)
     auto fetch = [&](int j) {
-        const int skip = first ? mypart
-                               : (!SNAKE ? NPARTS - 1
-                                         : ((round & 1) ? 2 * mypart : 2 * NPARTS - 2 - 2 * mypart));
-        if (!first) ++round;
-        nb[j] = live ? prod.next(&sb[j], skip) : 0;
-        first = 0;
+        nb[j] = 0;
+        sb[j] = 0;
+        while (ctotal > 0) {
+            const int base = 32 * CFG::WARPS * (round * KS + krank);
+            if (base + warp < ctotal) {
+                ++round;
+                nb[j] = min(32, (ctotal - base - warp + CFG::WARPS - 1) / CFG::WARPS);
+                while (base >= sm.chunk.pre[r0 + 1]) ++r0;
+                const int v = base + CFG::WARPS * lane + warp;
+                if (v < ctotal) {
+                    int r = r0;
+                    while (v >= sm.chunk.pre[r + 1]) ++r;
+                    sb[j] = sm.chunk.st[r] + (v - sm.chunk.pre[r]);
+                }
+                break;
+            }
+            // chunk exhausted by this warp: once every warp is here, warp 0 builds the next one
+            // (every warp walks the same chunk sequence, so the barriers match)
+            if (sm.chunk.cy_next > vs.cy_hi) break;
+            __syncthreads();
+            if (warp == 0) vs.build(sm.chunk, sm.chunk.cy_next, lane);
+            __syncthreads();
+            ctotal = sm.chunk.pre[32];
+            r0 = 0;
+            round = 0;
+        }
         rb[j] = make_int4(0, 0, 0, 0);
         cb[j] = 0;
         if (lane < nb[j]) {
-            rb[j] = __ldg(rects + sb[j] + lane);
-            cb[j] = __ldg(cls + sb[j] + lane);
+            rb[j] = __ldg(rects + sb[j]);
+            cb[j] = __ldg(cls + sb[j]);
         }
     };
 
@@ -589,7 +670,7 @@ __global__ void __launch_bounds__(CFG::WARPS * 32, 16 / CFG::WARPS) k_render_fwd
                 const int slot = front ? cnt + __popc(mf & lt)
                                        : FWD_BUF - 1 - (cntb + __popc(mb & lt));
                 sm.path[warp][b][slot] = (uint8_t)pth;
-                const float4* src = rec + (long long)REC_F4 * (sb[0] + lane);
+                const float4* src = rec + (long long)REC_F4 * sb[0];
                 float4* dst = &sm.rec[warp][b][REC_F4 * slot];
 #pragma unroll
                 for (int q = 0; q < REC_F4; ++q) cp_async16(dst + q, src + q);
@@ -601,7 +682,7 @@ __global__ void __launch_bounds__(CFG::WARPS * 32, 16 / CFG::WARPS) k_render_fwd
             if (keep) {
                 const int slot = cnt + __popc(m & lt);
                 sm.path[warp][b][slot] = (uint8_t)pth;
-                const float4* src = rec + (long long)REC_F4 * (sb[0] + lane);
+                const float4* src = rec + (long long)REC_F4 * sb[0];
                 float4* dst = &sm.rec[warp][b][REC_F4 * slot];
 #pragma unroll
                 for (int q = 0; q < REC_F4; ++q) cp_async16(dst + q, src + q);
@@ -638,7 +719,7 @@ __global__ void __launch_bounds__(CFG::WARPS * 32, 16 / CFG::WARPS) k_render_fwd
         if (end && pend < 0) break;
     }
 #pragma unroll
-    for (int a = 0; a < NACC; ++a) sm.tot[warp][a][lane] = acc[a];
+    for (int a = 0; a < NACC; ++a) sm.wp[warp].tot[a][lane] = acc[a];
     fwd_epilogue<KS, LOSS, CFG>(sm, im, Tx0, Ty0, krank, out, gt, loss_acc);
 }
 
@@ -684,7 +765,8 @@ cudaError_t launch_ks3(const ImgTable& tab, const Workspace& ws, float* out, con
     cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, k_render_fwd2<KS, LOSS, CFG>, tab, (const float4*)ws.rec,
                               (const int4*)ws.rects, (const uint8_t*)ws.cls,
-                              (const int*)ws.cell_start, (const int*)ws.ext, out, gt, loss_acc);
+                              (const int*)ws.cell_start, (const int*)ws.ext,
+                              (const int2*)ws.reach, out, gt, loss_acc);
 }
 
 template <int KS, bool LOSS>
