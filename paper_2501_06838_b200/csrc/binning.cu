@@ -89,10 +89,17 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_hist(const uint32_t* __restri
     __shared__ int cnt[256];
     for (int d = threadIdx.x; d < 256; d += RS_THREADS) cnt[d] = 0;
     __syncthreads();
-    long long b0 = (long long)blockIdx.x * RS_BLOCK;
-    long long b1 = min(b0 + RS_BLOCK, n);
-    for (long long i = b0 + threadIdx.x; i < b1; i += RS_THREADS)
-        atomicAdd(&cnt[(keys[i] >> shift) & 255u], 1);
+    const long long b0 = (long long)blockIdx.x * RS_BLOCK;
+    constexpr int NI = RS_BLOCK / RS_THREADS;
+    uint32_t k[NI];
+#pragma unroll
+    for (int c = 0; c < NI; ++c) {                  // loads together, then the counts
+        const long long i = b0 + c * RS_THREADS + threadIdx.x;
+        k[c] = i < n ? keys[i] : 0xffffffffu;
+    }
+#pragma unroll
+    for (int c = 0; c < NI; ++c)
+        if (b0 + c * RS_THREADS + threadIdx.x < n) atomicAdd(&cnt[(k[c] >> shift) & 255u], 1);
     __syncthreads();
     for (int d = threadIdx.x; d < 256; d += RS_THREADS)
         hist[(long long)d * nblocks + blockIdx.x] = cnt[d];
@@ -108,15 +115,26 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_scatter(
     __syncthreads();
     const long long seg = (long long)blockIdx.x * RS_BLOCK + (long long)warp * RS_SEG;
     const unsigned lt = (1u << lane) - 1u;
+    // the warp's RS_SEG keys and values, loaded together (one round of memory latency instead
+    // of one per 32 items: small sorts are latency-bound, C1 has 18 blocks)
+    constexpr int NI = RS_SEG / 32;
+    uint32_t key[NI];
+    int val[NI];
+#pragma unroll
+    for (int c = 0; c < NI; ++c) {
+        const long long i = seg + 32 * c + lane;
+        key[c] = i < n ? keys_in[i] : 0u;
+        val[c] = i < n ? vals_in[i] : 0;
+    }
     // pass 1: per-warp digit counts
-    for (int c = 0; c < RS_SEG; c += 32) {
-        long long i = seg + c + lane;
-        bool valid = i < n;
-        unsigned vm = __ballot_sync(0xffffffffu, valid);
+#pragma unroll
+    for (int c = 0; c < NI; ++c) {
+        const bool valid = seg + 32 * c + lane < n;
+        const unsigned vm = __ballot_sync(0xffffffffu, valid);
         if (vm == 0) break;
         if (valid) {
-            unsigned d = (keys_in[i] >> shift) & 255u;
-            unsigned peers = __match_any_sync(vm, d);
+            const unsigned d = (key[c] >> shift) & 255u;
+            const unsigned peers = __match_any_sync(vm, d);
             if ((peers & lt) == 0) wcnt[warp][d] += __popc(peers);
         }
         __syncwarp();
@@ -133,24 +151,23 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_scatter(
     }
     __syncthreads();
     // pass 2: stable ranks and scatter
-    for (int c = 0; c < RS_SEG; c += 32) {
-        long long i = seg + c + lane;
-        bool valid = i < n;
-        unsigned vm = __ballot_sync(0xffffffffu, valid);
+#pragma unroll
+    for (int c = 0; c < NI; ++c) {
+        const bool valid = seg + 32 * c + lane < n;
+        const unsigned vm = __ballot_sync(0xffffffffu, valid);
         if (vm == 0) break;
-        uint32_t key = 0; int val = 0; unsigned d = 0, peers = 0; int pos = 0;
+        unsigned d = 0, peers = 0;
+        int pos = 0;
         if (valid) {
-            key = keys_in[i];
-            val = vals_in[i];
-            d = (key >> shift) & 255u;
+            d = (key[c] >> shift) & 255u;
             peers = __match_any_sync(vm, d);
             pos = wcnt[warp][d] + __popc(peers & lt);
         }
         __syncwarp();
         if (valid) {
             if ((peers & lt) == 0) wcnt[warp][d] += __popc(peers);
-            keys_out[pos] = key;
-            vals_out[pos] = val;
+            keys_out[pos] = key[c];
+            vals_out[pos] = val[c];
         }
         __syncwarp();
     }
@@ -231,6 +248,37 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan_down(const int* __restric
     for (int j = 0; j < SCAN_ITEMS; ++j) {
         if (base + j < n) out[base + j] = run;
         run += v[j];
+    }
+}
+
+// single block, whole array: sequential SCAN_BLOCK chunks with a carry (small scans: one
+// launch instead of three)
+__global__ void __launch_bounds__(SCAN_THREADS) k_scan_single(const int* __restrict__ in,
+                                                              long long n,
+                                                              int* __restrict__ out) {
+    __shared__ int sh[32];
+    __shared__ int last;
+    int carry = 0;
+    for (long long c = 0; c < n; c += SCAN_BLOCK) {
+        const long long base = c + (long long)threadIdx.x * SCAN_ITEMS;
+        int v[SCAN_ITEMS];
+        int t = 0;
+#pragma unroll
+        for (int j = 0; j < SCAN_ITEMS; ++j) {
+            v[j] = (base + j < n) ? in[base + j] : 0;
+            t += v[j];
+        }
+        const int incl = block_incl_scan(t, sh);
+        int run = carry + incl - t;
+#pragma unroll
+        for (int j = 0; j < SCAN_ITEMS; ++j) {
+            if (base + j < n) out[base + j] = run;
+            run += v[j];
+        }
+        if (threadIdx.x == SCAN_THREADS - 1) last = incl;
+        __syncthreads();
+        carry += last;
+        __syncthreads();
     }
 }
 
@@ -482,6 +530,11 @@ void carve_workspace(void* base, long long n, int total_cells, int total_tiles, 
 cudaError_t exclusive_scan_i32(const int* in, int* out, long long n, int* tmp, cudaStream_t st) {
     if (n <= 0) return cudaSuccess;
     long long nb = scan_blocks(n);
+    if (nb <= 4) {                                 // in-place safe: each chunk reads before it writes
+        count_launches(1);
+        k_scan_single<<<1, SCAN_THREADS, 0, st>>>(in, n, out);
+        return cudaGetLastError();
+    }
     count_launches(3);
     k_scan_reduce<<<(unsigned)nb, SCAN_THREADS, 0, st>>>(in, n, tmp);
     k_scan_sums<<<1, SCAN_THREADS, 0, st>>>(tmp, nb);

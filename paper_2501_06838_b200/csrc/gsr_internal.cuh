@@ -483,6 +483,93 @@ __device__ __forceinline__ bool reach_trim(const int2* __restrict__ reach, int r
     return true;
 }
 
+// Candidate stream of a forward tile: the cell-row spans of up to 32 rows at a time (a chunk),
+// each trimmed to the cells whose reach meets the tile (GSR_CELL_REACH), concatenated into one
+// sequence of positions, so the kernel walks it in full batches of 32 across row ends (the
+// backward's scan on the same stream measured +1.6% at C5). Warp 0 builds the chunk table (row starts + exclusive prefix of the row
+// lengths) in shared memory for the CTA; every warp walks the same chunk sequence.
+#ifndef GSR_CELL_REACH
+#define GSR_CELL_REACH 1          // trim the tiles' cell rows by the cell reach (A/B)
+#endif
+struct CandChunk {
+    int pre[33];             // exclusive prefix of the rows' lengths; pre[32] = total
+    int st[32];              // first record of each row
+    int cy_next;             // first cell row after the chunk
+};
+struct CandStream {
+    int cy_hi, row0, row_stride, cx_lo, cx_hi, X0, Y0;
+    const int* cs;
+    const int2* reach;
+    // warp 0: the chunk from cell row cy on with at least one candidate (or none left: total 0)
+    __device__ __noinline__ void build(CandChunk& ch, int cy, int lane) const {
+        while (true) {
+            const int nrows = cy <= cy_hi ? min(32, cy_hi - cy + 1) : 0;
+            int mylo = 0, myhi = -1;
+            if (!GSR_CELL_REACH) {
+                mylo = cx_lo;
+                myhi = cx_hi;
+            } else if (cx_hi - cx_lo < 32) {
+                for (int i0 = 0; i0 < nrows; i0 += 4) {      // 4 rows' reach loads in flight
+                    bool okv[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int c = cx_lo + lane;
+                        okv[u] = false;
+                        if (i0 + u < nrows && c <= cx_hi) {
+                            const int2 r = __ldg(reach + row0 + (cy + i0 + u) * row_stride + c);
+                            okv[u] = r.x >= X0 && r.y >= Y0;
+                        }
+                    }
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const unsigned m = __ballot_sync(0xffffffffu, okv[u]);
+                        if (lane == i0 + u && m) {
+                            mylo = cx_lo + __ffs(m) - 1;
+                            myhi = cx_lo + 31 - __clz(m);
+                        }
+                    }
+                }
+            } else {
+                for (int i = 0; i < nrows; ++i) {
+                    int lo, hi;
+                    const bool any = reach_trim(reach, row0 + (cy + i) * row_stride, cx_lo,
+                                                cx_hi, X0, Y0, lane, &lo, &hi);
+                    if (any && lane == i) { mylo = lo; myhi = hi; }
+                }
+            }
+            int s0 = 0, len = 0;
+            if (lane < nrows && myhi >= mylo) {
+                const int row = row0 + (cy + lane) * row_stride;
+                s0 = cs[row + mylo];
+                len = cs[row + myhi + 1] - s0;
+            }
+            int inc = len;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int t = __shfl_up_sync(0xffffffffu, inc, o);
+                if (lane >= o) inc += t;
+            }
+            cy += nrows;
+            const int total = __shfl_sync(0xffffffffu, inc, 31);
+            if (total > 0 || nrows == 0) {
+                ch.st[lane] = s0;
+                ch.pre[lane + 1] = inc;
+                if (lane == 0) {
+                    ch.pre[0] = 0;
+                    ch.cy_next = cy;
+                }
+                return;
+            }
+        }
+    }
+};
+
+// position v of the chunk -> record index (r: a chunk row at or before v's row)
+__device__ __forceinline__ int cand_index(const CandChunk& ch, int v, int r) {
+    while (v >= ch.pre[r + 1]) ++r;
+    return ch.st[r] + (v - ch.pre[r]);
+}
+
 // Tile candidate query over the cell grid (binning.cu): the Gaussians whose unclipped support
 // origin lies in [T0 - ext + 1, T1]; ext >= 1 keeps the cell range non-empty and in bounds.
 __device__ __forceinline__ int query_ext(const int* ext, int k, int axis) {

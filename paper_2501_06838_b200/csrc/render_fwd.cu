@@ -9,7 +9,7 @@
 // {0..3, 16..19} and rows Ty0 + 2 (l >> 2) + {0, 1} -- for its own share of the tile's Gaussians;
 // the partial images are summed in warp order.
 //   * candidates: the tile's cell-row spans (binning.cu), each trimmed to the cells whose reach
-//     meets the tile, concatenated into one stream (FwdStream) and walked in rounds of 32 W
+//     meets the tile, concatenated into one stream (CandStream) and walked in rounds of 32 W
 //     positions (round i to cluster CTA i mod KS under split-K; warp w takes positions w, w + W,
 //     ...), filtered from the 16-B rect stream + the record class byte: keep if the support
 //     rect (R21) meets the tile; the filter also decides the Gaussian's evaluation PATH (below).
@@ -35,9 +35,6 @@
 
 #include "gsr_internal.cuh"
 
-#ifndef GSR_CELL_REACH
-#define GSR_CELL_REACH 1          // trim the tiles' cell rows by the cell reach (A/B)
-#endif
 #ifndef GSR_FWD_SCAN_D
 #define GSR_FWD_SCAN_D 2          // candidate batches per warp in the scan pipeline (>= 2)
 #endif
@@ -62,87 +59,6 @@ __device__ __forceinline__ float ld_dsmem_f(const float* local_addr, uint32_t ra
     asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(ra) : "memory");
     return v;
 }
-
-// Candidate stream of a tile: the cell-row spans of up to 32 rows at a time
-// (a chunk), each trimmed by the cell reach, concatenated into one sequence of positions. Warp 0
-// builds the chunk table (row starts + exclusive prefix of the row lengths) in shared memory
-// for the CTA. The positions are taken in rounds of 32 W per CTA (split-K: round i to cluster
-// CTA i mod KS), and inside a round warp w takes positions w, w + W, w + 2 W, ...: the kept
-// candidates cluster along the sequence (the cells nearest the tile), and the interleave gives
-// every warp an even share of each cluster (whole batches per warp left one warp waiting at the
-// epilogue for up to 20% of the samples at C4), with a fixed, deterministic assignment.
-struct FwdChunk {
-    int pre[33];             // exclusive prefix of the rows' lengths; pre[32] = total
-    int st[32];              // first record of each row
-    int cy_next;             // first cell row after the chunk
-};
-struct FwdStream {
-    int cy_hi, row0, row_stride, cx_lo, cx_hi, X0, Y0;
-    const int* cs;
-    const int2* reach;
-    // warp 0: the chunk from cell row cy on with at least one candidate (or none left: total 0)
-    __device__ __noinline__ void build(FwdChunk& ch, int cy, int lane) const {
-        while (true) {
-            const int nrows = cy <= cy_hi ? min(32, cy_hi - cy + 1) : 0;
-            int mylo = 0, myhi = -1;
-            if (!GSR_CELL_REACH) {
-                mylo = cx_lo;
-                myhi = cx_hi;
-            } else if (cx_hi - cx_lo < 32) {
-                for (int i0 = 0; i0 < nrows; i0 += 4) {      // 4 rows' reach loads in flight
-                    bool okv[4];
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        const int c = cx_lo + lane;
-                        okv[u] = false;
-                        if (i0 + u < nrows && c <= cx_hi) {
-                            const int2 r = __ldg(reach + row0 + (cy + i0 + u) * row_stride + c);
-                            okv[u] = r.x >= X0 && r.y >= Y0;
-                        }
-                    }
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        const unsigned m = __ballot_sync(0xffffffffu, okv[u]);
-                        if (lane == i0 + u && m) {
-                            mylo = cx_lo + __ffs(m) - 1;
-                            myhi = cx_lo + 31 - __clz(m);
-                        }
-                    }
-                }
-            } else {
-                for (int i = 0; i < nrows; ++i) {
-                    int lo, hi;
-                    const bool any = reach_trim(reach, row0 + (cy + i) * row_stride, cx_lo,
-                                                cx_hi, X0, Y0, lane, &lo, &hi);
-                    if (any && lane == i) { mylo = lo; myhi = hi; }
-                }
-            }
-            int s0 = 0, len = 0;
-            if (lane < nrows && myhi >= mylo) {
-                const int row = row0 + (cy + lane) * row_stride;
-                s0 = cs[row + mylo];
-                len = cs[row + myhi + 1] - s0;
-            }
-            int inc = len;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const int t = __shfl_up_sync(0xffffffffu, inc, o);
-                if (lane >= o) inc += t;
-            }
-            cy += nrows;
-            const int total = __shfl_sync(0xffffffffu, inc, 31);
-            if (total > 0 || nrows == 0) {
-                ch.st[lane] = s0;
-                ch.pre[lane + 1] = inc;
-                if (lane == 0) {
-                    ch.pre[0] = 0;
-                    ch.cy_next = cy;
-                }
-                return;
-            }
-        }
-    }
-};
 
 // Column halves (large configuration): lane l owns columns 4 (l & 3) + t and 16 + 4 (l & 3) + t
 // (t = 0..3) of its two rows, so anchor h = 0 of every lane lies in the tile's left 16 columns
@@ -332,7 +248,7 @@ struct FwdSmem2 {
     struct PerWarp {
         float2 tot[FwdAcc<CFG>::NACC][32];                 // the warp's image (epilogue)
     } wp[CFG::WARPS];
-    FwdChunk chunk;                                        // candidate stream table
+    CandChunk chunk;                                        // candidate stream table
 };
 
 // Stores the tile from the HWC staging area (every thread), with the fused L1 loss.
@@ -471,7 +387,7 @@ __global__ void __launch_bounds__(CFG::WARPS * 32, 16 / CFG::WARPS) k_render_fwd
     const float yf0 = (float)yl0;
 
     const bool live = fy0 <= fy1;
-    FwdStream vs;
+    CandStream vs;
     vs.cs = cell_start;
     vs.reach = reach;
     vs.row0 = im.cell_base;
@@ -492,7 +408,7 @@ __global__ void __launch_bounds__(CFG::WARPS * 32, 16 / CFG::WARPS) k_render_fwd
     int4 rb[SD];
     int cb[SD];
     // positions: rounds of 32 W per CTA (round i to cluster CTA i mod KS), warp w takes
-    // positions w, w + W, ... of its CTA's rounds (FwdStream)
+    // positions w, w + W, ... of its CTA's rounds (CandStream)
     auto fetch = [&](int j) {
         nb[j] = 0;
         sb[j] = 0;
@@ -503,11 +419,7 @@ __global__ void __launch_bounds__(CFG::WARPS * 32, 16 / CFG::WARPS) k_render_fwd
                 nb[j] = min(32, (ctotal - base - warp + CFG::WARPS - 1) / CFG::WARPS);
                 while (base >= sm.chunk.pre[r0 + 1]) ++r0;
                 const int v = base + CFG::WARPS * lane + warp;
-                if (v < ctotal) {
-                    int r = r0;
-                    while (v >= sm.chunk.pre[r + 1]) ++r;
-                    sb[j] = sm.chunk.st[r] + (v - sm.chunk.pre[r]);
-                }
+                if (v < ctotal) sb[j] = cand_index(sm.chunk, v, r0);
                 break;
             }
             // chunk exhausted by this warp: once every warp is here, warp 0 builds the next one
