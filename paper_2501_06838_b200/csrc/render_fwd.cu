@@ -9,10 +9,10 @@
 // {0..3, 16..19} and rows Ty0 + 2 (l >> 2) + {0, 1} -- for its own share of the tile's Gaussians;
 // the partial images are summed in warp order.
 //   * candidates: the tile's cell-row spans (binning.cu), each trimmed to the cells whose reach
-//     meets the tile, concatenated into one stream (CandStream) and walked in rounds of 32 W
-//     positions (round i to cluster CTA i mod KS under split-K; warp w takes positions w, w + W,
-//     ...), filtered from the 16-B rect stream + the record class byte: keep if the support
-//     rect (R21) meets the tile; the filter also decides the Gaussian's evaluation PATH (below).
+//     meets the tile, concatenated into one stream (CandStream) and interleaved over the KS W
+//     warps of the (split-K cluster of) CTA(s) at the lane level, filtered from the 16-B rect
+//     stream + the record class byte: keep if the support rect (R21) meets the tile; the filter
+//     also decides the Gaussian's evaluation PATH (below).
 //   * staging: each lane whose candidate is kept copies its 64-B record with four 16-B cp.async
 //     into the warp's own double buffer in shared memory -- the dominant path (recurrence over
 //     both column halves / the unmasked small tile) from the buffer's front, every other path
@@ -81,10 +81,13 @@ __device__ __forceinline__ float2 f2(float a) { return make_float2(a, a); }
 
 // Staged record (binning.cu K1b): r0 = {-ax, ay, dl_y, a1/s},  r1 = {-a1 dl_x, b1, c1, c'_r},
 //   r2 = {c'_g, c'_b, window x0|x1, y0|y1}  (recurrence path: {c'_g, c'_b, G1, G2})
+// Masked (FULL = false): mw = the window rect as tile masks written by the filter (bit c of
+// mw.x: tile column c inside the window, bit r of mw.y: tile row r), xo / yo = the lane's
+// first column / row in the tile.
 template <class CFG, bool FULL, int HSEL = 3>
 __device__ __forceinline__ void fwd_gauss(const float4 r0, const float4 r1, const float4 r2,
-                                          const float2 (&xj)[CFG::STRIP / 2], float yf0,
-                                          const int (&yi)[CFG::ROWS], int xl0, float invs,
+                                          uint2 mw, const float2 (&xj)[CFG::STRIP / 2],
+                                          float yf0, int xo, int yo, float invs,
                                           float2 (&acc)[FwdAcc<CFG>::NACC]) {
     constexpr int FWD_STRIP = CFG::STRIP, FWD_ROWS = CFG::ROWS;
     const float2 D2 = f2(r0.w);
@@ -97,12 +100,12 @@ __device__ __forceinline__ void fwd_gauss(const float4 r0, const float4 r1, cons
     for (int jp = 0; jp < FWD_STRIP / 2; ++jp)
         if (live(jp)) kx[jp] = __fadd2_rn(xj[jp], nax);
     bool cin[FWD_STRIP];
+    unsigned rin = 0u;
     if (!FULL) {
-        const unsigned xs = __float_as_uint(r2.z);
-        const int x0 = (int)(xs & 0xffffu), x1 = (int)(xs >> 16);
+        const unsigned cm = mw.x >> xo;
 #pragma unroll
-        for (int j = 0; j < FWD_STRIP; ++j)
-            cin[j] = (xl0 + colx<FWD_STRIP>(j) >= x0) && (xl0 + colx<FWD_STRIP>(j) <= x1);
+        for (int j = 0; j < FWD_STRIP; ++j) cin[j] = (cm >> colx<FWD_STRIP>(j)) & 1u;
+        rin = mw.y >> yo;
     }
     const float2 cr = f2(r1.w), cg = f2(r2.x), cb = f2(r2.y);
     float dy = fmaf(yf0 - r0.y, invs, -r0.z);
@@ -111,11 +114,7 @@ __device__ __forceinline__ void fwd_gauss(const float4 r0, const float4 r1, cons
         if (r > 0) dy += invs;                               // consecutive rows: exact to 1 ulp(1/s)
         const float v = r1.z * dy;                           // c1 dy
         float u = -(v * v);
-        if (!FULL) {                                         // lane's row outside [y0, y1]
-            const unsigned ys = __float_as_uint(r2.w);
-            const int y0 = (int)(ys & 0xffffu), y1 = (int)(ys >> 16);
-            u = (yi[r] >= y0 && yi[r] <= y1) ? u : -INFINITY;
-        }
+        if (!FULL) u = ((rin >> r) & 1u) ? u : -INFINITY;    // lane's row outside [y0, y1]
         const float tau = fmaf(r1.y, dy, r1.x);              // b1 dy - a1 dl_x
         const float2 T2 = f2(tau), U2 = f2(u);
 #pragma unroll
@@ -245,6 +244,8 @@ struct FwdSmem2 {
         float stage[CFG::TH][CFG::TW * 3];                 // HWC tile (epilogue)
     };
     uint8_t path[CFG::WARPS][2][FWD_BUF];
+    // window masks of the staged masked-path records (small configuration only, fwd_gauss)
+    uint2 mw[CFG::WARPS][2][CFG::ROWS == 1 ? FWD_BUF : 1];
     struct PerWarp {
         float2 tot[FwdAcc<CFG>::NACC][32];                 // the warp's image (epilogue)
     } wp[CFG::WARPS];
@@ -372,8 +373,9 @@ __global__ void __launch_bounds__(CFG::WARPS * 32, 16 / CFG::WARPS) k_render_fwd
     const float invs = im.invsy;     // rows: dy = (y - ay)/sy - dl_y
 
     // lane geometry (every warp covers the whole tile)
-    const int xl0 = Tx0 + lane_x0<FWD_STRIP>(lane);
-    const int yl0 = Ty0 + FWD_ROWS * (lane >> 2);
+    const int xo = lane_x0<FWD_STRIP>(lane), yo = FWD_ROWS * (lane >> 2);   // in the tile
+    const int xl0 = Tx0 + xo;
+    const int yl0 = Ty0 + yo;
     float2 xj[FWD_STRIP / 2];
 #pragma unroll
     for (int jp = 0; jp < FWD_STRIP / 2; ++jp)
@@ -407,18 +409,24 @@ __global__ void __launch_bounds__(CFG::WARPS * 32, 16 / CFG::WARPS) k_render_fwd
     int nb[SD], sb[SD];                 // candidates in the batch, the lane's candidate position
     int4 rb[SD];
     int cb[SD];
-    // positions: rounds of 32 W per CTA (round i to cluster CTA i mod KS), warp w takes
-    // positions w, w + W, ... of its CTA's rounds (CandStream)
+    // positions: the P = KS W parts (the warps of the split-K cluster) interleave at the lane
+    // level, part p = krank W + w takes positions p, p + P, p + 2P, ... (CandStream): the kept
+    // candidates cluster along the stream (the cells nearest the tile), and the interleave
+    // gives every warp and every cluster CTA an even share of each cluster, with a fixed,
+    // deterministic assignment (whole batches per warp left one warp waiting at the epilogue
+    // for up to 20% of the samples at C4)
+    constexpr int NPARTS = KS * CFG::WARPS;
+    const int part = krank * CFG::WARPS + warp;
     auto fetch = [&](int j) {
         nb[j] = 0;
         sb[j] = 0;
         while (ctotal > 0) {
-            const int base = 32 * CFG::WARPS * (round * KS + krank);
-            if (base + warp < ctotal) {
+            const int base = 32 * NPARTS * round;
+            if (base + part < ctotal) {
                 ++round;
-                nb[j] = min(32, (ctotal - base - warp + CFG::WARPS - 1) / CFG::WARPS);
+                nb[j] = min(32, (ctotal - base - part + NPARTS - 1) / NPARTS);
                 while (base >= sm.chunk.pre[r0 + 1]) ++r0;
-                const int v = base + CFG::WARPS * lane + warp;
+                const int v = base + NPARTS * lane + part;
                 if (v < ctotal) sb[j] = cand_index(sm.chunk, v, r0);
                 break;
             }
@@ -462,13 +470,14 @@ __global__ void __launch_bounds__(CFG::WARPS * 32, 16 / CFG::WARPS) k_render_fwd
                 const float4 r2g = make_float4(r2.x, r2.y, r3.x, r3.y);
                 fwd_gauss_r2h<2, FWD_STRIP, 3>(r0, r1, r2g, r3.z, xlf, yrow, yi, xl0, invs, acc);
             } else {
-                fwd_gauss<CFG, true, 3>(r0, r1, r2, xj, yf0, yi, xl0, invs, acc);
+                fwd_gauss<CFG, true, 3>(r0, r1, r2, make_uint2(0u, 0u), xj, yf0, xo, yo, invs, acc);
             }
         }
     };
     auto process = [&](int pbuf, int pbeg, int pcnt) {
         const float4* sr = &sm.rec[warp][pbuf][0];
         const uint8_t* pp = &sm.path[warp][pbuf][0];
+        const uint2* mws = &sm.mw[warp][pbuf][0];
 #ifdef GSR_DIAG_FWD_NOEVAL       // timing diagnostic only (wrong results): no evaluation
         if (pcnt > pbeg) pcnt = sr[0].x == 12345.f ? pbeg + 1 : pbeg;
 #endif
@@ -476,7 +485,7 @@ __global__ void __launch_bounds__(CFG::WARPS * 32, 16 / CFG::WARPS) k_render_fwd
             if (GSR_FWD_SPLIT) {          // the small tiles' other path is the masked one
                 const float4* q = sr + REC_F4 * pbeg;
                 for (int g = pbeg; g < pcnt; ++g, q += REC_F4)
-                    fwd_gauss<CFG, false, 3>(q[0], q[1], q[2], xj, yf0, yi, xl0, invs, acc);
+                    fwd_gauss<CFG, false, 3>(q[0], q[1], q[2], mws[g], xj, yf0, xo, yo, invs, acc);
                 return;
             }
         }
@@ -518,12 +527,12 @@ __global__ void __launch_bounds__(CFG::WARPS * 32, 16 / CFG::WARPS) k_render_fwd
                         fwd_gauss_r2h<1, FWD_STRIP, 2>(r0, r1, r2, 0.f, xlf, yrow, yi, xl0, invs, acc);
                 }
             } else {   // 0..2 full (both / left / right half), 3..5 masked
-                if (pth == 0) fwd_gauss<CFG, true, 3>(r0, r1, r2, xj, yf0, yi, xl0, invs, acc);
-                else if (pth == 1) fwd_gauss<CFG, true, 1>(r0, r1, r2, xj, yf0, yi, xl0, invs, acc);
-                else if (pth == 2) fwd_gauss<CFG, true, 2>(r0, r1, r2, xj, yf0, yi, xl0, invs, acc);
-                else if (pth == 3) fwd_gauss<CFG, false, 3>(r0, r1, r2, xj, yf0, yi, xl0, invs, acc);
-                else if (pth == 4) fwd_gauss<CFG, false, 1>(r0, r1, r2, xj, yf0, yi, xl0, invs, acc);
-                else fwd_gauss<CFG, false, 2>(r0, r1, r2, xj, yf0, yi, xl0, invs, acc);
+                if (pth == 0) fwd_gauss<CFG, true, 3>(r0, r1, r2, make_uint2(0u, 0u), xj, yf0, xo, yo, invs, acc);
+                else if (pth == 1) fwd_gauss<CFG, true, 1>(r0, r1, r2, make_uint2(0u, 0u), xj, yf0, xo, yo, invs, acc);
+                else if (pth == 2) fwd_gauss<CFG, true, 2>(r0, r1, r2, make_uint2(0u, 0u), xj, yf0, xo, yo, invs, acc);
+                else if (pth == 3) fwd_gauss<CFG, false, 3>(r0, r1, r2, mws[g], xj, yf0, xo, yo, invs, acc);
+                else if (pth == 4) fwd_gauss<CFG, false, 1>(r0, r1, r2, mws[g], xj, yf0, xo, yo, invs, acc);
+                else fwd_gauss<CFG, false, 2>(r0, r1, r2, mws[g], xj, yf0, xo, yo, invs, acc);
             }
         }
     };
@@ -545,6 +554,7 @@ __global__ void __launch_bounds__(CFG::WARPS * 32, 16 / CFG::WARPS) k_render_fwd
         if (!end) {
             bool keep = false;
             int pth = 0;
+            uint2 mwd = make_uint2(0u, 0u);
             if (lane < nb[0]) {
                 const unsigned sxs = (unsigned)rb[0].x, sys = (unsigned)rb[0].y;
                 const int sx0 = (int)(sxs & 0xffffu), sx1 = (int)(sxs >> 16);
@@ -569,10 +579,17 @@ __global__ void __launch_bounds__(CFG::WARPS * 32, 16 / CFG::WARPS) k_render_fwd
                 // column halves the support meets (left 16 / right 16 columns)
                 const bool hl = sx0 <= fx0 + 15, hr = sx1 >= fx0 + 16;
                 const int hv = !GSR_FWD_HALVES || !use_halves<FWD_STRIP>() || (hl && hr) ? 0 : (hl ? 1 : 2);
-                if constexpr (FWD_ROWS == 2)
+                if constexpr (FWD_ROWS == 2) {
                     pth = (full ? ((cb[0] & 1) ? P_REC3 : P_DIR3) : P_MSK3) + hv;
-                else
+                } else {
                     pth = (full ? 0 : 3) + hv;
+                    if (keep && !full) {           // the window rect as tile column / row masks
+                        const int c0 = max(x0 - fx0, 0), c1 = min(x1 - fx0, 31);
+                        const int w0 = max(y0 - fy0, 0), w1 = min(y1 - fy0, 31);
+                        mwd.x = c1 < c0 ? 0u : (unsigned)(((2ull << c1) - 1ull) & ~((1ull << c0) - 1ull));
+                        mwd.y = w1 < w0 ? 0u : (unsigned)(((2ull << w1) - 1ull) & ~((1ull << w0) - 1ull));
+                    }
+                }
             }
 #if GSR_FWD_SPLIT
             const bool front = keep && pth == FRONT_PATH;
@@ -582,6 +599,7 @@ __global__ void __launch_bounds__(CFG::WARPS * 32, 16 / CFG::WARPS) k_render_fwd
                 const int slot = front ? cnt + __popc(mf & lt)
                                        : FWD_BUF - 1 - (cntb + __popc(mb & lt));
                 sm.path[warp][b][slot] = (uint8_t)pth;
+                if constexpr (FWD_ROWS == 1) sm.mw[warp][b][slot] = mwd;
                 const float4* src = rec + (long long)REC_F4 * sb[0];
                 float4* dst = &sm.rec[warp][b][REC_F4 * slot];
 #pragma unroll
@@ -594,6 +612,7 @@ __global__ void __launch_bounds__(CFG::WARPS * 32, 16 / CFG::WARPS) k_render_fwd
             if (keep) {
                 const int slot = cnt + __popc(m & lt);
                 sm.path[warp][b][slot] = (uint8_t)pth;
+                if constexpr (FWD_ROWS == 1) sm.mw[warp][b][slot] = mwd;
                 const float4* src = rec + (long long)REC_F4 * sb[0];
                 float4* dst = &sm.rec[warp][b][REC_F4 * slot];
 #pragma unroll
