@@ -131,6 +131,7 @@ gsr_status build_table(const gsr_image* imgs, int32_t n_imgs, int64_t n_total, d
         } else {
             d.ncx = d.ncy = d.ntx = d.nty = d.fntx = d.fnty = 0;
         }
+        d.dense = (double)d.g_cnt * (CELL * CELL) >= 16.0 * (double)d.Ws * (double)d.Hs ? 1 : 0;
         d.cell_base = (int)cells;
         d.tile_base = (int)tiles;
         d.ftile_base = (int)ftiles;

@@ -399,6 +399,7 @@ __global__ void __launch_bounds__(CFG::WARPS * 32, 16 / CFG::WARPS) k_render_fwd
     vs.cy_hi = min(im.ncy - 1, (fy1 - im.row_begin + im.offy) / CELL);
     vs.X0 = fx0;
     vs.Y0 = fy0;
+    vs.trim = im.dense && vs.cx_hi - vs.cx_lo + 1 >= 6;
     const int cy_first = (Ty0 - im.row_begin - query_ext(ext, kimg, 1) + 1 + im.offy) / CELL;
     if (warp == 0) vs.build(sm.chunk, live ? cy_first : vs.cy_hi + 1, lane);
     __syncthreads();
