@@ -3,9 +3,12 @@
 #include <algorithm>
 #include <atomic>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <vector>
+
+#include <nvtx3/nvToolsExt.h>
 
 #include "../../include/gsr.h"
 #include "gsr_internal.cuh"
@@ -32,9 +35,25 @@ struct Profiler {
 } g_prof;
 }  // namespace
 
+namespace {
+// NVTX ranges around the phases' launches (GSR_NVTX=1, read once): binning (K1-K3),
+// forward (K4), backward (K5), finalize (K6) -- host ranges around the enqueue, which nsys / ncu
+// correlate with the kernels
+bool nvtx_on() {
+    static const bool on = [] {
+        const char* e = std::getenv("GSR_NVTX");
+        return e && e[0] && e[0] != '0';
+    }();
+    return on;
+}
+const char* const kPhaseName[4] = {"gsr:binning", "gsr:render_fwd", "gsr:render_bwd",
+                                   "gsr:finalize"};
+}  // namespace
+
 namespace gsr {
 void count_launches(long long k) { g_launches += k; }
 int prof_begin(int phase, cudaStream_t st) {
+    if (nvtx_on()) nvtxRangePushA(kPhaseName[phase & 3]);
     std::lock_guard<std::mutex> lk(g_prof.mu);
     if (!g_prof.on) return -1;
     Profiler::Rec r{phase, g_prof.get(), g_prof.get()};
@@ -43,6 +62,7 @@ int prof_begin(int phase, cudaStream_t st) {
     return (int)g_prof.open_.size() - 1;
 }
 void prof_end(int handle, cudaStream_t st) {
+    if (nvtx_on()) nvtxRangePop();
     if (handle < 0) return;
     std::lock_guard<std::mutex> lk(g_prof.mu);
     if (handle >= (int)g_prof.open_.size()) return;

@@ -29,7 +29,9 @@ is tested on CPU with gloo and a CPU stand-in, and runs on B200 with the CUDA pa
 """
 from __future__ import annotations
 
+import functools
 import math
+import os
 from typing import Callable, List, Sequence
 
 import numpy as np
@@ -218,6 +220,23 @@ def rank_numels(bounds: Sequence[Sequence[int]], widths3: Sequence[int], world: 
     return [sum((b[r + 1] - b[r]) * w3 for b, w3 in zip(bounds, widths3)) for r in range(world)]
 
 
+def _nvtx(fn):
+    """NVTX range "gsr:<name>" around an exchange step when GSR_NVTX=1 (libgsr marks
+    its kernel phases the same way)."""
+    @functools.wraps(fn)
+    def wrap(*a, **k):
+        if os.environ.get("GSR_NVTX", "0") in ("", "0"):
+            return fn(*a, **k)
+        import torch
+        torch.cuda.nvtx.range_push("gsr:" + fn.__name__)
+        try:
+            return fn(*a, **k)
+        finally:
+            torch.cuda.nvtx.range_pop()
+    return wrap
+
+
+@_nvtx
 def gather_bands(out, numels: Sequence[int], group=None, async_op: bool = False):
     """All-gather every rank's flat band buffer, padded to the largest: -> [world, max]
     (async_op: -> ([world, max], work); the buffer is valid after work.wait())."""
@@ -258,6 +277,7 @@ def reduce_moments(moments, group=None):
     return moments
 
 
+@_nvtx
 def reduce_seam(grads, seam_idx, group=None, full: bool = False):
     """Seam reduce of per-rank partial gradients: `grads` is one [n, k] tensor or a sequence of
     [n] / [n, k] tensors (the finalize's d_alpha, d_mu, ...); the rows `seam_idx` (int64 tensor on
@@ -378,6 +398,7 @@ class RankPlan:
                 "multi_allreduce": 36 * self.n_multi}
 
 
+@_nvtx
 def exchange_seams(grads, plan: RankPlan, group=None):
     """Neighbour seam exchange of a rank's COMPACT partial gradients (the finalize of its halo
     moments, rows = plan.idx): the rows shared with rank +- 1 are swapped with that neighbour

@@ -7,6 +7,7 @@ PyTorch fallback: CPU tensors, a missing library or a launch failure raise.
 from __future__ import annotations
 
 import ctypes
+import os
 from dataclasses import dataclass
 from typing import List, Optional, Sequence, Tuple
 
@@ -42,7 +43,12 @@ def _check_param(t: torch.Tensor, name: str, n: Optional[int] = None,
 _FLOATS = (torch.float32, torch.bfloat16)
 
 
-def _params(alpha, mu, sigma, rho, color):
+# GSR_DEBUG=1: every render call first runs gsr_validate_params on its parameters
+# and raises on a Gaussian outside the domain (synchronises; a debugging aid, off by default)
+DEBUG = os.environ.get("GSR_DEBUG", "0") not in ("", "0")
+
+
+def _params(alpha, mu, sigma, rho, color, validate: bool = True):
     """Checked parameter tensors: float32, or all bfloat16 (GSR_PARAMS_BF16, NEXT-4)."""
     n = alpha.shape[0] if isinstance(alpha, torch.Tensor) else None
     ts = [_check_param(t, k, n, _FLOATS) for t, k in zip((alpha, mu, sigma, rho, color), PARAMS)]
@@ -52,6 +58,11 @@ def _params(alpha, mu, sigma, rho, color):
             raise ValueError("all parameters must live on the same device")
         if t.dtype != ts[0].dtype:
             raise TypeError("all parameters must have the same dtype")
+    if DEBUG and validate and n:
+        cnt, first = _validate(ts, n)
+        if cnt:
+            raise ValueError(f"GSR_DEBUG: {cnt} Gaussian(s) outside the parameter domain "
+                             f"(non-finite, sigma <= 0 or |rho| >= 1), first index {first}")
     return ts, n
 
 
@@ -308,7 +319,11 @@ def render_bwd_batched(alpha, mu, sigma, rho, color, lay: Layout, grad_out: torc
 def validate_params(alpha, mu, sigma, rho, color):
     """(count, first index or -1) of the Gaussians outside the parameter domain (R20:
     non-finite field, sigma <= 0 or |rho| >= 1) -- gsr_validate_params; synchronises."""
-    params, n = _params(alpha, mu, sigma, rho, color)
+    params, n = _params(alpha, mu, sigma, rho, color, validate=False)
+    return _validate(params, n)
+
+
+def _validate(params, n):
     dev = params[0].device
     res = torch.empty(2, dtype=torch.int64, device=dev)
     check(_lib.load().gsr_validate_params(*[_ptr(t) for t in params], n, _fmt_flags(params),

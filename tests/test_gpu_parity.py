@@ -400,3 +400,36 @@ def test_validate_params(gsr):
     assert cnt == int(bad.sum()) > 0 and first == int(np.nonzero(bad)[0][0])
     ok = S.gaussians(10, 10, seed=1)
     assert gsr.validate_params(*to_dev(ok)) == (0, -1)
+
+
+def test_debug_validation_and_nvtx_env(tmp_path):
+    """GSR_DEBUG=1: a render call on parameters outside the domain raises before any kernel runs
+    (SURVEY §5); GSR_NVTX=1: the NVTX phase ranges leave the results unchanged."""
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    code = """
+import sys, numpy as np, torch
+sys.path.insert(0, %r)
+import gsr_synth as S, paper_2501_06838_b200 as gsr
+c = S.gaussians(12, 14, seed=3)
+dev = [torch.from_numpy(c[k]).cuda() for k in ("alpha", "mu", "sigma", "rho", "color")]
+ok = gsr.render(*dev, 12, 14, 3.0)
+dev[2][5, 1] = -1.0
+try:
+    gsr.render(*dev, 12, 14, 3.0)
+    print("NO-RAISE")
+except ValueError as e:
+    print("RAISED", "first index 5" in str(e))
+np.save(sys.argv[1], ok.cpu().numpy())
+""" % str(root)
+    outs = {}
+    for env in ({"GSR_DEBUG": "1"}, {"GSR_DEBUG": "1", "GSR_NVTX": "1"}):
+        f = tmp_path / ("nvtx.npy" if "GSR_NVTX" in env else "plain.npy")
+        r = subprocess.run([sys.executable, "-c", code, str(f)], capture_output=True, text=True,
+                           env={**__import__("os").environ, **env}, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        assert "RAISED True" in r.stdout, r.stdout
+        outs[f.name] = np.load(f)
+    assert np.array_equal(outs["plain.npy"], outs["nvtx.npy"])
