@@ -348,11 +348,11 @@ __global__ void k_records(const T* __restrict__ alpha, const T* __restrict__ mu,
     unsigned ys = (unsigned)r.y0 | ((unsigned)r.y1 << 16);
     float4 r2 = make_float4((float)(w * c1f), (float)(w * c2f), __uint_as_float(xs),
                             __uint_as_float(ys));
-    // r3: the forward's exponential-recurrence constants G_t = 2^(-D^2 t^2), t = 1..3, and the
-    // flag "recurrence allowed" (D <= FWD_REC_DMAX, render_fwd.cu MODE 2)
+    // r3: the forward's exponential-recurrence constants G_t = 2^(-D^2 t^2), t = 1..3, and -2D
+    // (exact in fp32), when the recurrence is allowed (D <= FWD_REC_DMAX, render_fwd.cu MODE 2)
     const bool rec_ok = Df <= FWD_REC_DMAX;
     float4 r3 = make_float4(rec_ok ? exp2f(-d2) : 0.f, rec_ok ? exp2f(-4.f * d2) : 0.f,
-                            rec_ok ? exp2f(-9.f * d2) : 0.f, rec_ok ? 1.f : 0.f);
+                            rec_ok ? exp2f(-9.f * d2) : 0.f, rec_ok ? -2.f * Df : 0.f);
     rec[REC_F4 * p + 0] = r0;
     rec[REC_F4 * p + 1] = r1;
     rec[REC_F4 * p + 2] = r2;

@@ -152,7 +152,8 @@ __device__ __forceinline__ void fwd_gauss(const float4 r0, const float4 r1, cons
 //           D^2 t^2 <= 9). Error: the exponent of B^t carries t * 2 D |w_a| * 2^-24 relative.
 template <int MODE, int STRIP, int HSEL = 3>
 __device__ __forceinline__ void fwd_gauss_r2h(const float4 r0, const float4 r1, const float4 r2,
-                                              float g3, float xlf, float2 yrow, const int (&yi)[2],
+                                              float g3, float m2d, float xlf, float2 yrow,
+                                              const int (&yi)[2],
                                               int xl0, float invs, float2 (&acc)[3 * STRIP]) {
     constexpr int hmask = HSEL;
     const float D = r0.w;
@@ -177,11 +178,21 @@ __device__ __forceinline__ void fwd_gauss_r2h(const float4 r0, const float4 r1, 
         acc[3 * j + 2] = __ffma2_rn(cb, e, acc[3 * j + 2]);
     };
     if (MODE == 2) {
-        const float2 G1 = f2(r2.z), G2 = f2(r2.w), G3 = f2(g3), M2D = f2(-2.f * D);
+        const float2 G1 = f2(r2.z), G2 = f2(r2.w), G3 = f2(g3), M2D = f2(m2d);   // m2d = -2D
+        float2 w0 = make_float2(0.f, 0.f);
 #pragma unroll
         for (int h = 0; h < STRIP / 4; ++h) {
             if (use_halves<STRIP>() && !((hmask >> h) & 1)) continue;   // compile-time skip
-            const float2 w = __ffma2_rn(D2, f2(kx0 + (float)colx<STRIP>(4 * h)), T);
+            // anchor column 16 h: w = D kx + T; the second anchor of a Gaussian that evaluates
+            // both halves as w0 + 16 D (one FFMA2 instead of an FADD for kx and an FFMA2)
+            float2 w;
+            if (h == 0)
+                w = __ffma2_rn(D2, f2(kx0), T);
+            else if (use_halves<STRIP>() && (hmask & 1))
+                w = __ffma2_rn(D2, f2((float)colx<STRIP>(4 * h)), w0);
+            else
+                w = __ffma2_rn(D2, f2(kx0 + (float)colx<STRIP>(4 * h)), T);
+            if (h == 0) w0 = w;
             const float2 q = __ffma2_rn(make_float2(-w.x, -w.y), w, U);
             float2 b = __fmul2_rn(w, M2D);
             b.x = fminf(b.x, 40.f);
@@ -464,12 +475,12 @@ __global__ void __launch_bounds__(CFG::WARPS * 32, 16 / CFG::WARPS) k_render_fwd
         if (nf > 0) nf = q[0].x == 12345.f ? 1 : 0;
 #endif
 #pragma unroll kFrontUnroll
-        for (int g = 0; g < nf; ++g, q += REC_F4) {
+        for (const float4* qe = q + REC_F4 * nf; q != qe; q += REC_F4) {
             const float4 r0 = q[0], r1 = q[1], r2 = q[2];
             if constexpr (FWD_ROWS == 2) {
                 const float4 r3 = q[3];
                 const float4 r2g = make_float4(r2.x, r2.y, r3.x, r3.y);
-                fwd_gauss_r2h<2, FWD_STRIP, 3>(r0, r1, r2g, r3.z, xlf, yrow, yi, xl0, invs, acc);
+                fwd_gauss_r2h<2, FWD_STRIP, 3>(r0, r1, r2g, r3.z, r3.w, xlf, yrow, yi, xl0, invs, acc);
             } else {
                 fwd_gauss<CFG, true, 3>(r0, r1, r2, make_uint2(0u, 0u), xj, yf0, xo, yo, invs, acc);
             }
@@ -507,25 +518,25 @@ __global__ void __launch_bounds__(CFG::WARPS * 32, 16 / CFG::WARPS) k_render_fwd
                     const float4 r3 = q[3];
                     const float4 r2g = make_float4(r2.x, r2.y, r3.x, r3.y);
                     if (pth == P_REC1)
-                        fwd_gauss_r2h<2, FWD_STRIP, 1>(r0, r1, r2g, r3.z, xlf, yrow, yi, xl0, invs, acc);
+                        fwd_gauss_r2h<2, FWD_STRIP, 1>(r0, r1, r2g, r3.z, r3.w, xlf, yrow, yi, xl0, invs, acc);
                     else if (pth == P_REC2)
-                        fwd_gauss_r2h<2, FWD_STRIP, 2>(r0, r1, r2g, r3.z, xlf, yrow, yi, xl0, invs, acc);
+                        fwd_gauss_r2h<2, FWD_STRIP, 2>(r0, r1, r2g, r3.z, r3.w, xlf, yrow, yi, xl0, invs, acc);
                     else
-                        fwd_gauss_r2h<2, FWD_STRIP, 3>(r0, r1, r2g, r3.z, xlf, yrow, yi, xl0, invs, acc);
+                        fwd_gauss_r2h<2, FWD_STRIP, 3>(r0, r1, r2g, r3.z, r3.w, xlf, yrow, yi, xl0, invs, acc);
                 } else if (pth >= P_MSK3) {
                     if (pth == P_MSK3)
-                        fwd_gauss_r2h<0, FWD_STRIP, 3>(r0, r1, r2, 0.f, xlf, yrow, yi, xl0, invs, acc);
+                        fwd_gauss_r2h<0, FWD_STRIP, 3>(r0, r1, r2, 0.f, 0.f, xlf, yrow, yi, xl0, invs, acc);
                     else if (pth == P_MSK1)
-                        fwd_gauss_r2h<0, FWD_STRIP, 1>(r0, r1, r2, 0.f, xlf, yrow, yi, xl0, invs, acc);
+                        fwd_gauss_r2h<0, FWD_STRIP, 1>(r0, r1, r2, 0.f, 0.f, xlf, yrow, yi, xl0, invs, acc);
                     else
-                        fwd_gauss_r2h<0, FWD_STRIP, 2>(r0, r1, r2, 0.f, xlf, yrow, yi, xl0, invs, acc);
+                        fwd_gauss_r2h<0, FWD_STRIP, 2>(r0, r1, r2, 0.f, 0.f, xlf, yrow, yi, xl0, invs, acc);
                 } else {
                     if (pth == P_DIR3)
-                        fwd_gauss_r2h<1, FWD_STRIP, 3>(r0, r1, r2, 0.f, xlf, yrow, yi, xl0, invs, acc);
+                        fwd_gauss_r2h<1, FWD_STRIP, 3>(r0, r1, r2, 0.f, 0.f, xlf, yrow, yi, xl0, invs, acc);
                     else if (pth == P_DIR1)
-                        fwd_gauss_r2h<1, FWD_STRIP, 1>(r0, r1, r2, 0.f, xlf, yrow, yi, xl0, invs, acc);
+                        fwd_gauss_r2h<1, FWD_STRIP, 1>(r0, r1, r2, 0.f, 0.f, xlf, yrow, yi, xl0, invs, acc);
                     else
-                        fwd_gauss_r2h<1, FWD_STRIP, 2>(r0, r1, r2, 0.f, xlf, yrow, yi, xl0, invs, acc);
+                        fwd_gauss_r2h<1, FWD_STRIP, 2>(r0, r1, r2, 0.f, 0.f, xlf, yrow, yi, xl0, invs, acc);
                 }
             } else {   // 0..2 full (both / left / right half), 3..5 masked
                 if (pth == 0) fwd_gauss<CFG, true, 3>(r0, r1, r2, make_uint2(0u, 0u), xj, yf0, xo, yo, invs, acc);

@@ -172,6 +172,19 @@ def test_fwd_c4_rows(gsr):
         assert_fwd_close(got[rows[0]:rows[1]], want)
 
 
+def test_fwd_stream_chunks_and_reach(gsr):
+    """A dense image (64 Gaussians per cell) with very wide supports (every 50th Gaussian at
+    sigma = 3 LR px, r = 1): the forward's candidate stream spans > 32 cell rows per tile
+    (several chunks, rebuilt under the CTA barriers) and trims them by the cell reach."""
+    H, W, s = 40, 60, 8.0
+    c = S.gaussians(H, W, seed=1005)
+    c["sigma"][::50] = 3.0
+    got = fwd(gsr, c, H, W, s, r=1.0)
+    for rows in [(0, 3), (150, 153), (317, 320)]:
+        want = O.render_fwd(c, H, W, s, 1.0, rows=rows)
+        assert_fwd_close(got[rows[0]:rows[1]], want)
+
+
 def test_fwd_c3_pixels(gsr):
     """C3: 510x339 at x4 -> 2040x1356, N = 2.77M; sampled pixels vs the brute-force oracle."""
     H, W, s = 339, 510, 4.0
