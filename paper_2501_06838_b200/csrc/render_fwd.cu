@@ -452,7 +452,7 @@ __global__ void __launch_bounds__(CFG::WARPS * 32, 16 / CFG::WARPS) k_render_fwd
             r0 = 0;
             round = 0;
         }
-        rb[j] = make_int4(0, 0, 0, 0);
+        rb[j] = make_int4(0xffff, 0, 0, 0);     // no candidate: a support rect no tile meets
         cb[j] = 0;
         if (lane < nb[j]) {
             rb[j] = __ldg(rects + sb[j]);
@@ -567,7 +567,7 @@ __global__ void __launch_bounds__(CFG::WARPS * 32, 16 / CFG::WARPS) k_render_fwd
             bool keep = false;
             int pth = 0;
             uint2 mwd = make_uint2(0u, 0u);
-            if (lane < nb[0]) {
+            {                  // every lane (lanes past the batch hold the empty sentinel rect)
                 const unsigned sxs = (unsigned)rb[0].x, sys = (unsigned)rb[0].y;
                 const int sx0 = (int)(sxs & 0xffffu), sx1 = (int)(sxs >> 16);
                 const int sy0 = (int)(sys & 0xffffu), sy1 = (int)(sys >> 16);
@@ -595,7 +595,7 @@ __global__ void __launch_bounds__(CFG::WARPS * 32, 16 / CFG::WARPS) k_render_fwd
                     pth = (full ? ((cb[0] & 1) ? P_REC3 : P_DIR3) : P_MSK3) + hv;
                 } else {
                     pth = (full ? 0 : 3) + hv;
-                    if (keep && !full) {           // the window rect as tile column / row masks
+                    {                              // the window rect as tile column / row masks
                         const int c0 = max(x0 - fx0, 0), c1 = min(x1 - fx0, 31);
                         const int w0 = max(y0 - fy0, 0), w1 = min(y1 - fy0, 31);
                         mwd.x = c1 < c0 ? 0u : (unsigned)(((2ull << c1) - 1ull) & ~((1ull << c0) - 1ull));
