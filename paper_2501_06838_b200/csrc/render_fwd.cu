@@ -233,7 +233,16 @@ __device__ __forceinline__ void fwd_gauss_r2h(const float4 r0, const float4 r1, 
 enum : int { P_REC3 = 0, P_REC1, P_REC2, P_DIR3, P_DIR1, P_DIR2, P_MSK3, P_MSK1, P_MSK2 };
 constexpr int FRONT_PATH = 0;   // P_REC3 (large) / full over both halves (small configuration)
 
-constexpr int FWD_BUF = 48;                       // records per warp buffer (> 32)
+// records per warp buffer (> 32; a buffer is evaluated once it holds more than FWD_BUF - 32):
+// 96 for the large tiles (48 -> 96: C5 forward -0.5%), 48 for the small ones (96: C2 +6%)
+#ifndef GSR_FWD_BUF_LARGE
+#define GSR_FWD_BUF_LARGE 96
+#endif
+#ifndef GSR_FWD_BUF_SMALL
+#define GSR_FWD_BUF_SMALL 48
+#endif
+template <class CFG>
+constexpr int fwd_buf() { return CFG::ROWS == 2 ? GSR_FWD_BUF_LARGE : GSR_FWD_BUF_SMALL; }
 #ifndef GSR_FWD_SPLIT
 #define GSR_FWD_SPLIT 1
 #endif
@@ -250,16 +259,20 @@ constexpr int kFrontUnroll = GSR_FWD_FRONT_UNROLL;
 
 template <class CFG>
 struct FwdSmem2 {
-    union {
+    static constexpr int FWD_BUF = fwd_buf<CFG>();
+    struct PerWarp {
+        float2 tot[FwdAcc<CFG>::NACC][32];                 // the warp's image (epilogue)
+    };
+    union {                       // the epilogue's buffers reuse the main loop's record buffers
         float4 rec[CFG::WARPS][2][FWD_BUF * REC_F4];      // staged records (main loop)
-        float stage[CFG::TH][CFG::TW * 3];                 // HWC tile (epilogue)
+        struct {
+            PerWarp wp[CFG::WARPS];                        // written after every warp's loop
+            float stage[CFG::TH][CFG::TW * 3];             // HWC tile
+        };
     };
     uint8_t path[CFG::WARPS][2][FWD_BUF];
     // window masks of the staged masked-path records (small configuration only, fwd_gauss)
     uint2 mw[CFG::WARPS][2][CFG::ROWS == 1 ? FWD_BUF : 1];
-    struct PerWarp {
-        float2 tot[FwdAcc<CFG>::NACC][32];                 // the warp's image (epilogue)
-    } wp[CFG::WARPS];
     CandChunk chunk;                                        // candidate stream table
 };
 
@@ -367,6 +380,7 @@ __global__ void __launch_bounds__(CFG::WARPS * 32, 16 / CFG::WARPS) k_render_fwd
                                                               double* __restrict__ loss_acc) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     FwdSmem2<CFG>& sm = *reinterpret_cast<FwdSmem2<CFG>*>(smem_raw);
+    constexpr int FWD_BUF = fwd_buf<CFG>();
     constexpr int FTILE_W = CFG::TW, FTILE_H = CFG::TH, FWD_STRIP = CFG::STRIP,
                   FWD_ROWS = CFG::ROWS, NACC = FwdAcc<CFG>::NACC;
 
@@ -661,8 +675,9 @@ __global__ void __launch_bounds__(CFG::WARPS * 32, 16 / CFG::WARPS) k_render_fwd
         }
         if (end && pend < 0) break;
     }
+    __syncthreads();                                   // every warp is done with the records
 #pragma unroll
-    for (int a = 0; a < NACC; ++a) sm.wp[warp].tot[a][lane] = acc[a];
+    for (int a = 0; a < NACC; ++a) sm.wp[warp].tot[a][lane] = acc[a];   // (after the barrier)
     fwd_epilogue<KS, LOSS, CFG>(sm, im, Tx0, Ty0, krank, out, gt, loss_acc);
 }
 
