@@ -79,6 +79,14 @@ struct FwdAcc { static constexpr int NACC = CFG::ROWS * (CFG::STRIP / 2) * 3; };
 
 __device__ __forceinline__ float2 f2(float a) { return make_float2(a, a); }
 
+// 16-B shared load at a 32-bit shared-window address (volatile: stays after the cp.async wait)
+__device__ __forceinline__ float4 lds_f4(uint32_t a) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+    return v;
+}
+
 // Staged record (binning.cu K1b): r0 = {-ax, ay, dl_y, a1/s},  r1 = {-a1 dl_x, b1, c1, c'_r},
 //   r2 = {c'_g, c'_b, window x0|x1, y0|y1}  (recurrence path: {c'_g, c'_b, G1, G2})
 // Masked (FULL = false): mw = the window rect as tile masks written by the filter (bit c of
@@ -488,11 +496,15 @@ __global__ void __launch_bounds__(CFG::WARPS * 32, 16 / CFG::WARPS) k_render_fwd
 #ifdef GSR_DIAG_FWD_NOEVAL
         if (nf > 0) nf = q[0].x == 12345.f ? 1 : 0;
 #endif
+        // one 32-bit shared address as the loop variable and the load base (a generic pointer
+        // kept a second register and an add per Gaussian)
+        uint32_t a = smem_u32(q);
+        const uint32_t ae = a + (uint32_t)(16 * REC_F4 * nf);
 #pragma unroll kFrontUnroll
-        for (const float4* qe = q + REC_F4 * nf; q != qe; q += REC_F4) {
-            const float4 r0 = q[0], r1 = q[1], r2 = q[2];
+        for (; a != ae; a += 16 * REC_F4) {
+            const float4 r0 = lds_f4(a), r1 = lds_f4(a + 16), r2 = lds_f4(a + 32);
             if constexpr (FWD_ROWS == 2) {
-                const float4 r3 = q[3];
+                const float4 r3 = lds_f4(a + 48);
                 const float4 r2g = make_float4(r2.x, r2.y, r3.x, r3.y);
                 fwd_gauss_r2h<2, FWD_STRIP, 3>(r0, r1, r2g, r3.z, r3.w, xlf, yrow, yi, xl0, invs, acc);
             } else {
