@@ -521,27 +521,28 @@ __global__ void __launch_bounds__(CFG::WARPS * 32, 16 / CFG::WARPS) k_render_fwd
 #endif
         if constexpr (FWD_ROWS == 1 && !use_halves<FWD_STRIP>()) {
             if (GSR_FWD_SPLIT) {          // the small tiles' other path is the masked one
-                const float4* q = sr + REC_F4 * pbeg;
-                for (int g = pbeg; g < pcnt; ++g, q += REC_F4)
-                    fwd_gauss<CFG, false, 3>(q[0], q[1], q[2], mws[g], xj, yf0, xo, yo, invs, acc);
+                uint32_t qa = smem_u32(sr) + (uint32_t)(16 * REC_F4 * pbeg);
+                for (int g = pbeg; g < pcnt; ++g, qa += 16 * REC_F4)
+                    fwd_gauss<CFG, false, 3>(lds_f4(qa), lds_f4(qa + 16), lds_f4(qa + 32), mws[g],
+                                             xj, yf0, xo, yo, invs, acc);
                 return;
             }
         }
         int pnext = pcnt > pbeg ? pp[pbeg] : 0;
-        for (int g = pbeg; g < pcnt; ++g) {
+        uint32_t ra = smem_u32(sr) + (uint32_t)(16 * REC_F4 * pbeg);   // record g's address
+        for (int g = pbeg; g < pcnt; ++g, ra += 16 * REC_F4) {
 #ifdef GSR_DIAG_FWD_NOMASK       // timing diagnostic only (wrong results): masked -> full paths
             const int pth = FWD_ROWS == 2 ? (pnext >= P_MSK3 ? pnext - 3 : pnext) : (pnext >= 3 ? pnext - 3 : pnext);
 #else
             const int pth = pnext;
 #endif
             if (g + 1 < pcnt) pnext = pp[g + 1];          // next Gaussian's path, one ahead
-            const float4* q = sr + REC_F4 * g;
-            const float4 r0 = q[0], r1 = q[1], r2 = q[2];
+            const float4 r0 = lds_f4(ra), r1 = lds_f4(ra + 16), r2 = lds_f4(ra + 32);
             if constexpr (FWD_ROWS == 2) {
                 // the back's common paths first: the single-half recurrences (P_REC3 is only
                 // here without GSR_FWD_SPLIT)
                 if ((unsigned)(pth - P_REC1) <= (unsigned)(P_REC2 - P_REC1) || pth == P_REC3) {
-                    const float4 r3 = q[3];
+                    const float4 r3 = lds_f4(ra + 48);
                     const float4 r2g = make_float4(r2.x, r2.y, r3.x, r3.y);
                     if (pth == P_REC1)
                         fwd_gauss_r2h<2, FWD_STRIP, 1>(r0, r1, r2g, r3.z, r3.w, xlf, yrow, yi, xl0, invs, acc);
