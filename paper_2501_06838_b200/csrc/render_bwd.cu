@@ -18,8 +18,9 @@
 // Layout of K5: one CTA (4 warps) per 64 x 8 HR tile with the tile's dL/dI staged in shared
 // memory as column pairs. Lanes own Gaussians: each warp scans its share of the tile's
 // candidate spans (support rect vs tile; SCAN_U chunks of loads in flight), queues the hits with
-// a key = their clipped column range, sorts each batch of 512 hits by key and evaluates groups of
-// 32: all 32 lanes walk the same pixels (warp-uniform loop bounds from the union of their support
+// a key = their clipped column range; the CTA sorts the first <= 512 hits of every warp's queue
+// together by key (GSR_BWD_CTASORT) and the warps evaluate its groups of 32 round-robin: all 32
+// lanes of a group walk the same pixels (warp-uniform loop bounds from the union of their support
 // rects), reading dL/dI as shared-memory broadcasts. Per-pair work is paired over two pixels with
 // FFMA2. Within a row the vq-dependent moments are factored out (sum_row w vq = vq sum_row w, ...),
 // so a pair costs 12.5 FP32 lane-ops + 1 ex2 (kx shared by a row pair, w, q, 3 e g, 3 g.c',
