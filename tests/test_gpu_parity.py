@@ -154,8 +154,12 @@ def test_fwd_adversarial_and_empty(gsr):
     assert out.shape == (54, 89, 3) and not out.abs().sum().item()
 
 
-def test_fwd_deterministic(gsr):
-    H, W, s = 30, 30, 3.0
+@pytest.mark.parametrize("H,W,s", [(30, 30, 3.0), (60, 80, 8.0), (170, 255, 8.0)],
+                         ids=["small-tiles", "large-tiles-split-k", "c5-image"])
+def test_fwd_deterministic(gsr, H, W, s):
+    """Bitwise run-to-run reproducibility: the candidate stream's lane interleave assigns every
+    candidate to a fixed warp (and split-K cluster CTA), and the warp images are summed in a
+    fixed order -- small tiles, large tiles under split-K, and a C5 image (cell-reach trim)."""
     c = S.gaussians(H, W, seed=5)
     a = fwd(gsr, c, H, W, s)
     b = fwd(gsr, c, H, W, s)
