@@ -385,6 +385,22 @@ gsr_status gsr_debug_tile_lists(const float* alpha, const float* mu, const float
                                 int32_t* ids, int32_t* cells, void* workspace,
                                 size_t workspace_bytes, void* stream);
 
+/* Forward tile lists, materialised (test-only): for every forward render tile of the single
+ * image (K4's tiles: ftile_w x ftile_h HR px in row-major order; the tile configuration is chosen
+ * per call from the window width), the Gaussians K4 keeps -- its candidate stream (the tile's
+ * cell rows, each trimmed by the cell reach on dense images) filtered by its support-rect test
+ * (R21), in stream order -- and the evaluation path K4 assigns each (render_fwd.cu P_*). The
+ * same device code as K4 (CandStream, fwd_classify). geom: host int32[3] <- {ftile_w, ftile_h,
+ * number of forward tiles}. Two calls: offsets == NULL fills counts[ntiles] (device int32);
+ * then offsets (device int32, exclusive prefix of counts) with ids (device int32, Gaussian
+ * indices) and paths (device uint8), sum(counts) entries each, CSR by tile. */
+gsr_status gsr_debug_fwd_tile_lists(const float* alpha, const float* mu, const float* sigma,
+                                    const float* rho, const float* color, int64_t n,
+                                    int32_t lr_h, int32_t lr_w, double scale, double ratio,
+                                    int32_t* geom, const int32_t* offsets, int32_t* counts,
+                                    int32_t* ids, uint8_t* paths, void* workspace,
+                                    size_t workspace_bytes, void* stream);
+
 /* ---- measurement ------------------------------------------------------------------------ */
 
 /* Phase timing for benchmarks (process-global, not thread-safe; off by default). While enabled,

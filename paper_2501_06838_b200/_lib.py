@@ -27,7 +27,8 @@ EXPORTS = ["gsr_version", "gsr_out_dims", "gsr_out_dims_v", "gsr_workspace_bytes
            "gsr_finalize_grads_ex", "gsr_row_pair_counts_batched", "gsr_row_pair_counts_host",
            "gsr_band_span_batched", "gsr_band_span_host", "gsr_workspace_bytes_subset",
            "gsr_render_fwd_subset", "gsr_render_bwd_moments_subset", "gsr_finalize_grads_subset",
-           "gsr_validate_params", "gsr_rank_halo_workspace_bytes", "gsr_rank_halo"]
+           "gsr_validate_params", "gsr_rank_halo_workspace_bytes", "gsr_rank_halo",
+           "gsr_debug_fwd_tile_lists"]
 GSR_REUSE_BINNING = 0x1
 GSR_SUPPORT = 0x2
 GSR_OUT_BF16 = 0x4
@@ -100,6 +101,8 @@ def load(path: Path | str | None = None):
         "gsr_debug_rects": (par + [_I64, _I32, _I32, _D, _D, _P, _P], None),
         "gsr_debug_rects_ex": (par + [_I64, _I32, _I32, _D, _D, ctypes.c_uint32, _P, _P], None),
         "gsr_debug_tile_lists": (par + [_I64, _I32, _I32, _D, _D, _P, _P, _P, _P, _SZ, _P], None),
+        "gsr_debug_fwd_tile_lists": (par + [_I64, _I32, _I32, _D, _D, _P, _P, _P, _P, _P, _P, _SZ,
+                                            _P], None),
         "gsr_row_pair_counts_batched": (par + [_I64, _IMGP, _I32, _D, ctypes.c_uint32, _P, _P],
                                         None),
         "gsr_row_pair_counts_host": (par + [_I64, _IMGP, _I32, _D, ctypes.c_uint32, _P], None),

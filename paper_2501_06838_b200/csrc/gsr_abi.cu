@@ -786,4 +786,23 @@ gsr_status gsr_debug_tile_lists(const float* alpha, const float* mu, const float
     return finish(launch_debug_tile_lists(P.tab, P.ws, P.perm, P.keys, counts, ids, cells, st));
 }
 
+gsr_status gsr_debug_fwd_tile_lists(const float* alpha, const float* mu, const float* sigma,
+                                    const float* rho, const float* color, int64_t n,
+                                    int32_t lr_h, int32_t lr_w, double scale, double ratio,
+                                    int32_t* geom, const int32_t* offsets, int32_t* counts,
+                                    int32_t* ids, uint8_t* paths, void* workspace,
+                                    size_t workspace_bytes, void* stream) {
+    if (!geom || (!offsets && !counts) || (offsets && (!ids || !paths))) return GSR_EINVAL;
+    gsr_image g = single(n, lr_h, lr_w, scale);
+    cudaStream_t st = (cudaStream_t)stream;
+    Prepared P;
+    gsr_status s = prepare(alpha, mu, sigma, rho, color, n, &g, 1, ratio, workspace,
+                           workspace_bytes, st, &P, true);
+    if (s != GSR_OK) return s;
+    geom[0] = P.tab.ftile_w;
+    geom[1] = P.tab.ftile_h;
+    geom[2] = P.tab.total_ftiles;
+    return finish(launch_debug_fwd_lists(P.tab, P.ws, P.perm, offsets, counts, ids, paths, st));
+}
+
 }  // extern "C"

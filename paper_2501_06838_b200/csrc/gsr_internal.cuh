@@ -636,6 +636,10 @@ cudaError_t launch_rank_halo(const void* alpha, const void* mu, const void* sigm
 cudaError_t launch_render_fwd(const ImgTable& tab, const Workspace& ws, float* out,
                               cudaStream_t st, const float* gt = nullptr,
                               double* loss_acc = nullptr);
+// test-only: the forward tiles' kept candidates (offs == nullptr: counts[total_ftiles] only)
+cudaError_t launch_debug_fwd_lists(const ImgTable& tab, const Workspace& ws, const int* perm,
+                                   const int* offs, int* counts, int* ids, uint8_t* paths,
+                                   cudaStream_t st);
 // render_bwd.cu
 // grad_out = dL/dI, or (img, gt != nullptr) the fused L1 gradient sign(img - gt) * inv_numel
 cudaError_t launch_render_bwd_moments(const ImgTable& tab, const Workspace& ws, const int* perm,

@@ -375,6 +375,49 @@ __device__ __forceinline__ void fwd_epilogue(FwdSmem2<CFG>& sm, const DevImg& im
     fwd_store<LOSS, CFG>(sm.stage, im, Tx0, Ty0, out, gt, loss_acc);
 }
 
+// The filter's decision for one candidate of a forward tile (columns fx0..fx1, rows fy0..fyc
+// inside the image / band): keep = its support rect (R21) meets the tile; pth = its evaluation
+// path; mwd = the window rect as tile column / row bit masks (small tiles' masked path). Shared
+// by K4 and the debug lists.
+template <class CFG>
+__device__ __forceinline__ void fwd_classify(const int4 rc, int cl, int fx0, int fx1, int fy0,
+                                             int fyc, bool& keep, int& pth, uint2& mwd) {
+    constexpr int FTILE_H = CFG::TH, FWD_ROWS = CFG::ROWS, FWD_STRIP = CFG::STRIP;
+    const unsigned sxs = (unsigned)rc.x, sys = (unsigned)rc.y;
+    const int sx0 = (int)(sxs & 0xffffu), sx1 = (int)(sxs >> 16);
+    const int sy0 = (int)(sys & 0xffffu), sy1 = (int)(sys >> 16);
+    const int fy1 = fy0 + FTILE_H - 1;                 // the tile's last row (unclipped)
+    keep = !(sx1 < fx0 || sx0 > fx1 || sy1 < fy0 || sy0 > fyc);
+    const unsigned xs = (unsigned)rc.z, ys = (unsigned)rc.w;
+    const int x0 = (int)(xs & 0xffffu), x1 = (int)(xs >> 16);
+    const int y0 = (int)(ys & 0xffffu), y1 = (int)(ys >> 16);
+    bool full;
+    if (FWD_ROWS == 1 && GSR_FWD_CUTMASK) {
+        // small tiles (narrow windows, where the window often cuts the support): the mask
+        // matters only on a side where the window edge lies inside the tile AND cuts the
+        // +-13.5 sigma box (the support ends at the window edge); where the support edge lies
+        // inside the window, every pixel beyond it is outside the box and evaluates to exactly
+        // 0 (R21). C2 -3%; the large tiles keep the plain test (their windows rarely end inside
+        // a tile)
+        full = !((x0 > fx0 && sx0 == x0) || (x1 < fx1 && sx1 == x1) ||
+                 (y0 > fy0 && sy0 == y0) || (y1 < fy1 && sy1 == y1));
+    } else {
+        full = x0 <= fx0 && x1 >= fx1 && y0 <= fy0 && y1 >= fy1;
+    }
+    // column halves the support meets (left 16 / right 16 columns)
+    const bool hl = sx0 <= fx0 + 15, hr = sx1 >= fx0 + 16;
+    const int hv = !GSR_FWD_HALVES || !use_halves<FWD_STRIP>() || (hl && hr) ? 0 : (hl ? 1 : 2);
+    if constexpr (FWD_ROWS == 2) {
+        pth = (full ? ((cl & 1) ? P_REC3 : P_DIR3) : P_MSK3) + hv;
+    } else {
+        pth = (full ? 0 : 3) + hv;
+        const int c0 = max(x0 - fx0, 0), c1 = min(x1 - fx0, 31);
+        const int w0 = max(y0 - fy0, 0), w1 = min(y1 - fy0, 31);
+        mwd.x = c1 < c0 ? 0u : (unsigned)(((2ull << c1) - 1ull) & ~((1ull << c0) - 1ull));
+        mwd.y = w1 < w0 ? 0u : (unsigned)(((2ull << w1) - 1ull) & ~((1ull << w0) - 1ull));
+    }
+}
+
 template <int KS, bool LOSS, class CFG>
 __global__ void __launch_bounds__(CFG::WARPS * 32, 16 / CFG::WARPS) k_render_fwd2(const ImgTable tab,
                                                               const float4* __restrict__ rec,
@@ -594,42 +637,8 @@ __global__ void __launch_bounds__(CFG::WARPS * 32, 16 / CFG::WARPS) k_render_fwd
             bool keep = false;
             int pth = 0;
             uint2 mwd = make_uint2(0u, 0u);
-            {                  // every lane (lanes past the batch hold the empty sentinel rect)
-                const unsigned sxs = (unsigned)rb[0].x, sys = (unsigned)rb[0].y;
-                const int sx0 = (int)(sxs & 0xffffu), sx1 = (int)(sxs >> 16);
-                const int sy0 = (int)(sys & 0xffffu), sy1 = (int)(sys >> 16);
-                keep = !(sx1 < fx0 || sx0 > fx1 || sy1 < fy0 || sy0 > fy1);
-                const unsigned xs = (unsigned)rb[0].z, ys = (unsigned)rb[0].w;
-                const int x0 = (int)(xs & 0xffffu), x1 = (int)(xs >> 16);
-                const int y0 = (int)(ys & 0xffffu), y1 = (int)(ys >> 16);
-                bool full;
-                if (FWD_ROWS == 1 && GSR_FWD_CUTMASK) {
-                    // small tiles (narrow windows, where the window often cuts the support):
-                    // the mask matters only on a side where the window edge lies inside the
-                    // tile AND cuts the +-13.5 sigma box (the support ends at the window edge);
-                    // where the support edge lies inside the window, every pixel beyond it is
-                    // outside the box and evaluates to exactly 0 (R21). C2 -3%; the large
-                    // tiles keep the plain test (their windows rarely end inside a tile)
-                    full = !((x0 > fx0 && sx0 == x0) || (x1 < fx1 && sx1 == x1) ||
-                             (y0 > fy0 && sy0 == y0) || (y1 < fy0 + FTILE_H - 1 && sy1 == y1));
-                } else {
-                    full = x0 <= fx0 && x1 >= fx1 && y0 <= fy0 && y1 >= fy0 + FTILE_H - 1;
-                }
-                // column halves the support meets (left 16 / right 16 columns)
-                const bool hl = sx0 <= fx0 + 15, hr = sx1 >= fx0 + 16;
-                const int hv = !GSR_FWD_HALVES || !use_halves<FWD_STRIP>() || (hl && hr) ? 0 : (hl ? 1 : 2);
-                if constexpr (FWD_ROWS == 2) {
-                    pth = (full ? ((cb[0] & 1) ? P_REC3 : P_DIR3) : P_MSK3) + hv;
-                } else {
-                    pth = (full ? 0 : 3) + hv;
-                    {                              // the window rect as tile column / row masks
-                        const int c0 = max(x0 - fx0, 0), c1 = min(x1 - fx0, 31);
-                        const int w0 = max(y0 - fy0, 0), w1 = min(y1 - fy0, 31);
-                        mwd.x = c1 < c0 ? 0u : (unsigned)(((2ull << c1) - 1ull) & ~((1ull << c0) - 1ull));
-                        mwd.y = w1 < w0 ? 0u : (unsigned)(((2ull << w1) - 1ull) & ~((1ull << w0) - 1ull));
-                    }
-                }
-            }
+            // every lane (lanes past the batch hold the empty sentinel rect)
+            fwd_classify<CFG>(rb[0], cb[0], fx0, fx1, fy0, fy1, keep, pth, mwd);
 #if GSR_FWD_SPLIT
             const bool front = keep && pth == FRONT_PATH;
             const unsigned mf = __ballot_sync(0xffffffffu, front);
@@ -692,6 +701,68 @@ __global__ void __launch_bounds__(CFG::WARPS * 32, 16 / CFG::WARPS) k_render_fwd
 #pragma unroll
     for (int a = 0; a < NACC; ++a) sm.wp[warp].tot[a][lane] = acc[a];   // (after the barrier)
     fwd_epilogue<KS, LOSS, CFG>(sm, im, Tx0, Ty0, krank, out, gt, loss_acc);
+}
+
+// Materialised forward tile lists (test-only, gsr_debug_fwd_tile_lists): one warp per forward
+// tile in image order walks the tile's candidate stream exactly as K4 does (CandStream::build,
+// cand_index) and applies K4's filter decision (fwd_classify); the kept candidates' Gaussian
+// indices and paths in stream order. offs == nullptr: counts only.
+template <class CFG>
+__global__ void __launch_bounds__(32) k_debug_fwd_lists(
+    const ImgTable tab, const int4* __restrict__ rects, const uint8_t* __restrict__ cls,
+    const int* __restrict__ cell_start, const int* __restrict__ ext,
+    const int2* __restrict__ reach, const int* __restrict__ perm, const int* __restrict__ offs,
+    int* __restrict__ counts, int* __restrict__ ids, uint8_t* __restrict__ paths) {
+    __shared__ CandChunk ch;
+    const int tile = blockIdx.x, lane = threadIdx.x;
+    const int kimg = find_image_by_ftile(tab, tile);
+    const DevImg& im = tab.img[kimg];
+    const int t = tile - im.ftile_base;
+    const int Tx0 = (t % im.fntx) * CFG::TW;
+    const int Ty0 = im.row_begin + (t / im.fntx) * CFG::TH;
+    const int fx0 = Tx0, fx1 = min(Tx0 + CFG::TW - 1, im.Ws - 1);
+    const int fy0 = Ty0, fy1 = min(Ty0 + CFG::TH - 1, im.row_end - 1);
+    CandStream vs;
+    vs.cs = cell_start;
+    vs.reach = reach;
+    vs.row0 = im.cell_base;
+    vs.row_stride = im.ncx;
+    vs.cx_lo = (Tx0 - query_ext(ext, kimg, 0) + 1 + im.offx) / CELL;
+    vs.cx_hi = min(im.ncx - 1, (fx1 + im.offx) / CELL);
+    vs.cy_hi = min(im.ncy - 1, (fy1 - im.row_begin + im.offy) / CELL);
+    vs.X0 = fx0;
+    vs.Y0 = fy0;
+    vs.trim = im.dense && vs.cx_hi - vs.cx_lo + 1 >= 6;
+    int cy = fy0 <= fy1 ? (Ty0 - im.row_begin - query_ext(ext, kimg, 1) + 1 + im.offy) / CELL
+                        : vs.cy_hi + 1;
+    const int base = offs ? offs[tile] : 0;
+    int c = 0;
+    while (true) {
+        vs.build(ch, cy, lane);
+        __syncwarp();
+        const int total = ch.pre[32];
+        for (int v0 = 0; v0 < total; v0 += 32) {
+            const int v = v0 + lane;
+            bool keep = false;
+            int pth = 0, p = 0;
+            uint2 mwd = make_uint2(0u, 0u);
+            if (v < total) {
+                p = cand_index(ch, v, 0);
+                fwd_classify<CFG>(rects[p], cls[p], fx0, fx1, fy0, fy1, keep, pth, mwd);
+            }
+            const unsigned m = __ballot_sync(0xffffffffu, keep);
+            if (keep && offs) {
+                const int o = base + c + __popc(m & ((1u << lane) - 1u));
+                ids[o] = perm[p];
+                paths[o] = (uint8_t)pth;
+            }
+            c += __popc(m);
+        }
+        __syncwarp();
+        if (ch.cy_next > vs.cy_hi) break;
+        cy = ch.cy_next;
+    }
+    if (!offs && lane == 0) counts[tile] = c;
 }
 
 // Per-device one-time setup of an instance (the dynamic shared-memory opt-in is a property of
@@ -805,6 +876,19 @@ cudaError_t launch_render_fwd(const ImgTable& tab, const Workspace& ws, float* o
     }
     prof_end(h, st);
     if (e != cudaSuccess) return e;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_debug_fwd_lists(const ImgTable& tab, const Workspace& ws, const int* perm,
+                                   const int* offs, int* counts, int* ids, uint8_t* paths,
+                                   cudaStream_t st) {
+    if (tab.total_ftiles <= 0) return cudaSuccess;
+    if (tab.fwd_small)
+        k_debug_fwd_lists<FwdCfgSmall><<<tab.total_ftiles, 32, 0, st>>>(
+            tab, ws.rects, ws.cls, ws.cell_start, ws.ext, ws.reach, perm, offs, counts, ids, paths);
+    else
+        k_debug_fwd_lists<FwdCfgWide><<<tab.total_ftiles, 32, 0, st>>>(
+            tab, ws.rects, ws.cls, ws.cell_start, ws.ext, ws.reach, perm, offs, counts, ids, paths);
     return cudaGetLastError();
 }
 

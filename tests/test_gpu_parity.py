@@ -450,3 +450,63 @@ np.save(sys.argv[1], ok.cpu().numpy())
         assert "RAISED True" in r.stdout, r.stdout
         outs[f.name] = np.load(f)
     assert np.array_equal(outs["plain.npy"], outs["nvtx.npy"])
+
+
+def _tile_pairs(rects, Hs, Ws, tw, th):
+    """Brute force: sorted (tile, gaussian) keys of every support rect x forward tile overlap."""
+    x0, x1, y0, y1 = (rects[:, k].astype(np.int64) for k in range(4))
+    ok = (x0 <= x1) & (y0 <= y1)
+    ntx = -(-Ws // tw)
+    keys = []
+    for i in np.nonzero(ok)[0]:
+        txs = np.arange(x0[i] // tw, x1[i] // tw + 1)
+        tys = np.arange(y0[i] // th, y1[i] // th + 1)
+        t = (tys[:, None] * ntx + txs[None, :]).ravel()
+        keys.append(t * (1 << 32) + i)
+    return np.sort(np.concatenate(keys)) if keys else np.zeros(0, np.int64)
+
+
+@pytest.mark.parametrize("H,W,s,r,wide", [(48, 48, 4.0, 0.1, False), (60, 80, 8.0, 0.1, False),
+                                          (40, 60, 8.0, 1.0, True)],
+                         ids=["small-tiles", "large-tiles-reach-trim", "multi-chunk"])
+def test_fwd_tile_lists_bit_exact(gsr, H, W, s, r, wide):
+    """K4's kept candidates per forward tile (its candidate stream -- cell rows trimmed by the
+    cell reach -- and filter, materialised through gsr_debug_fwd_tile_lists) equal the brute-force
+    set of support rects (R21) meeting the tile, without duplicates; every path is consistent
+    with the rects: a single column half only when the support misses the other, the full-window
+    paths only where the window covers the tile (large) / cuts no support edge inside it (small)."""
+    import torch
+    from paper_2501_06838_b200 import debug
+    c = S.gaussians(H, W, seed=1007)
+    if wide:
+        c["sigma"][::50] = 3.0
+    dev = to_dev(c)
+    (tw, th, nt), counts, ids, paths = debug.fwd_tile_lists(*dev, H, W, s, r)
+    sup = debug.rects(*dev, H, W, s, r, support=True).cpu().numpy()
+    win = debug.rects(*dev, H, W, s, r).cpu().numpy()
+    Hs, Ws = O.out_dims(H, W, s)
+    assert (tw, th) in ((16, 8), (32, 16))
+    counts, ids, paths = counts.cpu().numpy(), ids.cpu().numpy(), paths.cpu().numpy()
+    tiles = np.repeat(np.arange(nt), counts)
+    got = tiles.astype(np.int64) * (1 << 32) + ids
+    assert len(np.unique(got)) == len(got), "a candidate kept twice in one tile"
+    assert np.array_equal(np.sort(got), _tile_pairs(sup, Hs, Ws, tw, th))
+    ntx = -(-Ws // tw)
+    tx0 = (tiles % ntx) * tw
+    ty0 = (tiles // ntx) * th
+    sx0, sx1, wx0, wx1 = sup[ids, 0], sup[ids, 1], win[ids, 0], win[ids, 1]
+    sy0, sy1, wy0, wy1 = sup[ids, 2], sup[ids, 3], win[ids, 2], win[ids, 3]
+    if tw == 32:
+        hv = paths % 3
+        assert np.all(sx1[hv == 1] <= tx0[hv == 1] + 15)
+        assert np.all(sx0[hv == 2] >= tx0[hv == 2] + 16)
+        both = hv == 0
+        assert np.all((sx0[both] <= tx0[both] + 15) & (sx1[both] >= tx0[both] + 16))
+        covers = (wx0 <= tx0) & (wx1 >= np.minimum(tx0 + tw - 1, Ws - 1)) & (wy0 <= ty0) & \
+                 (wy1 >= ty0 + th - 1)
+        assert np.array_equal(paths < 6, covers)       # recurrence / direct only when covered
+    else:
+        fx1 = np.minimum(tx0 + tw - 1, Ws - 1)
+        cut = ((wx0 > tx0) & (sx0 == wx0)) | ((wx1 < fx1) & (sx1 == wx1)) | \
+              ((wy0 > ty0) & (sy0 == wy0)) | ((wy1 < ty0 + th - 1) & (sy1 == wy1))
+        assert np.array_equal(paths >= 3, cut)
