@@ -373,10 +373,10 @@ gsr_status gsr_debug_rects_ex(const float* alpha, const float* mu, const float* 
                               int32_t lr_w, double scale, double ratio, uint32_t flags,
                               int32_t* rects, void* stream);
 
-/* Tile binning, materialised: for every render tile of the single image (tiles of
+/* Tile binning, materialised: for every backward render tile of the single image (tiles of
  * tile_w x tile_h HR px in row-major tile order, as reported by gsr_tile_shape), the exact list of
- * Gaussians whose support rect (R21) intersects the tile, in the order the render kernels visit them (cell
- * order, ascending index within a cell). Two calls: first with ids == NULL to fill
+ * Gaussians whose support rect (R21) intersects the tile, in the order the backward kernel visits
+ * them (cell order, ascending index within a cell). Two calls: first with ids == NULL to fill
  * counts[ntiles] (device int32); then with ids (device int32, sum(counts) entries, CSR by tile)
  * and cells (device int32, same length, the sort key = cell of each entry). */
 gsr_status gsr_debug_tile_lists(const float* alpha, const float* mu, const float* sigma,

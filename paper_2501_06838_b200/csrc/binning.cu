@@ -434,12 +434,11 @@ __global__ void k_debug_rects(const float* __restrict__ alpha, const float* __re
     rects[i] = o;
 }
 
-// Materialised per-tile candidate lists, walking the same cell spans as the render kernels (cell
-// rows trimmed by the cell reach as reach_trim does) and keeping the candidates whose rect
-// intersects the tile. One thread per tile (test-only).
+// Materialised per-tile candidate lists of the backward's tiles, walking the same cell spans as
+// K5 (untrimmed cell rows) and keeping the candidates whose rect intersects the tile. One thread
+// per tile (test-only; the forward's walk is materialised by k_debug_fwd_lists).
 __global__ void k_debug_tile_lists(ImgTable tab, const int* __restrict__ ext,
                                    const int* __restrict__ cell_start,
-                                   const int2* __restrict__ reach,
                                    const int4* __restrict__ rects, const int* __restrict__ perm,
                                    const uint32_t* __restrict__ keys,
                                    const int* __restrict__ tile_off, int* __restrict__ counts,
@@ -459,12 +458,7 @@ __global__ void k_debug_tile_lists(ImgTable tab, const int* __restrict__ ext,
     int base = ids ? tile_off[tile] : 0;
     for (int cy = cy_lo; cy <= cy_hi; ++cy) {
         int row = im.cell_base + cy * im.ncx;
-        auto ok = [&](int cx) { return reach[row + cx].x >= Tx0 && reach[row + cx].y >= Ty0; };
-        int lo = cx_lo, hi = cx_hi;
-        while (lo <= cx_hi && !ok(lo)) ++lo;
-        while (hi >= lo && !ok(hi)) --hi;
-        if (lo > hi) continue;
-        for (int p = cell_start[row + lo]; p < cell_start[row + hi + 1]; ++p) {
+        for (int p = cell_start[row + cx_lo]; p < cell_start[row + cx_hi + 1]; ++p) {
             const int4 rc = rects[p];
             unsigned xs = (unsigned)rc.x, ys = (unsigned)rc.y;
             int x0 = xs & 0xffff, x1 = xs >> 16, y0 = ys & 0xffff, y1 = ys >> 16;
@@ -665,16 +659,16 @@ cudaError_t launch_debug_tile_lists(const ImgTable& tab, const Workspace& ws, co
     int nt = tab.total_tiles;
     if (nt <= 0) return cudaSuccess;
     if (!ids) {
-        k_debug_tile_lists<<<grid1d(nt, 64), 64, 0, st>>>(tab, ws.ext, ws.cell_start, ws.reach, ws.rects, perm,
+        k_debug_tile_lists<<<grid1d(nt, 64), 64, 0, st>>>(tab, ws.ext, ws.cell_start, ws.rects, perm,
                                                           keys_sorted, nullptr, counts, nullptr,
                                                           nullptr);
     } else {
-        k_debug_tile_lists<<<grid1d(nt, 64), 64, 0, st>>>(tab, ws.ext, ws.cell_start, ws.reach, ws.rects, perm,
+        k_debug_tile_lists<<<grid1d(nt, 64), 64, 0, st>>>(tab, ws.ext, ws.cell_start, ws.rects, perm,
                                                           keys_sorted, nullptr, ws.tile_off,
                                                           nullptr, nullptr);
         cudaError_t e = exclusive_scan_i32(ws.tile_off, ws.tile_off, nt, ws.scan_tmp, st);
         if (e != cudaSuccess) return e;
-        k_debug_tile_lists<<<grid1d(nt, 64), 64, 0, st>>>(tab, ws.ext, ws.cell_start, ws.reach, ws.rects, perm,
+        k_debug_tile_lists<<<grid1d(nt, 64), 64, 0, st>>>(tab, ws.ext, ws.cell_start, ws.rects, perm,
                                                           keys_sorted, ws.tile_off, counts, ids,
                                                           cells);
     }
