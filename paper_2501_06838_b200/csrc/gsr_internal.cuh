@@ -11,6 +11,16 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+// GSR_BOUNDS_CHECK builds (tests only, tools/gpu_calls/gpu_r02_ci.sh): device asserts on the
+// indices the kernels derive (compute-sanitizer is not available on the GPU pool); no-ops in the
+// shipped build
+#ifdef GSR_BOUNDS_CHECK
+#include <cassert>
+#define GSR_CHECK(c) assert(c)
+#else
+#define GSR_CHECK(c) ((void)0)
+#endif
+
 namespace gsr {
 
 // ---- compile-time geometry -------------------------------------------------------------
@@ -571,6 +581,7 @@ struct CandStream {
 // position v of the chunk -> record index (r: a chunk row at or before v's row)
 __device__ __forceinline__ int cand_index(const CandChunk& ch, int v, int r) {
     while (v >= ch.pre[r + 1]) ++r;
+    GSR_CHECK(r >= 0 && r < 32 && v >= ch.pre[r]);
     return ch.st[r] + (v - ch.pre[r]);
 }
 

@@ -646,6 +646,8 @@ __global__ void __launch_bounds__(CFG::WARPS * 32, 16 / CFG::WARPS) k_render_fwd
             if (keep) {
                 const int slot = front ? cnt + __popc(mf & lt)
                                        : FWD_BUF - 1 - (cntb + __popc(mb & lt));
+                GSR_CHECK(slot >= 0 && slot < FWD_BUF && cnt + cntb + __popc(mf | mb) <= FWD_BUF);
+                GSR_CHECK(sb[0] >= 0 && sb[0] < cell_start[tab.total_cells]);
                 sm.path[warp][b][slot] = (uint8_t)pth;
                 if constexpr (FWD_ROWS == 1) sm.mw[warp][b][slot] = mwd;
                 const float4* src = rec + (long long)REC_F4 * sb[0];
