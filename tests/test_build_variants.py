@@ -13,7 +13,7 @@ CSRC = ROOT / "paper_2501_06838_b200" / "csrc"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 VARIANTS = [
-    ("render_fwd.cu", ["-DGSR_FWD_SPLIT=0", "-DGSR_CELL_REACH=0", "-DGSR_FWD_HALVES=0",
+    ("render_fwd.cu", ["-DGSR_FWD_SPLIT=0", "-DGSR_CELL_REACH=0", "-DGSR_BOUNDS_CHECK", "-DGSR_FWD_HALVES=0",
                        "-DGSR_FWD_CUTMASK=0", "-DGSR_FWD_SCAN_D=3", "-DGSR_FWD_SMALL_STRIP=8",
                        "-DGSR_FWD_WARPS_LARGE=4", "-DGSR_FWD_WARPS_SMALL=2"]),
     ("render_bwd.cu", ["-DGSR_BWD_UNROLL=4", "-DGSR_BWD_UNROLL_MASKED=8", "-DGSR_BWD_KQ=8", "-DGSR_BWD_CTASORT=0",
