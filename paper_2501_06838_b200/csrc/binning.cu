@@ -166,6 +166,7 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_scatter(
         __syncwarp();
         if (valid) {
             if ((peers & lt) == 0) wcnt[warp][d] += __popc(peers);
+            GSR_CHECK(pos >= 0 && pos < n);
             keys_out[pos] = key[c];
             vals_out[pos] = val[c];
         }
@@ -366,6 +367,7 @@ __global__ void k_records(const T* __restrict__ alpha, const T* __restrict__ mu,
     const int mx1 = (int)__reduce_max_sync(grp, (unsigned)sr.x1);
     const int my1 = (int)__reduce_max_sync(grp, (unsigned)sr.y1);
     if ((threadIdx.x & 31) == __ffs(grp) - 1) {
+        GSR_CHECK(key < (uint32_t)tab.total_cells && mx1 >= 0 && my1 >= 0);
         atomicMax(&reach[key].x, mx1);
         atomicMax(&reach[key].y, my1);
     }
