@@ -304,7 +304,11 @@ __device__ __forceinline__ void fwd_store(const float (*stage)[CFG::TW * 3], con
         const int lane = threadIdx.x & 31;
         const long long o = im.out_off + ((long long)(r + Ty0 - im.row_begin) * im.Ws + Tx0) * 3;
         const int nf = nx * 3;
-        if (nx == TW && (o & 3) == 0) {
+        // whole rows as float4 where the row starts on a 16-B boundary of the caller's buffer
+        // (the ABI does not require `out` / `gt` themselves to be 16-B aligned)
+        const uintptr_t al = reinterpret_cast<uintptr_t>(out + o) |
+                             (LOSS ? reinterpret_cast<uintptr_t>(gt + o) : uintptr_t(0));
+        if (nx == TW && (al & 15) == 0) {
             for (int c4 = lane; c4 < ROWF / 4; c4 += 32) {
                 const float4 v = *reinterpret_cast<const float4*>(&stage[r][4 * c4]);
                 *reinterpret_cast<float4*>(out + o + 4 * c4) = v;

@@ -643,16 +643,26 @@ class StreamedFwdBwd:
     shaped like host_params. The call returns after enqueueing; the current stream waits for all
     work (synchronize it, or record an event, before reading the host outputs)."""
 
-    def __init__(self, lay: Layout, ratio: float = 0.1, groups: int = 16, device=None):
+    def __init__(self, lay: Layout, ratio: float = 0.1, groups: int = 16, device=None,
+                 ramp: bool = True):
         self.lay, self.ratio = lay, float(ratio)
         self.dev = torch.device(device if device is not None else "cuda")
         ims = lay.images
         n = max((im.g_off + im.g_cnt for im in ims), default=0)
         self.n = n
         G = max(1, min(groups, len(ims)))
+        # image-group boundaries; ramp: the first and the last group hold one image each (the
+        # first group's host->device copy and the last group's device->host copy are the only
+        # ones no kernel hides), the rest split evenly
+        N = len(ims)
+        if ramp and G >= 4 and N >= G:
+            mid = [1 + (q * (N - 2)) // (G - 2) for q in range(G - 1)]
+            bounds = [0] + mid + [N]
+        else:
+            bounds = [(q * N) // G for q in range(G + 1)]
         self.groups = []
         for q in range(G):
-            k0, k1 = (q * len(ims)) // G, ((q + 1) * len(ims)) // G
+            k0, k1 = bounds[q], bounds[q + 1]
             if k0 == k1:
                 continue
             g0 = min(ims[k].g_off for k in range(k0, k1))

@@ -510,3 +510,21 @@ def test_fwd_tile_lists_bit_exact(gsr, H, W, s, r, wide):
         cut = ((wx0 > tx0) & (sx0 == wx0)) | ((wx1 < fx1) & (sx1 == wx1)) | \
               ((wy0 > ty0) & (sy0 == wy0)) | ((wy1 < ty0 + th - 1) & (sy1 == wy1))
         assert np.array_equal(paths >= 3, cut)
+
+
+def test_fwd_output_at_any_float_offset(gsr):
+    """The caller's output buffer need not be 16-B aligned (a view one float into a tensor): the
+    epilogue's float4 row stores fall back to scalar stores where the row is misaligned, and the
+    image is bit-identical to the aligned render (large and small tiles)."""
+    import torch
+    for H, W, s in [(21, 30, 8.0), (15, 19, 2.5)]:
+        c = S.gaussians(H, W, seed=9)
+        dev = to_dev(c)
+        lay = gsr.layout([gsr.Image(H, W, s, 0, c["alpha"].shape[0])])
+        ref = gsr.render_fwd_batched(*dev, lay)
+        for shift in (1, 2, 3):
+            buf = torch.full((lay.out_numel + 4,), float("nan"), device="cuda")
+            out = buf[shift:shift + lay.out_numel]
+            gsr.render_fwd_batched(*dev, lay, out=out)
+            torch.cuda.synchronize()
+            assert torch.equal(out, ref)

@@ -11,7 +11,9 @@ from _util import assert_fwd_close
 pytestmark = pytest.mark.gpu
 
 
-def test_streamed_matches_batched():
+@pytest.mark.parametrize("groups,sizes", [(3, [1, 2, 2]), (4, [1, 1, 2, 1])],
+                         ids=["even", "ramped"])
+def test_streamed_matches_batched(groups, sizes):
     import torch
     import paper_2501_06838_b200 as gsr
     imgs = [(20, 24, 3.0), (17, 13, 2.5), (24, 24, 4.0), (9, 30, 1.7), (16, 16, 8.0)]
@@ -32,8 +34,9 @@ def test_streamed_matches_batched():
     hg = torch.from_numpy(g).pin_memory()
     h_out = torch.empty(lay.out_numel, dtype=torch.float32).pin_memory()
     h_grads = [torch.empty_like(t).pin_memory() for t in hp]
-    step = gsr.StreamedFwdBwd(lay, 0.1, groups=3)
-    assert len(step.groups) == 3
+    step = gsr.StreamedFwdBwd(lay, 0.1, groups=groups)
+    # >= 4 groups: the first and the last hold one image each (ramp)
+    assert [len(sub.images) for *_, sub in step.groups] == sizes
     for _ in range(2):                      # reuse of the cached buffers
         step(hp, hg, h_out, h_grads)
         torch.cuda.synchronize()
